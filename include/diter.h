@@ -1,0 +1,183 @@
+/*
+ * diter.h -- C ABI of libditer.so, the B200 (sm_100a) D-iteration diffusion
+ * sweep (D. Hong, "D-iteration: Evaluation of the Asynchronous Distributed
+ * Computation", arXiv 1202.6168).
+ *
+ * Problem:  X = P X + B with spectral radius of P < 1.
+ *   p_ij is the weight of the edge j -> i; column j of P holds the out-edges
+ *   of j, stored as CSC.  PageRank: P = d Q,
+ *   q_ij = 1/#out_j, B = (1-d) V, V uniform; a dangling column (#out_j = 0)
+ *   stays zero, so its fluid leaves the system (BASELINE.json configs[1]).
+ *
+ * Method:  fluid F_0 = B, history H_0 = 0; a
+ *   diffusion of node i does  sent = F_i; H_i += sent; F_i = 0;
+ *   F_j += p_ji * sent  for every child j (eq. defF/defH).  The library runs
+ *   it as snapshot passes: pass p selects S_p = {i : |F_i| > T_p} (cyclic
+ *   threshold test), takes every i in S_p, then pushes
+ *   their fluid (eq. defF with J_S = sum_{i in S_p} J_i), and lowers T by
+ *   alpha per the threshold policy.  It stops when the
+ *   residual |F|_1 falls below the caller's target; |X - H|_1 <= |F|_1/(1-d)
+ *   (PAPER.md:104-107).
+ *
+ * Conventions (all functions):
+ *   - Every function returns a di_status and never throws or aborts.
+ *   - All array arguments of di_create / di_create_dist / helpers are HOST
+ *     pointers, copied before the call returns; the caller keeps ownership.
+ *     Output buffers are caller-owned (host unless the name says _device).
+ *   - The library owns all device memory and its own CUDA stream.
+ *   - A context is not thread-safe: one owner at a time.
+ *   - Invalid inputs are rejected at create time (DI_ERR_INVALID_ARG /
+ *     DI_ERR_CONTRACTION) and leave *out = NULL.
+ *   - di_last_error(ctx) gives a message for the last failure on ctx, or on
+ *     the calling thread when ctx == NULL.
+ */
+#ifndef DITER_H
+#define DITER_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct di_ctx di_ctx;
+
+typedef enum {
+  DI_OK = 0,
+  DI_ERR_INVALID_ARG = 1,   /* bad sizes, non-monotone col_ptr, row out of range, d not in (0,1) */
+  DI_ERR_CONTRACTION = 2,   /* signed mode: some column has sum_i |p_ij| > d */
+  DI_ERR_OOM = 3,           /* device or host allocation failed */
+  DI_ERR_CUDA = 4,          /* CUDA runtime error (message in di_last_error) */
+  DI_ERR_NCCL = 5,          /* NCCL error (distributed contexts) */
+  DI_ERR_NOT_CONVERGED = 6, /* max_passes reached before the target; state stays valid and resumable */
+  DI_ERR_STATE = 7,         /* call not valid in the context's current state */
+  DI_ERR_UNSUPPORTED = 8    /* feature not built into this library */
+} di_status;
+
+/* Threshold policies for T_{p+1} (readings R4). */
+enum {
+  DI_POLICY_GEOM = 0,      /* T <- T/alpha after every pass (literal "scale down progressively") */
+  DI_POLICY_HYBRID = 1     /* T <- T/alpha iff |S_p| <= hybrid_frac * N, else T unchanged */
+};
+
+/* Exchange modes of distributed contexts. */
+enum {
+  DI_EXCHANGE_SYNC = 0,    /* exchange + merge after every pass (reproduces the 1-GPU passes) */
+  DI_EXCHANGE_ASYNC = 1    /* send when s_k > r_k / K (eq. send) */
+};
+
+typedef struct {
+  int32_t policy;          /* DI_POLICY_*; default HYBRID */
+  int32_t check_interval;  /* passes per captured CUDA graph between host checks; default 16 */
+  double alpha;            /* threshold factor alpha > 1; default 1.5 */
+  double hybrid_frac;      /* HYBRID frontier fraction f; default 0.05 */
+  double t0;               /* initial threshold; <= 0 means max_i |B_i| / alpha (reading R5) */
+  int64_t max_passes;      /* guard -> DI_ERR_NOT_CONVERGED; default 1000000 */
+  int32_t exchange_mode;   /* DI_EXCHANGE_*; distributed only; default ASYNC */
+  int32_t device;          /* CUDA device ordinal; -1 = current device (default) */
+  int32_t scatter_kernel;  /* 0 = degree-binned (default); reserved for variants */
+  int32_t reserved[7];
+} di_options;
+
+/* One record per executed pass (device-logged, read with di_get_pass_log). */
+typedef struct {
+  int64_t pass;            /* p */
+  double T;                /* T_p used for the selection */
+  double r;                /* r_p = |F|_1 (local part if distributed) before the pass */
+  int64_t frontier;        /* |S_p| (all bins, dangling included) */
+  int64_t edges;           /* E_p = sum_{i in S_p} #out_i (elementary diffusions) */
+  int64_t dangling;        /* nodes of S_p with #out = 0 */
+  int64_t bin_low;         /* nodes of S_p with 1 <= #out <= 32      (thread per node)  */
+  int64_t bin_mid;         /* nodes of S_p with 33 <= #out <= 2048   (warp per node)    */
+  int64_t bin_hub;         /* nodes of S_p with #out > 2048          (CTA(s) per node)  */
+} di_pass_log;
+
+typedef struct {
+  int64_t passes;          /* passes executed since create */
+  int64_t edges;           /* elementary diffusions since create (sum of E_p) */
+  int64_t nodes;           /* node diffusions since create (sum of |S_p|) */
+  double residual;         /* last measured/predicted |F|_1 (exact after di_get_residual) */
+  double threshold;        /* current T */
+  double run_ms;           /* device time of the last di_run (CUDA events on the library stream) */
+  double run_ms_total;     /* summed over all di_run calls */
+  int64_t alg_bytes;       /* algorithmic bytes moved since create: 8 N_scan + 40 |S| + 20 E (+8 E signed) */
+  int64_t exchanged_bytes; /* payload bytes sent to peers since create (distributed) */
+  int64_t exchanges;       /* number of outbox flushes (distributed) */
+  int64_t n_local;         /* nodes owned by this context */
+  int64_t nnz_local;       /* stored edges owned by this context */
+  int64_t graph_launches;  /* CUDA graph launches by di_run since create */
+  int64_t kernel_launches; /* kernels launched by the library since create (counting graph nodes) */
+} di_stats;
+
+/* Fill *opt with the defaults above. */
+void di_default_options(di_options *opt);
+
+/* Single-GPU context.  n nodes; col_ptr[n+1] (int64, col_ptr[0] = 0,
+ * non-decreasing, col_ptr[n] = nnz); row_idx[nnz] (int32 in [0,n)).
+ *  values == NULL -> PageRank mode: p_ji = d / #out_i for each stored edge,
+ *                    derived on the device from col_ptr (never stored).
+ *  values != NULL -> signed mode: p_ji = values[e]; d is the contraction
+ *                    factor of the bound; validated: max_j sum_i |p_ij| <= d < 1.
+ *  b == NULL -> B_i = (1-d)/n; else b[n] is copied.
+ * Duplicate rows within a column are allowed (they add). */
+di_status di_create(di_ctx **out, int64_t n, const int64_t *col_ptr, const int32_t *row_idx,
+                    const double *values, const double *b, double d, const di_options *opt);
+
+/* Distributed context, one call per rank (collective).  This rank owns the
+ * node range [bounds[rank], bounds[rank+1]) (PID_k computes
+ * [F]_k and [H]_k), and the columns of that range:
+ * col_ptr_local[hi-lo+1] (starting at 0), row_idx_local with GLOBAL row ids.
+ * bounds[world+1] must be identical on all ranks (di_partition_cb).
+ * comm_id: the 128-byte ncclUniqueId created by rank 0 and broadcast by the
+ * caller.  Returns DI_ERR_UNSUPPORTED if the library was built without NCCL. */
+di_status di_create_dist(di_ctx **out, int32_t rank, int32_t world, const void *comm_id,
+                         const int64_t *bounds, int64_t n_global,
+                         const int64_t *col_ptr_local, const int32_t *row_idx_local,
+                         const double *values_local, const double *b_local, double d,
+                         const di_options *opt);
+
+/* 128-byte ncclUniqueId for di_create_dist (call on rank 0 only). */
+di_status di_get_unique_id(void *comm_id_out);
+
+/* Run passes until |F|_1 < residual_target (absolute; global if distributed).
+ * Resumable: call again with a smaller target to continue from (F, H).
+ * Collective for distributed contexts.  Returns DI_OK when the target is met,
+ * DI_ERR_NOT_CONVERGED when max_passes was reached first. */
+di_status di_run(di_ctx *ctx, double residual_target);
+
+/* Copy H (n, or hi-lo when distributed) into the caller's host buffer. */
+di_status di_get_history(const di_ctx *ctx, double *h_out);
+/* Copy F likewise (for invariant checks, e.g. F = B - (I-P) H). */
+di_status di_get_fluid(const di_ctx *ctx, double *f_out);
+/* Device-to-device variants: d_out is a device pointer on the context's device. */
+di_status di_get_history_device(const di_ctx *ctx, double *d_out);
+di_status di_get_fluid_device(const di_ctx *ctx, double *d_out);
+/* Exact |F|_1 by a deterministic two-level reduction (global if distributed;
+ * collective then).  Also refreshes stats.residual. */
+di_status di_get_residual(di_ctx *ctx, double *r_out);
+di_status di_get_stats(const di_ctx *ctx, di_stats *s);
+/* Copy pass records [first, first+count) into out; *n_copied receives the
+ * number copied (passes beyond the log capacity are not recorded). */
+di_status di_get_pass_log(const di_ctx *ctx, int64_t first, int64_t count, di_pass_log *out,
+                          int64_t *n_copied);
+const char *di_last_error(const di_ctx *ctx);
+void di_destroy(di_ctx *ctx);
+
+/* ---- setup helpers (integer work, bit-exact against the oracle) ---- */
+
+/* COO (src[e] -> dst[e]) to CSC on the GPU: sort by (src, dst), drop
+ * duplicates, histogram + scan -> col_ptr[n+1]; row_idx must hold m entries;
+ * *nnz_out receives the deduplicated count.  Host pointers. (
+ * BASELINE.json configs[2] "duplicate edges dropped") */
+di_status di_csc_from_coo(int64_t n, int64_t m, const int32_t *src, const int32_t *dst,
+                          int64_t *col_ptr, int32_t *row_idx, int64_t *nnz_out);
+
+/* Cost-balanced contiguous partition (reading R10):
+ * bounds[0] = 0, bounds[K] = n, bounds[k] = min{i : C[i] >= ceil(k C[n] / K)}
+ * forced strictly increasing, where C = cost_prefix[n+1] (e.g. col_ptr). */
+di_status di_partition_cb(int64_t n, const int64_t *cost_prefix, int32_t K, int64_t *bounds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DITER_H */
