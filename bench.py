@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""bench.py -- D-iteration diffusion sweep (arXiv 1202.6168) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+
+A "step" is one whole solve of the hot path: di_reset (F = B, H = 0) then
+di_run until |F|_1 < the config's metric target (BASELINE.json), on the
+synthetic input already resident in HBM.  value = edges diffused per second
+(sum of E_p over the solve / device time of di_run, CUDA events on the
+library's stream), max over ranks for N > 1.
+
+One JSON line on rank 0:
+  roofline      -- the dominant kernel (k_scatter): algorithmic bytes 20 E per
+                   launch / its average launch time, events recorded inside the
+                   captured graph during the timed region; peak = measured HBM
+                   copy bandwidth (MEASURED_PEAKS.json)
+  cpu_baseline  -- the CPU oracle (1 core) on a bounded sample of the same solve
+  e2e           -- same metric through the public C ABI with host buffers:
+                   di_create (H2D of the graph from pinned host memory) + di_run +
+                   di_get_history (D2H) + di_destroy per step
+  clocks        -- nvidia-smi samples taken during the timed region
+--impl reference runs the oracle arm (the reference of this tier) instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "edges diffused/s and time to |F|_1<1e-9 at 1/2/4/8 B200; % HBM roofline"
+
+WORKLOADS = {
+    "C1": "configs[0]: uniform out-degree 1..10 PageRank, N=1e3, stop |F|_1<1e-12",
+    "C2": "configs[1]: web-like PageRank N=1e6 (~7.0e6 edges, 15% dangling), stop |F|_1<1e-9",
+    "C3": "configs[2]: R-MAT scale 24 PageRank (ids permuted, dedup), stop |F|_1<1e-9",
+    "C4": "configs[3]: web-like PageRank N=1e8 (~1.6e9 edges, 15% dangling), stop |F|_1<1e-9",
+    "C5": "configs[4]: signed sparse N=1e6, 20 nnz/col, |col|_1=0.9, stop |F|_1<1e-9|B|_1",
+}
+L2_BYTES = 126 * 2 ** 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4", choices=sorted(WORKLOADS))
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--policy", default=None, choices=[None, "geom", "hybrid"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0,
+                    help="bound on the oracle sample for cpu_baseline / reference steps")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scale", type=int, default=None, help="C3 scale override (tests)")
+    ap.add_argument("--n", type=int, default=None, help="node-count override (tests)")
+    return ap.parse_args()
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------ inputs --
+
+def load_problem(args):
+    """Seeded synthetic input of the config (host arrays)."""
+    import diter_inputs as gen
+    t = time.perf_counter()
+    p = gen.config(args.config, args.seed, n=args.n, scale=args.scale)
+    if args.config == "C3":
+        # configs[2]: CSC built from the raw R-MAT COO on the GPU (K8, di_csc_from_coo)
+        import paper_1202_6168_b200 as di
+        src, dst = gen.rmat_coo(args.scale or 24, args.seed)
+        p.col_ptr, p.row_idx = di.di_csc_from_coo(p.n, src, dst)
+        del src, dst
+    log(f"[bench] generated {args.config}: n={p.n} nnz={p.nnz} in {time.perf_counter() - t:.1f}s")
+    return p
+
+
+def policy_of(args):
+    import paper_1202_6168_b200 as di
+    if args.policy == "geom":
+        return di.DI_POLICY_GEOM
+    if args.policy == "hybrid":
+        return di.DI_POLICY_HYBRID
+    # SURVEY §8c-Q4 / DESIGN R4: HYBRID on web-like and signed, GEOM on R-MAT
+    return di.DI_POLICY_GEOM if args.config == "C3" else di.DI_POLICY_HYBRID
+
+
+# ------------------------------------------------------------------ clocks --
+
+class ClockSampler:
+    """nvidia-smi samples during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ cpu baseline --
+
+def oracle_sample(p, policy_geom: bool, seconds: float, state=None):
+    """Time the CPU oracle (as it stands, 1 thread) on snapshot passes of the same
+    solve until `seconds` elapse; returns (edges, secs, passes, state)."""
+    import oracle
+    P = oracle.Problem(p.n, p.col_ptr, p.row_idx, p.values, p.b, p.d)
+    st = state or P.init()
+    pol = oracle.GEOM if policy_geom else oracle.HYBRID
+    e0, p0 = st.edges, st.passes
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        rc = P.snapshot(st, p.stop, pol, max_passes=1)
+        if rc == oracle.OK:
+            break
+    dt = time.perf_counter() - t0
+    return st.edges - e0, dt, st.passes - p0, st
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(config):
+    """dram bytes per k_scatter launch from the committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(config, {}).get("k_scatter_dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# -------------------------------------------------------------- reference arm --
+
+def run_reference(args, rank, world):
+    """The oracle arm (this tier's reference): rank 0 only, each step one bounded
+    sample of the same solve on the host cores."""
+    if rank != 0:
+        return
+    p = load_problem(args)
+    geom = policy_of(args) == 0
+    per = max(1.0, args.cpu_seconds / max(1, args.steps + args.warmup))
+    st = None
+    for _ in range(args.warmup):
+        _, _, _, st = oracle_sample(p, geom, per, st)
+    edges, secs, passes = 0, 0.0, 0
+    for _ in range(args.steps):
+        e, dt, np_, st = oracle_sample(p, geom, per, st)
+        edges += e
+        secs += dt
+        passes += np_
+    v = edges / secs if secs > 0 else 0.0
+    sample = (f"{passes} snapshot passes of the {args.config} solve continued from pass "
+              f"{st.passes - passes} (~{per:.1f}s per step), full graph")
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "edges/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3 / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic",
+           "config": {"workload": WORKLOADS[args.config], "n": p.n, "nnz": p.nnz},
+           "cpu_baseline": {"value": v, "unit": "edges/s", "cores": 1, "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------ our arm --
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import paper_1202_6168_b200 as di
+
+    torch.cuda.set_device(local_rank)
+    dist = world > 1
+    p = load_problem(args)
+    pol = policy_of(args)
+    opts = di.default_options(policy=pol, device=local_rank, profile=1)
+    if dist:
+        raise SystemExit("multi-GPU bench needs the distributed context (dist.cu)")
+    t = time.perf_counter()
+    ctx = di.di_create(p.n, p.col_ptr, p.row_idx, p.values, p.b, p.d, opts)
+    log(f"[bench] di_create {time.perf_counter() - t:.2f}s")
+    graph_bytes = 8 * (p.n + 1) + 4 * p.nnz + (8 * p.nnz if p.values is not None else 0)
+    resident = graph_bytes + 16 * p.n
+    flush = None
+    if resident < 4 * L2_BYTES:
+        flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device="cuda")
+
+    def step():
+        if flush is not None:
+            flush.fill_(1.0)                     # evict L2 between timed solves
+            torch.cuda.synchronize()
+        di.di_reset(ctx)
+        di.di_run(ctx, p.stop)
+        return di.di_get_stats(ctx)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        torch.distributed.barrier()
+    tot = {"run_ms": 0.0, "edges": 0, "passes": 0, "kt_scatter_ms": 0.0, "kt_select_ms": 0.0,
+           "kt_finalize_ms": 0.0, "scatter_bytes": 0, "alg_bytes": 0, "kernel_launches": 0,
+           "nodes": 0}
+    wall0 = time.perf_counter()
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            s = step()
+            for k in tot:
+                tot[k] += s[k]
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    r_final = di.di_get_residual(ctx)
+    assert r_final < p.stop, r_final
+    run_s = tot["run_ms"] / 1e3
+    value = tot["edges"] / run_s
+    peak, peak_kind = measured_peaks()
+    scat_gbs = tot["scatter_bytes"] / (tot["kt_scatter_ms"] / 1e3) / 1e9
+    n_launch = tot["passes"]                       # executed k_scatter launches
+    traffic = ncu_traffic(args.config)
+    kt_sum = tot["kt_scatter_ms"] + tot["kt_select_ms"] + tot["kt_finalize_ms"]
+    roofline = {"bound": "hbm", "achieved": scat_gbs, "peak": peak, "unit": "GB/s",
+                "frac": scat_gbs / peak, "traffic": traffic,
+                "kernel": "k_scatter", "peak_kind": peak_kind,
+                "bytes_per_launch": tot["scatter_bytes"] / max(1, n_launch),
+                "avg_launch_ms": tot["kt_scatter_ms"] / max(1, n_launch),
+                "share_of_step": tot["kt_scatter_ms"] / tot["run_ms"],
+                "kernel_shares": {"k_select": tot["kt_select_ms"] / kt_sum,
+                                  "k_scatter": tot["kt_scatter_ms"] / kt_sum,
+                                  "k_finalize": tot["kt_finalize_ms"] / kt_sum},
+                "path_alg_GBps": tot["alg_bytes"] / run_s / 1e9}
+    # ---- e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, p, opts, di, torch)
+    # ---- cpu baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        e, dt, npass, st = oracle_sample(p, pol == di.DI_POLICY_GEOM, args.cpu_seconds)
+        cpu = {"value": e / dt if dt > 0 else None, "unit": "edges/s", "cores": 1, "kind": "oracle",
+               "sample": f"first {npass} snapshot passes ({e} edges) of the same {args.config} solve "
+                         f"on the full graph, {dt:.1f}s on 1 host core"}
+    clocks = clk.summary()
+    di.di_destroy(ctx)
+    out = {"metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot["run_ms"] / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic",
+           "config": {"workload": WORKLOADS[args.config], "n": p.n, "nnz": p.nnz,
+                      "stop": p.stop, "policy": "geom" if pol == 0 else "hybrid", "seed": args.seed,
+                      "l2": ("flushed between steps (252 MB write)" if flush is not None else
+                             f"inputs ({resident / 1e9:.1f} GB resident) larger than L2 (126 MB)")},
+           "time_to_target_ms": tot["run_ms"] / args.steps,
+           "passes_per_solve": tot["passes"] / args.steps,
+           "normalized_iterations": tot["edges"] / args.steps / p.nnz,
+           "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+           "gpu_launches": int(tot["kernel_launches"]),
+           "clocks": clocks, "nvlink_bytes_per_round": 0,
+           "wall_s_timed": wall}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def run_e2e(args, p, opts, di, torch):
+    """Same metric through di_create/di_run/di_get_history with pinned host buffers."""
+    cp = torch.from_numpy(p.col_ptr).pin_memory()
+    ri = torch.from_numpy(p.row_idx).pin_memory()
+    vv = torch.from_numpy(p.values).pin_memory() if p.values is not None else None
+    bb = torch.from_numpy(p.b).pin_memory() if p.b is not None else None
+    H = torch.empty(p.n, dtype=torch.float64).pin_memory()
+    h2d = cp.numel() * 8 + ri.numel() * 4 + (vv.numel() * 8 if vv is not None else 0) + \
+        (bb.numel() * 8 if bb is not None else 0)
+    d2h = p.n * 8
+    import copy
+    o2 = copy.copy(opts)
+    o2.profile = 0
+
+    def one():
+        ctx = di.di_create(p.n, cp, ri, vv, bb, p.d, o2)
+        di.di_run(ctx, p.stop)
+        di.di_get_history(ctx, H)
+        e = di.di_get_stats(ctx)["edges"]
+        di.di_destroy(ctx)
+        return e
+
+    one()                                          # warm (allocator, module load)
+    torch.cuda.synchronize()
+    edges = 0
+    t0 = time.perf_counter()
+    steps = max(1, min(args.steps, 3))
+    for _ in range(steps):
+        edges += one()
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    return {"value": edges / dt, "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": steps, "ms_per_step": dt * 1e3 / steps}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -40,6 +40,12 @@
 extern "C" {
 #endif
 
+#if defined(__GNUC__)
+#define DI_API __attribute__((visibility("default")))
+#else
+#define DI_API
+#endif
+
 typedef struct di_ctx di_ctx;
 
 typedef enum {
@@ -76,7 +82,9 @@ typedef struct {
   int32_t exchange_mode;   /* DI_EXCHANGE_*; distributed only; default ASYNC */
   int32_t device;          /* CUDA device ordinal; -1 = current device (default) */
   int32_t scatter_kernel;  /* 0 = degree-binned (default); reserved for variants */
-  int32_t reserved[7];
+  int32_t profile;         /* 1: time each kernel of each executed pass with CUDA events
+                              recorded inside the captured graph (di_stats.kt_*); default 0 */
+  int32_t reserved[6];
 } di_options;
 
 /* One record per executed pass (device-logged, read with di_get_pass_log). */
@@ -107,10 +115,15 @@ typedef struct {
   int64_t nnz_local;       /* stored edges owned by this context */
   int64_t graph_launches;  /* CUDA graph launches by di_run since create */
   int64_t kernel_launches; /* kernels launched by the library since create (counting graph nodes) */
+  double kt_select_ms;     /* profile=1: summed device time of k_select over executed passes */
+  double kt_scatter_ms;    /* profile=1: summed device time of k_scatter over executed passes */
+  double kt_finalize_ms;   /* profile=1: summed device time of k_finalize over executed passes */
+  int64_t kt_passes;       /* profile=1: executed passes those sums cover */
+  int64_t scatter_bytes;   /* algorithmic bytes of the scatter kernel since create: 20 E (28 E signed) */
 } di_stats;
 
 /* Fill *opt with the defaults above. */
-void di_default_options(di_options *opt);
+DI_API void di_default_options(di_options *opt);
 
 /* Single-GPU context.  n nodes; col_ptr[n+1] (int64, col_ptr[0] = 0,
  * non-decreasing, col_ptr[n] = nnz); row_idx[nnz] (int32 in [0,n)).
@@ -120,7 +133,7 @@ void di_default_options(di_options *opt);
  *                    factor of the bound; validated: max_j sum_i |p_ij| <= d < 1.
  *  b == NULL -> B_i = (1-d)/n; else b[n] is copied.
  * Duplicate rows within a column are allowed (they add). */
-di_status di_create(di_ctx **out, int64_t n, const int64_t *col_ptr, const int32_t *row_idx,
+DI_API di_status di_create(di_ctx **out, int64_t n, const int64_t *col_ptr, const int32_t *row_idx,
                     const double *values, const double *b, double d, const di_options *opt);
 
 /* Distributed context, one call per rank (collective).  This rank owns the
@@ -130,38 +143,43 @@ di_status di_create(di_ctx **out, int64_t n, const int64_t *col_ptr, const int32
  * bounds[world+1] must be identical on all ranks (di_partition_cb).
  * comm_id: the 128-byte ncclUniqueId created by rank 0 and broadcast by the
  * caller.  Returns DI_ERR_UNSUPPORTED if the library was built without NCCL. */
-di_status di_create_dist(di_ctx **out, int32_t rank, int32_t world, const void *comm_id,
+DI_API di_status di_create_dist(di_ctx **out, int32_t rank, int32_t world, const void *comm_id,
                          const int64_t *bounds, int64_t n_global,
                          const int64_t *col_ptr_local, const int32_t *row_idx_local,
                          const double *values_local, const double *b_local, double d,
                          const di_options *opt);
 
 /* 128-byte ncclUniqueId for di_create_dist (call on rank 0 only). */
-di_status di_get_unique_id(void *comm_id_out);
+DI_API di_status di_get_unique_id(void *comm_id_out);
+
+/* Reset the state to F = B, H = 0, T = T_0 keeping the
+ * uploaded graph, and clear the pass counters, the pass log and the stats, so
+ * the next di_run solves from scratch.  Collective for distributed contexts. */
+DI_API di_status di_reset(di_ctx *ctx);
 
 /* Run passes until |F|_1 < residual_target (absolute; global if distributed).
  * Resumable: call again with a smaller target to continue from (F, H).
  * Collective for distributed contexts.  Returns DI_OK when the target is met,
  * DI_ERR_NOT_CONVERGED when max_passes was reached first. */
-di_status di_run(di_ctx *ctx, double residual_target);
+DI_API di_status di_run(di_ctx *ctx, double residual_target);
 
 /* Copy H (n, or hi-lo when distributed) into the caller's host buffer. */
-di_status di_get_history(const di_ctx *ctx, double *h_out);
+DI_API di_status di_get_history(const di_ctx *ctx, double *h_out);
 /* Copy F likewise (for invariant checks, e.g. F = B - (I-P) H). */
-di_status di_get_fluid(const di_ctx *ctx, double *f_out);
+DI_API di_status di_get_fluid(const di_ctx *ctx, double *f_out);
 /* Device-to-device variants: d_out is a device pointer on the context's device. */
-di_status di_get_history_device(const di_ctx *ctx, double *d_out);
-di_status di_get_fluid_device(const di_ctx *ctx, double *d_out);
+DI_API di_status di_get_history_device(const di_ctx *ctx, double *d_out);
+DI_API di_status di_get_fluid_device(const di_ctx *ctx, double *d_out);
 /* Exact |F|_1 by a deterministic two-level reduction (global if distributed;
  * collective then).  Also refreshes stats.residual. */
-di_status di_get_residual(di_ctx *ctx, double *r_out);
-di_status di_get_stats(const di_ctx *ctx, di_stats *s);
+DI_API di_status di_get_residual(di_ctx *ctx, double *r_out);
+DI_API di_status di_get_stats(const di_ctx *ctx, di_stats *s);
 /* Copy pass records [first, first+count) into out; *n_copied receives the
  * number copied (passes beyond the log capacity are not recorded). */
-di_status di_get_pass_log(const di_ctx *ctx, int64_t first, int64_t count, di_pass_log *out,
+DI_API di_status di_get_pass_log(const di_ctx *ctx, int64_t first, int64_t count, di_pass_log *out,
                           int64_t *n_copied);
-const char *di_last_error(const di_ctx *ctx);
-void di_destroy(di_ctx *ctx);
+DI_API const char *di_last_error(const di_ctx *ctx);
+DI_API void di_destroy(di_ctx *ctx);
 
 /* ---- setup helpers (integer work, bit-exact against the oracle) ---- */
 
@@ -169,13 +187,13 @@ void di_destroy(di_ctx *ctx);
  * duplicates, histogram + scan -> col_ptr[n+1]; row_idx must hold m entries;
  * *nnz_out receives the deduplicated count.  Host pointers. (
  * BASELINE.json configs[2] "duplicate edges dropped") */
-di_status di_csc_from_coo(int64_t n, int64_t m, const int32_t *src, const int32_t *dst,
+DI_API di_status di_csc_from_coo(int64_t n, int64_t m, const int32_t *src, const int32_t *dst,
                           int64_t *col_ptr, int32_t *row_idx, int64_t *nnz_out);
 
 /* Cost-balanced contiguous partition (reading R10):
  * bounds[0] = 0, bounds[K] = n, bounds[k] = min{i : C[i] >= ceil(k C[n] / K)}
  * forced strictly increasing, where C = cost_prefix[n+1] (e.g. col_ptr). */
-di_status di_partition_cb(int64_t n, const int64_t *cost_prefix, int32_t K, int64_t *bounds);
+DI_API di_status di_partition_cb(int64_t n, const int64_t *cost_prefix, int32_t K, int64_t *bounds);
 
 #ifdef __cplusplus
 }

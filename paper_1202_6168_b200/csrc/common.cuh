@@ -1,0 +1,77 @@
+// common.cuh -- device helpers shared by the libditer kernels (sm_100a only).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libditer is built for sm_100a (B200) only"
+#endif
+
+namespace diter {
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Fire-and-forget fp64 add in L2 (RED.E.ADD.F64.RN): the scatter of the
+// diffusion F_j += p_ji * sent.
+__device__ __forceinline__ void red_add(double *addr, double v) {
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(addr), "d"(v) : "memory");
+}
+
+// Streaming 16-byte load of 4 row indices that bypasses L1 allocation
+// (each row index is read once per diffusion of its column).
+__device__ __forceinline__ int4 ld_stream_i4(const int4 *p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ int ld_stream_i1(const int *p) {
+  int r;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ double2 ld_stream_d2(const double2 *p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+               : "=d"(r.x), "=d"(r.y)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ double ld_stream_d1(const double *p) {
+  double r;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
+
+// Warp-aggregated append: every lane of the warp calls it (uniform control
+// flow); lanes with pred get consecutive slots of *counter.
+__device__ __forceinline__ unsigned warp_append(unsigned *counter, bool pred) {
+  const unsigned mask = __ballot_sync(0xffffffffu, pred);
+  if (mask == 0u) return 0u;
+  const int leader = __ffs(mask) - 1;
+  unsigned base = 0u;
+  if ((int)lane_id() == leader) base = atomicAdd(counter, (unsigned)__popc(mask));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  return base + (unsigned)__popc(mask & lanemask_lt());
+}
+
+}  // namespace diter

@@ -1,0 +1,73 @@
+// ctx.cuh -- the opaque di_ctx behind include/diter.h (host-side layout).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/diter.h"
+#include "types.cuh"
+
+struct DistState;  // dist.cu
+
+struct di_ctx {
+  // problem
+  long long n_rows = 0;     // N (global)
+  long long n_local = 0;    // owned nodes (= N on one GPU)
+  long long nnz_local = 0;  // stored edges of the owned columns
+  long long lo = 0;         // first owned node id
+  double d = 0.85;
+  di_options opt{};
+  int check_interval = 16;
+  int device = -1;
+  int rank = 0, world = 1;
+
+  // device state (HBM)
+  long long *col_ptr = nullptr;  // [n_local+1]
+  int *row_idx = nullptr;        // [nnz_local] global row ids
+  double *vals = nullptr;        // [nnz_local] signed mode only
+  double *d_b = nullptr;         // B [n_local] when given (kept for di_reset)
+  double *F = nullptr;           // fluid [n_local]
+  double *H = nullptr;           // history [n_local]
+  diter::Bins bins{};
+  unsigned long long cap_low = 0, cap_mid = 0, cap_hub = 0;
+  diter::Partial *part = nullptr;
+  double *l1_part = nullptr;
+  double *l1_out = nullptr;
+  diter::Ctl *ctl = nullptr;
+  di_pass_log *log = nullptr;
+  long long log_cap = 0;
+
+  // launch
+  cudaStream_t stream = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int num_sms = 0, grid_select = 0, grid_scatter = 0, grid_l1 = 0;
+  void *h_ctl = nullptr;  // pinned mirror of Ctl
+  diter::Ctl ctl_init{};  // control block right after create (di_reset restores it)
+  double b_uniform = 0.0;
+  std::vector<cudaEvent_t> prof_ev;  // profile=1: 4 events per captured pass
+
+  // stats
+  long long passes_done = 0, edges = 0, nodes = 0;
+  long long graph_launches = 0, kernel_launches = 0;
+  long long exchanged_bytes = 0, exchanges = 0, alg_bytes_exchange = 0;
+  double residual = 0.0, threshold = 0.0, run_ms = 0.0, run_ms_total = 0.0;
+  double kt_ms[3] = {0.0, 0.0, 0.0};
+  long long kt_passes = 0;
+
+  DistState *dist = nullptr;
+  std::string err;
+};
+
+void diter_set_err(di_ctx *ctx, const char *fmt, ...);
+di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_idx,
+                      const double *values, const double *b, const di_options *opt);
+di_status diter_l1_launch(di_ctx *ctx);
+
+// distributed hooks (dist.cu); identities / no-ops on single-GPU contexts
+void diter_dist_free(di_ctx *ctx);
+double diter_dist_max(di_ctx *ctx, double v);
+double diter_dist_sum(di_ctx *ctx, double v);
+di_status diter_dist_run(di_ctx *ctx, double target);
+di_status diter_dist_reset(di_ctx *ctx);

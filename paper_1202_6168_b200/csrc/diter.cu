@@ -1,0 +1,496 @@
+// diter.cu -- libditer.so: C ABI (include/diter.h) over the sm_100a kernels.
+//
+// Host side of one context: upload + validation (di_create), the pass loop
+// captured as a CUDA graph of `check_interval` passes (di_run), getters.
+// No CPU fallback exists: every step of a pass runs in the kernels of
+// kernels.cuh; the host only launches graphs and reads the stop flag.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/diter.h"
+#include "ctx.cuh"
+#include "kernels.cuh"
+
+using namespace diter;
+
+static thread_local std::string g_thread_err;
+
+void diter_set_err(di_ctx *ctx, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf;
+  g_thread_err = buf;
+}
+
+#define CK(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess) {                                                           \
+      diter_set_err(ctx, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_),       \
+                    __FILE__, __LINE__);                                               \
+      return e_ == cudaErrorMemoryAllocation ? DI_ERR_OOM : DI_ERR_CUDA;               \
+    }                                                                                  \
+  } while (0)
+
+extern "C" void di_default_options(di_options *o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->policy = DI_POLICY_HYBRID;
+  o->check_interval = 16;
+  o->alpha = 1.5;
+  o->hybrid_frac = 0.05;
+  o->t0 = 0.0;
+  o->max_passes = 1000000;
+  o->exchange_mode = DI_EXCHANGE_ASYNC;
+  o->device = -1;
+  o->scatter_kernel = 0;
+  o->profile = 0;
+}
+
+template <typename T>
+static di_status dalloc(di_ctx *ctx, T **p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  CK(cudaMalloc((void **)p, count * sizeof(T)));
+  return DI_OK;
+}
+
+#define TRY(x)                      \
+  do {                              \
+    di_status s_ = (x);             \
+    if (s_ != DI_OK) return s_;     \
+  } while (0)
+
+static void free_ctx(di_ctx *c) {
+  if (!c) return;
+  if (c->device >= 0) cudaSetDevice(c->device);
+  if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+  for (cudaEvent_t e : c->prof_ev)
+    if (e) cudaEventDestroy(e);
+  void *ptrs[] = {c->col_ptr, c->row_idx, c->vals, c->d_b, c->F, c->H, c->bins.low_idx, c->bins.low_w,
+                  c->bins.mid_idx, c->bins.mid_w, c->bins.hub_idx, c->bins.hub_w,
+                  c->bins.hub_chunk, c->part, c->l1_part, c->l1_out, c->ctl, c->log};
+  for (void *p : ptrs)
+    if (p) cudaFree(p);
+  if (c->h_ctl) cudaFreeHost(c->h_ctl);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  diter_dist_free(c);
+  delete c;
+}
+
+// Launch geometry: grid-stride kernels sized to the SM count x resident CTAs.
+static di_status setup_geometry(di_ctx *ctx) {
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, ctx->device));
+  ctx->num_sms = prop.multiProcessorCount;
+  int occ_sel = 0, occ_sc = 0, occ_sc_s = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sel, k_select, kSelectThreads, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sc, k_scatter<false>, kScatterThreads, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sc_s, k_scatter<true>, kScatterThreads, 0));
+  ctx->grid_select = ctx->num_sms * std::max(1, std::min(occ_sel, 8));
+  // never more select CTAs than warps of work
+  long long need = (ctx->n_local + kSelectThreads - 1) / kSelectThreads;
+  if (need < ctx->grid_select) ctx->grid_select = (int)std::max(1LL, need);
+  ctx->grid_scatter = ctx->num_sms * std::max(1, ctx->vals ? occ_sc_s : occ_sc);
+  ctx->grid_l1 = ctx->grid_select;
+  return DI_OK;
+}
+
+// Capture check_interval passes of (select, scatter, finalize) once.
+static di_status capture_graph(di_ctx *ctx) {
+  cudaGraph_t graph;
+  CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  Graph g{ctx->col_ptr, ctx->row_idx, ctx->vals, ctx->n_local, ctx->d};
+  const bool prof = ctx->opt.profile != 0;
+  if (prof && ctx->prof_ev.empty()) {
+    ctx->prof_ev.assign(4 * ctx->check_interval, nullptr);
+    for (auto &e : ctx->prof_ev) CK(cudaEventCreate(&e));
+  }
+  for (int k = 0; k < ctx->check_interval; ++k) {
+    if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 0], ctx->stream, cudaEventRecordExternal));
+    k_select<<<ctx->grid_select, kSelectThreads, 0, ctx->stream>>>(g, ctx->F, ctx->H, ctx->bins,
+                                                                  ctx->ctl, ctx->part);
+    if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 1], ctx->stream, cudaEventRecordExternal));
+    if (ctx->vals)
+      k_scatter<true><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->bins, ctx->ctl);
+    else
+      k_scatter<false><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->bins, ctx->ctl);
+    if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 2], ctx->stream, cudaEventRecordExternal));
+    k_finalize<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->ctl, ctx->part, ctx->grid_select, ctx->log);
+    if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 3], ctx->stream, cudaEventRecordExternal));
+  }
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+  if (e != cudaSuccess) {
+    diter_set_err(ctx, "graph capture failed: %s", cudaGetErrorString(e));
+    return DI_ERR_CUDA;
+  }
+  e = cudaGraphInstantiate(&ctx->graph_exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) {
+    diter_set_err(ctx, "graph instantiate failed: %s", cudaGetErrorString(e));
+    return DI_ERR_CUDA;
+  }
+  return DI_OK;
+}
+
+// Shared by di_create and di_create_dist: upload, validate, allocate, init.
+di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_idx,
+                      const double *values, const double *b, const di_options *opt) {
+  di_options o;
+  if (opt) o = *opt; else di_default_options(&o);
+  if (!(o.alpha > 1.0) || o.check_interval < 1 || o.check_interval > 4096 || o.max_passes < 1 ||
+      (o.policy != DI_POLICY_GEOM && o.policy != DI_POLICY_HYBRID) || !(o.hybrid_frac >= 0.0)) {
+    diter_set_err(ctx, "invalid options");
+    return DI_ERR_INVALID_ARG;
+  }
+  ctx->opt = o;
+  ctx->check_interval = o.check_interval;
+  if (o.device >= 0) {
+    CK(cudaSetDevice(o.device));
+    ctx->device = o.device;
+  } else {
+    CK(cudaGetDevice(&ctx->device));
+  }
+  CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&ctx->ev0));
+  CK(cudaEventCreate(&ctx->ev1));
+  const long long n = ctx->n_local, nnz = ctx->nnz_local;
+  TRY(dalloc(ctx, &ctx->col_ptr, (size_t)n + 1));
+  TRY(dalloc(ctx, &ctx->row_idx, (size_t)nnz));
+  if (values) TRY(dalloc(ctx, &ctx->vals, (size_t)nnz));
+  TRY(dalloc(ctx, &ctx->F, (size_t)n));
+  TRY(dalloc(ctx, &ctx->H, (size_t)n));
+  CK(cudaMemcpyAsync(ctx->col_ptr, col_ptr, sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, ctx->stream));
+  if (nnz)
+    CK(cudaMemcpyAsync(ctx->row_idx, row_idx, sizeof(int) * nnz, cudaMemcpyHostToDevice, ctx->stream));
+  if (values && nnz)
+    CK(cudaMemcpyAsync(ctx->vals, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, ctx->stream));
+  if (b) {
+    TRY(dalloc(ctx, &ctx->d_b, (size_t)n));
+    CK(cudaMemcpyAsync(ctx->d_b, b, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  TRY(setup_geometry(ctx));
+  // validation + bin census on the device
+  Census *d_c = nullptr;
+  TRY(dalloc(ctx, &d_c, 1));
+  CK(cudaMemsetAsync(d_c, 0, sizeof(Census), ctx->stream));
+  k_census<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->col_ptr, n, ctx->row_idx, nnz, ctx->vals,
+                                                      ctx->d, d_c);
+  Census hc;
+  CK(cudaMemcpyAsync(&hc, d_c, sizeof(Census), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  cudaFree(d_c);
+  CK(cudaGetLastError());
+  if (hc.bad_ptr) {
+    diter_set_err(ctx, "col_ptr is not non-decreasing (%llu columns)", hc.bad_ptr);
+    return DI_ERR_INVALID_ARG;
+  }
+  if (hc.bad_row) {
+    diter_set_err(ctx, "%llu row indices out of range [0,%lld)", hc.bad_row, ctx->n_rows);
+    return DI_ERR_INVALID_ARG;
+  }
+  if (hc.bad_contraction) {
+    diter_set_err(ctx, "%llu columns have sum |p_ij| > d = %g (not contractive)", hc.bad_contraction, ctx->d);
+    return DI_ERR_CONTRACTION;
+  }
+  ctx->cap_low = hc.n_low;
+  ctx->cap_mid = hc.n_mid;
+  ctx->cap_hub = hc.n_hub;
+  TRY(dalloc(ctx, &ctx->bins.low_idx, hc.n_low));
+  TRY(dalloc(ctx, &ctx->bins.low_w, hc.n_low));
+  TRY(dalloc(ctx, &ctx->bins.mid_idx, hc.n_mid));
+  TRY(dalloc(ctx, &ctx->bins.mid_w, hc.n_mid));
+  TRY(dalloc(ctx, &ctx->bins.hub_idx, hc.n_hub));
+  TRY(dalloc(ctx, &ctx->bins.hub_w, hc.n_hub));
+  TRY(dalloc(ctx, &ctx->bins.hub_chunk, hc.n_hub));
+  TRY(dalloc(ctx, &ctx->part, (size_t)ctx->grid_select));
+  TRY(dalloc(ctx, &ctx->l1_part, (size_t)ctx->grid_l1));
+  TRY(dalloc(ctx, &ctx->l1_out, 1));
+  TRY(dalloc(ctx, &ctx->ctl, 1));
+  ctx->log_cap = 1 << 18;  // passes logged since create/reset (di_run is resumable)
+  TRY(dalloc(ctx, &ctx->log, (size_t)ctx->log_cap));
+  CK(cudaHostAlloc((void **)&ctx->h_ctl, sizeof(Ctl), cudaHostAllocDefault));
+  // state: F = B, H = 0
+  ctx->b_uniform = (1.0 - ctx->d) / (double)ctx->n_rows;
+  k_init_state<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->F, ctx->H, ctx->d_b, ctx->b_uniform, n);
+  // T_0 = max |B_i| / alpha (reading R5) unless given
+  double T0 = o.t0;
+  if (!(T0 > 0.0)) {
+    double mx = 0.0;
+    if (n > 0) {
+      k_max_abs<<<ctx->grid_l1, 256, 0, ctx->stream>>>(ctx->F, n, ctx->l1_part);
+      std::vector<double> hp(ctx->grid_l1);
+      CK(cudaMemcpyAsync(hp.data(), ctx->l1_part, sizeof(double) * ctx->grid_l1, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      for (double v : hp) mx = std::max(mx, v);
+    }
+    mx = diter_dist_max(ctx, mx);   // global max over ranks (identity when not distributed)
+    T0 = mx / o.alpha;
+  }
+  Ctl hc0;
+  std::memset(&hc0, 0, sizeof(hc0));
+  hc0.T = T0;
+  hc0.alpha = o.alpha;
+  hc0.hybrid_frac = o.hybrid_frac;
+  hc0.n_total = (double)ctx->n_rows;
+  hc0.policy = o.policy;
+  hc0.done = 1;
+  hc0.max_pass = o.max_passes;
+  hc0.log_cap = ctx->log_cap;
+  hc0.r = hc0.r_pred = INFINITY;
+  ctx->ctl_init = hc0;
+  CK(cudaMemcpyAsync(ctx->ctl, &ctx->ctl_init, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->threshold = T0;
+  TRY(capture_graph(ctx));
+  return DI_OK;
+}
+
+extern "C" di_status di_create(di_ctx **out, int64_t n, const int64_t *col_ptr, const int32_t *row_idx,
+                               const double *values, const double *b, double d, const di_options *opt) {
+  if (!out) { diter_set_err(nullptr, "out is NULL"); return DI_ERR_INVALID_ARG; }
+  *out = nullptr;
+  if (n < 1 || n > 2147483647LL || !col_ptr || !(d > 0.0 && d < 1.0)) {
+    diter_set_err(nullptr, "invalid arguments: need 1 <= n < 2^31, col_ptr, 0 < d < 1");
+    return DI_ERR_INVALID_ARG;
+  }
+  const long long nnz = col_ptr[n];
+  if (col_ptr[0] != 0 || nnz < 0 || (nnz > 0 && !row_idx)) {
+    diter_set_err(nullptr, "col_ptr[0] must be 0 and col_ptr[n] = nnz >= 0 (row_idx required when nnz > 0)");
+    return DI_ERR_INVALID_ARG;
+  }
+  di_ctx *ctx = new (std::nothrow) di_ctx();
+  if (!ctx) { diter_set_err(nullptr, "host OOM"); return DI_ERR_OOM; }
+  ctx->n_rows = n;
+  ctx->n_local = n;
+  ctx->nnz_local = nnz;
+  ctx->lo = 0;
+  ctx->d = d;
+  di_status s = diter_setup(ctx, col_ptr, row_idx, values, b, opt);
+  if (s != DI_OK) {
+    g_thread_err = ctx->err;
+    free_ctx(ctx);
+    return s;
+  }
+  *out = ctx;
+  return DI_OK;
+}
+
+// Exact |F|_1 of this context's slice into ctx->l1_out (device), deterministic.
+di_status diter_l1_launch(di_ctx *ctx) {
+  k_l1_partial<<<ctx->grid_l1, kSelectThreads, 0, ctx->stream>>>(ctx->F, ctx->n_local, ctx->l1_part);
+  k_l1_final<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->l1_part, ctx->grid_l1, ctx->l1_out);
+  ctx->kernel_launches += 2;
+  CK(cudaGetLastError());
+  return DI_OK;
+}
+
+static di_status read_ctl(di_ctx *ctx) {
+  CK(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return DI_OK;
+}
+
+extern "C" di_status di_run(di_ctx *ctx, double target) {
+  if (!ctx) { diter_set_err(nullptr, "ctx is NULL"); return DI_ERR_INVALID_ARG; }
+  if (!(target >= 0.0)) { diter_set_err(ctx, "target must be >= 0"); return DI_ERR_INVALID_ARG; }
+  if (ctx->world > 1) return diter_dist_run(ctx, target);
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  di_status st = DI_OK;
+  const long long max_pass_abs = ctx->passes_done + ctx->opt.max_passes;
+  for (;;) {
+    // exact residual first: the stop test of the previous launch is a prediction
+    TRY(diter_l1_launch(ctx));
+    k_begin_run<<<1, 1, 0, ctx->stream>>>(ctx->ctl, target, max_pass_abs, ctx->l1_out);
+    ctx->kernel_launches += 1;
+    TRY(read_ctl(ctx));
+    const Ctl *h = reinterpret_cast<const Ctl *>(ctx->h_ctl);
+    ctx->residual = h->r_pred;
+    if (h->r_pred < target) break;                       // converged (exact |F|_1)
+    if (h->pass >= max_pass_abs) { st = DI_ERR_NOT_CONVERGED; break; }
+    // graph launches until the device sets done
+    for (;;) {
+      const long long pass_before = h->pass;
+      CK(cudaGraphLaunch(ctx->graph_exec, ctx->stream));
+      ctx->graph_launches += 1;
+      ctx->kernel_launches += 3LL * ctx->check_interval;
+      TRY(read_ctl(ctx));
+      if (ctx->opt.profile) {
+        const long long active = std::min<long long>(h->pass - pass_before, ctx->check_interval);
+        for (long long k = 0; k < active; ++k) {
+          for (int q = 0; q < 3; ++q) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, ctx->prof_ev[4 * k + q], ctx->prof_ev[4 * k + q + 1]));
+            ctx->kt_ms[q] += ms;
+          }
+        }
+        ctx->kt_passes += active;
+      }
+      if (h->done) break;
+    }
+    ctx->passes_done = h->pass;
+    if (h->done == 2) {
+      TRY(diter_l1_launch(ctx));
+      double r;
+      CK(cudaMemcpyAsync(&r, ctx->l1_out, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      ctx->residual = r;
+      st = (r < target) ? DI_OK : DI_ERR_NOT_CONVERGED;
+      break;
+    }
+  }
+  CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  CK(cudaEventSynchronize(ctx->ev1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  ctx->run_ms = ms;
+  ctx->run_ms_total += ms;
+  const Ctl *h = reinterpret_cast<const Ctl *>(ctx->h_ctl);
+  ctx->passes_done = h->pass;
+  ctx->edges = h->edges;
+  ctx->nodes = h->nodes;
+  ctx->threshold = h->T;
+  if (st == DI_ERR_NOT_CONVERGED) diter_set_err(ctx, "max_passes reached before |F|_1 < %g", target);
+  return st;
+}
+
+extern "C" di_status di_reset(di_ctx *ctx) {
+  if (!ctx) { diter_set_err(nullptr, "ctx is NULL"); return DI_ERR_INVALID_ARG; }
+  CK(cudaSetDevice(ctx->device));
+  k_init_state<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->F, ctx->H, ctx->d_b, ctx->b_uniform,
+                                                          ctx->n_local);
+  CK(cudaMemcpyAsync(ctx->ctl, &ctx->ctl_init, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaGetLastError());
+  ctx->kernel_launches += 1;
+  ctx->passes_done = ctx->edges = ctx->nodes = 0;
+  ctx->kt_ms[0] = ctx->kt_ms[1] = ctx->kt_ms[2] = 0.0;
+  ctx->kt_passes = 0;
+  ctx->run_ms = ctx->run_ms_total = 0.0;
+  ctx->graph_launches = 0;
+  ctx->threshold = ctx->ctl_init.T;
+  ctx->exchanged_bytes = ctx->exchanges = ctx->alg_bytes_exchange = 0;
+  return diter_dist_reset(ctx);
+}
+
+static di_status copy_out(const di_ctx *cctx, const double *src, double *dst, cudaMemcpyKind kind) {
+  di_ctx *ctx = const_cast<di_ctx *>(cctx);
+  if (!ctx || !dst) { diter_set_err(ctx, "NULL argument"); return DI_ERR_INVALID_ARG; }
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMemcpyAsync(dst, src, sizeof(double) * ctx->n_local, kind, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return DI_OK;
+}
+
+extern "C" di_status di_get_history(const di_ctx *ctx, double *h) {
+  return copy_out(ctx, ctx ? ctx->H : nullptr, h, cudaMemcpyDeviceToHost);
+}
+extern "C" di_status di_get_fluid(const di_ctx *ctx, double *f) {
+  return copy_out(ctx, ctx ? ctx->F : nullptr, f, cudaMemcpyDeviceToHost);
+}
+extern "C" di_status di_get_history_device(const di_ctx *ctx, double *h) {
+  return copy_out(ctx, ctx ? ctx->H : nullptr, h, cudaMemcpyDeviceToDevice);
+}
+extern "C" di_status di_get_fluid_device(const di_ctx *ctx, double *f) {
+  return copy_out(ctx, ctx ? ctx->F : nullptr, f, cudaMemcpyDeviceToDevice);
+}
+
+extern "C" di_status di_get_residual(di_ctx *ctx, double *r_out) {
+  if (!ctx || !r_out) { diter_set_err(ctx, "NULL argument"); return DI_ERR_INVALID_ARG; }
+  CK(cudaSetDevice(ctx->device));
+  TRY(diter_l1_launch(ctx));
+  double r = 0.0;
+  CK(cudaMemcpyAsync(&r, ctx->l1_out, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  r = diter_dist_sum(ctx, r);
+  ctx->residual = r;
+  *r_out = r;
+  return DI_OK;
+}
+
+extern "C" di_status di_get_stats(const di_ctx *ctx, di_stats *s) {
+  if (!ctx || !s) { diter_set_err(nullptr, "NULL argument"); return DI_ERR_INVALID_ARG; }
+  std::memset(s, 0, sizeof(*s));
+  s->passes = ctx->passes_done;
+  s->edges = ctx->edges;
+  s->nodes = ctx->nodes;
+  s->residual = ctx->residual;
+  s->threshold = ctx->threshold;
+  s->run_ms = ctx->run_ms;
+  s->run_ms_total = ctx->run_ms_total;
+  s->alg_bytes = 8LL * ctx->n_local * ctx->passes_done + 40LL * ctx->nodes +
+                 (ctx->vals ? 28LL : 20LL) * ctx->edges + ctx->alg_bytes_exchange;
+  s->exchanged_bytes = ctx->exchanged_bytes;
+  s->exchanges = ctx->exchanges;
+  s->n_local = ctx->n_local;
+  s->nnz_local = ctx->nnz_local;
+  s->graph_launches = ctx->graph_launches;
+  s->kernel_launches = ctx->kernel_launches;
+  s->kt_select_ms = ctx->kt_ms[0];
+  s->kt_scatter_ms = ctx->kt_ms[1];
+  s->kt_finalize_ms = ctx->kt_ms[2];
+  s->kt_passes = ctx->kt_passes;
+  s->scatter_bytes = (ctx->vals ? 28LL : 20LL) * ctx->edges;
+  return DI_OK;
+}
+
+extern "C" di_status di_get_pass_log(const di_ctx *cctx, int64_t first, int64_t count, di_pass_log *out,
+                                     int64_t *n_copied) {
+  di_ctx *ctx = const_cast<di_ctx *>(cctx);
+  if (!ctx || (!out && count > 0) || first < 0 || count < 0) {
+    diter_set_err(ctx, "invalid arguments");
+    return DI_ERR_INVALID_ARG;
+  }
+  long long avail = std::min<long long>(ctx->passes_done, ctx->log_cap);
+  long long k = std::max<long long>(0, std::min<long long>(count, avail - first));
+  if (k > 0) {
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaMemcpyAsync(out, ctx->log + first, sizeof(di_pass_log) * k, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  if (n_copied) *n_copied = k;
+  return DI_OK;
+}
+
+extern "C" const char *di_last_error(const di_ctx *ctx) {
+  if (ctx) return ctx->err.c_str();
+  return g_thread_err.c_str();
+}
+
+extern "C" void di_destroy(di_ctx *ctx) { free_ctx(ctx); }
+
+// ---------------------------------------------------------- partition (K9) --
+// bounds[k] = min{ i : C[i] >= ceil(k C[n] / K) } by binary search (C is
+// non-decreasing), then forced strictly increasing and leaving >= 1 node per
+// later range (reading R10).
+extern "C" di_status di_partition_cb(int64_t n, const int64_t *C, int32_t K, int64_t *bounds) {
+  if (n < 1 || K < 1 || K > n || !C || !bounds) {
+    diter_set_err(nullptr, "di_partition_cb: need 1 <= K <= n and non-NULL arrays");
+    return DI_ERR_INVALID_ARG;
+  }
+  const long long total = C[n];
+  bounds[0] = 0;
+  for (int k = 1; k < K; ++k) {
+    const __int128 num = (__int128)k * total;
+    const long long goal = (long long)((num + K - 1) / K);
+    long long i = std::lower_bound(C, C + n + 1, (int64_t)goal) - C;
+    i = std::max<long long>(i, bounds[k - 1] + 1);
+    i = std::min<long long>(i, n - (K - k));
+    bounds[k] = i;
+  }
+  bounds[K] = n;
+  return DI_OK;
+}

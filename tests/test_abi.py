@@ -1,0 +1,61 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol that
+include/diter.h declares, fills default options, and its host-side helper
+di_partition_cb matches the oracle bit for bit."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import diter_inputs as gen
+import oracle
+import paper_1202_6168_b200 as di
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    hdr = open(os.path.join(ROOT, "include", "diter.h")).read()
+    return sorted(set(re.findall(r"DI_API\s+[\w\s\*]*?\b(di_\w+)\s*\(", hdr)))
+
+
+def test_header_declares_binding_exports():
+    assert declared_symbols() == sorted(di.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = di.load_library()
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+
+
+def test_default_options():
+    o = di.default_options()
+    assert o.policy == di.DI_POLICY_HYBRID and o.alpha == 1.5 and o.hybrid_frac == 0.05
+    assert o.check_interval == 16 and o.max_passes == 1_000_000 and o.device == -1
+
+
+def test_struct_sizes_match_header():
+    import ctypes
+    assert ctypes.sizeof(di.di_pass_log) == 72
+    assert ctypes.sizeof(di.di_stats) == 19 * 8
+    assert ctypes.sizeof(di.di_options) == 4 + 4 + 8 + 8 + 8 + 8 + 4 + 4 + 4 + 28
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 4, 8])
+def test_partition_cb_matches_oracle(K):
+    cp, _ = gen.web_graph(100_000, 3)
+    for cost in (cp, cp + np.arange(len(cp), dtype=np.int64)):
+        np.testing.assert_array_equal(di.di_partition_cb(cost, K), oracle.partition_cb(cost, K))
+
+
+def test_partition_cb_edge_cases():
+    # all-zero cost: ranges forced non-empty
+    cost = np.zeros(9, dtype=np.int64)
+    np.testing.assert_array_equal(di.di_partition_cb(cost, 4), oracle.partition_cb(cost, 4))
+    # one huge node
+    cost = np.concatenate([[0], np.cumsum([1000, 1, 1, 1, 1])]).astype(np.int64)
+    np.testing.assert_array_equal(di.di_partition_cb(cost, 3), oracle.partition_cb(cost, 3))
+    np.testing.assert_array_equal(di.di_partition_cb(cost, 5), [0, 1, 2, 3, 4, 5])
+    with pytest.raises(di.DiError):
+        di.di_partition_cb(cost, 6)
