@@ -64,6 +64,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scale", type=int, default=None, help="C3 scale override (tests)")
     ap.add_argument("--n", type=int, default=None, help="node-count override (tests)")
+    ap.add_argument("--pass-csv", default=None, help="write the last solve's per-pass log here")
     return ap.parse_args()
 
 
@@ -277,6 +278,12 @@ def run_ours(args, rank, world, local_rank):
                 tot[k] += s[k]
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
+    if args.pass_csv and rank == 0:
+        lg = di.di_get_pass_log(ctx)
+        with open(args.pass_csv, "w") as fcsv:
+            fcsv.write(",".join(lg.dtype.names) + "\n")
+            for row in lg:
+                fcsv.write(",".join(str(x) for x in row) + "\n")
     r_final = di.di_get_residual(ctx)
     assert r_final < p.stop, r_final
     run_s = tot["run_ms"] / 1e3

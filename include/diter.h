@@ -95,9 +95,11 @@ typedef struct {
   int64_t frontier;        /* |S_p| (all bins, dangling included) */
   int64_t edges;           /* E_p = sum_{i in S_p} #out_i (elementary diffusions) */
   int64_t dangling;        /* nodes of S_p with #out = 0 */
-  int64_t bin_low;         /* nodes of S_p with 1 <= #out <= 32      (thread per node)  */
-  int64_t bin_mid;         /* nodes of S_p with 33 <= #out <= 2048   (warp per node)    */
-  int64_t bin_hub;         /* nodes of S_p with #out > 2048          (CTA(s) per node)  */
+  int64_t bin_low;         /* nodes of S_p with 1 <= #out <= 32      (32 per warp, edge-balanced) */
+  int64_t bin_mid;         /* nodes of S_p with 33 <= #out <= 8192   (warp per node)    */
+  int64_t bin_hub;         /* nodes of S_p with #out > 8192          (CTA per 2048-edge chunk) */
+  double t_select_us;      /* profile=1: device time of k_select in this pass, else 0 */
+  double t_scatter_us;     /* profile=1: device time of k_scatter in this pass, else 0 */
 } di_pass_log;
 
 typedef struct {

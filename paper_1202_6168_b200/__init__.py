@@ -56,7 +56,8 @@ class di_pass_log(ctypes.Structure):
     _fields_ = [("pass_", ctypes.c_int64), ("T", ctypes.c_double), ("r", ctypes.c_double),
                 ("frontier", ctypes.c_int64), ("edges", ctypes.c_int64),
                 ("dangling", ctypes.c_int64), ("bin_low", ctypes.c_int64),
-                ("bin_mid", ctypes.c_int64), ("bin_hub", ctypes.c_int64)]
+                ("bin_mid", ctypes.c_int64), ("bin_hub", ctypes.c_int64),
+                ("t_select_us", ctypes.c_double), ("t_scatter_us", ctypes.c_double)]
 
 
 class di_stats(ctypes.Structure):
@@ -268,7 +269,8 @@ def di_get_pass_log(ctx: Context, first: int = 0, count: int | None = None) -> n
            ctx.handle)
     dt = np.dtype([("pass", np.int64), ("T", np.float64), ("r", np.float64), ("frontier", np.int64),
                    ("edges", np.int64), ("dangling", np.int64), ("bin_low", np.int64),
-                   ("bin_mid", np.int64), ("bin_hub", np.int64)])
+                   ("bin_mid", np.int64), ("bin_hub", np.int64), ("t_select_us", np.float64),
+                   ("t_scatter_us", np.float64)])
     arr = np.frombuffer(bytes(buf), dtype=dt, count=max(count, 1))[: got.value].copy()
     return arr
 

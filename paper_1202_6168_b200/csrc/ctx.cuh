@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/diter.h"
@@ -16,6 +17,7 @@ struct di_ctx {
   long long n_local = 0;    // owned nodes (= N on one GPU)
   long long nnz_local = 0;  // stored edges of the owned columns
   long long lo = 0;         // first owned node id
+  int hot_lo = 0;           // shared-memory hot window of the scatter (global row id)
   double d = 0.85;
   di_options opt{};
   int check_interval = 16;
@@ -29,9 +31,10 @@ struct di_ctx {
   double *d_b = nullptr;         // B [n_local] when given (kept for di_reset)
   double *F = nullptr;           // fluid [n_local]
   double *H = nullptr;           // history [n_local]
-  diter::Bins bins{};
+  diter::Frontier fr{};
   unsigned long long cap_low = 0, cap_mid = 0, cap_hub = 0;
-  diter::Partial *part = nullptr;
+  diter::SelPartial *sel_part = nullptr;
+  diter::ScPartial *sc_part = nullptr;
   double *l1_part = nullptr;
   double *l1_out = nullptr;
   diter::Ctl *ctl = nullptr;
@@ -42,7 +45,7 @@ struct di_ctx {
   cudaStream_t stream = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  int num_sms = 0, grid_select = 0, grid_scatter = 0, grid_l1 = 0;
+  int num_sms = 0, grid_select = 0, grid_scatter = 0, grid_l1 = 0, gsplit = 1;
   void *h_ctl = nullptr;  // pinned mirror of Ctl
   diter::Ctl ctl_init{};  // control block right after create (di_reset restores it)
   double b_uniform = 0.0;
@@ -55,6 +58,7 @@ struct di_ctx {
   double residual = 0.0, threshold = 0.0, run_ms = 0.0, run_ms_total = 0.0;
   double kt_ms[3] = {0.0, 0.0, 0.0};
   long long kt_passes = 0;
+  std::vector<std::pair<double, double>> pass_us;  // profile=1: (select, scatter) us per pass
 
   DistState *dist = nullptr;
   std::string err;

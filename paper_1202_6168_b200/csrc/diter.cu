@@ -77,9 +77,9 @@ static void free_ctx(di_ctx *c) {
   if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
   for (cudaEvent_t e : c->prof_ev)
     if (e) cudaEventDestroy(e);
-  void *ptrs[] = {c->col_ptr, c->row_idx, c->vals, c->d_b, c->F, c->H, c->bins.low_idx, c->bins.low_w,
-                  c->bins.mid_idx, c->bins.mid_w, c->bins.hub_idx, c->bins.hub_w,
-                  c->bins.hub_chunk, c->part, c->l1_part, c->l1_out, c->ctl, c->log};
+  void *ptrs[] = {c->col_ptr, c->row_idx, c->vals, c->d_b, c->F, c->H, c->fr.bits, c->fr.S,
+                  c->fr.hub_w, c->fr.hub_b0, c->fr.hub_deg, c->fr.hub_chunk, c->sel_part, c->sc_part,
+                  c->l1_part, c->l1_out, c->ctl, c->log};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
@@ -99,12 +99,44 @@ static di_status setup_geometry(di_ctx *ctx) {
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sel, k_select, kSelectThreads, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sc, k_scatter<false>, kScatterThreads, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sc_s, k_scatter<true>, kScatterThreads, 0));
-  ctx->grid_select = ctx->num_sms * std::max(1, std::min(occ_sel, 8));
-  // never more select CTAs than warps of work
-  long long need = (ctx->n_local + kSelectThreads - 1) / kSelectThreads;
-  if (need < ctx->grid_select) ctx->grid_select = (int)std::max(1LL, need);
+  // persistent grids: SM count x resident CTAs, never more CTAs than work items
+  const long long n_words = (ctx->n_local + 31) / 32;
+  const long long sel_items = (n_words + kSelectItems - 1) / kSelectItems;           // warp iterations
+  const long long sel_need = (sel_items + kSelectThreads / 32 - 1) / (kSelectThreads / 32);
+  ctx->grid_select = (int)std::max(1LL, std::min<long long>(sel_need, (long long)ctx->num_sms * std::max(1, occ_sel)));
   ctx->grid_scatter = ctx->num_sms * std::max(1, ctx->vals ? occ_sc_s : occ_sc);
-  ctx->grid_l1 = ctx->grid_select;
+  // small graphs: spread the groups of one superword over several warps
+  const long long n_super = (n_words + kWordsPerSuper - 1) / kWordsPerSuper;
+  const long long sc_warps = (long long)ctx->grid_scatter * (kScatterThreads / 32);
+  ctx->gsplit = (int)std::max(1LL, std::min(32LL, (2 * sc_warps + n_super - 1) / std::max(1LL, n_super)));
+  ctx->grid_l1 = (int)std::min<long long>(ctx->num_sms * 8LL,
+                                          std::max(1LL, (ctx->n_local + 255) / 256));
+  return DI_OK;
+}
+
+// The shared-memory hot window of the scatter: the 2048 consecutive rows (aligned
+// to 1024) whose sampled in-degree is largest.  Rows are global ids; on a
+// distributed context only rows of the local range are candidates.
+static di_status choose_hot_window(di_ctx *ctx) {
+  const long long n = ctx->n_rows;
+  ctx->hot_lo = 0;
+  if (n <= kHot || ctx->nnz_local == 0) return DI_OK;
+  const long long nb = (n >> 10) + 1;
+  unsigned *blk = nullptr;
+  TRY(dalloc(ctx, &blk, (size_t)nb));
+  CK(cudaMemsetAsync(blk, 0, sizeof(unsigned) * nb, ctx->stream));
+  const int stride = ctx->nnz_local > (1LL << 24) ? 64 : 1;
+  k_hot_sample<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->row_idx, ctx->nnz_local, stride, blk);
+  std::vector<unsigned> h(nb);
+  CK(cudaMemcpyAsync(h.data(), blk, sizeof(unsigned) * nb, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  cudaFree(blk);
+  long long best = 0, best_mass = -1;
+  for (long long b = 0; b + 1 < nb; ++b) {
+    const long long m = (long long)h[b] + h[b + 1];
+    if (m > best_mass) { best_mass = m; best = b; }
+  }
+  ctx->hot_lo = (int)std::min<long long>(best << 10, n - kHot);
   return DI_OK;
 }
 
@@ -112,7 +144,7 @@ static di_status setup_geometry(di_ctx *ctx) {
 static di_status capture_graph(di_ctx *ctx) {
   cudaGraph_t graph;
   CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-  Graph g{ctx->col_ptr, ctx->row_idx, ctx->vals, ctx->n_local, ctx->d};
+  Graph g{ctx->col_ptr, ctx->row_idx, ctx->vals, ctx->n_local, ctx->d, ctx->hot_lo};
   const bool prof = ctx->opt.profile != 0;
   if (prof && ctx->prof_ev.empty()) {
     ctx->prof_ev.assign(4 * ctx->check_interval, nullptr);
@@ -120,15 +152,22 @@ static di_status capture_graph(di_ctx *ctx) {
   }
   for (int k = 0; k < ctx->check_interval; ++k) {
     if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 0], ctx->stream, cudaEventRecordExternal));
-    k_select<<<ctx->grid_select, kSelectThreads, 0, ctx->stream>>>(g, ctx->F, ctx->H, ctx->bins,
-                                                                  ctx->ctl, ctx->part);
+    k_select<<<ctx->grid_select, kSelectThreads, 0, ctx->stream>>>(ctx->F, ctx->H, ctx->fr, ctx->n_local,
+                                                                  ctx->ctl, ctx->sel_part);
     if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 1], ctx->stream, cudaEventRecordExternal));
     if (ctx->vals)
-      k_scatter<true><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->bins, ctx->ctl);
+      k_scatter<true><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part, ctx->gsplit);
     else
-      k_scatter<false><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->bins, ctx->ctl);
+      k_scatter<false><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part, ctx->gsplit);
+    if (ctx->cap_hub > 0) {
+      if (ctx->vals)
+        k_scatter_hubs<true><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
+      else
+        k_scatter_hubs<false><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
+    }
     if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 2], ctx->stream, cudaEventRecordExternal));
-    k_finalize<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->ctl, ctx->part, ctx->grid_select, ctx->log);
+    k_finalize<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->ctl, ctx->sel_part, ctx->grid_select, ctx->sc_part,
+                                                        ctx->grid_scatter, ctx->log);
     if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 3], ctx->stream, cudaEventRecordExternal));
   }
   cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
@@ -205,17 +244,20 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
     diter_set_err(ctx, "%llu columns have sum |p_ij| > d = %g (not contractive)", hc.bad_contraction, ctx->d);
     return DI_ERR_CONTRACTION;
   }
+  TRY(choose_hot_window(ctx));
   ctx->cap_low = hc.n_low;
   ctx->cap_mid = hc.n_mid;
   ctx->cap_hub = hc.n_hub;
-  TRY(dalloc(ctx, &ctx->bins.low_idx, hc.n_low));
-  TRY(dalloc(ctx, &ctx->bins.low_w, hc.n_low));
-  TRY(dalloc(ctx, &ctx->bins.mid_idx, hc.n_mid));
-  TRY(dalloc(ctx, &ctx->bins.mid_w, hc.n_mid));
-  TRY(dalloc(ctx, &ctx->bins.hub_idx, hc.n_hub));
-  TRY(dalloc(ctx, &ctx->bins.hub_w, hc.n_hub));
-  TRY(dalloc(ctx, &ctx->bins.hub_chunk, hc.n_hub));
-  TRY(dalloc(ctx, &ctx->part, (size_t)ctx->grid_select));
+  ctx->fr.n_words = (n + 31) / 32;
+  TRY(dalloc(ctx, &ctx->fr.bits, (size_t)ctx->fr.n_words));
+  TRY(dalloc(ctx, &ctx->fr.S, (size_t)n));
+  TRY(dalloc(ctx, &ctx->fr.hub_w, hc.n_hub));
+  TRY(dalloc(ctx, &ctx->fr.hub_b0, hc.n_hub));
+  TRY(dalloc(ctx, &ctx->fr.hub_deg, hc.n_hub));
+  TRY(dalloc(ctx, &ctx->fr.hub_chunk, hc.n_hub));
+  TRY(dalloc(ctx, &ctx->sel_part, (size_t)ctx->grid_select));
+  TRY(dalloc(ctx, &ctx->sc_part, (size_t)ctx->grid_scatter));
+
   TRY(dalloc(ctx, &ctx->l1_part, (size_t)ctx->grid_l1));
   TRY(dalloc(ctx, &ctx->l1_out, 1));
   TRY(dalloc(ctx, &ctx->ctl, 1));
@@ -326,16 +368,17 @@ extern "C" di_status di_run(di_ctx *ctx, double target) {
       const long long pass_before = h->pass;
       CK(cudaGraphLaunch(ctx->graph_exec, ctx->stream));
       ctx->graph_launches += 1;
-      ctx->kernel_launches += 3LL * ctx->check_interval;
+      ctx->kernel_launches += (ctx->cap_hub > 0 ? 4LL : 3LL) * ctx->check_interval;
       TRY(read_ctl(ctx));
       if (ctx->opt.profile) {
         const long long active = std::min<long long>(h->pass - pass_before, ctx->check_interval);
         for (long long k = 0; k < active; ++k) {
+          float ms3[3] = {0.f, 0.f, 0.f};
           for (int q = 0; q < 3; ++q) {
-            float ms = 0.f;
-            CK(cudaEventElapsedTime(&ms, ctx->prof_ev[4 * k + q], ctx->prof_ev[4 * k + q + 1]));
-            ctx->kt_ms[q] += ms;
+            CK(cudaEventElapsedTime(&ms3[q], ctx->prof_ev[4 * k + q], ctx->prof_ev[4 * k + q + 1]));
+            ctx->kt_ms[q] += ms3[q];
           }
+          ctx->pass_us.push_back({ms3[0] * 1e3, ms3[1] * 1e3});
         }
         ctx->kt_passes += active;
       }
@@ -379,6 +422,7 @@ extern "C" di_status di_reset(di_ctx *ctx) {
   ctx->passes_done = ctx->edges = ctx->nodes = 0;
   ctx->kt_ms[0] = ctx->kt_ms[1] = ctx->kt_ms[2] = 0.0;
   ctx->kt_passes = 0;
+  ctx->pass_us.clear();
   ctx->run_ms = ctx->run_ms_total = 0.0;
   ctx->graph_launches = 0;
   ctx->threshold = ctx->ctl_init.T;
@@ -460,6 +504,13 @@ extern "C" di_status di_get_pass_log(const di_ctx *cctx, int64_t first, int64_t 
     CK(cudaSetDevice(ctx->device));
     CK(cudaMemcpyAsync(out, ctx->log + first, sizeof(di_pass_log) * k, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    for (long long j = 0; j < k; ++j) {
+      const long long p = first + j;
+      if (p < (long long)ctx->pass_us.size()) {
+        out[j].t_select_us = ctx->pass_us[p].first;
+        out[j].t_scatter_us = ctx->pass_us[p].second;
+      }
+    }
   }
   if (n_copied) *n_copied = k;
   return DI_OK;

@@ -1,207 +1,365 @@
 // kernels.cuh -- the D-iteration hot path on sm_100a.
 //
-// One pass p:
-//   k_select   (K1): r_p = sum |F_i| (warp-shuffle reduction), S_p = {i : |F_i| > T_p},
-//                    take (s = F_i, F_i = 0, H_i += s), per-node push value, degree bin.
-//   k_scatter  (K2-K4 fused, persistent): F_j += push for every edge of every node of S_p,
-//                    hubs CTA-per-chunk, mid-degree warp-per-node, low-degree thread-per-node.
-//   k_finalize (K5): deterministic second-level reduction, pass log, T_{p+1}, stop flag.
+// One pass p, snapshot semantics:
+//   k_select        (K1) stream F once: r_p = sum |F_i| (warp-shuffle reduction),
+//                   S_p = {i : |F_i| > T_p}; take every i in S_p (s_i = F_i,
+//                   F_i = 0, H_i += s_i); selection bitmap + s_i for the scatter.
+//   k_scatter       (K2/K3) F_j += p_ji s_i for every edge of every selected node of
+//                   degree <= kMidMax: 32 selected nodes per warp, lanes spread over
+//                   the group's concatenated out-edges (edge-balanced, coalesced).
+//   k_scatter_hubs  (K4) selected columns of > kMidMax edges, one CTA per 2048-edge chunk.
+//   k_finalize      (K5) deterministic second-level reduction, pass log, T_{p+1},
+//                   stop flag.
 // Every kernel returns at once when the control block says the run is done, so a
 // captured graph of m passes can overrun convergence at the cost of empty launches.
 #pragma once
+#include "../../include/diter.h"
 #include "common.cuh"
 #include "types.cuh"
 
 namespace diter {
 
 // ---------------------------------------------------------------- K1 select --
-// Grid-stride over nodes with a warp-uniform loop; lanes read consecutive F_i
-// (coalesced 256 B per warp load).  Selected nodes read col_ptr[i..i+1] to bin
-// and to derive p_ji = d/#out_i (PageRank weights are never stored, BASELINE
-// north_star) -- push = s * (d / #out_i), the same two roundings as the oracle.
-__global__ void __launch_bounds__(kSelectThreads)
-k_select(Graph g, double *__restrict__ F, double *__restrict__ H, Bins bins, Ctl *ctl,
-         Partial *__restrict__ part) {
+// Warp-tiled stream over F: each warp iteration covers 8 words of 32 nodes;
+// lane l loads F[base + 32k + l] for k < 8 (eight coalesced 256-byte loads in
+// flight per warp, no dependent load, no block barrier), so the kernel runs at
+// full occupancy and streams F at HBM rate.  |F_i| > T_p (strict, PAPER.md:215,
+// reading R7) selects; a selected node is taken: s_i = F_i, F_i = 0 (store),
+// H_i += s_i (fire-and-forget RED, one writer per pass), S[i] = s_i, and its bit
+// is set in the word written by lane k.  Per-CTA partials (r_p, |S_p|) in a
+// fixed order make r_p deterministic for given F bytes.
+__global__ void __launch_bounds__(kSelectThreads, 6)
+k_select(double *__restrict__ F, double *__restrict__ H, Frontier fr, long long n, const Ctl *ctl,
+         SelPartial *__restrict__ part) {
   if (ctl->done) return;
   const double T = ctl->T;
-  const bool is_signed = (g.vals != nullptr);
-  double r = 0.0, loss = 0.0;
-  long long edges = 0;
-  int cnt = 0, dang = 0;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  const long long warp_base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
-  for (long long base = warp_base; base < g.n; base += stride) {
-    const long long i = base + lane_id();
-    const bool valid = i < g.n;
-    double f = valid ? F[i] : 0.0;
-    const double af = fabs(f);
-    r += af;
-    const bool sel = valid && (af > T);
-    long long deg = 0;
-    double push = 0.0;
-    if (sel) {
-      F[i] = 0.0;
-      H[i] += f;
-      const long long b0 = g.col_ptr[i], b1 = g.col_ptr[i + 1];
-      deg = b1 - b0;
-      push = is_signed ? f : f * (g.d / (double)deg);
-      // |F|_1 decreases by at least (1 - sum_j |p_ji|)|s| >= (1-d)|s| (App. A.2);
-      // a dangling column pushes nothing, so all of |s| leaves.
-      loss += (deg > 0) ? (1.0 - g.d) * af : af;
-      edges += deg;
-      cnt += 1;
-      dang += (deg == 0);
+  const unsigned lane = lane_id();
+  const long long warps = (long long)gridDim.x * (kSelectThreads / 32);
+  const long long gw = (long long)blockIdx.x * (kSelectThreads / 32) + (threadIdx.x >> 5);
+  const long long n_iter = (fr.n_words + kSelectItems - 1) / kSelectItems;
+  double r = 0.0;
+  long long cnt = 0;
+  for (long long it = gw; it < n_iter; it += warps) {
+    const long long base = it * (32LL * kSelectItems);
+    double f[kSelectItems];
+#pragma unroll
+    for (int k = 0; k < kSelectItems; ++k) {
+      const long long i = base + 32 * k + lane;
+      f[k] = (i < n) ? F[i] : 0.0;
     }
-    const bool is_low = sel && deg >= 1 && deg <= kLowMax;
-    const bool is_mid = sel && deg > kLowMax && deg <= kMidMax;
-    const bool is_hub = sel && deg > kMidMax;
-    const unsigned slot_low = warp_append(&ctl->n_low, is_low);
-    const unsigned slot_mid = warp_append(&ctl->n_mid, is_mid);
-    if (is_low) { bins.low_idx[slot_low] = (int)i; bins.low_w[slot_low] = push; }
-    if (is_mid) { bins.mid_idx[slot_mid] = (int)i; bins.mid_w[slot_mid] = push; }
-    if (is_hub) {
-      // one 64-bit atomic hands out the slot AND the first chunk id, so hub_chunk[]
-      // is sorted by slot and the scatter can binary-search it.
-      const unsigned long long nch = (unsigned long long)((deg + kHubChunk - 1) / kHubChunk);
-      const unsigned long long old = atomicAdd(&ctl->hub_packed, (1ull << 32) | nch);
-      const unsigned s = (unsigned)(old >> 32);
-      bins.hub_idx[s] = (int)i;
-      bins.hub_w[s] = push;
-      bins.hub_chunk[s] = (unsigned)(old & 0xffffffffull);
+    unsigned my_word = 0u;
+#pragma unroll
+    for (int k = 0; k < kSelectItems; ++k) {
+      const long long i = base + 32 * k + lane;
+      const double af = fabs(f[k]);
+      r += af;
+      const bool sel = (i < n) && (af > T);
+      const unsigned wbits = __ballot_sync(0xffffffffu, sel);
+      if ((int)lane == k) my_word = wbits;
+      if (sel) {
+        F[i] = 0.0;            // F_i := 0
+        red_add(H + i, f[k]);  // H_i += sent
+        fr.S[i] = f[k];        // sent, for the scatter
+        ++cnt;
+      }
     }
+    const long long wi = it * kSelectItems + lane;
+    if ((int)lane < kSelectItems && wi < fr.n_words) fr.bits[wi] = my_word;
   }
-  // block reduction (fixed order -> deterministic given F)
   r = warp_sum(r);
-  loss = warp_sum(loss);
-  edges = warp_sum(edges);
   cnt = warp_sum(cnt);
-  dang = warp_sum(dang);
-  __shared__ double s_r[kSelectThreads / 32], s_l[kSelectThreads / 32];
-  __shared__ long long s_e[kSelectThreads / 32];
-  __shared__ int s_c[kSelectThreads / 32], s_d[kSelectThreads / 32];
-  const int w = threadIdx.x >> 5;
-  if (lane_id() == 0) { s_r[w] = r; s_l[w] = loss; s_e[w] = edges; s_c[w] = cnt; s_d[w] = dang; }
+  __shared__ double s_r[kSelectThreads / 32];
+  __shared__ long long s_c[kSelectThreads / 32];
+  if (lane == 0) { s_r[threadIdx.x >> 5] = r; s_c[threadIdx.x >> 5] = cnt; }
   __syncthreads();
   if (threadIdx.x == 0) {
-    Partial p{0.0, 0.0, 0, 0, 0};
-    for (int k = 0; k < kSelectThreads / 32; ++k) {
-      p.r += s_r[k]; p.loss += s_l[k]; p.edges += s_e[k]; p.cnt += s_c[k]; p.dang += s_d[k];
-    }
+    SelPartial p{0.0, 0};
+    for (int k = 0; k < kSelectThreads / 32; ++k) { p.r += s_r[k]; p.cnt += s_c[k]; }
     part[blockIdx.x] = p;
   }
 }
 
 // ------------------------------------------------------------ K2-K4 scatter --
-// Push `w` (x vals[e] in signed mode) along edges [beg, end) with `nt` cooperating
-// threads (t = this thread's rank): scalar head up to 16-byte alignment of
-// row_idx, int4 body (4 rows per load, coalesced across the group), scalar tail.
+// Where one push F_j += v lands.  Rows inside the hot window [hot_lo, hot_lo+kHot)
+// (chosen at create time as the 2048 consecutive rows with the largest sampled
+// in-degree; for the Zipf-over-id configs that is the id prefix) accumulate in
+// shared memory and are flushed once per CTA per pass, so a row receiving
+// millions of pushes per pass costs one RED per CTA instead of one RED per
+// edge serialised at one L2 slice.  Every other row gets a fire-and-forget
+// RED.E.ADD.F64 in L2.
+struct Sink {
+  double *F;
+  double *s_hot;
+  int hot_lo;
+};
+
+__device__ __forceinline__ void push(const Sink &s, int row, double v) {
+  const unsigned h = (unsigned)(row - s.hot_lo);
+  if (h < (unsigned)kHot) atomicAdd(s.s_hot + h, v);
+  else red_add(s.F + row, v);
+}
+
+__device__ __forceinline__ int ld_row(const int *p) { return __ldcs(p); }
+__device__ __forceinline__ int4 ld_row4(const int4 *p) { return __ldcs(p); }
+__device__ __forceinline__ double ld_val(const double *p) { return __ldcs(p); }
+__device__ __forceinline__ double2 ld_val2(const double2 *p) { return __ldcs(p); }
+
+// Push `w` (x vals[e] in signed mode) along edges [beg, end) with `nt` >= 4
+// cooperating threads (t = this thread's rank): scalar head up to the 16-byte
+// alignment of row_idx, int4 body with two vector loads in flight per thread
+// before their REDs issue, scalar tail.
 template <bool SIGNED>
-__device__ __forceinline__ void push_range(const Graph &g, double *__restrict__ F, long long beg,
+__device__ __forceinline__ void push_range(const Graph &g, const Sink &s, long long beg,
                                            long long end, double w, int t, int nt) {
   long long a = (beg + 3) & ~3ll;
   if (a > end) a = end;
-  for (long long e = beg + t; e < a; e += nt) {
-    const int row = ld_stream_i1(g.row_idx + e);
-    red_add(F + row, SIGNED ? w * ld_stream_d1(g.vals + e) : w);
+  if (beg + t < a) {
+    const long long e = beg + t;
+    push(s, ld_row(g.row_idx + e), SIGNED ? w * ld_val(g.vals + e) : w);
   }
   const long long nv = (end - a) >> 2;
   const int4 *r4 = reinterpret_cast<const int4 *>(g.row_idx + a);
-  for (long long k = t; k < nv; k += nt) {
-    const int4 rr = ld_stream_i4(r4 + k);
+  const double2 *v2 = reinterpret_cast<const double2 *>(g.vals + a);
+  for (long long k = t; k < nv; k += 2 * (long long)nt) {
+    const bool two = k + nt < nv;
+    const int4 x = ld_row4(r4 + k);
+    int4 y = make_int4(0, 0, 0, 0);
+    if (two) y = ld_row4(r4 + k + nt);
     if (SIGNED) {
-      const double2 *v2 = reinterpret_cast<const double2 *>(g.vals + a) + 2 * k;
-      const double2 va = ld_stream_d2(v2), vb = ld_stream_d2(v2 + 1);
-      red_add(F + rr.x, w * va.x);
-      red_add(F + rr.y, w * va.y);
-      red_add(F + rr.z, w * vb.x);
-      red_add(F + rr.w, w * vb.y);
+      const double2 xa = ld_val2(v2 + 2 * k), xb = ld_val2(v2 + 2 * k + 1);
+      double2 ya = make_double2(0, 0), yb = make_double2(0, 0);
+      if (two) { ya = ld_val2(v2 + 2 * (k + nt)); yb = ld_val2(v2 + 2 * (k + nt) + 1); }
+      push(s, x.x, w * xa.x); push(s, x.y, w * xa.y); push(s, x.z, w * xb.x); push(s, x.w, w * xb.y);
+      if (two) { push(s, y.x, w * ya.x); push(s, y.y, w * ya.y); push(s, y.z, w * yb.x); push(s, y.w, w * yb.y); }
     } else {
-      red_add(F + rr.x, w);
-      red_add(F + rr.y, w);
-      red_add(F + rr.z, w);
-      red_add(F + rr.w, w);
+      push(s, x.x, w); push(s, x.y, w); push(s, x.z, w); push(s, x.w, w);
+      if (two) { push(s, y.x, w); push(s, y.y, w); push(s, y.z, w); push(s, y.w, w); }
     }
   }
-  for (long long e = a + nv * 4 + t; e < end; e += nt) {
-    const int row = ld_stream_i1(g.row_idx + e);
-    red_add(F + row, SIGNED ? w * ld_stream_d1(g.vals + e) : w);
+  const long long e = a + nv * 4 + t;
+  if (e < end) push(s, ld_row(g.row_idx + e), SIGNED ? w * ld_val(g.vals + e) : w);
+}
+
+// One group of up to 32 selected nodes held one per lane (b0, deg, w): the warp
+// scans the degrees, then lane l takes edges l, l+32, ... of the group's
+// concatenated edge list (edge-balanced inside the warp; consecutive lanes read
+// consecutive row indices within a column, and adjacent columns of consecutive
+// ids are adjacent in row_idx).  The owner lane of an edge is found by a 5-step
+// shuffle binary search over the exclusive degree prefix.
+constexpr int kGroupUnroll = 4;
+
+template <bool SIGNED>
+__device__ __forceinline__ void push_group(const Graph &g, const Sink &s, long long b0, int deg, double w) {
+  const unsigned lane = lane_id();
+  int incl = deg;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((int)lane >= o) incl += t;
+  }
+  const int excl = incl - deg;
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  for (int base = 0; base < total; base += 32 * kGroupUnroll) {
+    int rows[kGroupUnroll];
+    double vals[kGroupUnroll];
+#pragma unroll
+    for (int u = 0; u < kGroupUnroll; ++u) {
+      const int e = base + (int)lane + 32 * u;
+      int lo = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int cand = lo + step;
+        if (__shfl_sync(0xffffffffu, excl, cand) <= e) lo = cand;
+      }
+      const long long ob = __shfl_sync(0xffffffffu, b0, lo);
+      const int oe = __shfl_sync(0xffffffffu, excl, lo);
+      const double ow = __shfl_sync(0xffffffffu, w, lo);
+      const bool ok = e < total;
+      const long long ei = ob + (e - oe);
+      rows[u] = ok ? ld_row(g.row_idx + ei) : -1;
+      vals[u] = ok ? (SIGNED ? ow * ld_val(g.vals + ei) : ow) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kGroupUnroll; ++u)
+      if (rows[u] >= 0) push(s, rows[u], vals[u]);
   }
 }
 
-// Persistent, one launch per pass: phase A hub chunks (CTA per 2048-edge chunk),
-// phase B mid nodes (warp per node), phase C low nodes (thread per node).  The
-// phases need no barrier between them: all pushes commute (fp64 RED in L2).
+struct ScAcc {
+  double loss = 0.0;
+  long long edges = 0;
+  int dang = 0, lo = 0, mi = 0, hu = 0;
+};
+
+// Persistent grid-stride over "superwords" of 32 bitmap words (1024 nodes): a
+// warp loads the 32 words (one 128-byte access), ranks the selected nodes by a
+// warp scan of popcounts, and processes them 32 at a time: lane t finds its
+// node (shuffle binary search over the words + __fns), gathers s_i and
+// col_ptr[i..i+1] (independent loads across lanes), derives the push value
+// s_i * (d / #out_i) (PageRank weights are never stored, BASELINE north_star; the
+// oracle's two roundings), and the group's edges are pushed by push_group.
+// Columns of more than kMidMax edges are appended to the hub list for
+// k_scatter_hubs.  The guaranteed |F|_1 drop sum (1 - c_i)|s_i| (App. A.2: c_i = d,
+// 0 for a dangling column) and the frontier census go to per-CTA partials.
 template <bool SIGNED>
 __global__ void __launch_bounds__(kScatterThreads)
-k_scatter(Graph g, double *__restrict__ F, Bins bins, const Ctl *ctl) {
+k_scatter(Graph g, double *__restrict__ F, Frontier fr, Ctl *ctl, ScPartial *__restrict__ part, int gsplit) {
   if (ctl->done) return;
-  // phase A: hubs
+  __shared__ double s_hot[kHot];
+  for (int t = threadIdx.x; t < kHot; t += blockDim.x) s_hot[t] = 0.0;
+  __syncthreads();
+  const Sink s{F, s_hot, g.hot_lo};
+  const unsigned lane = lane_id();
+  const long long warps = (long long)gridDim.x * (kScatterThreads / 32);
+  const long long gw = (long long)blockIdx.x * (kScatterThreads / 32) + (threadIdx.x >> 5);
+  const long long n_super = (fr.n_words + kWordsPerSuper - 1) / kWordsPerSuper;
+  ScAcc acc;
+  // work item = (superword, group residue): with gsplit > 1 (small graphs) the
+  // groups of one superword spread over gsplit warps
+  const long long n_items = n_super * gsplit;
+  for (long long it = gw; it < n_items; it += warps) {
+    const long long sw = it / gsplit;
+    const int gi = (int)(it - sw * gsplit);
+    const long long wi = sw * kWordsPerSuper + lane;
+    const unsigned word = (wi < fr.n_words) ? fr.bits[wi] : 0u;
+    const int c = __popc(word);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if ((int)lane >= o) incl += t;
+    }
+    const int excl = incl - c;
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    for (int g0 = 32 * gi; g0 < total; g0 += 32 * gsplit) {
+      const int rank = g0 + (int)lane;
+      int lo = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int cand = lo + step;
+        if (__shfl_sync(0xffffffffu, excl, cand) <= rank) lo = cand;
+      }
+      const unsigned wbits = __shfl_sync(0xffffffffu, word, lo);
+      const int wex = __shfl_sync(0xffffffffu, excl, lo);
+      long long b0 = 0;
+      int deg_eff = 0;
+      double w = 0.0;
+      if (rank < total) {
+        const int bit = (int)__fns(wbits, 0u, rank - wex + 1);
+        const long long i = (sw * kWordsPerSuper + lo) * 32 + bit;
+        const double sv = fr.S[i];
+        b0 = __ldg(g.col_ptr + i);
+        const long long deg = __ldg(g.col_ptr + i + 1) - b0;
+        const double asv = fabs(sv);
+        acc.loss += (deg > 0) ? (1.0 - g.d) * asv : asv;
+        acc.edges += deg;
+        if (deg == 0) {
+          acc.dang += 1;
+        } else {
+          w = SIGNED ? sv : sv * (g.d / (double)deg);
+          if (deg <= kLowMax) { acc.lo += 1; deg_eff = (int)deg; }
+          else if (deg <= kMidMax) { acc.mi += 1; deg_eff = (int)deg; }
+          else {
+            // one 64-bit atomic hands out the slot AND the first chunk id, so
+            // hub_chunk[] is sorted by slot and k_scatter_hubs can binary-search it
+            acc.hu += 1;
+            const unsigned long long nch = (unsigned long long)((deg + kHubChunk - 1) / kHubChunk);
+            const unsigned long long old = atomicAdd(&ctl->hub_packed, (1ull << 32) | nch);
+            const unsigned sl = (unsigned)(old >> 32);
+            fr.hub_w[sl] = w; fr.hub_b0[sl] = b0; fr.hub_deg[sl] = deg;
+            fr.hub_chunk[sl] = (unsigned)(old & 0xffffffffull);
+          }
+        }
+      }
+      push_group<SIGNED>(g, s, b0, deg_eff, w);
+    }
+  }
+  // flush the hot window: one RED per touched row per CTA
+  __syncthreads();
+  for (int t = threadIdx.x; t < kHot; t += blockDim.x) {
+    const double v = s_hot[t];
+    if (v != 0.0) red_add(F + g.hot_lo + t, v);
+  }
+  // per-CTA partials
+  acc.loss = warp_sum(acc.loss);
+  acc.edges = warp_sum(acc.edges);
+  acc.dang = warp_sum(acc.dang);
+  acc.lo = warp_sum(acc.lo);
+  acc.mi = warp_sum(acc.mi);
+  acc.hu = warp_sum(acc.hu);
+  __shared__ ScAcc s_acc[kScatterThreads / 32];
+  if (lane == 0) s_acc[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ScPartial p{0.0, 0, 0, 0, 0, 0};
+    for (int k = 0; k < kScatterThreads / 32; ++k) {
+      p.loss += s_acc[k].loss; p.edges += s_acc[k].edges; p.dang += s_acc[k].dang;
+      p.n_low += s_acc[k].lo; p.n_mid += s_acc[k].mi; p.n_hub += s_acc[k].hu;
+    }
+    part[blockIdx.x] = p;
+  }
+}
+
+// Hub columns (> kMidMax edges), one CTA per 2048-edge chunk (chunks of a hub
+// spread over CTAs; int4 row loads, two in flight per thread).
+template <bool SIGNED>
+__global__ void __launch_bounds__(kScatterThreads)
+k_scatter_hubs(Graph g, double *__restrict__ F, Frontier fr, const Ctl *ctl) {
+  if (ctl->done) return;
   const unsigned long long hp = ctl->hub_packed;
   const unsigned n_hub = (unsigned)(hp >> 32), n_chunks = (unsigned)(hp & 0xffffffffull);
+  if (n_chunks == 0u) return;
+  const Sink s{F, nullptr, -2147483647 - 1};   // no hot window: h >= kHot for every row
   for (unsigned c = blockIdx.x; c < n_chunks; c += gridDim.x) {
     unsigned lo = 0, hi = n_hub - 1;
     while (lo < hi) {
       const unsigned mid = (lo + hi + 1) >> 1;
-      if (bins.hub_chunk[mid] <= c) lo = mid; else hi = mid - 1;
+      if (fr.hub_chunk[mid] <= c) lo = mid; else hi = mid - 1;
     }
-    const int i = bins.hub_idx[lo];
-    const double w = bins.hub_w[lo];
-    const long long cb = g.col_ptr[i], ce = g.col_ptr[i + 1];
-    const long long beg = cb + (long long)(c - bins.hub_chunk[lo]) * kHubChunk;
+    const double w = fr.hub_w[lo];
+    const long long cb = fr.hub_b0[lo], ce = cb + fr.hub_deg[lo];
+    const long long beg = cb + (long long)(c - fr.hub_chunk[lo]) * kHubChunk;
     const long long end = min(beg + (long long)kHubChunk, ce);
-    push_range<SIGNED>(g, F, beg, end, w, threadIdx.x, blockDim.x);
-  }
-  // phase B: mid-degree, one warp per node
-  const unsigned n_mid = ctl->n_mid;
-  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  for (long long k = gw; k < n_mid; k += warps) {
-    const int i = bins.mid_idx[k];
-    const double w = bins.mid_w[k];
-    push_range<SIGNED>(g, F, g.col_ptr[i], g.col_ptr[i + 1], w, lane_id(), 32);
-  }
-  // phase C: low-degree, one thread per node
-  const unsigned n_low = ctl->n_low;
-  const long long threads = (long long)gridDim.x * blockDim.x;
-  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n_low; k += threads) {
-    const int i = bins.low_idx[k];
-    const double w = bins.low_w[k];
-    const long long b0 = g.col_ptr[i], b1 = g.col_ptr[i + 1];
-    for (long long e = b0; e < b1; ++e) {
-      const int row = ld_stream_i1(g.row_idx + e);
-      red_add(F + row, SIGNED ? w * ld_stream_d1(g.vals + e) : w);
-    }
+    push_range<SIGNED>(g, s, beg, end, w, threadIdx.x, blockDim.x);
   }
 }
 
 // -------------------------------------------------------------- K5 finalize --
 __global__ void __launch_bounds__(kFinalizeThreads)
-k_finalize(Ctl *ctl, const Partial *__restrict__ part, int n_part, di_pass_log *log) {
+k_finalize(Ctl *ctl, const SelPartial *__restrict__ sp, int n_sp, const ScPartial *__restrict__ cp,
+           int n_cp, di_pass_log *log) {
   if (ctl->done) return;
   double r = 0.0, loss = 0.0;
-  long long edges = 0, cnt = 0, dang = 0;
-  for (int k = threadIdx.x; k < n_part; k += blockDim.x) {
-    const Partial p = part[k];
-    r += p.r; loss += p.loss; edges += p.edges; cnt += p.cnt; dang += p.dang;
+  long long cnt = 0, edges = 0, dang = 0, nlo = 0, nmi = 0, nhu = 0;
+  for (int k = threadIdx.x; k < n_sp; k += blockDim.x) { r += sp[k].r; cnt += sp[k].cnt; }
+  for (int k = threadIdx.x; k < n_cp; k += blockDim.x) {
+    const ScPartial p = cp[k];
+    loss += p.loss; edges += p.edges; dang += p.dang; nlo += p.n_low; nmi += p.n_mid; nhu += p.n_hub;
   }
-  r = warp_sum(r); loss = warp_sum(loss); edges = warp_sum(edges);
-  cnt = warp_sum(cnt); dang = warp_sum(dang);
-  __shared__ double s_r[kFinalizeThreads / 32], s_l[kFinalizeThreads / 32];
-  __shared__ long long s_e[kFinalizeThreads / 32], s_c[kFinalizeThreads / 32], s_d[kFinalizeThreads / 32];
+  r = warp_sum(r); loss = warp_sum(loss); cnt = warp_sum(cnt); edges = warp_sum(edges);
+  dang = warp_sum(dang); nlo = warp_sum(nlo); nmi = warp_sum(nmi); nhu = warp_sum(nhu);
+  constexpr int W = kFinalizeThreads / 32;
+  __shared__ double s_r[W], s_l[W];
+  __shared__ long long s_i[6][W];
   const int w = threadIdx.x >> 5;
-  if (lane_id() == 0) { s_r[w] = r; s_l[w] = loss; s_e[w] = edges; s_c[w] = cnt; s_d[w] = dang; }
+  if (lane_id() == 0) {
+    s_r[w] = r; s_l[w] = loss;
+    s_i[0][w] = cnt; s_i[1][w] = edges; s_i[2][w] = dang; s_i[3][w] = nlo; s_i[4][w] = nmi; s_i[5][w] = nhu;
+  }
   __syncthreads();
   if (threadIdx.x != 0) return;
-  r = 0.0; loss = 0.0; edges = 0; cnt = 0; dang = 0;
-  for (int k = 0; k < kFinalizeThreads / 32; ++k) {
-    r += s_r[k]; loss += s_l[k]; edges += s_e[k]; cnt += s_c[k]; dang += s_d[k];
+  r = 0.0; loss = 0.0; cnt = edges = dang = nlo = nmi = nhu = 0;
+  for (int k = 0; k < W; ++k) {
+    r += s_r[k]; loss += s_l[k];
+    cnt += s_i[0][k]; edges += s_i[1][k]; dang += s_i[2][k]; nlo += s_i[3][k]; nmi += s_i[4][k]; nhu += s_i[5][k];
   }
   const long long p = ctl->pass;
   const double T = ctl->T;
   if (p < ctl->log_cap) {
     di_pass_log L;
     L.pass = p; L.T = T; L.r = r; L.frontier = cnt; L.edges = edges; L.dangling = dang;
-    L.bin_low = ctl->n_low; L.bin_mid = ctl->n_mid; L.bin_hub = (long long)(ctl->hub_packed >> 32);
+    L.bin_low = nlo; L.bin_mid = nmi; L.bin_hub = nhu;
+    L.t_select_us = 0.0; L.t_scatter_us = 0.0;
     log[p] = L;
   }
   ctl->edges += edges;
@@ -215,8 +373,6 @@ k_finalize(Ctl *ctl, const Partial *__restrict__ part, int n_part, di_pass_log *
   ctl->pass = p + 1;
   if (r < ctl->target || pred < ctl->target) ctl->done = 1;
   else if (p + 1 >= ctl->max_pass) ctl->done = 2;
-  ctl->n_low = 0;
-  ctl->n_mid = 0;
   ctl->hub_packed = 0ull;
 }
 
@@ -309,14 +465,19 @@ __global__ void k_max_abs(const double *b, long long n, double *part) {
   }
 }
 
+// Hot-window census (setup): sampled in-degree per 1024-row block.
+__global__ void k_hot_sample(const int *row_idx, long long nnz, int stride, unsigned *blk) {
+  const long long step = (long long)gridDim.x * blockDim.x * stride;
+  for (long long e = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * stride; e < nnz; e += step)
+    atomicAdd(&blk[row_idx[e] >> 10], 1u);
+}
+
 // Start-of-run control update (no host->device memcpy inside di_run's timed path).
 __global__ void k_begin_run(Ctl *ctl, double target, long long max_pass, const double *r_exact) {
   ctl->target = target;
   ctl->max_pass = max_pass;
   ctl->r_pred = *r_exact;
   ctl->done = 0;
-  ctl->n_low = 0;
-  ctl->n_mid = 0;
   ctl->hub_packed = 0ull;
 }
 

@@ -1,17 +1,22 @@
 // types.cuh -- plain data shared between the host code and the kernels.
 #pragma once
 #include <cstdint>
+#include <vector_types.h>
 
 namespace diter {
 
-// Degree bins (edges of the column = #out_i).
-constexpr int kLowMax = 32;      // 1..32     : thread per node
-constexpr int kMidMax = 2048;    // 33..2048  : warp per node
-constexpr int kHubChunk = 2048;  // > 2048    : one CTA per 2048-edge chunk of the column
+// Degree classes (edges of the column = #out_i).
+constexpr int kLowMax = 32;      // 1..32     : "low"  (statistics only; same warp path as mid)
+constexpr int kMidMax = 8192;    // 33..8192  : "mid"  -- both: 32 selected nodes per warp,
+                                 //             lanes over the group's concatenated edges
+constexpr int kHubChunk = 2048;  // > 8192    : "hub"  -- one CTA per 2048-edge chunk
+constexpr int kHot = 2048;       // rows staged in shared memory by each scatter CTA
 
 constexpr int kSelectThreads = 256;
+constexpr int kSelectItems = 8;                      // 32-node words per warp iteration
 constexpr int kScatterThreads = 256;
 constexpr int kFinalizeThreads = 512;
+constexpr int kWordsPerSuper = 32;                   // bitmap words per scatter superword (1024 nodes)
 
 // Device-resident control block of one context.
 struct Ctl {
@@ -28,18 +33,21 @@ struct Ctl {
   long long nodes;     // cumulative |S_p|
   int done;            // 0 running, 1 converged, 2 max passes reached
   int policy;          // DI_POLICY_*
-  unsigned n_low;      // per-pass bin counters (reset by k_finalize)
-  unsigned n_mid;
-  unsigned long long hub_packed;  // (hub slots << 32) | hub chunks
+  unsigned long long hub_packed;  // (hub slots << 32) | hub chunks; reset by k_finalize
   long long log_cap;
 };
 
-struct Partial {
-  double r;       // sum |F_i| over the block's nodes (before the take)
-  double loss;    // guaranteed |F|_1 decrease: sum (1 - c_i)|s_i|
-  long long edges;
-  int cnt;
-  int dang;
+// k_select partials (one per CTA): r_p and |S_p|.
+struct SelPartial {
+  double r;
+  long long cnt;
+};
+
+// k_scatter partials (one per CTA): guaranteed |F|_1 drop and frontier census.
+struct ScPartial {
+  double loss;      // sum over taken nodes of (1 - c_i)|s_i|, c_i = d (0 if dangling)
+  long long edges;  // E_p
+  int dang, n_low, n_mid, n_hub;
 };
 
 struct Graph {
@@ -48,19 +56,22 @@ struct Graph {
   const double *vals;        // [nnz] or nullptr (PageRank)
   long long n;
   double d;
+  int hot_lo;                // first row of the shared-memory hot window
 };
 
-struct Bins {
-  int *low_idx;
-  double *low_w;
-  int *mid_idx;
-  double *mid_w;
-  int *hub_idx;
-  double *hub_w;
-  unsigned *hub_chunk;
+// Frontier of one pass: selection bitmap (bit i%32 of word i/32) and the taken
+// values s_i (valid where the bit is set); hubs go to a separate list.
+struct Frontier {
+  unsigned *bits;        // [n_words_pad]
+  double *S;             // [n]
+  long long n_words;     // ceil(n / 32)
+  double *hub_w;         // push value per edge of the hub (s d/#out or s)
+  long long *hub_b0;
+  long long *hub_deg;
+  unsigned *hub_chunk;   // first 2048-edge chunk id of the hub (prefix in slot order)
 };
 
-// Validation + degree-bin census in one pass over the columns.
+// Validation + degree census in one pass over the columns.
 struct Census {
   unsigned long long bad_ptr;     // non-monotone col_ptr
   unsigned long long bad_row;     // row out of range

@@ -37,7 +37,7 @@ def test_default_options():
 
 def test_struct_sizes_match_header():
     import ctypes
-    assert ctypes.sizeof(di.di_pass_log) == 72
+    assert ctypes.sizeof(di.di_pass_log) == 88
     assert ctypes.sizeof(di.di_stats) == 19 * 8
     assert ctypes.sizeof(di.di_options) == 4 + 4 + 8 + 8 + 8 + 8 + 4 + 4 + 4 + 28
 

@@ -177,9 +177,10 @@ def test_c5_signed_parity(n):
 
 
 def test_c3_small_csc_and_parity():
-    """configs[2] shape at scale 16: GPU COO->CSC bit-exact vs the oracle builder; parity."""
-    src, dst = gen.rmat_coo(16, 1)
-    n = 1 << 16
+    """configs[2] shape at scale 18: GPU COO->CSC bit-exact vs the oracle builder; parity
+    (max out-degree ~1.6e4 > kMidMax, so the hub path runs)."""
+    src, dst = gen.rmat_coo(18, 1)
+    n = 1 << 18
     cp_o, ri_o = oracle.csc_from_coo(n, src, dst)
     cp_g, ri_g = di.di_csc_from_coo(n, src, dst)
     np.testing.assert_array_equal(cp_g, cp_o)
