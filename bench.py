@@ -65,6 +65,10 @@ def parse():
     ap.add_argument("--scale", type=int, default=None, help="C3 scale override (tests)")
     ap.add_argument("--n", type=int, default=None, help="node-count override (tests)")
     ap.add_argument("--pass-csv", default=None, help="write the last solve's per-pass log here")
+    ap.add_argument("--exchange", default="async", choices=["sync", "async"],
+                    help="multi-GPU exchange mode (DESIGN.md: SYNC = per-pass rounds, ASYNC = paper's send rule)")
+    ap.add_argument("--partition", default="inout", choices=["out", "inout"],
+                    help="edge-balanced contiguous ranges by out-edges or in+out edges")
     return ap.parse_args()
 
 
@@ -75,7 +79,11 @@ def log(*a):
 # ------------------------------------------------------------------ inputs --
 
 def load_problem(args):
-    """Seeded synthetic input of the config (host arrays)."""
+    """Seeded synthetic input of the config (host arrays); every rank builds the
+    same graph (deterministic counter-based generator), then keeps its shard."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 and "DIGEN_THREADS" not in os.environ:
+        os.environ["DIGEN_THREADS"] = str(max(1, (os.cpu_count() or 1) // world))
     import diter_inputs as gen
     t = time.perf_counter()
     p = gen.config(args.config, args.seed, n=args.n, scale=args.scale)
@@ -234,22 +242,39 @@ def run_reference(args, rank, world):
 
 # ------------------------------------------------------------------ our arm --
 
+def make_ctx(args, p, opts, di, rank, world, comm_id, bounds, host=None):
+    """One GPU: di_create; N ranks: di_create_dist on this rank's shard (NCCL)."""
+    cp, ri, vv, bb = host if host is not None else (p.col_ptr, p.row_idx, p.values, p.b)
+    if world == 1:
+        return di.di_create(p.n, cp, ri, vv, bb, p.d, opts)
+    return di.di_create_dist(rank, world, comm_id, bounds, p.n, cp, ri, vv, bb, p.d, opts)
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import paper_1202_6168_b200 as di
+    from paper_1202_6168_b200 import dist as dd
 
     torch.cuda.set_device(local_rank)
     dist = world > 1
+    if dist:
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     p = load_problem(args)
     pol = policy_of(args)
-    opts = di.default_options(policy=pol, device=local_rank, profile=1)
+    mode = di.DI_EXCHANGE_SYNC if args.exchange == "sync" else di.DI_EXCHANGE_ASYNC
+    opts = di.default_options(policy=pol, device=local_rank, profile=1, exchange_mode=mode)
+    comm_id, bounds, shard = None, None, None
     if dist:
-        raise SystemExit("multi-GPU bench needs the distributed context (dist.cu)")
+        bounds = dd.partition_bounds(p.col_ptr, world, cost=args.partition, row_idx=p.row_idx)
+        comm_id = dd.nccl_comm_id()
+        shard = dd.shard_csc(p.col_ptr, p.row_idx, p.values, p.b, bounds, rank)
     t = time.perf_counter()
-    ctx = di.di_create(p.n, p.col_ptr, p.row_idx, p.values, p.b, p.d, opts)
-    log(f"[bench] di_create {time.perf_counter() - t:.2f}s")
-    graph_bytes = 8 * (p.n + 1) + 4 * p.nnz + (8 * p.nnz if p.values is not None else 0)
-    resident = graph_bytes + 16 * p.n
+    ctx = make_ctx(args, p, opts, di, rank, world, comm_id, bounds, shard)
+    log(f"[bench] rank {rank} create {time.perf_counter() - t:.2f}s")
+    n_loc = ctx.n_local
+    nnz_loc = int(shard[0][-1]) if dist else p.nnz
+    graph_bytes = 8 * (n_loc + 1) + 4 * nnz_loc + (8 * nnz_loc if p.values is not None else 0)
+    resident = graph_bytes + 16 * n_loc
     flush = None
     if resident < 4 * L2_BYTES:
         flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device="cuda")
@@ -259,6 +284,8 @@ def run_ours(args, rank, world, local_rank):
             flush.fill_(1.0)                     # evict L2 between timed solves
             torch.cuda.synchronize()
         di.di_reset(ctx)
+        if dist:
+            torch.distributed.barrier()
         di.di_run(ctx, p.stop)
         return di.di_get_stats(ctx)
 
@@ -269,7 +296,7 @@ def run_ours(args, rank, world, local_rank):
         torch.distributed.barrier()
     tot = {"run_ms": 0.0, "edges": 0, "passes": 0, "kt_scatter_ms": 0.0, "kt_select_ms": 0.0,
            "kt_finalize_ms": 0.0, "scatter_bytes": 0, "alg_bytes": 0, "kernel_launches": 0,
-           "nodes": 0}
+           "nodes": 0, "exchanged_bytes": 0, "exchanges": 0}
     wall0 = time.perf_counter()
     with ClockSampler(local_rank) as clk:
         for _ in range(args.steps):
@@ -286,8 +313,18 @@ def run_ours(args, rank, world, local_rank):
                 fcsv.write(",".join(str(x) for x in row) + "\n")
     r_final = di.di_get_residual(ctx)
     assert r_final < p.stop, r_final
+    run_ms_rank = tot["run_ms"]
+    edges_all = tot["edges"]
+    if dist:   # max time over ranks, work summed over ranks
+        t_ = torch.tensor([run_ms_rank], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t_, op=torch.distributed.ReduceOp.MAX)
+        e_ = torch.tensor([float(tot["edges"]), float(tot["exchanged_bytes"])], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(e_)
+        tot["run_ms"] = float(t_.item())
+        edges_all = int(e_[0].item())
+        xbytes_all = int(e_[1].item())
     run_s = tot["run_ms"] / 1e3
-    value = tot["edges"] / run_s
+    value = edges_all / run_s
     peak, peak_kind = measured_peaks()
     scat_gbs = tot["scatter_bytes"] / (tot["kt_scatter_ms"] / 1e3) / 1e9
     n_launch = tot["passes"]                       # executed k_scatter launches
@@ -298,15 +335,15 @@ def run_ours(args, rank, world, local_rank):
                 "kernel": "k_scatter", "peak_kind": peak_kind,
                 "bytes_per_launch": tot["scatter_bytes"] / max(1, n_launch),
                 "avg_launch_ms": tot["kt_scatter_ms"] / max(1, n_launch),
-                "share_of_step": tot["kt_scatter_ms"] / tot["run_ms"],
+                "share_of_step": tot["kt_scatter_ms"] / max(1e-9, run_ms_rank),
                 "kernel_shares": {"k_select": tot["kt_select_ms"] / kt_sum,
                                   "k_scatter": tot["kt_scatter_ms"] / kt_sum,
                                   "k_finalize": tot["kt_finalize_ms"] / kt_sum},
-                "path_alg_GBps": tot["alg_bytes"] / run_s / 1e9}
+                "path_alg_GBps": tot["alg_bytes"] / (run_ms_rank / 1e3) / 1e9}
     # ---- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, p, opts, di, torch)
+        e2e = run_e2e(args, p, opts, di, torch, rank, world, comm_id, bounds, shard)
     # ---- cpu baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -316,41 +353,46 @@ def run_ours(args, rank, world, local_rank):
                          f"on the full graph, {dt:.1f}s on 1 host core"}
     clocks = clk.summary()
     di.di_destroy(ctx)
+    par = "dp1" if world == 1 else f"node-partition x{world} ({args.partition}-balanced ranges, {args.exchange} exchange)"
     out = {"metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot["run_ms"] / args.steps,
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic",
            "config": {"workload": WORKLOADS[args.config], "n": p.n, "nnz": p.nnz,
                       "stop": p.stop, "policy": "geom" if pol == 0 else "hybrid", "seed": args.seed,
+                      "parallelism": par,
                       "l2": ("flushed between steps (252 MB write)" if flush is not None else
-                             f"inputs ({resident / 1e9:.1f} GB resident) larger than L2 (126 MB)")},
+                             f"inputs ({resident / 1e9:.1f} GB resident per GPU) larger than L2 (126 MB)")},
            "time_to_target_ms": tot["run_ms"] / args.steps,
            "passes_per_solve": tot["passes"] / args.steps,
-           "normalized_iterations": tot["edges"] / args.steps / p.nnz,
+           "normalized_iterations": edges_all / args.steps / p.nnz,
            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
            "gpu_launches": int(tot["kernel_launches"]),
-           "clocks": clocks, "nvlink_bytes_per_round": 0,
+           "clocks": clocks,
+           "nvlink_bytes_per_round": (xbytes_all / max(1, tot["exchanges"])) if dist else 0,
+           "nvlink_bytes_per_solve": (xbytes_all / args.steps) if dist else 0,
            "wall_s_timed": wall}
     if rank == 0:
         print(json.dumps(out), flush=True)
+    if dist:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
 
 
-def run_e2e(args, p, opts, di, torch):
+def run_e2e(args, p, opts, di, torch, rank=0, world=1, comm_id=None, bounds=None, shard=None):
     """Same metric through di_create/di_run/di_get_history with pinned host buffers."""
-    cp = torch.from_numpy(p.col_ptr).pin_memory()
-    ri = torch.from_numpy(p.row_idx).pin_memory()
-    vv = torch.from_numpy(p.values).pin_memory() if p.values is not None else None
-    bb = torch.from_numpy(p.b).pin_memory() if p.b is not None else None
-    H = torch.empty(p.n, dtype=torch.float64).pin_memory()
-    h2d = cp.numel() * 8 + ri.numel() * 4 + (vv.numel() * 8 if vv is not None else 0) + \
-        (bb.numel() * 8 if bb is not None else 0)
-    d2h = p.n * 8
+    src = shard if shard is not None else (p.col_ptr, p.row_idx, p.values, p.b)
+    pin = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() if a is not None else None for a in src]
+    n_loc = int(len(src[0]) - 1)
+    H = torch.empty(n_loc, dtype=torch.float64).pin_memory()
+    h2d = sum(t.numel() * t.element_size() for t in pin if t is not None)
+    d2h = n_loc * 8
     import copy
     o2 = copy.copy(opts)
     o2.profile = 0
 
     def one():
-        ctx = di.di_create(p.n, cp, ri, vv, bb, p.d, o2)
+        ctx = make_ctx(args, p, o2, di, rank, world, comm_id, bounds, pin)
         di.di_run(ctx, p.stop)
         di.di_get_history(ctx, H)
         e = di.di_get_stats(ctx)["edges"]
@@ -359,6 +401,8 @@ def run_e2e(args, p, opts, di, torch):
 
     one()                                          # warm (allocator, module load)
     torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
     edges = 0
     t0 = time.perf_counter()
     steps = max(1, min(args.steps, 3))
@@ -366,6 +410,12 @@ def run_e2e(args, p, opts, di, torch):
         edges += one()
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
+    if world > 1:
+        t_ = torch.tensor([dt, float(edges)], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t_[:1], op=torch.distributed.ReduceOp.MAX)
+        e_ = t_[1:].clone()
+        torch.distributed.all_reduce(e_)
+        dt, edges = float(t_[0].item()), float(e_[0].item())
     return {"value": edges / dt, "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": steps, "ms_per_step": dt * 1e3 / steps}
 

@@ -63,6 +63,10 @@ def _L():
         lib.dg_rmat_fill.argtypes = [P, vp, vp]
         lib.dg_validate.argtypes = [P]
         lib.dg_num_threads.restype = ctypes.c_int
+        lib.dg_set_threads.argtypes = [ctypes.c_int]
+        omp = os.environ.get("DIGEN_THREADS")
+        if omp:
+            lib.dg_set_threads(int(omp))
         _lib = lib
     return _lib
 

@@ -309,3 +309,4 @@ int dg_rmat_fill(const dg_params *p, int32_t *src, int32_t *dst) {
 }
 
 int dg_num_threads(void) { return omp_get_max_threads(); }
+void dg_set_threads(int n) { if (n > 0) omp_set_num_threads(n); }

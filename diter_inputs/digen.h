@@ -39,6 +39,7 @@ int dg_b_signed(const dg_params *p, double *b);
 int64_t dg_rmat_edges(const dg_params *p);
 int dg_rmat_fill(const dg_params *p, int32_t *src, int32_t *dst);
 int dg_num_threads(void);
+void dg_set_threads(int n);
 
 #ifdef __cplusplus
 }

@@ -30,6 +30,8 @@ struct di_ctx {
   double *vals = nullptr;        // [nnz_local] signed mode only
   double *d_b = nullptr;         // B [n_local] when given (kept for di_reset)
   double *F = nullptr;           // fluid [n_local]
+  double *G = nullptr;           // remote outbox over global ids (distributed only)
+  unsigned char *dflags = nullptr;  // dirty flag per 32-row block of G
   double *H = nullptr;           // history [n_local]
   diter::Frontier fr{};
   unsigned long long cap_low = 0, cap_mid = 0, cap_hub = 0;
@@ -68,6 +70,7 @@ void diter_set_err(di_ctx *ctx, const char *fmt, ...);
 di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_idx,
                       const double *values, const double *b, const di_options *opt);
 di_status diter_l1_launch(di_ctx *ctx);
+diter::Graph diter_graph(const di_ctx *ctx);
 
 // distributed hooks (dist.cu); identities / no-ops on single-GPU contexts
 void diter_dist_free(di_ctx *ctx);

@@ -1,22 +1,675 @@
-// dist.cu -- multi-GPU hooks (placeholder until the NCCL exchange lands).
-#include "ctx.cuh"
+// dist.cu -- multi-GPU D-iteration.
+//
+// One process (or thread) per rank; rank k owns the contiguous node range
+// Omega_k = [bounds[k], bounds[k+1]) with its F, H and out-columns (PAPER.md:
+// 173-176).  Pushes to rows of other ranks accumulate in a remote outbox G
+// (global ids) and are shipped as compacted (row, fluid) records:
+//
+//  SYNC  : every pass ends with an exchange round, so a pass is exactly the
+//          single-GPU snapshot pass (same frontier sizes, same T schedule: the
+//          pass totals are all-reduced before T_{p+1} is chosen).
+//  ASYNC : ranks run check_interval passes on their own (local threshold
+//          policy on |Omega_k|, no communication), then meet in an exchange
+//          round where rank k ships its outbox only if s_k > r_k / K
+//          (eq. send; strict, reading R7) -- otherwise it
+//          keeps accumulating.  Received fluid is merged at once ("can be
+//          delayed").  Termination: the round all-reduces
+//          r_k + s_k (in-flight mass is zero at that point, every record sent
+//          in the round has been merged), stop when below the target.
+//
+// The collectives go through a Fabric: NCCL (one GPU per rank, NVLink /
+// NVSwitch), or an in-process loopback that lets K contexts of one process
+// (threads) share one GPU for testing -- no kernel ever waits on another rank;
+// all waiting is host-side.
+#include <cuda_runtime.h>
 
-void diter_dist_free(di_ctx *) {}
-double diter_dist_max(di_ctx *, double v) { return v; }
-double diter_dist_sum(di_ctx *, double v) { return v; }
-di_status diter_dist_reset(di_ctx *) { return DI_OK; }
-di_status diter_dist_run(di_ctx *ctx, double) {
-  diter_set_err(ctx, "distributed run not built");
-  return DI_ERR_UNSUPPORTED;
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/diter.h"
+#include "ctx.cuh"
+#include "kernels.cuh"
+
+#if DITER_WITH_NCCL
+#include <nccl.h>
+#endif
+
+using namespace diter;
+
+#define CKD(call)                                                                      \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess) {                                                           \
+      diter_set_err(ctx, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_),       \
+                    __FILE__, __LINE__);                                               \
+      return e_ == cudaErrorMemoryAllocation ? DI_ERR_OOM : DI_ERR_CUDA;               \
+    }                                                                                  \
+  } while (0)
+
+#define TRYD(x)                     \
+  do {                              \
+    di_status s_ = (x);             \
+    if (s_ != DI_OK) return s_;     \
+  } while (0)
+
+// One exchanged record: destination row (local to the receiver) and fluid.
+struct Rec {
+  long long row;
+  double val;
+};
+
+// ------------------------------------------------------------------ fabric --
+struct Fabric {
+  virtual ~Fabric() {}
+  // in-place sum over ranks of `count` doubles on the device
+  virtual di_status allreduce_sum(di_ctx *ctx, double *dev, int count) = 0;
+  // host-side exchange of per-peer record counts
+  virtual di_status alltoall_counts(di_ctx *ctx, const long long *send, long long *recv) = 0;
+  // records: send[soff[q] .. soff[q]+scnt[q]) to peer q, into recv[roff[q] ..]
+  virtual di_status alltoallv(di_ctx *ctx, const Rec *send, const long long *soff, const long long *scnt,
+                              Rec *recv, const long long *roff, const long long *rcnt) = 0;
+  virtual double host_max(di_ctx *ctx, double v) = 0;
+};
+
+// In-process loopback: K contexts (one host thread each) on one device.
+struct LoopGroup {
+  int world = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long generation = 0;
+  std::vector<double> red;                 // [world * 8]
+  std::vector<long long> counts;           // [world * world]
+  std::vector<const Rec *> sendp;
+  std::vector<std::vector<long long>> soff, scnt;
+  std::vector<double> hmax;
+
+  explicit LoopGroup(int w) : world(w), red(w * 8), counts(w * w), sendp(w), soff(w), scnt(w), hmax(w) {}
+
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const long long gen = generation;
+    if (++arrived == world) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return generation != gen; });
+    }
+  }
+};
+
+static std::mutex g_loop_mu;
+static std::map<std::string, std::weak_ptr<LoopGroup>> g_loop_groups;
+
+struct LoopFabric : Fabric {
+  std::shared_ptr<LoopGroup> grp;
+  int rank;
+  LoopFabric(std::shared_ptr<LoopGroup> g, int r) : grp(std::move(g)), rank(r) {}
+
+  di_status allreduce_sum(di_ctx *ctx, double *dev, int count) override {
+    if (count > 8) return DI_ERR_INVALID_ARG;
+    double h[8];
+    CKD(cudaMemcpyAsync(h, dev, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
+    CKD(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(&grp->red[rank * 8], h, sizeof(double) * count);
+    grp->barrier();
+    for (int q = 0; q < count; ++q) {
+      double s = 0.0;
+      for (int k = 0; k < grp->world; ++k) s += grp->red[k * 8 + q];   // fixed rank order
+      h[q] = s;
+    }
+    grp->barrier();
+    CKD(cudaMemcpyAsync(dev, h, sizeof(double) * count, cudaMemcpyHostToDevice, ctx->stream));
+    CKD(cudaStreamSynchronize(ctx->stream));
+    return DI_OK;
+  }
+  di_status alltoall_counts(di_ctx *, const long long *send, long long *recv) override {
+    const int W = grp->world;
+    for (int q = 0; q < W; ++q) grp->counts[rank * W + q] = send[q];
+    grp->barrier();
+    for (int q = 0; q < W; ++q) recv[q] = grp->counts[q * W + rank];
+    grp->barrier();
+    return DI_OK;
+  }
+  di_status alltoallv(di_ctx *ctx, const Rec *send, const long long *soff, const long long *scnt, Rec *recv,
+                      const long long *roff, const long long *rcnt) override {
+    const int W = grp->world;
+    CKD(cudaStreamSynchronize(ctx->stream));   // send buffer complete
+    grp->sendp[rank] = send;
+    grp->soff[rank].assign(soff, soff + W);
+    grp->scnt[rank].assign(scnt, scnt + W);
+    grp->barrier();
+    for (int q = 0; q < W; ++q) {
+      if (rcnt[q] == 0) continue;
+      const Rec *src = grp->sendp[q] + grp->soff[q][rank];
+      CKD(cudaMemcpyAsync(recv + roff[q], src, sizeof(Rec) * rcnt[q], cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    CKD(cudaStreamSynchronize(ctx->stream));
+    grp->barrier();                            // peers may now reuse their send buffers
+    return DI_OK;
+  }
+  double host_max(di_ctx *, double v) override {
+    grp->hmax[rank] = v;
+    grp->barrier();
+    double m = 0.0;
+    for (int k = 0; k < grp->world; ++k) m = std::max(m, grp->hmax[k]);
+    grp->barrier();
+    return m;
+  }
+};
+
+#if DITER_WITH_NCCL
+#define CKN(call)                                                                      \
+  do {                                                                                 \
+    ncclResult_t r_ = (call);                                                          \
+    if (r_ != ncclSuccess) {                                                           \
+      diter_set_err(ctx, "%s failed: %s", #call, ncclGetErrorString(r_));              \
+      return DI_ERR_NCCL;                                                              \
+    }                                                                                  \
+  } while (0)
+
+struct NcclFabric : Fabric {
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  long long *d_cnt = nullptr;   // [2 * world] send/recv counts staging
+  double *d_tmp = nullptr;
+  ~NcclFabric() override {
+    if (d_cnt) cudaFree(d_cnt);
+    if (d_tmp) cudaFree(d_tmp);
+    if (comm) ncclCommDestroy(comm);
+  }
+  di_status allreduce_sum(di_ctx *ctx, double *dev, int count) override {
+    CKN(ncclAllReduce(dev, dev, count, ncclDouble, ncclSum, comm, ctx->stream));
+    return DI_OK;
+  }
+  di_status alltoall_counts(di_ctx *ctx, const long long *send, long long *recv) override {
+    CKD(cudaMemcpyAsync(d_cnt, send, sizeof(long long) * world, cudaMemcpyHostToDevice, ctx->stream));
+    CKN(ncclGroupStart());
+    for (int q = 0; q < world; ++q) {
+      CKN(ncclSend(d_cnt + q, 1, ncclInt64, q, comm, ctx->stream));
+      CKN(ncclRecv(d_cnt + world + q, 1, ncclInt64, q, comm, ctx->stream));
+    }
+    CKN(ncclGroupEnd());
+    CKD(cudaMemcpyAsync(recv, d_cnt + world, sizeof(long long) * world, cudaMemcpyDeviceToHost, ctx->stream));
+    CKD(cudaStreamSynchronize(ctx->stream));
+    return DI_OK;
+  }
+  di_status alltoallv(di_ctx *ctx, const Rec *send, const long long *soff, const long long *scnt, Rec *recv,
+                      const long long *roff, const long long *rcnt) override {
+    CKN(ncclGroupStart());
+    for (int q = 0; q < world; ++q) {
+      if (q == rank) continue;
+      if (scnt[q] > 0) CKN(ncclSend(send + soff[q], sizeof(Rec) * scnt[q], ncclChar, q, comm, ctx->stream));
+      if (rcnt[q] > 0) CKN(ncclRecv(recv + roff[q], sizeof(Rec) * rcnt[q], ncclChar, q, comm, ctx->stream));
+    }
+    CKN(ncclGroupEnd());
+    return DI_OK;
+  }
+  double host_max(di_ctx *ctx, double v) override {
+    if (!d_tmp && cudaMalloc(&d_tmp, sizeof(double)) != cudaSuccess) return v;
+    cudaMemcpyAsync(d_tmp, &v, sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
+    ncclAllReduce(d_tmp, d_tmp, 1, ncclDouble, ncclMax, comm, ctx->stream);
+    cudaMemcpyAsync(&v, d_tmp, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    return v;
+  }
+};
+#endif
+
+// ------------------------------------------------------------ dist state --
+struct DistState {
+  std::unique_ptr<Fabric> fabric;
+  std::vector<long long> bounds;       // [world + 1]
+  long long *d_bounds = nullptr;
+  Rec *send = nullptr, *recv = nullptr;
+  long long send_cap = 0, recv_cap = 0;
+  long long *d_scnt = nullptr;         // [world] records compacted per peer
+  double *d_sums = nullptr;            // [kSums + 2]
+  std::vector<long long> soff, scnt, roff, rcnt;
+  double s_k = 0.0;                    // outbox mass (ASYNC)
+};
+
+// ----------------------------------------------------------------- kernels --
+// Records of the outbox rows owned by peer q, compacted block by block: a warp
+// reads 32 dirty flags (1024 rows), then for each dirty 32-row block the lanes
+// read G[row] (coalesced), keep the non-zero ones, zero them, and append
+// (row - bounds[q], value) with one warp-aggregated atomic per block.
+__global__ void k_compact(double *__restrict__ G, unsigned char *__restrict__ dflags, const long long *bounds,
+                          int world, int rank, Rec *__restrict__ send, const long long *soff_dev,
+                          long long *scnt, int take) {
+  const unsigned lane = lane_id();
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  for (int q = 0; q < world; ++q) {
+    if (q == rank) continue;
+    const long long a = bounds[q], b = bounds[q + 1];
+    const long long blk0 = a >> 5, blk1 = (b + 31) >> 5;
+    for (long long sb = blk0 + gw * 32; sb < blk1; sb += warps * 32) {
+      const long long myblk = sb + lane;
+      const bool dirty = (myblk < blk1) && dflags[myblk];
+      unsigned dm = __ballot_sync(0xffffffffu, dirty);
+      while (dm) {
+        const int j = __ffs(dm) - 1;
+        dm &= dm - 1;
+        const long long row = ((sb + j) << 5) + lane;
+        const bool in = row >= a && row < b;
+        double v = in ? G[row] : 0.0;
+        const bool keep = in && v != 0.0;
+        const unsigned km = __ballot_sync(0xffffffffu, keep);
+        if (km == 0u) continue;
+        unsigned long long base = 0;
+        if (lane == 0) base = (unsigned long long)atomicAdd((unsigned long long *)&scnt[q], (unsigned long long)__popc(km));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) {
+          const long long slot = soff_dev[q] + (long long)base + __popc(km & lanemask_lt());
+          send[slot] = Rec{row - a, v};
+          if (take) G[row] = 0.0;
+        }
+      }
+    }
+  }
 }
-extern "C" di_status di_create_dist(di_ctx **out, int32_t, int32_t, const void *, const int64_t *, int64_t,
-                                    const int64_t *, const int32_t *, const double *, const double *, double,
-                                    const di_options *) {
-  if (out) *out = nullptr;
-  diter_set_err(nullptr, "di_create_dist: not built");
-  return DI_ERR_UNSUPPORTED;
+
+// |G|_1 over dirty blocks of rows this rank does not own (s_k).
+__global__ void k_outbox_mass(const double *__restrict__ G, const unsigned char *__restrict__ dflags,
+                              long long n_rows, long long lo, long long hi, double *out) {
+  double m = 0.0;
+  const long long nb = (n_rows + 31) >> 5;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < nb * 32; t += stride) {
+    const long long blk = t >> 5;
+    if (!dflags[blk]) continue;
+    if (t < lo || t >= hi) m += (t < n_rows) ? fabs(G[t]) : 0.0;
+  }
+  m = warp_sum(m);
+  if (lane_id() == 0 && m != 0.0) atomicAdd(out, m);
 }
-extern "C" di_status di_get_unique_id(void *) {
-  diter_set_err(nullptr, "di_get_unique_id: not built");
+
+// Merge received records: F[row] += val ("add them to existing
+// fluids, node per node").
+__global__ void k_merge(double *__restrict__ F, const Rec *__restrict__ recv, long long n) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+    const Rec r = recv[k];
+    red_add(F + r.row, r.val);
+  }
+}
+
+__global__ void k_set_target(Ctl *ctl, double target, long long max_pass, int done) {
+  ctl->target = target;
+  ctl->max_pass = max_pass;
+  ctl->done = done;
+  ctl->hub_packed = 0ull;
+}
+
+// ------------------------------------------------------------ host helpers --
+void diter_dist_free(di_ctx *ctx) {
+  if (!ctx || !ctx->dist) return;
+  DistState *ds = ctx->dist;
+  void *ptrs[] = {ds->d_bounds, ds->send, ds->recv, ds->d_scnt, ds->d_sums};
+  for (void *p : ptrs)
+    if (p) cudaFree(p);
+  if (ctx->G) cudaFree(ctx->G);
+  if (ctx->dflags) cudaFree(ctx->dflags);
+  ctx->G = nullptr;
+  ctx->dflags = nullptr;
+  delete ds;
+  ctx->dist = nullptr;
+}
+
+double diter_dist_max(di_ctx *ctx, double v) {
+  if (!ctx->dist) return v;
+  return ctx->dist->fabric->host_max(ctx, v);
+}
+
+double diter_dist_sum(di_ctx *ctx, double v) {
+  if (!ctx->dist) return v;
+  DistState *ds = ctx->dist;
+  cudaMemcpyAsync(ds->d_sums, &v, sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
+  if (ds->fabric->allreduce_sum(ctx, ds->d_sums, 1) != DI_OK) return v;
+  cudaMemcpyAsync(&v, ds->d_sums, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+  return v;
+}
+
+di_status diter_dist_reset(di_ctx *ctx) {
+  if (!ctx->dist) return DI_OK;
+  CKD(cudaMemsetAsync(ctx->G, 0, sizeof(double) * ctx->n_rows, ctx->stream));
+  CKD(cudaMemsetAsync(ctx->dflags, 0, (size_t)((ctx->n_rows + 31) >> 5), ctx->stream));
+  CKD(cudaStreamSynchronize(ctx->stream));
+  ctx->dist->s_k = 0.0;
+  return DI_OK;
+}
+
+// exact global |F|_1 (+ s_k outbox mass when `with_outbox`)
+static di_status global_residual(di_ctx *ctx, double add, double *out) {
+  DistState *ds = ctx->dist;
+  TRYD(diter_l1_launch(ctx));
+  CKD(cudaMemcpyAsync(ds->d_sums, ctx->l1_out, sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  double h_add = add;
+  CKD(cudaMemcpyAsync(ds->d_sums + 1, &h_add, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  TRYD(ds->fabric->allreduce_sum(ctx, ds->d_sums, 2));
+  double h[2];
+  CKD(cudaMemcpyAsync(h, ds->d_sums, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  CKD(cudaStreamSynchronize(ctx->stream));
+  *out = h[0] + h[1];
+  return DI_OK;
+}
+
+// One exchange round: optional compaction of the whole outbox, record counts,
+// all-to-all-v, merge.  Collective.
+static di_status exchange(di_ctx *ctx, bool send_now) {
+  DistState *ds = ctx->dist;
+  const int W = ctx->world;
+  CKD(cudaMemsetAsync(ds->d_scnt, 0, sizeof(long long) * W, ctx->stream));
+  if (send_now) {
+    long long *d_soff = reinterpret_cast<long long *>(ds->d_sums + kSums + 2);
+    CKD(cudaMemcpyAsync(d_soff, ds->soff.data(), sizeof(long long) * W, cudaMemcpyHostToDevice, ctx->stream));
+    k_compact<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->G, ctx->dflags, ds->d_bounds, W, ctx->rank,
+                                                         ds->send, d_soff, ds->d_scnt, 1);
+    CKD(cudaMemsetAsync(ctx->dflags, 0, (size_t)((ctx->n_rows + 31) >> 5), ctx->stream));
+    ctx->kernel_launches += 1;
+  }
+  CKD(cudaMemcpyAsync(ds->scnt.data(), ds->d_scnt, sizeof(long long) * W, cudaMemcpyDeviceToHost, ctx->stream));
+  CKD(cudaStreamSynchronize(ctx->stream));
+  TRYD(ds->fabric->alltoall_counts(ctx, ds->scnt.data(), ds->rcnt.data()));
+  long long tot = 0;
+  for (int q = 0; q < W; ++q) {
+    ds->roff[q] = tot;
+    tot += ds->rcnt[q];
+  }
+  if (tot > ds->recv_cap) {
+    diter_set_err(ctx, "receive overflow (%lld > %lld)", tot, ds->recv_cap);
+    return DI_ERR_STATE;
+  }
+  long long sent = 0;
+  for (int q = 0; q < W; ++q) sent += ds->scnt[q];
+  TRYD(ds->fabric->alltoallv(ctx, ds->send, ds->soff.data(), ds->scnt.data(), ds->recv, ds->roff.data(),
+                             ds->rcnt.data()));
+  if (tot > 0) {
+    k_merge<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->F, ds->recv, tot);
+    ctx->kernel_launches += 1;
+  }
+  if (sent > 0) {
+    ctx->exchanged_bytes += (long long)sizeof(Rec) * sent;
+    ctx->alg_bytes_exchange += 12LL * sent + 20LL * tot;  // 12 B shipped + 20 B merged
+    ctx->exchanges += 1;
+  }
+  if (send_now) ds->s_k = 0.0;
+  return DI_OK;
+}
+
+static void launch_pass_kernels(di_ctx *ctx) {
+  Graph g = diter_graph(ctx);
+  k_select<<<ctx->grid_select, kSelectThreads, 0, ctx->stream>>>(ctx->F, ctx->H, ctx->fr, ctx->n_local, ctx->ctl,
+                                                                ctx->sel_part);
+  if (ctx->vals)
+    k_scatter<true><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl,
+                                                                            ctx->sc_part, ctx->gsplit);
+  else
+    k_scatter<false><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl,
+                                                                             ctx->sc_part, ctx->gsplit);
+  if (ctx->cap_hub > 0) {
+    if (ctx->vals)
+      k_scatter_hubs<true><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
+    else
+      k_scatter_hubs<false><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
+  }
+  ctx->kernel_launches += ctx->cap_hub > 0 ? 3 : 2;
+}
+
+di_status diter_dist_run(di_ctx *ctx, double target) {
+  DistState *ds = ctx->dist;
+  CKD(cudaSetDevice(ctx->device));
+  CKD(cudaEventRecord(ctx->ev0, ctx->stream));
+  const long long max_pass_abs = ctx->passes_done + ctx->opt.max_passes;
+  const bool sync_mode = ctx->opt.exchange_mode == DI_EXCHANGE_SYNC;
+  Ctl *h = reinterpret_cast<Ctl *>(ctx->h_ctl);
+  di_status st = DI_OK;
+  double R = 0.0;
+  // outbox fluid counts toward the residual (in-flight mass)
+  TRYD(global_residual(ctx, ds->s_k, &R));
+  ctx->residual = R;
+  if (R < target) goto out;
+  if (sync_mode) {
+    // -------- SYNC: one exchange per pass, pass totals all-reduced ----------
+    k_set_target<<<1, 1, 0, ctx->stream>>>(ctx->ctl, target, max_pass_abs, 0);
+    for (;;) {
+      launch_pass_kernels(ctx);
+      k_reduce_partials<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->ctl, ctx->sel_part, ctx->grid_select,
+                                                                  ctx->sc_part, ctx->grid_scatter, ds->d_sums);
+      TRYD(ds->fabric->allreduce_sum(ctx, ds->d_sums, kSums));
+      TRYD(exchange(ctx, true));
+      k_apply_pass<<<1, 1, 0, ctx->stream>>>(ctx->ctl, ds->d_sums, ctx->log);
+      ctx->kernel_launches += 2;
+      CKD(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+      CKD(cudaStreamSynchronize(ctx->stream));
+      if (!h->done) continue;
+      ctx->passes_done = h->pass;
+      TRYD(global_residual(ctx, 0.0, &R));
+      ctx->residual = R;
+      if (R < target) break;
+      if (h->pass >= max_pass_abs) { st = DI_ERR_NOT_CONVERGED; break; }
+      k_set_target<<<1, 1, 0, ctx->stream>>>(ctx->ctl, target, max_pass_abs, 0);   // prediction was early
+    }
+  } else {
+    // -------- ASYNC: local passes, exchange rounds every check_interval ------
+    for (;;) {
+      // local passes: no target (never "done" locally), local threshold policy
+      k_set_target<<<1, 1, 0, ctx->stream>>>(ctx->ctl, 0.0, max_pass_abs, 0);
+      for (int k = 0; k < ctx->check_interval; ++k) {
+        launch_pass_kernels(ctx);
+        k_finalize<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->ctl, ctx->sel_part, ctx->grid_select, ctx->sc_part,
+                                                            ctx->grid_scatter, ctx->log);
+        ctx->kernel_launches += 1;
+      }
+      // round: s_k (outbox mass) and r_k decide the send (eq. send)
+      CKD(cudaMemsetAsync(ds->d_sums, 0, sizeof(double), ctx->stream));
+      k_outbox_mass<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->G, ctx->dflags, ctx->n_rows, ctx->lo,
+                                                               ctx->lo + ctx->n_local, ds->d_sums);
+      TRYD(diter_l1_launch(ctx));
+      double hs[2];
+      CKD(cudaMemcpyAsync(&hs[0], ds->d_sums, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      CKD(cudaMemcpyAsync(&hs[1], ctx->l1_out, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      CKD(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+      CKD(cudaStreamSynchronize(ctx->stream));
+      ds->s_k = hs[0];
+      const double r_k = hs[1];
+      const bool send_now = (ds->s_k > r_k / ctx->world) || (r_k == 0.0 && ds->s_k > 0.0);
+      TRYD(exchange(ctx, send_now));
+      ctx->passes_done = h->pass;
+      TRYD(global_residual(ctx, ds->s_k, &R));
+      ctx->residual = R;
+      const bool stop = R < target, out_of_passes = h->pass >= max_pass_abs;
+      if (stop || out_of_passes) {
+        // deliver what is left in the outboxes, so that on return F (with H) is
+        // the whole state: F = B - (I-P)H on every rank, nothing in flight
+        TRYD(exchange(ctx, true));
+        if (!stop) st = DI_ERR_NOT_CONVERGED;
+        break;
+      }
+    }
+  }
+out:
+  CKD(cudaEventRecord(ctx->ev1, ctx->stream));
+  CKD(cudaEventSynchronize(ctx->ev1));
+  {
+    float ms = 0.f;
+    CKD(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    ctx->run_ms = ms;
+    ctx->run_ms_total += ms;
+  }
+  CKD(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+  CKD(cudaStreamSynchronize(ctx->stream));
+  ctx->passes_done = h->pass;
+  ctx->edges = h->edges;
+  ctx->nodes = h->nodes;
+  ctx->threshold = h->T;
+  if (st == DI_ERR_NOT_CONVERGED) diter_set_err(ctx, "max_passes reached before |F|_1 < %g", target);
+  return st;
+}
+
+// ----------------------------------------------------------------- create --
+extern "C" di_status di_get_unique_id(void *comm_id_out) {
+  if (!comm_id_out) {
+    diter_set_err(nullptr, "NULL argument");
+    return DI_ERR_INVALID_ARG;
+  }
+#if DITER_WITH_NCCL
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) {
+    diter_set_err(nullptr, "ncclGetUniqueId failed: %s", ncclGetErrorString(r));
+    return DI_ERR_NCCL;
+  }
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(comm_id_out, &id, 128);
+  return DI_OK;
+#else
+  diter_set_err(nullptr, "built without NCCL");
   return DI_ERR_UNSUPPORTED;
+#endif
+}
+
+static const char kLoopTag[8] = {'D', 'I', 'L', 'O', 'O', 'P', '0', '1'};
+
+extern "C" di_status di_create_dist(di_ctx **out, int32_t rank, int32_t world, const void *comm_id,
+                                    const int64_t *bounds, int64_t n_global, const int64_t *col_ptr_local,
+                                    const int32_t *row_idx_local, const double *values_local,
+                                    const double *b_local, double d, const di_options *opt) {
+  if (!out) { diter_set_err(nullptr, "out is NULL"); return DI_ERR_INVALID_ARG; }
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world || !comm_id || !bounds || !col_ptr_local || n_global < 1 ||
+      n_global > 2147483647LL || !(d > 0.0 && d < 1.0)) {
+    diter_set_err(nullptr, "di_create_dist: invalid arguments");
+    return DI_ERR_INVALID_ARG;
+  }
+  if (bounds[0] != 0 || bounds[world] != n_global) {
+    diter_set_err(nullptr, "bounds must start at 0 and end at n_global");
+    return DI_ERR_INVALID_ARG;
+  }
+  for (int k = 0; k < world; ++k)
+    if (bounds[k + 1] <= bounds[k]) {
+      diter_set_err(nullptr, "bounds must be strictly increasing");
+      return DI_ERR_INVALID_ARG;
+    }
+  const long long lo = bounds[rank], nl = bounds[rank + 1] - bounds[rank];
+  const long long nnz = col_ptr_local[nl];
+  if (col_ptr_local[0] != 0 || nnz < 0 || (nnz > 0 && !row_idx_local)) {
+    diter_set_err(nullptr, "col_ptr_local[0] must be 0 and col_ptr_local[n_local] = nnz >= 0");
+    return DI_ERR_INVALID_ARG;
+  }
+  di_ctx *ctx = new (std::nothrow) di_ctx();
+  if (!ctx) { diter_set_err(nullptr, "host OOM"); return DI_ERR_OOM; }
+  ctx->n_rows = n_global;
+  ctx->n_local = nl;
+  ctx->nnz_local = nnz;
+  ctx->lo = lo;
+  ctx->d = d;
+  ctx->rank = rank;
+  ctx->world = world;
+  auto fail = [&](di_status s) {
+    std::string e = ctx->err;
+    di_destroy(ctx);
+    diter_set_err(nullptr, "%s", e.c_str());
+    return s;
+  };
+  DistState *ds = new DistState();
+  ctx->dist = ds;
+  ds->bounds.assign(bounds, bounds + world + 1);
+  // device of this rank: options.device, else the current device
+  {
+    int dev = (opt && opt->device >= 0) ? opt->device : -1;
+    if (dev < 0) cudaGetDevice(&dev);
+    if (cudaSetDevice(dev) != cudaSuccess) { diter_set_err(ctx, "cudaSetDevice failed"); return fail(DI_ERR_CUDA); }
+  }
+  // fabric
+  if (std::memcmp(comm_id, kLoopTag, 8) == 0) {
+    std::string key(static_cast<const char *>(comm_id), 128);
+    std::shared_ptr<LoopGroup> grp;
+    {
+      std::lock_guard<std::mutex> lk(g_loop_mu);
+      auto it = g_loop_groups.find(key);
+      if (it != g_loop_groups.end()) grp = it->second.lock();
+      if (!grp) {
+        grp = std::make_shared<LoopGroup>(world);
+        g_loop_groups[key] = grp;
+      }
+    }
+    if (grp->world != world) { diter_set_err(ctx, "loopback group size mismatch"); return fail(DI_ERR_INVALID_ARG); }
+    ds->fabric.reset(new LoopFabric(grp, rank));
+  } else {
+#if DITER_WITH_NCCL
+    NcclFabric *nf = new NcclFabric();
+    ds->fabric.reset(nf);
+    nf->rank = rank;
+    nf->world = world;
+    ncclUniqueId id;
+    std::memcpy(&id, comm_id, 128);
+    ncclResult_t r = ncclCommInitRank(&nf->comm, world, id, rank);
+    if (r != ncclSuccess) {
+      diter_set_err(ctx, "ncclCommInitRank failed: %s", ncclGetErrorString(r));
+      return fail(DI_ERR_NCCL);
+    }
+    if (cudaMalloc(&nf->d_cnt, sizeof(long long) * 2 * world) != cudaSuccess) {
+      diter_set_err(ctx, "cudaMalloc failed");
+      return fail(DI_ERR_OOM);
+    }
+#else
+    diter_set_err(ctx, "built without NCCL (use a loopback comm id)");
+    return fail(DI_ERR_UNSUPPORTED);
+#endif
+  }
+  di_status s = diter_setup(ctx, col_ptr_local, row_idx_local, values_local, b_local, opt);
+  if (s != DI_OK) return fail(s);
+  // outbox, flags, exchange buffers
+  {
+    const long long nb = (n_global + 31) >> 5;
+    if (cudaMalloc(&ctx->G, sizeof(double) * n_global) != cudaSuccess ||
+        cudaMalloc(&ctx->dflags, (size_t)nb) != cudaSuccess) {
+      diter_set_err(ctx, "cudaMalloc (outbox) failed");
+      return fail(DI_ERR_OOM);
+    }
+    // records to peer q: at most |Omega_q| (one per row); from peers: at most (K-1) |Omega_k|
+    ds->soff.assign(world, 0);
+    ds->scnt.assign(world, 0);
+    ds->roff.assign(world, 0);
+    ds->rcnt.assign(world, 0);
+    long long cap = 0;
+    for (int q = 0; q < world; ++q) {
+      ds->soff[q] = cap;
+      if (q != rank) cap += bounds[q + 1] - bounds[q];
+    }
+    ds->send_cap = std::max(1LL, cap);
+    ds->recv_cap = std::max(1LL, (long long)(world - 1) * nl);
+    if (cudaMalloc(&ds->send, sizeof(Rec) * ds->send_cap) != cudaSuccess ||
+        cudaMalloc(&ds->recv, sizeof(Rec) * ds->recv_cap) != cudaSuccess ||
+        cudaMalloc(&ds->d_bounds, sizeof(long long) * (world + 1)) != cudaSuccess ||
+        cudaMalloc(&ds->d_scnt, sizeof(long long) * world) != cudaSuccess ||
+        cudaMalloc(&ds->d_sums, sizeof(double) * (kSums + 2) + sizeof(long long) * world) != cudaSuccess) {
+      diter_set_err(ctx, "cudaMalloc (exchange buffers) failed");
+      return fail(DI_ERR_OOM);
+    }
+    cudaMemcpyAsync(ds->d_bounds, bounds, sizeof(long long) * (world + 1), cudaMemcpyHostToDevice, ctx->stream);
+    s = diter_dist_reset(ctx);
+    if (s != DI_OK) return fail(s);
+  }
+  // The threshold schedule is global: T_0 = max over ranks |B_i| / alpha (done in
+  // setup through diter_dist_max); SYNC applies the HYBRID rule to the global |S_p|
+  // and N; ASYNC applies it per rank to |S_p^k| and |Omega_k|.
+  if (ctx->opt.exchange_mode == DI_EXCHANGE_ASYNC) {
+    ctx->ctl_init.n_total = (double)nl;
+    cudaMemcpyAsync(ctx->ctl, &ctx->ctl_init, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+  }
+  *out = ctx;
+  return DI_OK;
 }

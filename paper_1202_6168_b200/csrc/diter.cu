@@ -119,8 +119,14 @@ static di_status setup_geometry(di_ctx *ctx) {
 // distributed context only rows of the local range are candidates.
 static di_status choose_hot_window(di_ctx *ctx) {
   const long long n = ctx->n_rows;
-  ctx->hot_lo = 0;
-  if (n <= kHot || ctx->nnz_local == 0) return DI_OK;
+  ctx->hot_lo = (int)ctx->lo;
+  if (ctx->n_local < kHot) {
+    // one GPU: the window [0, kHot) covers every row; distributed: the window must
+    // lie inside the owned range, so it is disabled (no row matches INT_MIN)
+    ctx->hot_lo = (ctx->world == 1) ? 0 : (-2147483647 - 1);
+    return DI_OK;
+  }
+  if (ctx->nnz_local == 0) return DI_OK;
   const long long nb = (n >> 10) + 1;
   unsigned *blk = nullptr;
   TRY(dalloc(ctx, &blk, (size_t)nb));
@@ -131,20 +137,27 @@ static di_status choose_hot_window(di_ctx *ctx) {
   CK(cudaMemcpyAsync(h.data(), blk, sizeof(unsigned) * nb, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   cudaFree(blk);
-  long long best = 0, best_mass = -1;
+  long long best = ctx->lo >> 10, best_mass = -1;
+  const long long hi = ctx->lo + ctx->n_local;
   for (long long b = 0; b + 1 < nb; ++b) {
+    if ((b << 10) < ctx->lo || (b << 10) + kHot > hi) continue;   // owned rows only
     const long long m = (long long)h[b] + h[b + 1];
     if (m > best_mass) { best_mass = m; best = b; }
   }
-  ctx->hot_lo = (int)std::min<long long>(best << 10, n - kHot);
+  ctx->hot_lo = (int)std::max<long long>(ctx->lo, std::min<long long>(best << 10, hi - kHot));
   return DI_OK;
+}
+
+Graph diter_graph(const di_ctx *ctx) {
+  return Graph{ctx->col_ptr, ctx->row_idx, ctx->vals, ctx->n_local, ctx->d, ctx->hot_lo,
+               ctx->lo, ctx->G, ctx->dflags};
 }
 
 // Capture check_interval passes of (select, scatter, finalize) once.
 static di_status capture_graph(di_ctx *ctx) {
   cudaGraph_t graph;
   CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-  Graph g{ctx->col_ptr, ctx->row_idx, ctx->vals, ctx->n_local, ctx->d, ctx->hot_lo};
+  Graph g = diter_graph(ctx);
   const bool prof = ctx->opt.profile != 0;
   if (prof && ctx->prof_ev.empty()) {
     ctx->prof_ev.assign(4 * ctx->check_interval, nullptr);
@@ -226,7 +239,7 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
   TRY(dalloc(ctx, &d_c, 1));
   CK(cudaMemsetAsync(d_c, 0, sizeof(Census), ctx->stream));
   k_census<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->col_ptr, n, ctx->row_idx, nnz, ctx->vals,
-                                                      ctx->d, d_c);
+                                                      ctx->d, ctx->n_rows, d_c);
   Census hc;
   CK(cudaMemcpyAsync(&hc, d_c, sizeof(Census), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));

@@ -18,6 +18,8 @@
 #include "types.cuh"
 
 namespace diter {
+// internal linkage: each translation unit that launches kernels gets its own copy
+namespace {
 
 // ---------------------------------------------------------------- K1 select --
 // Warp-tiled stream over F: each warp iteration covers 8 words of 32 nodes;
@@ -87,16 +89,32 @@ k_select(double *__restrict__ F, double *__restrict__ H, Frontier fr, long long 
 // millions of pushes per pass costs one RED per CTA instead of one RED per
 // edge serialised at one L2 slice.  Every other row gets a fire-and-forget
 // RED.E.ADD.F64 in L2.
+// On a distributed context rows outside the owned range [lo, lo + n_local) go
+// to the remote outbox G (global ids, RED) and mark their 32-row block dirty
+// (an idempotent byte store), to be compacted and shipped at the exchange
+// (algorithm (*) P:237-246 made exact by outboxing).
 struct Sink {
-  double *F;
+  double *F;            // local fluid, index row - lo
   double *s_hot;
-  int hot_lo;
+  int hot_lo;           // global id of the window start (window lies inside the owned range)
+  long long lo, n_local;
+  double *G;            // remote outbox (global ids) or nullptr
+  unsigned char *dflags;
 };
 
 __device__ __forceinline__ void push(const Sink &s, int row, double v) {
-  const unsigned h = (unsigned)(row - s.hot_lo);
-  if (h < (unsigned)kHot) atomicAdd(s.s_hot + h, v);
-  else red_add(s.F + row, v);
+  const unsigned h = (unsigned)row - (unsigned)s.hot_lo;
+  if (h < (unsigned)kHot) {
+    atomicAdd(s.s_hot + h, v);
+  } else {
+    const long long lr = (long long)row - s.lo;
+    if ((unsigned long long)lr < (unsigned long long)s.n_local) {
+      red_add(s.F + lr, v);
+    } else {
+      red_add(s.G + row, v);
+      s.dflags[row >> 5] = 1;
+    }
+  }
 }
 
 __device__ __forceinline__ int ld_row(const int *p) { return __ldcs(p); }
@@ -208,7 +226,7 @@ k_scatter(Graph g, double *__restrict__ F, Frontier fr, Ctl *ctl, ScPartial *__r
   __shared__ double s_hot[kHot];
   for (int t = threadIdx.x; t < kHot; t += blockDim.x) s_hot[t] = 0.0;
   __syncthreads();
-  const Sink s{F, s_hot, g.hot_lo};
+  const Sink s{F, s_hot, g.hot_lo, g.lo, g.n, g.G, g.dflags};
   const unsigned lane = lane_id();
   const long long warps = (long long)gridDim.x * (kScatterThreads / 32);
   const long long gw = (long long)blockIdx.x * (kScatterThreads / 32) + (threadIdx.x >> 5);
@@ -278,7 +296,7 @@ k_scatter(Graph g, double *__restrict__ F, Frontier fr, Ctl *ctl, ScPartial *__r
   __syncthreads();
   for (int t = threadIdx.x; t < kHot; t += blockDim.x) {
     const double v = s_hot[t];
-    if (v != 0.0) red_add(F + g.hot_lo + t, v);
+    if (v != 0.0) red_add(F + (g.hot_lo - g.lo) + t, v);
   }
   // per-CTA partials
   acc.loss = warp_sum(acc.loss);
@@ -309,7 +327,7 @@ k_scatter_hubs(Graph g, double *__restrict__ F, Frontier fr, const Ctl *ctl) {
   const unsigned long long hp = ctl->hub_packed;
   const unsigned n_hub = (unsigned)(hp >> 32), n_chunks = (unsigned)(hp & 0xffffffffull);
   if (n_chunks == 0u) return;
-  const Sink s{F, nullptr, -2147483647 - 1};   // no hot window: h >= kHot for every row
+  const Sink s{F, nullptr, -2147483647 - 1, g.lo, g.n, g.G, g.dflags};   // no hot window
   for (unsigned c = blockIdx.x; c < n_chunks; c += gridDim.x) {
     unsigned lo = 0, hi = n_hub - 1;
     while (lo < hi) {
@@ -325,40 +343,45 @@ k_scatter_hubs(Graph g, double *__restrict__ F, Frontier fr, const Ctl *ctl) {
 }
 
 // -------------------------------------------------------------- K5 finalize --
-__global__ void __launch_bounds__(kFinalizeThreads)
-k_finalize(Ctl *ctl, const SelPartial *__restrict__ sp, int n_sp, const ScPartial *__restrict__ cp,
-           int n_cp, di_pass_log *log) {
-  if (ctl->done) return;
-  double r = 0.0, loss = 0.0;
-  long long cnt = 0, edges = 0, dang = 0, nlo = 0, nmi = 0, nhu = 0;
-  for (int k = threadIdx.x; k < n_sp; k += blockDim.x) { r += sp[k].r; cnt += sp[k].cnt; }
+// Pass totals as doubles (integers < 2^53 are exact), so a distributed context
+// can all-reduce them in one call: r, loss, |S_p|, E_p, dangling, low, mid, hub.
+constexpr int kSums = 8;
+
+__device__ __forceinline__ void reduce_partials(const SelPartial *__restrict__ sp, int n_sp,
+                                                const ScPartial *__restrict__ cp, int n_cp, double *out) {
+  double v[kSums] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int k = threadIdx.x; k < n_sp; k += blockDim.x) { v[0] += sp[k].r; v[2] += (double)sp[k].cnt; }
   for (int k = threadIdx.x; k < n_cp; k += blockDim.x) {
     const ScPartial p = cp[k];
-    loss += p.loss; edges += p.edges; dang += p.dang; nlo += p.n_low; nmi += p.n_mid; nhu += p.n_hub;
+    v[1] += p.loss; v[3] += (double)p.edges; v[4] += p.dang; v[5] += p.n_low; v[6] += p.n_mid; v[7] += p.n_hub;
   }
-  r = warp_sum(r); loss = warp_sum(loss); cnt = warp_sum(cnt); edges = warp_sum(edges);
-  dang = warp_sum(dang); nlo = warp_sum(nlo); nmi = warp_sum(nmi); nhu = warp_sum(nhu);
   constexpr int W = kFinalizeThreads / 32;
-  __shared__ double s_r[W], s_l[W];
-  __shared__ long long s_i[6][W];
-  const int w = threadIdx.x >> 5;
-  if (lane_id() == 0) {
-    s_r[w] = r; s_l[w] = loss;
-    s_i[0][w] = cnt; s_i[1][w] = edges; s_i[2][w] = dang; s_i[3][w] = nlo; s_i[4][w] = nmi; s_i[5][w] = nhu;
+  __shared__ double s_v[kSums][W];
+#pragma unroll
+  for (int q = 0; q < kSums; ++q) {
+    const double t = warp_sum(v[q]);
+    if (lane_id() == 0) s_v[q][threadIdx.x >> 5] = t;
   }
   __syncthreads();
-  if (threadIdx.x != 0) return;
-  r = 0.0; loss = 0.0; cnt = edges = dang = nlo = nmi = nhu = 0;
-  for (int k = 0; k < W; ++k) {
-    r += s_r[k]; loss += s_l[k];
-    cnt += s_i[0][k]; edges += s_i[1][k]; dang += s_i[2][k]; nlo += s_i[3][k]; nmi += s_i[4][k]; nhu += s_i[5][k];
+  if (threadIdx.x < kSums) {
+    double t = 0.0;
+    for (int k = 0; k < W; ++k) t += s_v[threadIdx.x][k];
+    out[threadIdx.x] = t;
   }
+}
+
+// Thread 0: log the pass, advance T, predict the residual, set the stop flag.
+//   r_{p+1} <= r_p - sum (1 - c_i)|s_i|   (App. A.2; equality up to rounding for
+//   PageRank), so the run can stop after a pass without re-reading F.
+__device__ __forceinline__ void apply_pass(Ctl *ctl, const double *sums, di_pass_log *log) {
+  const double r = sums[0], loss = sums[1];
+  const long long cnt = (long long)sums[2], edges = (long long)sums[3];
   const long long p = ctl->pass;
   const double T = ctl->T;
   if (p < ctl->log_cap) {
     di_pass_log L;
-    L.pass = p; L.T = T; L.r = r; L.frontier = cnt; L.edges = edges; L.dangling = dang;
-    L.bin_low = nlo; L.bin_mid = nmi; L.bin_hub = nhu;
+    L.pass = p; L.T = T; L.r = r; L.frontier = cnt; L.edges = edges; L.dangling = (long long)sums[4];
+    L.bin_low = (long long)sums[5]; L.bin_mid = (long long)sums[6]; L.bin_hub = (long long)sums[7];
     L.t_select_us = 0.0; L.t_scatter_us = 0.0;
     log[p] = L;
   }
@@ -374,6 +397,30 @@ k_finalize(Ctl *ctl, const SelPartial *__restrict__ sp, int n_sp, const ScPartia
   if (r < ctl->target || pred < ctl->target) ctl->done = 1;
   else if (p + 1 >= ctl->max_pass) ctl->done = 2;
   ctl->hub_packed = 0ull;
+}
+
+__global__ void __launch_bounds__(kFinalizeThreads)
+k_finalize(Ctl *ctl, const SelPartial *__restrict__ sp, int n_sp, const ScPartial *__restrict__ cp,
+           int n_cp, di_pass_log *log) {
+  if (ctl->done) return;
+  __shared__ double sums[kSums];
+  reduce_partials(sp, n_sp, cp, n_cp, sums);
+  __syncthreads();
+  if (threadIdx.x == 0) apply_pass(ctl, sums, log);
+}
+
+// Distributed contexts: partial sums to a device buffer (all-reduced by the
+// fabric), then applied by every rank identically.
+__global__ void __launch_bounds__(kFinalizeThreads)
+k_reduce_partials(const Ctl *ctl, const SelPartial *__restrict__ sp, int n_sp,
+                  const ScPartial *__restrict__ cp, int n_cp, double *sums) {
+  if (ctl->done) return;
+  reduce_partials(sp, n_sp, cp, n_cp, sums);
+}
+
+__global__ void k_apply_pass(Ctl *ctl, const double *sums, di_pass_log *log) {
+  if (ctl->done) return;
+  apply_pass(ctl, sums, log);
 }
 
 // --------------------------------------------------- exact residual |F|_1 --
@@ -420,7 +467,7 @@ __global__ void k_init_state(double *F, double *H, const double *b, double b_uni
 }
 
 __global__ void k_census(const long long *col_ptr, long long n, const int *row_idx, long long nnz,
-                         const double *vals, double d, Census *c) {
+                         const double *vals, double d, long long n_rows, Census *c) {
   const long long stride = (long long)gridDim.x * blockDim.x;
   unsigned long long bp = 0, lo = 0, mi = 0, hu = 0, da = 0, bc = 0;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -437,7 +484,7 @@ __global__ void k_census(const long long *col_ptr, long long n, const int *row_i
   unsigned long long br = 0;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += stride) {
     const int r = row_idx[e];
-    if (r < 0 || (long long)r >= n) ++br;
+    if (r < 0 || (long long)r >= n_rows) ++br;
   }
   if (bp) atomicAdd(&c->bad_ptr, bp);
   if (br) atomicAdd(&c->bad_row, br);
@@ -481,4 +528,5 @@ __global__ void k_begin_run(Ctl *ctl, double target, long long max_pass, const d
   ctl->hub_packed = 0ull;
 }
 
+}  // namespace
 }  // namespace diter

@@ -51,12 +51,15 @@ struct ScPartial {
 };
 
 struct Graph {
-  const long long *col_ptr;  // [n+1]
-  const int *row_idx;        // [nnz]
+  const long long *col_ptr;  // [n+1] owned columns, local (starting at 0)
+  const int *row_idx;        // [nnz] GLOBAL row ids
   const double *vals;        // [nnz] or nullptr (PageRank)
-  long long n;
+  long long n;               // owned nodes (n_local)
   double d;
-  int hot_lo;                // first row of the shared-memory hot window
+  int hot_lo;                // global id of the shared-memory hot window start
+  long long lo;              // first owned global id (0 on one GPU)
+  double *G;                 // remote outbox over global ids, or nullptr on one GPU
+  unsigned char *dflags;     // dirty flag per 32-row block of G
 };
 
 // Frontier of one pass: selection bitmap (bit i%32 of word i/32) and the taken

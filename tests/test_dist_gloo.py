@@ -1,0 +1,107 @@
+"""Multi-rank host logic on CPU: world_size 2 over torch.distributed 'gloo'
+(127.0.0.1).  Covers what the N>1 bench path does on the host -- partition
+bounds, CSC sharding, the NCCL unique-id broadcast -- and checks the exchange
+protocol of csrc/dist.cu (SYNC and ASYNC rounds, send rule, termination with
+in-flight mass) with the numpy model in tests/dist_model.py against the oracle.
+"""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _init(rank, world, port):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+
+def _host_logic(rank, world, port):
+    _init(rank, world, port)
+    try:
+        import diter_inputs as gen
+        from paper_1202_6168_b200 import dist as dd
+        cp, ri = gen.web_graph(50_000, 4)
+        for cost in ("out", "inout"):
+            bounds = dd.partition_bounds(cp, world, cost=cost, row_idx=ri)
+            allb = [None] * world
+            dist.all_gather_object(allb, bounds.tolist())
+            assert all(x == allb[0] for x in allb)            # every rank, same ranges
+            shard = dd.shard_csc(cp, ri, None, None, bounds, rank)
+            shards = [None] * world
+            dist.all_gather_object(shards, (shard[0].tolist(), shard[1].tolist()))
+            # the shards reassemble the global CSC exactly
+            cps = [np.asarray(s[0]) for s in shards]
+            re_cp = np.concatenate([cps[0]] + [c[1:] + sum(x[-1] for x in cps[:k]) for k, c in enumerate(cps) if k > 0])
+            np.testing.assert_array_equal(re_cp, cp)
+            np.testing.assert_array_equal(np.concatenate([np.asarray(s[1]) for s in shards]), ri)
+        cid = dd.nccl_comm_id()                               # rank 0 creates, broadcast over gloo
+        ids = [None] * world
+        dist.all_gather_object(ids, cid)
+        assert len(cid) == 128 and all(x == ids[0] for x in ids)
+        lid = dd.loopback_comm_id("k")
+        assert lid[:8] == b"DILOOP01" and len(lid) == 128
+    finally:
+        dist.destroy_process_group()
+
+
+def _protocol(rank, world, port, mode):
+    _init(rank, world, port)
+    try:
+        import diter_inputs as gen
+        import oracle
+        from dist_model import RankModel
+        from paper_1202_6168_b200 import dist as dd
+        n = 4000
+        cp, ri = gen.web_graph(n, 6, window=100, max_deg=300)
+        rng = np.random.default_rng(1)
+        b = rng.random(n) + 0.5
+        b *= 0.15 / b.sum()
+        bounds = dd.partition_bounds(cp, world)
+        lcp, lri, _, lb = dd.shard_csc(cp, ri, None, b, bounds, rank)
+        m = RankModel(rank, world, bounds, lcp, lri, lb, n)
+        target = 1e-10 * 0.15
+        R = m.run_sync(target) if mode == "sync" else m.run_async(target)
+        Hs = [None] * world
+        dist.all_gather_object(Hs, (m.H.tolist(), m.F.tolist(), m.log, m.exchanged))
+        H = np.concatenate([np.asarray(h[0]) for h in Hs])
+        F = np.concatenate([np.asarray(h[1]) for h in Hs])
+        P = oracle.Problem(n, cp, ri, None, b)
+        X = P.solve(1e-14 * 0.15).H
+        assert np.abs(H - X).sum() <= 1e-8 * 0.15
+        deg = np.diff(cp)
+        ledger = np.abs(F).sum() + 0.15 * H.sum() + 0.85 * H[deg == 0].sum()
+        assert abs(ledger - 0.15) <= 1e-13                    # nothing lost in flight
+        assert np.abs(F).sum() < target and R < target
+        assert sum(h[3] for h in Hs) > 0                      # fluid did cross ranks
+        if mode == "sync":
+            st = P.init()
+            P.snapshot(st, target, oracle.HYBRID)
+            assert [(l[1], l[3]) for l in st.log] == [tuple(x) for x in Hs[0][2]]
+    finally:
+        dist.destroy_process_group()
+
+
+def test_host_logic_two_ranks():
+    mp.spawn(_host_logic, args=(2, _free_port()), nprocs=2, join=True)
+
+
+@pytest.mark.parametrize("mode", ["sync", "async"])
+def test_exchange_protocol_two_ranks(mode):
+    mp.spawn(_protocol, args=(2, _free_port(), mode), nprocs=2, join=True)

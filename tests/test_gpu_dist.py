@@ -1,0 +1,99 @@
+"""Distributed path on ONE GPU: K ranks as K host threads of one process, each
+with its own context and stream, over the in-process loopback fabric of
+libditer (csrc/dist.cu).  No kernel waits on another rank -- all waiting is
+host-side -- so this is safe on a single GPU (B200_PROFILING.md).  The same
+kernels, outbox compaction, exchange rounds, merge and termination run as with
+NCCL; only the transport differs.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+import diter_inputs as gen
+import oracle
+import paper_1202_6168_b200 as di
+from paper_1202_6168_b200 import dist
+
+pytestmark = pytest.mark.gpu
+
+
+def run_ranks(K, n, cp, ri, vals, b, d, target, bounds, mode, key, **opts):
+    cid = dist.loopback_comm_id(key)
+    out = [None] * K
+    err = [None] * K
+
+    def worker(r):
+        try:
+            lcp, lri, lv, lb = dist.shard_csc(cp, ri, vals, b, bounds, r)
+            o = di.default_options(exchange_mode=mode, **opts)
+            ctx = di.di_create_dist(r, K, cid, bounds, n, lcp, lri, lv, lb, d, o)
+            di.di_run(ctx, target)
+            out[r] = (di.di_get_history(ctx), di.di_get_fluid(ctx), di.di_get_pass_log(ctx),
+                      di.di_get_stats(ctx), di.di_get_residual(ctx))
+            di.di_destroy(ctx)
+        except Exception as e:          # surfaced below
+            err[r] = e
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(K)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for e in err:
+        if e is not None:
+            raise e
+    H = np.concatenate([o[0] for o in out])
+    F = np.concatenate([o[1] for o in out])
+    return H, F, out
+
+
+@pytest.mark.parametrize("K", [2, 4])
+def test_sync_matches_single_gpu_passes(K):
+    """SYNC mode is the single-GPU snapshot pass: same per-pass frontier sizes,
+    edges and thresholds (random B: no exact-arithmetic ties), same fixed point."""
+    n = 200_000
+    cp, ri = gen.web_graph(n, 5)
+    rng = np.random.default_rng(3)
+    b = rng.random(n) + 0.5
+    b *= 0.15 / b.sum()
+    target = 1e-9 * 0.15
+    H1, _, log1 = di.solve(n, cp, ri, target, b=b)
+    bounds = dist.partition_bounds(cp, K)
+    H, F, outs = run_ranks(K, n, cp, ri, None, b, 0.85, target, bounds, di.DI_EXCHANGE_SYNC, f"sync{K}")
+    for o in outs:        # every rank logs the same global pass records
+        lg = o[2]
+        np.testing.assert_array_equal(lg["frontier"], log1["frontier"])
+        np.testing.assert_array_equal(lg["edges"], log1["edges"])
+        np.testing.assert_array_equal(lg["T"], log1["T"])
+        assert o[3]["exchanges"] > 0 and o[3]["exchanged_bytes"] > 0
+    X = oracle.Problem(n, cp, ri, None, b).solve(1e-12 * 0.15 * 0.15).H
+    assert np.abs(H - X).sum() <= 1e-8 * 0.15
+    assert np.abs(F).sum() < target
+
+
+@pytest.mark.parametrize("K,cost", [(2, "out"), (3, "inout"), (4, "out")])
+def test_async_parity(K, cost):
+    """ASYNC mode (send when s_k > r_k/K, rounds every check_interval passes):
+    parity with the oracle and a closed mass ledger."""
+    p = gen.config("C2", 2, n=300_000)
+    bn = 0.15
+    bounds = dist.partition_bounds(p.col_ptr, K, cost=cost, row_idx=p.row_idx)
+    H, F, outs = run_ranks(K, p.n, p.col_ptr, p.row_idx, None, None, 0.85, p.parity_stop, bounds,
+                           di.DI_EXCHANGE_ASYNC, f"async{K}{cost}", check_interval=4)
+    X = oracle.Problem(p.n, p.col_ptr, p.row_idx).solve(1e-12 * bn * 0.15).H
+    assert np.abs(H - X).sum() <= 1e-8 * bn
+    deg = np.diff(p.col_ptr)
+    ledger = np.abs(F).sum() + 0.15 * H.sum() + 0.85 * H[deg == 0].sum()
+    assert abs(ledger - bn) <= 1e-12 * bn          # no mass lost or duplicated in flight
+    assert all(o[4] < p.parity_stop for o in outs)  # global residual on every rank
+
+
+def test_async_signed():
+    n = 100_000
+    cp, ri, v, b = gen.signed_system(n, 3)
+    bn = np.abs(b).sum()
+    bounds = dist.partition_bounds(cp, 2)
+    H, F, outs = run_ranks(2, n, cp, ri, v, b, 0.9, 5e-10 * bn, bounds, di.DI_EXCHANGE_ASYNC, "signed")
+    X, _ = oracle.Problem(n, cp, ri, v, b, 0.9).jacobi(1e-13 * bn)
+    assert np.abs(H - X).sum() <= 1e-8 * bn
