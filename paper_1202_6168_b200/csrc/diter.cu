@@ -105,10 +105,10 @@ static di_status setup_geometry(di_ctx *ctx) {
   const long long sel_need = (sel_items + kSelectThreads / 32 - 1) / (kSelectThreads / 32);
   ctx->grid_select = (int)std::max(1LL, std::min<long long>(sel_need, (long long)ctx->num_sms * std::max(1, occ_sel)));
   ctx->grid_scatter = ctx->num_sms * std::max(1, ctx->vals ? occ_sc_s : occ_sc);
-  // small graphs: spread the groups of one superword over several warps
+  // superwords per dynamic grab of a scatter CTA: 8 on large graphs (few grabs),
+  // fewer on small ones so every CTA gets work
   const long long n_super = (n_words + kWordsPerSuper - 1) / kWordsPerSuper;
-  const long long sc_warps = (long long)ctx->grid_scatter * (kScatterThreads / 32);
-  ctx->gsplit = (int)std::max(1LL, std::min(32LL, (2 * sc_warps + n_super - 1) / std::max(1LL, n_super)));
+  ctx->spw = (int)std::max(1LL, std::min<long long>(kScatterThreads / 32, n_super / (4LL * ctx->grid_scatter)));
   ctx->grid_l1 = (int)std::min<long long>(ctx->num_sms * 8LL,
                                           std::max(1LL, (ctx->n_local + 255) / 256));
   return DI_OK;
@@ -169,9 +169,9 @@ static di_status capture_graph(di_ctx *ctx) {
                                                                   ctx->ctl, ctx->sel_part);
     if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 1], ctx->stream, cudaEventRecordExternal));
     if (ctx->vals)
-      k_scatter<true><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part, ctx->gsplit);
+      k_scatter<true><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part, ctx->spw);
     else
-      k_scatter<false><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part, ctx->gsplit);
+      k_scatter<false><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part, ctx->spw);
     if (ctx->cap_hub > 0) {
       if (ctx->vals)
         k_scatter_hubs<true><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);

@@ -221,35 +221,60 @@ struct ScAcc {
 // 0 for a dangling column) and the frontier census go to per-CTA partials.
 template <bool SIGNED>
 __global__ void __launch_bounds__(kScatterThreads)
-k_scatter(Graph g, double *__restrict__ F, Frontier fr, Ctl *ctl, ScPartial *__restrict__ part, int gsplit) {
+k_scatter(Graph g, double *__restrict__ F, Frontier fr, Ctl *ctl, ScPartial *__restrict__ part, int spw) {
   if (ctl->done) return;
   __shared__ double s_hot[kHot];
   for (int t = threadIdx.x; t < kHot; t += blockDim.x) s_hot[t] = 0.0;
   __syncthreads();
   const Sink s{F, s_hot, g.hot_lo, g.lo, g.n, g.G, g.dflags};
   const unsigned lane = lane_id();
-  const long long warps = (long long)gridDim.x * (kScatterThreads / 32);
-  const long long gw = (long long)blockIdx.x * (kScatterThreads / 32) + (threadIdx.x >> 5);
   const long long n_super = (fr.n_words + kWordsPerSuper - 1) / kWordsPerSuper;
   ScAcc acc;
-  // work item = (superword, group residue): with gsplit > 1 (small graphs) the
-  // groups of one superword spread over gsplit warps
-  const long long n_items = n_super * gsplit;
-  for (long long it = gw; it < n_items; it += warps) {
-    const long long sw = it / gsplit;
-    const int gi = (int)(it - sw * gsplit);
-    const long long wi = sw * kWordsPerSuper + lane;
-    const unsigned word = (wi < fr.n_words) ? fr.bits[wi] : 0u;
-    const int c = __popc(word);
-    int incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if ((int)lane >= o) incl += t;
+  // Dynamic load balance: the CTA grabs kChunkSW consecutive superwords at a
+  // time (one atomic per grab), its 8 warps count their groups, then take the
+  // chunk's groups round-robin.  Frontier density is very uneven across ids
+  // (the Zipf-over-id hot nodes keep their fluid longest), so a static split
+  // would leave most warps idle behind the dense superwords.
+  constexpr int kChunkSW = kScatterThreads / 32;
+  __shared__ unsigned s_chunk;
+  __shared__ int s_off[kChunkSW + 1];
+  const int warp = threadIdx.x >> 5;
+  const long long n_chunks = (n_super + spw - 1) / spw;   // spw <= kChunkSW superwords per grab
+  for (;;) {
+    if (threadIdx.x == 0) s_chunk = atomicAdd(&ctl->sc_next, 1u);
+    __syncthreads();
+    const long long ch = s_chunk;
+    if (ch >= n_chunks) break;
+    {
+      const long long sw = ch * spw + warp;
+      const long long wi = sw * kWordsPerSuper + lane;
+      const unsigned word = (warp < spw && sw < n_super && wi < fr.n_words) ? fr.bits[wi] : 0u;
+      const int tot = warp_sum(__popc(word));
+      if (lane == 0) s_off[warp + 1] = (tot + 31) >> 5;
     }
-    const int excl = incl - c;
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    for (int g0 = 32 * gi; g0 < total; g0 += 32 * gsplit) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_off[0] = 0;
+      for (int j = 1; j <= kChunkSW; ++j) s_off[j] += s_off[j - 1];
+    }
+    __syncthreads();
+    const int n_items = s_off[kChunkSW];
+    for (int k = warp; k < n_items; k += kChunkSW) {
+      int j = 0;
+      while (j + 1 < kChunkSW && s_off[j + 1] <= k) ++j;
+      const long long sw = ch * spw + j;
+      const int g0 = 32 * (k - s_off[j]);
+      const long long wi = sw * kWordsPerSuper + lane;
+      const unsigned word = (wi < fr.n_words) ? fr.bits[wi] : 0u;
+      const int c = __popc(word);
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((int)lane >= o) incl += t;
+      }
+      const int excl = incl - c;
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
       const int rank = g0 + (int)lane;
       int lo = 0;
 #pragma unroll
@@ -291,6 +316,7 @@ k_scatter(Graph g, double *__restrict__ F, Frontier fr, Ctl *ctl, ScPartial *__r
       }
       push_group<SIGNED>(g, s, b0, deg_eff, w);
     }
+    __syncthreads();   // s_chunk / s_off are rewritten by the next grab
   }
   // flush the hot window: one RED per touched row per CTA
   __syncthreads();
@@ -397,6 +423,7 @@ __device__ __forceinline__ void apply_pass(Ctl *ctl, const double *sums, di_pass
   if (r < ctl->target || pred < ctl->target) ctl->done = 1;
   else if (p + 1 >= ctl->max_pass) ctl->done = 2;
   ctl->hub_packed = 0ull;
+  ctl->sc_next = 0u;
 }
 
 __global__ void __launch_bounds__(kFinalizeThreads)
@@ -526,6 +553,7 @@ __global__ void k_begin_run(Ctl *ctl, double target, long long max_pass, const d
   ctl->r_pred = *r_exact;
   ctl->done = 0;
   ctl->hub_packed = 0ull;
+  ctl->sc_next = 0u;
 }
 
 }  // namespace

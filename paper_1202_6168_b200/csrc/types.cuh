@@ -35,6 +35,8 @@ struct Ctl {
   int policy;          // DI_POLICY_*
   unsigned long long hub_packed;  // (hub slots << 32) | hub chunks; reset by k_finalize
   long long log_cap;
+  unsigned sc_next;    // next superword chunk for the scatter's dynamic schedule (reset per pass)
+  int _pad;
 };
 
 // k_select partials (one per CTA): r_p and |S_p|.
