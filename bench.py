@@ -196,13 +196,16 @@ def measured_peaks():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(config):
-    """dram bytes per k_scatter launch from the committed ncu --set full capture."""
+def ncu_traffic(config, alg_bytes_per_launch):
+    """DRAM bytes (read + write) per k_scatter launch, from the committed ncu --set full
+    capture of one launch (profiles/ncu_traffic.json), scaled to the average launch by
+    that launch's traffic / algorithmic-bytes ratio.  None if not captured."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get(config, {}).get("k_scatter_dram_bytes_per_launch")
+        ratio = d[config]["traffic_over_algorithmic"]
+        return ratio * alg_bytes_per_launch
     except Exception:
         return None
 
@@ -328,7 +331,7 @@ def run_ours(args, rank, world, local_rank):
     peak, peak_kind = measured_peaks()
     scat_gbs = tot["scatter_bytes"] / (tot["kt_scatter_ms"] / 1e3) / 1e9
     n_launch = tot["passes"]                       # executed k_scatter launches
-    traffic = ncu_traffic(args.config)
+    traffic = ncu_traffic(args.config, tot["scatter_bytes"] / max(1, n_launch))
     kt_sum = tot["kt_scatter_ms"] + tot["kt_select_ms"] + tot["kt_finalize_ms"]
     roofline = {"bound": "hbm", "achieved": scat_gbs, "peak": peak, "unit": "GB/s",
                 "frac": scat_gbs / peak, "traffic": traffic,
