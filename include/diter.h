@@ -84,7 +84,12 @@ typedef struct {
   int32_t scatter_kernel;  /* 0 = degree-binned (default); reserved for variants */
   int32_t profile;         /* 1: time each kernel of each executed pass with CUDA events
                               recorded inside the captured graph (di_stats.kt_*); default 0 */
-  int32_t reserved[6];
+  int32_t pass_kernel;     /* 0 = auto (fused below 16M owned nodes), 1 = one kernel per phase in a
+                              captured CUDA graph, 2 = one cooperative persistent kernel per
+                              check_interval passes (grid barriers between phases); 1-GPU only */
+  int32_t hot_window;      /* 0 = stage the 2048 rows of largest in-degree in shared memory (default),
+                              -1 = off (every push is an L2 RED) */
+  int32_t reserved[4];
 } di_options;
 
 /* One record per executed pass (device-logged, read with di_get_pass_log). */

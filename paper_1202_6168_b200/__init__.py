@@ -49,7 +49,8 @@ class di_options(ctypes.Structure):
                 ("t0", ctypes.c_double), ("max_passes", ctypes.c_int64),
                 ("exchange_mode", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("scatter_kernel", ctypes.c_int32), ("profile", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 6)]
+                ("pass_kernel", ctypes.c_int32), ("hot_window", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 4)]
 
 
 class di_pass_log(ctypes.Structure):

@@ -55,6 +55,7 @@ extern "C" void di_default_options(di_options *o) {
   o->device = -1;
   o->scatter_kernel = 0;
   o->profile = 0;
+  o->pass_kernel = 0;
 }
 
 template <typename T>
@@ -108,7 +109,21 @@ static di_status setup_geometry(di_ctx *ctx) {
   // superwords per dynamic grab of a scatter CTA: 8 on large graphs (few grabs),
   // fewer on small ones so every CTA gets work
   const long long n_super = (n_words + kWordsPerSuper - 1) / kWordsPerSuper;
-  ctx->spw = (int)std::max(1LL, std::min<long long>(kScatterThreads / 32, n_super / (4LL * ctx->grid_scatter)));
+  ctx->spw = (int)std::max(1LL, std::min<long long>(kScatterThreads / 32, (4 * n_super) / (4LL * ctx->grid_scatter)));
+  // fused cooperative pass kernel: all CTAs co-resident
+  int occ_f = 0;
+  if (ctx->vals) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, k_pass_fused<true>, kScatterThreads, 0));
+  else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, k_pass_fused<false>, kScatterThreads, 0));
+  ctx->grid_fused = ctx->num_sms * std::max(1, occ_f);
+  const int pk = ctx->opt.pass_kernel;
+  ctx->fused = ctx->world == 1 && (pk == 2 || (pk == 0 && ctx->n_local <= (16LL << 20)));
+  if (ctx->fused) {
+    // the fused kernel reuses the per-CTA partial arrays with its own grid
+    ctx->grid_select = std::max(ctx->grid_select, ctx->grid_fused);
+    ctx->grid_scatter = std::max(ctx->grid_scatter, ctx->grid_fused);
+    const long long nsup = (n_words + kWordsPerSuper - 1) / kWordsPerSuper;
+    ctx->spw = (int)std::max(1LL, std::min<long long>(kScatterThreads / 32, (4 * nsup) / (4LL * ctx->grid_fused)));
+  }
   ctx->grid_l1 = (int)std::min<long long>(ctx->num_sms * 8LL,
                                           std::max(1LL, (ctx->n_local + 255) / 256));
   return DI_OK;
@@ -120,6 +135,10 @@ static di_status setup_geometry(di_ctx *ctx) {
 static di_status choose_hot_window(di_ctx *ctx) {
   const long long n = ctx->n_rows;
   ctx->hot_lo = (int)ctx->lo;
+  if (ctx->opt.hot_window < 0) {           // disabled: no row matches INT_MIN
+    ctx->hot_lo = -2147483647 - 1;
+    return DI_OK;
+  }
   if (ctx->n_local < kHot) {
     // one GPU: the window [0, kHot) covers every row; distributed: the window must
     // lie inside the owned range, so it is disabled (no row matches INT_MIN)
@@ -376,8 +395,31 @@ extern "C" di_status di_run(di_ctx *ctx, double target) {
     ctx->residual = h->r_pred;
     if (h->r_pred < target) break;                       // converged (exact |F|_1)
     if (h->pass >= max_pass_abs) { st = DI_ERR_NOT_CONVERGED; break; }
+    // fused: one cooperative kernel runs up to 4 x check_interval passes per launch
+    if (ctx->fused) {
+      Graph g = diter_graph(ctx);
+      int has_hubs = ctx->cap_hub > 0 ? 1 : 0, max_p = 4 * ctx->check_interval;
+      void *args[] = {&g, &ctx->F, &ctx->H, &ctx->fr, &ctx->ctl, &ctx->sel_part, &ctx->sc_part,
+                      &ctx->log, &ctx->spw, &has_hubs, &max_p};
+      for (;;) {
+        const long long pass_before = h->pass;
+        if (ctx->vals)
+          CK(cudaLaunchCooperativeKernel((void *)k_pass_fused<true>, ctx->grid_fused, kScatterThreads, args, 0,
+                                         ctx->stream));
+        else
+          CK(cudaLaunchCooperativeKernel((void *)k_pass_fused<false>, ctx->grid_fused, kScatterThreads, args, 0,
+                                         ctx->stream));
+        ctx->kernel_launches += 1;
+        ctx->graph_launches += 1;
+        TRY(read_ctl(ctx));
+        ctx->kt_passes += h->pass - pass_before;
+        ctx->kt_ms[0] = h->t_sel_us * 1e-3;
+        ctx->kt_ms[1] = h->t_sc_us * 1e-3;
+        if (h->done) break;
+      }
+    }
     // graph launches until the device sets done
-    for (;;) {
+    for (; !ctx->fused;) {
       const long long pass_before = h->pass;
       CK(cudaGraphLaunch(ctx->graph_exec, ctx->stream));
       ctx->graph_launches += 1;

@@ -14,8 +14,12 @@
 // captured graph of m passes can overrun convergence at the cost of empty launches.
 #pragma once
 #include "../../include/diter.h"
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "types.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace diter {
 // internal linkage: each translation unit that launches kernels gets its own copy
@@ -30,11 +34,8 @@ namespace {
 // H_i += s_i (fire-and-forget RED, one writer per pass), S[i] = s_i, and its bit
 // is set in the word written by lane k.  Per-CTA partials (r_p, |S_p|) in a
 // fixed order make r_p deterministic for given F bytes.
-__global__ void __launch_bounds__(kSelectThreads, 6)
-k_select(double *__restrict__ F, double *__restrict__ H, Frontier fr, long long n, const Ctl *ctl,
-         SelPartial *__restrict__ part) {
-  if (ctl->done) return;
-  const double T = ctl->T;
+__device__ __forceinline__ void select_body(double *__restrict__ F, double *__restrict__ H, const Frontier &fr,
+                                            long long n, const double T, SelPartial *__restrict__ part) {
   const unsigned lane = lane_id();
   const long long warps = (long long)gridDim.x * (kSelectThreads / 32);
   const long long gw = (long long)blockIdx.x * (kSelectThreads / 32) + (threadIdx.x >> 5);
@@ -79,6 +80,13 @@ k_select(double *__restrict__ F, double *__restrict__ H, Frontier fr, long long 
     for (int k = 0; k < kSelectThreads / 32; ++k) { p.r += s_r[k]; p.cnt += s_c[k]; }
     part[blockIdx.x] = p;
   }
+}
+
+__global__ void __launch_bounds__(kSelectThreads, 6)
+k_select(double *__restrict__ F, double *__restrict__ H, Frontier fr, long long n, const Ctl *ctl,
+         SelPartial *__restrict__ part) {
+  if (ctl->done) return;
+  select_body(F, H, fr, n, ctl->T, part);
 }
 
 // ------------------------------------------------------------ K2-K4 scatter --
@@ -220,50 +228,57 @@ struct ScAcc {
 // k_scatter_hubs.  The guaranteed |F|_1 drop sum (1 - c_i)|s_i| (App. A.2: c_i = d,
 // 0 for a dangling column) and the frontier census go to per-CTA partials.
 template <bool SIGNED>
-__global__ void __launch_bounds__(kScatterThreads)
-k_scatter(Graph g, double *__restrict__ F, Frontier fr, Ctl *ctl, ScPartial *__restrict__ part, int spw) {
-  if (ctl->done) return;
-  __shared__ double s_hot[kHot];
+__device__ __forceinline__ void scatter_body(const Graph &g, double *__restrict__ F, const Frontier &fr, Ctl *ctl,
+                                             ScPartial *__restrict__ part, int spw, double *s_hot) {
   for (int t = threadIdx.x; t < kHot; t += blockDim.x) s_hot[t] = 0.0;
   __syncthreads();
   const Sink s{F, s_hot, g.hot_lo, g.lo, g.n, g.G, g.dflags};
   const unsigned lane = lane_id();
   const long long n_super = (fr.n_words + kWordsPerSuper - 1) / kWordsPerSuper;
   ScAcc acc;
-  // Dynamic load balance: the CTA grabs kChunkSW consecutive superwords at a
-  // time (one atomic per grab), its 8 warps count their groups, then take the
-  // chunk's groups round-robin.  Frontier density is very uneven across ids
-  // (the Zipf-over-id hot nodes keep their fluid longest), so a static split
-  // would leave most warps idle behind the dense superwords.
-  constexpr int kChunkSW = kScatterThreads / 32;
+  // Dynamic load balance.  Work item = a quarter of a superword: groups
+  // [8q, 8q+8) of superword sw (at most one group per warp), so a dense superword
+  // (up to 32 groups) spreads over four grabs instead of pinning one CTA while
+  // the rest wait at the next barrier.  A CTA grabs `spw` consecutive items per
+  // atomic, its warps count the items' groups, then take them round-robin.  The
+  // frontier density is very uneven across ids (the Zipf-over-id hot nodes keep
+  // their fluid longest), so a static split would leave most warps idle.
+  constexpr int kItemsMax = kScatterThreads / 32;
+  constexpr int kQuarters = 4;
   __shared__ unsigned s_chunk;
-  __shared__ int s_off[kChunkSW + 1];
+  __shared__ int s_off[kItemsMax + 1];
   const int warp = threadIdx.x >> 5;
-  const long long n_chunks = (n_super + spw - 1) / spw;   // spw <= kChunkSW superwords per grab
+  const long long n_items_all = n_super * kQuarters;
+  const long long n_chunks = (n_items_all + spw - 1) / spw;   // spw <= kItemsMax items per grab
   for (;;) {
     if (threadIdx.x == 0) s_chunk = atomicAdd(&ctl->sc_next, 1u);
     __syncthreads();
     const long long ch = s_chunk;
     if (ch >= n_chunks) break;
     {
-      const long long sw = ch * spw + warp;
+      const long long item = ch * spw + warp;
+      const long long sw = item / kQuarters;
+      const int q = (int)(item - sw * kQuarters);
       const long long wi = sw * kWordsPerSuper + lane;
-      const unsigned word = (warp < spw && sw < n_super && wi < fr.n_words) ? fr.bits[wi] : 0u;
+      const unsigned word = (warp < spw && item < n_items_all && wi < fr.n_words) ? fr.bits[wi] : 0u;
       const int tot = warp_sum(__popc(word));
-      if (lane == 0) s_off[warp + 1] = (tot + 31) >> 5;
+      const int groups = (tot + 31) >> 5;
+      if (lane == 0) s_off[warp + 1] = max(0, min(8, groups - 8 * q));
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       s_off[0] = 0;
-      for (int j = 1; j <= kChunkSW; ++j) s_off[j] += s_off[j - 1];
+      for (int j = 1; j <= kItemsMax; ++j) s_off[j] += s_off[j - 1];
     }
     __syncthreads();
-    const int n_items = s_off[kChunkSW];
-    for (int k = warp; k < n_items; k += kChunkSW) {
+    const int n_items = s_off[kItemsMax];
+    for (int k = warp; k < n_items; k += kItemsMax) {
       int j = 0;
-      while (j + 1 < kChunkSW && s_off[j + 1] <= k) ++j;
-      const long long sw = ch * spw + j;
-      const int g0 = 32 * (k - s_off[j]);
+      while (j + 1 < kItemsMax && s_off[j + 1] <= k) ++j;
+      const long long item = ch * spw + j;
+      const long long sw = item / kQuarters;
+      const int q = (int)(item - sw * kQuarters);
+      const int g0 = 32 * (8 * q + (k - s_off[j]));
       const long long wi = sw * kWordsPerSuper + lane;
       const unsigned word = (wi < fr.n_words) ? fr.bits[wi] : 0u;
       const int c = __popc(word);
@@ -344,13 +359,19 @@ k_scatter(Graph g, double *__restrict__ F, Frontier fr, Ctl *ctl, ScPartial *__r
   }
 }
 
+template <bool SIGNED>
+__global__ void __launch_bounds__(kScatterThreads)
+k_scatter(Graph g, double *__restrict__ F, Frontier fr, Ctl *ctl, ScPartial *__restrict__ part, int spw) {
+  if (ctl->done) return;
+  __shared__ double s_hot[kHot];
+  scatter_body<SIGNED>(g, F, fr, ctl, part, spw, s_hot);
+}
+
 // Hub columns (> kMidMax edges), one CTA per 2048-edge chunk (chunks of a hub
 // spread over CTAs; int4 row loads, two in flight per thread).
 template <bool SIGNED>
-__global__ void __launch_bounds__(kScatterThreads)
-k_scatter_hubs(Graph g, double *__restrict__ F, Frontier fr, const Ctl *ctl) {
-  if (ctl->done) return;
-  const unsigned long long hp = ctl->hub_packed;
+__device__ __forceinline__ void hubs_body(const Graph &g, double *__restrict__ F, const Frontier &fr, const Ctl *ctl) {
+  const unsigned long long hp = *(volatile const unsigned long long *)&ctl->hub_packed;
   const unsigned n_hub = (unsigned)(hp >> 32), n_chunks = (unsigned)(hp & 0xffffffffull);
   if (n_chunks == 0u) return;
   const Sink s{F, nullptr, -2147483647 - 1, g.lo, g.n, g.G, g.dflags};   // no hot window
@@ -366,6 +387,13 @@ k_scatter_hubs(Graph g, double *__restrict__ F, Frontier fr, const Ctl *ctl) {
     const long long end = min(beg + (long long)kHubChunk, ce);
     push_range<SIGNED>(g, s, beg, end, w, threadIdx.x, blockDim.x);
   }
+}
+
+template <bool SIGNED>
+__global__ void __launch_bounds__(kScatterThreads)
+k_scatter_hubs(Graph g, double *__restrict__ F, Frontier fr, const Ctl *ctl) {
+  if (ctl->done) return;
+  hubs_body<SIGNED>(g, F, fr, ctl);
 }
 
 // -------------------------------------------------------------- K5 finalize --
@@ -448,6 +476,56 @@ k_reduce_partials(const Ctl *ctl, const SelPartial *__restrict__ sp, int n_sp,
 __global__ void k_apply_pass(Ctl *ctl, const double *sums, di_pass_log *log) {
   if (ctl->done) return;
   apply_pass(ctl, sums, log);
+}
+
+// ------------------------------------------------- fused persistent pass loop --
+// Small graphs are launch- and latency-bound (C2: ~1e6 nodes, ~0.8e6 edges per
+// pass): one cooperative kernel runs up to max_passes passes with grid-wide
+// barriers between the phases instead of 3-4 launches per pass.  Same phase code
+// (select_body / scatter_body / hubs_body / reduce_partials + apply_pass) as the
+// per-kernel path; phase times come from %globaltimer read by CTA 0.
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <bool SIGNED>
+__global__ void __launch_bounds__(kScatterThreads)
+k_pass_fused(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ctl *ctl,
+             SelPartial *__restrict__ sp, ScPartial *__restrict__ cp, di_pass_log *log, int spw,
+             int has_hubs, int max_passes) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double s_hot[kHot];
+  __shared__ double sums[kSums];
+  for (int k = 0; k < max_passes; ++k) {
+    if (*(volatile int *)&ctl->done) break;          // written by CTA 0 before the last barrier
+    unsigned long long t0 = 0, t1 = 0, t2 = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) t0 = globaltimer_ns();
+    select_body(F, H, fr, g.n, *(volatile double *)&ctl->T, sp);
+    grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) t1 = globaltimer_ns();
+    scatter_body<SIGNED>(g, F, fr, ctl, cp, spw, s_hot);
+    grid.sync();
+    if (has_hubs) {
+      hubs_body<SIGNED>(g, F, fr, ctl);
+      grid.sync();
+    }
+    if (blockIdx.x == 0) {
+      if (threadIdx.x == 0) t2 = globaltimer_ns();
+      reduce_partials(sp, gridDim.x, cp, gridDim.x, sums);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const long long p = ctl->pass;
+        apply_pass(ctl, sums, log);
+        const double us_sel = (double)(t1 - t0) * 1e-3, us_sc = (double)(t2 - t1) * 1e-3;
+        if (p < ctl->log_cap) { log[p].t_select_us = us_sel; log[p].t_scatter_us = us_sc; }
+        ctl->t_sel_us += us_sel;
+        ctl->t_sc_us += us_sc;
+      }
+    }
+    grid.sync();
+  }
 }
 
 // --------------------------------------------------- exact residual |F|_1 --

@@ -37,6 +37,8 @@ struct Ctl {
   long long log_cap;
   unsigned sc_next;    // next superword chunk for the scatter's dynamic schedule (reset per pass)
   int _pad;
+  double t_sel_us;     // fused kernel: accumulated select / scatter phase time (%globaltimer)
+  double t_sc_us;
 };
 
 // k_select partials (one per CTA): r_p and |S_p|.

@@ -11,7 +11,7 @@ ap.add_argument("--max-passes", type=int, default=40)
 ap.add_argument("--policy", default="hybrid")
 a = ap.parse_args()
 p = gen.config(a.config, 1, n=a.n)
-opts = di.default_options(max_passes=a.max_passes, check_interval=8,
+opts = di.default_options(max_passes=a.max_passes, check_interval=8, pass_kernel=1,
                           policy=di.DI_POLICY_GEOM if a.policy == "geom" else di.DI_POLICY_HYBRID)
 ctx = di.di_create(p.n, p.col_ptr, p.row_idx, p.values, p.b, p.d, opts)
 t = time.perf_counter()
