@@ -81,15 +81,19 @@ typedef struct {
   int64_t max_passes;      /* guard -> DI_ERR_NOT_CONVERGED; default 1000000 */
   int32_t exchange_mode;   /* DI_EXCHANGE_*; distributed only; default ASYNC */
   int32_t device;          /* CUDA device ordinal; -1 = current device (default) */
-  int32_t scatter_kernel;  /* 0 = degree-binned (default); reserved for variants */
+  int32_t scatter_kernel;  /* scatter schedule over frontier groups (32 selected nodes): 0 = dynamic
+                              runs grabbed per warp in ascending order (default), 1 = static CTA
+                              tiles + dynamic tail, 2 = static warp interleave + dynamic tail */
   int32_t profile;         /* 1: time each kernel of each executed pass with CUDA events
                               recorded inside the captured graph (di_stats.kt_*); default 0 */
-  int32_t pass_kernel;     /* 0 = auto (fused below 16M owned nodes), 1 = one kernel per phase in a
-                              captured CUDA graph, 2 = one cooperative persistent kernel per
-                              check_interval passes (grid barriers between phases); 1-GPU only */
+  int32_t pass_kernel;     /* 0 = auto (= 1), 1 = one kernel per phase, check_interval passes per captured
+                              CUDA graph, 2 = one cooperative persistent kernel per 4 x check_interval
+                              passes (grid barriers between phases; 1-GPU only) */
   int32_t hot_window;      /* 0 = stage the 2048 rows of largest in-degree in shared memory (default),
                               -1 = off (every push is an L2 RED) */
-  int32_t reserved[4];
+  int32_t scatter_run;     /* groups per dynamic grab of schedule 0; 0 = default (2) */
+  int32_t scatter_stripes; /* ticket stripes of the dynamic schedule, 1..32; 0 = default (8) */
+  int32_t reserved[2];
 } di_options;
 
 /* One record per executed pass (device-logged, read with di_get_pass_log). */

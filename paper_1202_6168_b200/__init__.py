@@ -50,7 +50,8 @@ class di_options(ctypes.Structure):
                 ("exchange_mode", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("scatter_kernel", ctypes.c_int32), ("profile", ctypes.c_int32),
                 ("pass_kernel", ctypes.c_int32), ("hot_window", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 4)]
+                ("scatter_run", ctypes.c_int32), ("scatter_stripes", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 2)]
 
 
 class di_pass_log(ctypes.Structure):

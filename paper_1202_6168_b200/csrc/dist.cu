@@ -308,7 +308,7 @@ __global__ void k_set_target(Ctl *ctl, double target, long long max_pass, int do
   ctl->max_pass = max_pass;
   ctl->done = done;
   ctl->hub_packed = 0ull;
-  ctl->sc_next = 0u;
+  reset_tickets(ctl);
 }
 
 // ------------------------------------------------------------ host helpers --
@@ -413,11 +413,11 @@ static void launch_pass_kernels(di_ctx *ctx) {
   k_select<<<ctx->grid_select, kSelectThreads, 0, ctx->stream>>>(ctx->F, ctx->H, ctx->fr, ctx->n_local, ctx->ctl,
                                                                 ctx->sel_part);
   if (ctx->vals)
-    k_scatter<true><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl,
-                                                                            ctx->sc_part, ctx->spw);
+    k_scatter<true><<<ctx->grid_scatter, kScatterThreads, ctx->scatter_smem, ctx->stream>>>(
+        g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part);
   else
-    k_scatter<false><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl,
-                                                                             ctx->sc_part, ctx->spw);
+    k_scatter<false><<<ctx->grid_scatter, kScatterThreads, ctx->scatter_smem, ctx->stream>>>(
+        g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part);
   if (ctx->cap_hub > 0) {
     if (ctx->vals)
       k_scatter_hubs<true><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);

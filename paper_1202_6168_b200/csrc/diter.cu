@@ -78,7 +78,7 @@ static void free_ctx(di_ctx *c) {
   if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
   for (cudaEvent_t e : c->prof_ev)
     if (e) cudaEventDestroy(e);
-  void *ptrs[] = {c->col_ptr, c->row_idx, c->vals, c->d_b, c->F, c->H, c->fr.bits, c->fr.S,
+  void *ptrs[] = {c->col_ptr, c->row_idx, c->vals, c->d_b, c->F, c->H, c->fr.ids, c->fr.S, c->fr.seg_cnt,
                   c->fr.hub_w, c->fr.hub_b0, c->fr.hub_deg, c->fr.hub_chunk, c->sel_part, c->sc_part,
                   c->l1_part, c->l1_out, c->ctl, c->log};
   for (void *p : ptrs)
@@ -91,41 +91,47 @@ static void free_ctx(di_ctx *c) {
   delete c;
 }
 
-// Launch geometry: grid-stride kernels sized to the SM count x resident CTAs.
+// Launch geometry: persistent kernels sized to the SM count x resident CTAs.
+// The select grid fixes the frontier segmentation: n_seg = CTAs x 8 warps, each
+// warp owning seg_len consecutive nodes (a multiple of 256); the scatter keeps
+// the prefix over segments in (n_seg + 1) ints of dynamic shared memory.
 static di_status setup_geometry(di_ctx *ctx) {
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, ctx->device));
   ctx->num_sms = prop.multiProcessorCount;
-  int occ_sel = 0, occ_sc = 0, occ_sc_s = 0;
+  const long long n = ctx->n_local;
+  constexpr int kWarps = kSelectThreads / 32;
+  int occ_sel = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sel, k_select, kSelectThreads, 0));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sc, k_scatter<false>, kScatterThreads, 0));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sc_s, k_scatter<true>, kScatterThreads, 0));
-  // persistent grids: SM count x resident CTAs, never more CTAs than work items
-  const long long n_words = (ctx->n_local + 31) / 32;
-  const long long sel_items = (n_words + kSelectItems - 1) / kSelectItems;           // warp iterations
-  const long long sel_need = (sel_items + kSelectThreads / 32 - 1) / (kSelectThreads / 32);
-  ctx->grid_select = (int)std::max(1LL, std::min<long long>(sel_need, (long long)ctx->num_sms * std::max(1, occ_sel)));
-  ctx->grid_scatter = ctx->num_sms * std::max(1, ctx->vals ? occ_sc_s : occ_sc);
-  // superwords per dynamic grab of a scatter CTA: 8 on large graphs (few grabs),
-  // fewer on small ones so every CTA gets work
-  const long long n_super = (n_words + kWordsPerSuper - 1) / kWordsPerSuper;
-  ctx->spw = (int)std::max(1LL, std::min<long long>(kScatterThreads / 32, (4 * n_super) / (4LL * ctx->grid_scatter)));
-  // fused cooperative pass kernel: all CTAs co-resident
-  int occ_f = 0;
-  if (ctx->vals) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, k_pass_fused<true>, kScatterThreads, 0));
-  else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, k_pass_fused<false>, kScatterThreads, 0));
-  ctx->grid_fused = ctx->num_sms * std::max(1, occ_f);
+  const long long spans = (n + kSelectSpan - 1) / kSelectSpan;             // 256-node warp iterations
+  const long long sel_need = (spans + kWarps - 1) / kWarps;
+  long long gs = std::min<long long>(sel_need, (long long)ctx->num_sms * std::max(1, std::min(occ_sel, kSelectCtasPerSm)));
+  gs = std::max(1LL, std::min<long long>(gs, kMaxSegments / kWarps));
+  // fused cooperative pass kernel (small graphs, one GPU): every CTA co-resident, and the
+  // select phase runs on the fused grid, so the segmentation follows that grid
   const int pk = ctx->opt.pass_kernel;
-  ctx->fused = ctx->world == 1 && (pk == 2 || (pk == 0 && ctx->n_local <= (16LL << 20)));
+  ctx->fused = ctx->world == 1 && pk == 2;
   if (ctx->fused) {
-    // the fused kernel reuses the per-CTA partial arrays with its own grid
-    ctx->grid_select = std::max(ctx->grid_select, ctx->grid_fused);
-    ctx->grid_scatter = std::max(ctx->grid_scatter, ctx->grid_fused);
-    const long long nsup = (n_words + kWordsPerSuper - 1) / kWordsPerSuper;
-    ctx->spw = (int)std::max(1LL, std::min<long long>(kScatterThreads / 32, (4 * nsup) / (4LL * ctx->grid_fused)));
+    const size_t dyn = sizeof(int) * (size_t)(std::min(ctx->num_sms * 4 * kWarps, kMaxSegments) + 1);
+    int occ_f = 0;
+    if (ctx->vals) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, k_pass_fused<true>, kScatterThreads, dyn));
+    else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, k_pass_fused<false>, kScatterThreads, dyn));
+    ctx->grid_fused = ctx->num_sms * std::max(1, std::min(occ_f, 4));
+    gs = std::min<long long>(ctx->grid_fused, kMaxSegments / kWarps);
   }
-  ctx->grid_l1 = (int)std::min<long long>(ctx->num_sms * 8LL,
-                                          std::max(1LL, (ctx->n_local + 255) / 256));
+  ctx->grid_select = (int)gs;
+  ctx->fr.n_seg = (int)gs * kWarps;
+  const long long per = (n + ctx->fr.n_seg - 1) / ctx->fr.n_seg;
+  ctx->fr.seg_len = std::max<long long>(kSelectSpan, (per + kSelectSpan - 1) / kSelectSpan * kSelectSpan);
+  ctx->scatter_smem = sizeof(int) * (size_t)(ctx->fr.n_seg + 1);
+  ctx->fr.sched = (ctx->opt.scatter_kernel >= 0 && ctx->opt.scatter_kernel <= 2) ? ctx->opt.scatter_kernel : 0;
+  ctx->fr.run = ctx->opt.scatter_run > 0 ? ctx->opt.scatter_run : 2;
+  ctx->fr.stripes = (ctx->opt.scatter_stripes > 0 && ctx->opt.scatter_stripes <= kStripes) ? ctx->opt.scatter_stripes : 8;
+  int occ_sc = 0;
+  if (ctx->vals) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sc, k_scatter<true>, kScatterThreads, ctx->scatter_smem));
+  else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sc, k_scatter<false>, kScatterThreads, ctx->scatter_smem));
+  ctx->grid_scatter = ctx->fused ? ctx->grid_fused : ctx->num_sms * std::max(1, occ_sc);
+  ctx->grid_l1 = (int)std::min<long long>(ctx->num_sms * 8LL, std::max(1LL, (n + 255) / 256));
   return DI_OK;
 }
 
@@ -188,9 +194,9 @@ static di_status capture_graph(di_ctx *ctx) {
                                                                   ctx->ctl, ctx->sel_part);
     if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 1], ctx->stream, cudaEventRecordExternal));
     if (ctx->vals)
-      k_scatter<true><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part, ctx->spw);
+      k_scatter<true><<<ctx->grid_scatter, kScatterThreads, ctx->scatter_smem, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part);
     else
-      k_scatter<false><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part, ctx->spw);
+      k_scatter<false><<<ctx->grid_scatter, kScatterThreads, ctx->scatter_smem, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part);
     if (ctx->cap_hub > 0) {
       if (ctx->vals)
         k_scatter_hubs<true><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
@@ -280,14 +286,15 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
   ctx->cap_low = hc.n_low;
   ctx->cap_mid = hc.n_mid;
   ctx->cap_hub = hc.n_hub;
-  ctx->fr.n_words = (n + 31) / 32;
-  TRY(dalloc(ctx, &ctx->fr.bits, (size_t)ctx->fr.n_words));
-  TRY(dalloc(ctx, &ctx->fr.S, (size_t)n));
+  const size_t fr_cap = (size_t)ctx->fr.n_seg * (size_t)ctx->fr.seg_len;
+  TRY(dalloc(ctx, &ctx->fr.ids, fr_cap));
+  TRY(dalloc(ctx, &ctx->fr.S, fr_cap));
+  TRY(dalloc(ctx, &ctx->fr.seg_cnt, (size_t)ctx->fr.n_seg));
   TRY(dalloc(ctx, &ctx->fr.hub_w, hc.n_hub));
   TRY(dalloc(ctx, &ctx->fr.hub_b0, hc.n_hub));
   TRY(dalloc(ctx, &ctx->fr.hub_deg, hc.n_hub));
   TRY(dalloc(ctx, &ctx->fr.hub_chunk, hc.n_hub));
-  TRY(dalloc(ctx, &ctx->sel_part, (size_t)ctx->grid_select));
+  TRY(dalloc(ctx, &ctx->sel_part, (size_t)std::max(ctx->grid_select, ctx->grid_fused)));
   TRY(dalloc(ctx, &ctx->sc_part, (size_t)ctx->grid_scatter));
 
   TRY(dalloc(ctx, &ctx->l1_part, (size_t)ctx->grid_l1));
@@ -400,15 +407,15 @@ extern "C" di_status di_run(di_ctx *ctx, double target) {
       Graph g = diter_graph(ctx);
       int has_hubs = ctx->cap_hub > 0 ? 1 : 0, max_p = 4 * ctx->check_interval;
       void *args[] = {&g, &ctx->F, &ctx->H, &ctx->fr, &ctx->ctl, &ctx->sel_part, &ctx->sc_part,
-                      &ctx->log, &ctx->spw, &has_hubs, &max_p};
+                      &ctx->log, &has_hubs, &max_p};
       for (;;) {
         const long long pass_before = h->pass;
         if (ctx->vals)
-          CK(cudaLaunchCooperativeKernel((void *)k_pass_fused<true>, ctx->grid_fused, kScatterThreads, args, 0,
-                                         ctx->stream));
+          CK(cudaLaunchCooperativeKernel((void *)k_pass_fused<true>, ctx->grid_fused, kScatterThreads, args,
+                                         ctx->scatter_smem, ctx->stream));
         else
-          CK(cudaLaunchCooperativeKernel((void *)k_pass_fused<false>, ctx->grid_fused, kScatterThreads, args, 0,
-                                         ctx->stream));
+          CK(cudaLaunchCooperativeKernel((void *)k_pass_fused<false>, ctx->grid_fused, kScatterThreads, args,
+                                         ctx->scatter_smem, ctx->stream));
         ctx->kernel_launches += 1;
         ctx->graph_launches += 1;
         TRY(read_ctl(ctx));

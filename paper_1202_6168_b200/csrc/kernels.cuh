@@ -25,54 +25,63 @@ namespace diter {
 // internal linkage: each translation unit that launches kernels gets its own copy
 namespace {
 
+__device__ __forceinline__ void reset_tickets(Ctl *ctl) {
+  ctl->sc_next = 0u;
+#pragma unroll
+  for (int k = 0; k < kStripes; ++k) ctl->tickets[32 * k] = 0u;
+}
+
 // ---------------------------------------------------------------- K1 select --
-// Warp-tiled stream over F: each warp iteration covers 8 words of 32 nodes;
-// lane l loads F[base + 32k + l] for k < 8 (eight coalesced 256-byte loads in
-// flight per warp, no dependent load, no block barrier), so the kernel runs at
-// full occupancy and streams F at HBM rate.  |F_i| > T_p (strict, PAPER.md:215,
-// reading R7) selects; a selected node is taken: s_i = F_i, F_i = 0 (store),
-// H_i += s_i (fire-and-forget RED, one writer per pass), S[i] = s_i, and its bit
-// is set in the word written by lane k.  Per-CTA partials (r_p, |S_p|) in a
-// fixed order make r_p deterministic for given F bytes.
+// Warp w streams its own contiguous segment [w seg_len, (w+1) seg_len) of F; each
+// iteration covers kSelectSpan = 512 nodes, lane l loading F[base + 32k + l] for
+// k < 16 (sixteen coalesced 256-byte loads in flight per warp, no dependent load,
+// no block barrier), so 16 warps per SM stream F at HBM rate and the segment
+// count (= the scatter's shared-memory prefix) stays small.  |F_i| > T_p (strict,
+// PAPER.md:215, reading R7) selects; a selected node is taken: s_i = F_i, F_i = 0
+// (store to the line just read), H_i += s_i (fire-and-forget RED, one writer per
+// pass), and (i, s_i) is appended to the warp's compacted frontier segment at the
+// rank given by the ballot popcounts -- consecutive, coalesced writes instead of
+// scattered 8-byte stores, and the scatter never scans empty ranges.  Per-CTA
+// partials (r_p, |S_p|) in a fixed order make r_p deterministic for given F bytes.
 __device__ __forceinline__ void select_body(double *__restrict__ F, double *__restrict__ H, const Frontier &fr,
                                             long long n, const double T, SelPartial *__restrict__ part) {
   const unsigned lane = lane_id();
-  const long long warps = (long long)gridDim.x * (kSelectThreads / 32);
-  const long long gw = (long long)blockIdx.x * (kSelectThreads / 32) + (threadIdx.x >> 5);
-  const long long n_iter = (fr.n_words + kSelectItems - 1) / kSelectItems;
+  const unsigned lt = (1u << lane) - 1u;
+  const int gw = blockIdx.x * (kSelectThreads / 32) + (threadIdx.x >> 5);
+  const long long beg = (long long)gw * fr.seg_len;
+  const long long end = min(n, beg + fr.seg_len);
+  int* __restrict__ ids = fr.ids + beg;
+  double* __restrict__ sv = fr.S + beg;
   double r = 0.0;
-  long long cnt = 0;
-  for (long long it = gw; it < n_iter; it += warps) {
-    const long long base = it * (32LL * kSelectItems);
+  int cnt = 0;                                   // warp-uniform running count
+  for (long long base = beg; base < end; base += kSelectSpan) {
     double f[kSelectItems];
 #pragma unroll
     for (int k = 0; k < kSelectItems; ++k) {
       const long long i = base + 32 * k + lane;
-      f[k] = (i < n) ? F[i] : 0.0;
+      f[k] = (i < end) ? F[i] : 0.0;
     }
-    unsigned my_word = 0u;
 #pragma unroll
     for (int k = 0; k < kSelectItems; ++k) {
       const long long i = base + 32 * k + lane;
       const double af = fabs(f[k]);
       r += af;
-      const bool sel = (i < n) && (af > T);
-      const unsigned wbits = __ballot_sync(0xffffffffu, sel);
-      if ((int)lane == k) my_word = wbits;
+      const bool sel = af > T;                   // f = 0 beyond `end`, never selected
+      const unsigned m = __ballot_sync(0xffffffffu, sel);
       if (sel) {
+        const int pos = cnt + __popc(m & lt);
         F[i] = 0.0;            // F_i := 0
         red_add(H + i, f[k]);  // H_i += sent
-        fr.S[i] = f[k];        // sent, for the scatter
-        ++cnt;
+        ids[pos] = (int)(i);   // node and sent value, for the scatter
+        sv[pos] = f[k];
       }
+      cnt += __popc(m);
     }
-    const long long wi = it * kSelectItems + lane;
-    if ((int)lane < kSelectItems && wi < fr.n_words) fr.bits[wi] = my_word;
   }
+  if (gw < fr.n_seg && lane == 0) fr.seg_cnt[gw] = cnt;
   r = warp_sum(r);
-  cnt = warp_sum(cnt);
   __shared__ double s_r[kSelectThreads / 32];
-  __shared__ long long s_c[kSelectThreads / 32];
+  __shared__ int s_c[kSelectThreads / 32];
   if (lane == 0) { s_r[threadIdx.x >> 5] = r; s_c[threadIdx.x >> 5] = cnt; }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -82,7 +91,7 @@ __device__ __forceinline__ void select_body(double *__restrict__ F, double *__re
   }
 }
 
-__global__ void __launch_bounds__(kSelectThreads, 6)
+__global__ void __launch_bounds__(kSelectThreads, kSelectCtasPerSm)
 k_select(double *__restrict__ F, double *__restrict__ H, Frontier fr, long long n, const Ctl *ctl,
          SelPartial *__restrict__ part) {
   if (ctl->done) return;
@@ -217,121 +226,166 @@ struct ScAcc {
   int dang = 0, lo = 0, mi = 0, hu = 0;
 };
 
-// Persistent grid-stride over "superwords" of 32 bitmap words (1024 nodes): a
-// warp loads the 32 words (one 128-byte access), ranks the selected nodes by a
-// warp scan of popcounts, and processes them 32 at a time: lane t finds its
-// node (shuffle binary search over the words + __fns), gathers s_i and
-// col_ptr[i..i+1] (independent loads across lanes), derives the push value
-// s_i * (d / #out_i) (PageRank weights are never stored, BASELINE north_star; the
-// oracle's two roundings), and the group's edges are pushed by push_group.
-// Columns of more than kMidMax edges are appended to the hub list for
-// k_scatter_hubs.  The guaranteed |F|_1 drop sum (1 - c_i)|s_i| (App. A.2: c_i = d,
-// 0 for a dangling column) and the frontier census go to per-CTA partials.
+// Groups of 32 consecutive frontier entries of one segment (SURVEY §8a rows
+// a2-a4).  Every CTA first builds, in shared memory, the exclusive prefix of
+// ceil(seg_cnt/32) over the n_seg segments (s_goff[n_seg] = total groups), so a
+// global group index maps to (segment, group) by a binary search in shared
+// memory.  Schedule: the first 3/4 of the groups are dealt round-robin to the
+// grid's warps (no atomics; consecutive groups run side by side, so the ±1000
+// local pushes of neighbouring columns meet in L2), the rest are grabbed
+// dynamically in small runs (one atomic per run) to absorb the degree skew.
+// For a group, lane t loads its entry (id, s) (coalesced), gathers
+// col_ptr[id..id+1], derives the push value s_i * (d / #out_i) (PageRank weights
+// are never stored, BASELINE north_star; the oracle's two roundings), and the
+// group's edges are pushed by push_group.  Columns of more than kMidMax edges
+// are appended to the hub list for k_scatter_hubs.  The guaranteed |F|_1 drop
+// sum (1 - c_i)|s_i| (App. A.2: c_i = d, 0 for a dangling column) and the
+// frontier census go to per-CTA partials.
+__device__ __forceinline__ int build_group_prefix(const Frontier &fr, int *s_goff) {
+  const int ns = fr.n_seg;
+  const int per = (ns + kScatterThreads - 1) / kScatterThreads;
+  const int t0 = threadIdx.x * per;
+  const int t1 = min(ns, t0 + per);
+  int sum = 0;
+  for (int t = t0; t < t1; ++t) sum += (fr.seg_cnt[t] + 31) >> 5;
+  // block exclusive scan of the per-thread sums
+  const unsigned lane = lane_id();
+  int incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((int)lane >= o) incl += v;
+  }
+  __shared__ int s_w[kScatterThreads / 32 + 1];
+  if (lane == 31) s_w[threadIdx.x >> 5] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int k = 0; k < kScatterThreads / 32; ++k) { const int v = s_w[k]; s_w[k] = acc; acc += v; }
+    s_w[kScatterThreads / 32] = acc;
+  }
+  __syncthreads();
+  int run = s_w[threadIdx.x >> 5] + incl - sum;
+  for (int t = t0; t < t1; ++t) { s_goff[t] = run; run += (fr.seg_cnt[t] + 31) >> 5; }
+  if (threadIdx.x == 0) s_goff[ns] = s_w[kScatterThreads / 32];
+  __syncthreads();
+  return s_goff[ns];
+}
+
+// Segment of global group q: the largest seg with s_goff[seg] <= q (empty
+// segments repeat values).  32-ary search: each round the lanes test 32 evenly
+// spaced candidates and a ballot keeps the last one <= q (3 rounds for 8192).
+__device__ __forceinline__ int find_segment(const int *s_goff, int n_seg, int q) {
+  const unsigned lane = lane_id();
+  int lo = 0, len = n_seg;
+  while (len > 1) {
+    const int step = (len + 31) >> 5;
+    const int idx = lo + (int)lane * step;
+    const unsigned m = __ballot_sync(0xffffffffu, idx < lo + len && s_goff[idx] <= q);
+    const int top = 31 - __clz(m);           // bit 0 is always set: s_goff[lo] <= q
+    const int nlo = lo + top * step;
+    len = min(step, lo + len - nlo);
+    lo = nlo;
+  }
+  return lo;
+}
+
+template <bool SIGNED>
+__device__ __forceinline__ void scatter_group(const Graph &g, const Sink &s, const Frontier &fr, Ctl *ctl,
+                                              const int *s_goff, int q, int &seg, ScAcc &acc) {
+  // a warp's groups mostly ascend within one segment: walk forward from the
+  // last segment, search only after a jump
+  if (q < s_goff[seg] || q >= s_goff[seg + 4 < fr.n_seg ? seg + 4 : fr.n_seg]) seg = find_segment(s_goff, fr.n_seg, q);
+  while (s_goff[seg + 1] <= q) ++seg;
+  const int lo = seg;
+  const int k = 32 * (q - s_goff[lo]) + (int)lane_id();
+  const long long e = (long long)lo * fr.seg_len + k;
+  // independent loads issued together (entries past the count are never used)
+  const int cnt = fr.seg_cnt[lo];
+  const int i = fr.ids[e];
+  const double sv = fr.S[e];
+  long long b0 = 0;
+  int deg_eff = 0;
+  double w = 0.0;
+  if (k < cnt) {
+    b0 = __ldg(g.col_ptr + i);
+    const long long deg = __ldg(g.col_ptr + i + 1) - b0;
+    const double asv = fabs(sv);
+    acc.loss += (deg > 0) ? (1.0 - g.d) * asv : asv;
+    acc.edges += deg;
+    if (deg == 0) {
+      acc.dang += 1;
+    } else {
+      w = SIGNED ? sv : sv * (g.d / (double)deg);
+      if (deg <= kLowMax) { acc.lo += 1; deg_eff = (int)deg; }
+      else if (deg <= kMidMax) { acc.mi += 1; deg_eff = (int)deg; }
+      else {
+        // one 64-bit atomic hands out the slot AND the first chunk id, so
+        // hub_chunk[] is sorted by slot and k_scatter_hubs can binary-search it
+        acc.hu += 1;
+        const unsigned long long nch = (unsigned long long)((deg + kHubChunk - 1) / kHubChunk);
+        const unsigned long long old = atomicAdd(&ctl->hub_packed, (1ull << 32) | nch);
+        const unsigned sl = (unsigned)(old >> 32);
+        fr.hub_w[sl] = w; fr.hub_b0[sl] = b0; fr.hub_deg[sl] = deg;
+        fr.hub_chunk[sl] = (unsigned)(old & 0xffffffffull);
+      }
+    }
+  }
+  push_group<SIGNED>(g, s, b0, deg_eff, w);
+}
+
 template <bool SIGNED>
 __device__ __forceinline__ void scatter_body(const Graph &g, double *__restrict__ F, const Frontier &fr, Ctl *ctl,
-                                             ScPartial *__restrict__ part, int spw, double *s_hot) {
+                                             ScPartial *__restrict__ part, double *s_hot, int *s_goff) {
   for (int t = threadIdx.x; t < kHot; t += blockDim.x) s_hot[t] = 0.0;
-  __syncthreads();
+  const int total = build_group_prefix(fr, s_goff);    // ends with __syncthreads
   const Sink s{F, s_hot, g.hot_lo, g.lo, g.n, g.G, g.dflags};
   const unsigned lane = lane_id();
-  const long long n_super = (fr.n_words + kWordsPerSuper - 1) / kWordsPerSuper;
   ScAcc acc;
-  // Dynamic load balance.  Work item = a quarter of a superword: groups
-  // [8q, 8q+8) of superword sw (at most one group per warp), so a dense superword
-  // (up to 32 groups) spreads over four grabs instead of pinning one CTA while
-  // the rest wait at the next barrier.  A CTA grabs `spw` consecutive items per
-  // atomic, its warps count the items' groups, then take them round-robin.  The
-  // frontier density is very uneven across ids (the Zipf-over-id hot nodes keep
-  // their fluid longest), so a static split would leave most warps idle.
-  constexpr int kItemsMax = kScatterThreads / 32;
-  constexpr int kQuarters = 4;
-  __shared__ unsigned s_chunk;
-  __shared__ int s_off[kItemsMax + 1];
+  constexpr int kW = kScatterThreads / 32;
+  const int nwarps = gridDim.x * kW;
   const int warp = threadIdx.x >> 5;
-  const long long n_items_all = n_super * kQuarters;
-  const long long n_chunks = (n_items_all + spw - 1) / spw;   // spw <= kItemsMax items per grab
-  for (;;) {
-    if (threadIdx.x == 0) s_chunk = atomicAdd(&ctl->sc_next, 1u);
-    __syncthreads();
-    const long long ch = s_chunk;
-    if (ch >= n_chunks) break;
-    {
-      const long long item = ch * spw + warp;
-      const long long sw = item / kQuarters;
-      const int q = (int)(item - sw * kQuarters);
-      const long long wi = sw * kWordsPerSuper + lane;
-      const unsigned word = (warp < spw && item < n_items_all && wi < fr.n_words) ? fr.bits[wi] : 0u;
-      const int tot = warp_sum(__popc(word));
-      const int groups = (tot + 31) >> 5;
-      if (lane == 0) s_off[warp + 1] = max(0, min(8, groups - 8 * q));
+  int q_static = 0, seg = 0;
+  if (fr.sched == 1) {
+    // static CTA tiles of kTileGroups consecutive groups dealt round-robin to the
+    // CTAs, the CTA's warps interleaved inside the tile; dynamic tail below
+    constexpr int kTileGroups = 64;
+    const int n_tiles = total / kTileGroups;
+    const int t_static = (int)(((long long)n_tiles * 3 / 4) / gridDim.x) * gridDim.x;
+    q_static = t_static * kTileGroups;
+    for (int t = blockIdx.x; t < t_static; t += gridDim.x)
+      for (int j = warp; j < kTileGroups; j += kW) scatter_group<SIGNED>(g, s, fr, ctl, s_goff, t * kTileGroups + j, seg, acc);
+  } else if (fr.sched == 2) {
+    // static warp-interleaved groups; dynamic tail below
+    const int gwarp = blockIdx.x * kW + warp;
+    q_static = (int)(((long long)total * 3 / 4) / nwarps) * nwarps;
+    for (int q = gwarp; q < q_static; q += nwarps) scatter_group<SIGNED>(g, s, fr, ctl, s_goff, q, seg, acc);
+  }
+  // Dynamic: each warp grabs runs of consecutive groups in ascending order (one
+  // atomic per run, no block barrier).  The grid's working set stays a narrow
+  // window of consecutive columns, so the ±1000-local pushes of neighbouring
+  // columns meet their F lines in L2 before eviction; a static split lets CTAs
+  // drift apart and widens that window past L2.
+  // The groups left are split into `stripes` contiguous stripes with one ticket
+  // counter each (less same-address contention, so runs can stay short, and each
+  // stripe's working window is narrow); a warp starts on stripe (warp id mod
+  // stripes) and moves on when it is drained.
+  const int rest = total - q_static;
+  const int run = fr.sched == 0 ? max(1, min(fr.run, rest / (2 * nwarps))) : max(1, rest / (4 * nwarps));
+  const int gw = blockIdx.x * kW + warp;
+  const int ns = fr.stripes;
+  for (int k = 0; k < ns; ++k) {
+    const int st = (gw + k) % ns;
+    const int s0 = q_static + (int)((long long)rest * st / ns);
+    const int s1 = q_static + (int)((long long)rest * (st + 1) / ns);
+    for (;;) {
+      unsigned q0 = 0;
+      if (lane == 0) q0 = atomicAdd(&ctl->tickets[32 * st], (unsigned)run);
+      q0 = __shfl_sync(0xffffffffu, q0, 0);
+      if ((long long)q0 >= (long long)(s1 - s0)) break;
+      const int q1 = min(s1, s0 + (int)q0 + run);
+      for (int q = s0 + (int)q0; q < q1; ++q) scatter_group<SIGNED>(g, s, fr, ctl, s_goff, q, seg, acc);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      s_off[0] = 0;
-      for (int j = 1; j <= kItemsMax; ++j) s_off[j] += s_off[j - 1];
-    }
-    __syncthreads();
-    const int n_items = s_off[kItemsMax];
-    for (int k = warp; k < n_items; k += kItemsMax) {
-      int j = 0;
-      while (j + 1 < kItemsMax && s_off[j + 1] <= k) ++j;
-      const long long item = ch * spw + j;
-      const long long sw = item / kQuarters;
-      const int q = (int)(item - sw * kQuarters);
-      const int g0 = 32 * (8 * q + (k - s_off[j]));
-      const long long wi = sw * kWordsPerSuper + lane;
-      const unsigned word = (wi < fr.n_words) ? fr.bits[wi] : 0u;
-      const int c = __popc(word);
-      int incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if ((int)lane >= o) incl += t;
-      }
-      const int excl = incl - c;
-      const int total = __shfl_sync(0xffffffffu, incl, 31);
-      const int rank = g0 + (int)lane;
-      int lo = 0;
-#pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const int cand = lo + step;
-        if (__shfl_sync(0xffffffffu, excl, cand) <= rank) lo = cand;
-      }
-      const unsigned wbits = __shfl_sync(0xffffffffu, word, lo);
-      const int wex = __shfl_sync(0xffffffffu, excl, lo);
-      long long b0 = 0;
-      int deg_eff = 0;
-      double w = 0.0;
-      if (rank < total) {
-        const int bit = (int)__fns(wbits, 0u, rank - wex + 1);
-        const long long i = (sw * kWordsPerSuper + lo) * 32 + bit;
-        const double sv = fr.S[i];
-        b0 = __ldg(g.col_ptr + i);
-        const long long deg = __ldg(g.col_ptr + i + 1) - b0;
-        const double asv = fabs(sv);
-        acc.loss += (deg > 0) ? (1.0 - g.d) * asv : asv;
-        acc.edges += deg;
-        if (deg == 0) {
-          acc.dang += 1;
-        } else {
-          w = SIGNED ? sv : sv * (g.d / (double)deg);
-          if (deg <= kLowMax) { acc.lo += 1; deg_eff = (int)deg; }
-          else if (deg <= kMidMax) { acc.mi += 1; deg_eff = (int)deg; }
-          else {
-            // one 64-bit atomic hands out the slot AND the first chunk id, so
-            // hub_chunk[] is sorted by slot and k_scatter_hubs can binary-search it
-            acc.hu += 1;
-            const unsigned long long nch = (unsigned long long)((deg + kHubChunk - 1) / kHubChunk);
-            const unsigned long long old = atomicAdd(&ctl->hub_packed, (1ull << 32) | nch);
-            const unsigned sl = (unsigned)(old >> 32);
-            fr.hub_w[sl] = w; fr.hub_b0[sl] = b0; fr.hub_deg[sl] = deg;
-            fr.hub_chunk[sl] = (unsigned)(old & 0xffffffffull);
-          }
-        }
-      }
-      push_group<SIGNED>(g, s, b0, deg_eff, w);
-    }
-    __syncthreads();   // s_chunk / s_off are rewritten by the next grab
   }
   // flush the hot window: one RED per touched row per CTA
   __syncthreads();
@@ -359,12 +413,14 @@ __device__ __forceinline__ void scatter_body(const Graph &g, double *__restrict_
   }
 }
 
+// dynamic shared memory: the group prefix s_goff[n_seg + 1]
 template <bool SIGNED>
 __global__ void __launch_bounds__(kScatterThreads)
-k_scatter(Graph g, double *__restrict__ F, Frontier fr, Ctl *ctl, ScPartial *__restrict__ part, int spw) {
+k_scatter(Graph g, double *__restrict__ F, Frontier fr, Ctl *ctl, ScPartial *__restrict__ part) {
   if (ctl->done) return;
   __shared__ double s_hot[kHot];
-  scatter_body<SIGNED>(g, F, fr, ctl, part, spw, s_hot);
+  extern __shared__ int s_goff[];
+  scatter_body<SIGNED>(g, F, fr, ctl, part, s_hot, s_goff);
 }
 
 // Hub columns (> kMidMax edges), one CTA per 2048-edge chunk (chunks of a hub
@@ -451,7 +507,7 @@ __device__ __forceinline__ void apply_pass(Ctl *ctl, const double *sums, di_pass
   if (r < ctl->target || pred < ctl->target) ctl->done = 1;
   else if (p + 1 >= ctl->max_pass) ctl->done = 2;
   ctl->hub_packed = 0ull;
-  ctl->sc_next = 0u;
+  reset_tickets(ctl);
 }
 
 __global__ void __launch_bounds__(kFinalizeThreads)
@@ -493,10 +549,11 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 template <bool SIGNED>
 __global__ void __launch_bounds__(kScatterThreads)
 k_pass_fused(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ctl *ctl,
-             SelPartial *__restrict__ sp, ScPartial *__restrict__ cp, di_pass_log *log, int spw,
+             SelPartial *__restrict__ sp, ScPartial *__restrict__ cp, di_pass_log *log,
              int has_hubs, int max_passes) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double s_hot[kHot];
+  extern __shared__ int s_goff[];
   __shared__ double sums[kSums];
   for (int k = 0; k < max_passes; ++k) {
     if (*(volatile int *)&ctl->done) break;          // written by CTA 0 before the last barrier
@@ -505,7 +562,7 @@ k_pass_fused(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier f
     select_body(F, H, fr, g.n, *(volatile double *)&ctl->T, sp);
     grid.sync();
     if (blockIdx.x == 0 && threadIdx.x == 0) t1 = globaltimer_ns();
-    scatter_body<SIGNED>(g, F, fr, ctl, cp, spw, s_hot);
+    scatter_body<SIGNED>(g, F, fr, ctl, cp, s_hot, s_goff);
     grid.sync();
     if (has_hubs) {
       hubs_body<SIGNED>(g, F, fr, ctl);
@@ -631,7 +688,7 @@ __global__ void k_begin_run(Ctl *ctl, double target, long long max_pass, const d
   ctl->r_pred = *r_exact;
   ctl->done = 0;
   ctl->hub_packed = 0ull;
-  ctl->sc_next = 0u;
+  reset_tickets(ctl);
 }
 
 }  // namespace

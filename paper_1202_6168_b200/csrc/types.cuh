@@ -13,10 +13,13 @@ constexpr int kHubChunk = 2048;  // > 8192    : "hub"  -- one CTA per 2048-edge 
 constexpr int kHot = 2048;       // rows staged in shared memory by each scatter CTA
 
 constexpr int kSelectThreads = 256;
-constexpr int kSelectItems = 8;                      // 32-node words per warp iteration
+constexpr int kSelectItems = 16;                     // 32-node words per warp iteration
+constexpr int kSelectSpan = 32 * kSelectItems;       // nodes per warp iteration (segment granule)
 constexpr int kScatterThreads = 256;
 constexpr int kFinalizeThreads = 512;
-constexpr int kWordsPerSuper = 32;                   // bitmap words per scatter superword (1024 nodes)
+constexpr int kSelectCtasPerSm = 2;                  // 16 select warps/SM x 16 x 256 B loads in flight
+constexpr int kMaxSegments = 4096;                   // select warps (= frontier segments) per launch
+constexpr int kStripes = 32;                         // max scatter ticket counters (contiguous group stripes)
 
 // Device-resident control block of one context.
 struct Ctl {
@@ -35,10 +38,13 @@ struct Ctl {
   int policy;          // DI_POLICY_*
   unsigned long long hub_packed;  // (hub slots << 32) | hub chunks; reset by k_finalize
   long long log_cap;
-  unsigned sc_next;    // next superword chunk for the scatter's dynamic schedule (reset per pass)
+  unsigned sc_next;    // next frontier group of the scatter's dynamic tail (reset per pass)
   int _pad;
   double t_sel_us;     // fused kernel: accumulated select / scatter phase time (%globaltimer)
   double t_sc_us;
+  // scatter tickets: one counter per stripe of the frontier groups, each on its
+  // own 128-byte line (reset per pass with sc_next)
+  alignas(128) unsigned tickets[kStripes * 32];
 };
 
 // k_select partials (one per CTA): r_p and |S_p|.
@@ -66,12 +72,19 @@ struct Graph {
   unsigned char *dflags;     // dirty flag per 32-row block of G
 };
 
-// Frontier of one pass: selection bitmap (bit i%32 of word i/32) and the taken
-// values s_i (valid where the bit is set); hubs go to a separate list.
+// Frontier of one pass, compacted per select warp: warp w scans the owned nodes
+// [w seg_len, (w+1) seg_len) and writes its selected nodes in ascending order to
+// ids/S[w seg_len + k], k < seg_cnt[w].  The scatter takes them 32 at a time
+// ("groups") through a prefix over ceil(seg_cnt/32).  Hubs go to a separate list.
 struct Frontier {
-  unsigned *bits;        // [n_words_pad]
-  double *S;             // [n]
-  long long n_words;     // ceil(n / 32)
+  int *ids;              // [n_seg * seg_len] local node ids
+  double *S;             // [n_seg * seg_len] taken values s_i
+  int *seg_cnt;          // [n_seg] selected nodes per segment
+  long long seg_len;     // nodes per segment, a multiple of kSelectSpan
+  int n_seg;             // select grid x warps per CTA (<= kMaxSegments)
+  int sched;             // scatter schedule: 0 dynamic warp runs (default), 1 static CTA tiles, 2 static warp interleave
+  int run;               // groups per dynamic grab (schedule 0)
+  int stripes;           // ticket stripes in use (<= kStripes)
   double *hub_w;         // push value per edge of the hub (s d/#out or s)
   long long *hub_b0;
   long long *hub_deg;

@@ -121,7 +121,18 @@ def test_c1_parity_dense(seed, policy):
     st = P.init()
     P.snapshot(st, 1e-12, policy)
     _compare_logs(log, st.log)
-    assert len(log) == st.passes
+    _same_stop_pass(log, st, 1e-12)
+
+
+def _same_stop_pass(log, st, target):
+    """The run stops after the same pass as the oracle, unless the residual at the
+    boundary pass sits within rounding of the target (a tie decided by summation
+    order, reading R8 applied to the stop test): then one pass more or fewer."""
+    if len(log) == st.passes:
+        return
+    assert abs(len(log) - st.passes) == 1, (len(log), st.passes)
+    r_edge = log["r"][st.passes] if len(log) > st.passes else st.log[len(log)][2]
+    assert abs(r_edge / target - 1.0) < 1e-9, r_edge
 
 
 @pytest.mark.parametrize("seed", [1, 2])
@@ -142,24 +153,48 @@ def test_c2_full_parity(seed):
     assert abs(stats["passes"] - st.passes) <= 2
 
 
+_ORACLE_CACHE = {}
+
+
+def _c2_random_b_oracle(policy):
+    """Oracle run (memoised per policy) on the configs[1] graph with a random B."""
+    if policy not in _ORACLE_CACHE:
+        p = gen.config("C2", 3)
+        rng = np.random.default_rng(7)
+        b = rng.random(p.n) + 0.5
+        b *= 0.15 / b.sum()
+        target = 1e-9 * 0.15
+        P = oracle.Problem(p.n, p.col_ptr, p.row_idx, None, b)
+        st, near = _oracle_passes_with_ties(P, target, policy)
+        _ORACLE_CACHE[policy] = (p, b, target, st, near)
+    return _ORACLE_CACHE[policy]
+
+
+VARIANTS = {
+    "default": {},
+    "fused": {"pass_kernel": 2},                       # cooperative persistent pass kernel
+    "tiles": {"scatter_kernel": 1},                    # static CTA tiles + dynamic tail
+    "interleave": {"scatter_kernel": 2},               # static warp interleave + dynamic tail
+    "runs": {"scatter_run": 7, "scatter_stripes": 3},  # other grab run / stripe counts
+    "nohot": {"hot_window": -1},                       # every push an L2 RED
+}
+
+
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
 @pytest.mark.parametrize("policy", [di.DI_POLICY_GEOM, di.DI_POLICY_HYBRID])
-def test_c2_graph_random_b_logs_exact(policy):
+def test_c2_graph_random_b_logs_exact(policy, variant):
     """configs[1] graph with a seeded random positive B: no exact-arithmetic ties with
-    T_p, so frontier sizes, edges and dangling counts match the oracle pass for pass."""
-    p = gen.config("C2", 3)
-    rng = np.random.default_rng(7)
-    b = rng.random(p.n) + 0.5
-    b *= 0.15 / b.sum()
-    target = 1e-9 * 0.15
-    H, F, log, r, stats = _gpu(p.n, p.col_ptr, p.row_idx, target, b=b, policy=policy)
-    P = oracle.Problem(p.n, p.col_ptr, p.row_idx, None, b)
-    st, near = _oracle_passes_with_ties(P, target, policy)
+    T_p, so frontier sizes, edges and dangling counts match the oracle pass for pass --
+    for every pass-kernel / scatter-schedule option."""
+    p, b, target, st, near = _c2_random_b_oracle(policy)
+    H, F, log, r, stats = _gpu(p.n, p.col_ptr, p.row_idx, target, b=b, policy=policy, **VARIANTS[variant])
     assert sum(near) == 0
     _compare_logs(log, st.log)
     assert len(log) == st.passes and stats["edges"] == st.edges
     # bins partition the frontier
     np.testing.assert_array_equal(log["bin_low"] + log["bin_mid"] + log["bin_hub"] + log["dangling"],
                                   log["frontier"])
+    _check_state(p.n, p.col_ptr, p.row_idx, None, b, 0.85, H, F, r, target)
 
 
 @pytest.mark.parametrize("n", [100_000, 1_000_000])
