@@ -51,7 +51,7 @@ class di_options(ctypes.Structure):
                 ("scatter_kernel", ctypes.c_int32), ("profile", ctypes.c_int32),
                 ("pass_kernel", ctypes.c_int32), ("hot_window", ctypes.c_int32),
                 ("scatter_run", ctypes.c_int32), ("scatter_stripes", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 2)]
+                ("far_push", ctypes.c_int32), ("far_warm_log2", ctypes.c_int32)]
 
 
 class di_pass_log(ctypes.Structure):

@@ -34,6 +34,11 @@ struct di_ctx {
   unsigned char *dflags = nullptr;  // dirty flag per 32-row block of G
   double *H = nullptr;           // history [n_local]
   diter::Frontier fr{};
+  diter::Far far{};               // far-push bins (propagation blocking), 1 GPU
+  long long *far_off = nullptr;   // [n_bins + 1] first chunk of each bin (device)
+  long long far_cap = 0;          // total chunks
+  std::vector<unsigned> blk_hist; // sampled in-degree per 1024-row block (setup)
+  int blk_stride = 1;
   unsigned long long cap_low = 0, cap_mid = 0, cap_hub = 0;
   diter::SelPartial *sel_part = nullptr;
   diter::ScPartial *sc_part = nullptr;

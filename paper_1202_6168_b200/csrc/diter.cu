@@ -80,7 +80,7 @@ static void free_ctx(di_ctx *c) {
     if (e) cudaEventDestroy(e);
   void *ptrs[] = {c->col_ptr, c->row_idx, c->vals, c->d_b, c->F, c->H, c->fr.ids, c->fr.S, c->fr.seg_cnt,
                   c->fr.hub_w, c->fr.hub_b0, c->fr.hub_deg, c->fr.hub_chunk, c->sel_part, c->sc_part,
-                  c->l1_part, c->l1_out, c->ctl, c->log};
+                  c->l1_part, c->l1_out, c->ctl, c->log, c->far_off, c->far.rows, c->far.vals, c->far.fill};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
@@ -158,7 +158,9 @@ static di_status choose_hot_window(di_ctx *ctx) {
   CK(cudaMemsetAsync(blk, 0, sizeof(unsigned) * nb, ctx->stream));
   const int stride = ctx->nnz_local > (1LL << 24) ? 64 : 1;
   k_hot_sample<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->row_idx, ctx->nnz_local, stride, blk);
-  std::vector<unsigned> h(nb);
+  std::vector<unsigned> &h = ctx->blk_hist;
+  h.assign(nb, 0u);
+  ctx->blk_stride = stride;
   CK(cudaMemcpyAsync(h.data(), blk, sizeof(unsigned) * nb, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   cudaFree(blk);
@@ -173,9 +175,71 @@ static di_status choose_hot_window(di_ctx *ctx) {
   return DI_OK;
 }
 
+// Far-push bins (propagation blocking, Far in types.cuh): one GPU, F too large to
+// stay L2-resident.  The warm range is the 2^far_warm_log2 consecutive rows of
+// largest sampled in-degree (kept on direct L2 REDs); bins of 2^shift rows, at
+// most kMaxBins, sized by an exact census of the edges that can be far.
+static di_status setup_far(di_ctx *ctx) {
+  ctx->far = Far{};
+  ctx->far.warm_len = 0u;
+  const int mode = ctx->opt.far_push;
+  const long long n = ctx->n_rows;
+  const bool want = mode > 0;   // auto = off: on C4 the emission costs more than the tail REDs it saves
+  if (!want || mode < 0 || ctx->world > 1 || ctx->fused || ctx->nnz_local == 0 || ctx->blk_hist.empty()) return DI_OK;
+  int shift = 20;
+  while (((n - 1) >> shift) + 1 > kMaxBins) ++shift;
+  const int n_bins = (int)(((n - 1) >> shift) + 1);
+  const int wl = ctx->opt.far_warm_log2 > 0 ? std::min(ctx->opt.far_warm_log2, 30) : 21;
+  const long long W = std::min<long long>(1LL << wl, n);
+  // warm window: W rows (W/1024 blocks) with the largest sampled in-degree mass
+  const std::vector<unsigned> &h = ctx->blk_hist;
+  const long long nbk = (long long)h.size(), wb = std::max<long long>(1, W >> 10);
+  long long best = 0, cur = 0, best_sum = -1;
+  for (long long b = 0; b < nbk; ++b) {
+    cur += h[b];
+    if (b >= wb) cur -= h[b - wb];
+    if (b + 1 >= wb && cur > best_sum) { best_sum = cur; best = b + 1 - wb; }
+  }
+  long long warm_lo = std::min<long long>(best << 10, std::max<long long>(0, n - W));
+  ctx->far.warm_lo = (int)warm_lo;
+  ctx->far.warm_len = (unsigned)W;
+  ctx->far.shift = shift;
+  ctx->far.n_bins = n_bins;
+  unsigned long long *d_cap = nullptr;
+  TRY(dalloc(ctx, &d_cap, (size_t)kMaxBins));
+  CK(cudaMemsetAsync(d_cap, 0, sizeof(unsigned long long) * kMaxBins, ctx->stream));
+  k_far_census<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->col_ptr, ctx->n_local, ctx->row_idx, ctx->lo,
+                                                          ctx->hot_lo, ctx->far.warm_lo, ctx->far.warm_len, shift, d_cap);
+  std::vector<unsigned long long> cap(kMaxBins);
+  CK(cudaMemcpyAsync(cap.data(), d_cap, sizeof(unsigned long long) * kMaxBins, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  cudaFree(d_cap);
+  // chunks per bin: every chunk closed before the end of a pass holds > kFarChunk - 32
+  // records, and each scatter warp leaves at most one partial chunk per bin
+  const long long warps = (long long)ctx->grid_scatter * (kScatterThreads / 32);
+  std::vector<long long> coff(n_bins + 1, 0);
+  long long recs = 0;
+  for (int b = 0; b < n_bins; ++b) {
+    recs += (long long)cap[b];
+    const long long nch = cap[b] ? (long long)(cap[b] + (kFarChunk - 32) - 1) / (kFarChunk - 32) + warps : 0;
+    coff[b + 1] = coff[b] + nch;
+  }
+  ctx->far_cap = coff[n_bins];
+  if (recs == 0) { ctx->far = Far{}; return DI_OK; }
+  TRY(dalloc(ctx, &ctx->far_off, (size_t)n_bins + 1));
+  CK(cudaMemcpyAsync(ctx->far_off, coff.data(), sizeof(long long) * (n_bins + 1), cudaMemcpyHostToDevice, ctx->stream));
+  TRY(dalloc(ctx, &ctx->far.rows, (size_t)ctx->far_cap * kFarChunk));
+  TRY(dalloc(ctx, &ctx->far.vals, (size_t)ctx->far_cap * kFarChunk));
+  TRY(dalloc(ctx, &ctx->far.fill, (size_t)ctx->far_cap));
+  ctx->far.coff = ctx->far_off;
+  ctx->far.on = 1;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return DI_OK;
+}
+
 Graph diter_graph(const di_ctx *ctx) {
   return Graph{ctx->col_ptr, ctx->row_idx, ctx->vals, ctx->n_local, ctx->d, ctx->hot_lo,
-               ctx->lo, ctx->G, ctx->dflags};
+               ctx->lo, ctx->G, ctx->dflags, ctx->far};
 }
 
 // Capture check_interval passes of (select, scatter, finalize) once.
@@ -203,6 +267,8 @@ static di_status capture_graph(di_ctx *ctx) {
       else
         k_scatter_hubs<false><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
     }
+    if (ctx->far.on)
+      k_apply_far<<<ctx->num_sms * 4, kApplyThreads, 0, ctx->stream>>>(ctx->F, ctx->far, ctx->lo, ctx->ctl);
     if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 2], ctx->stream, cudaEventRecordExternal));
     k_finalize<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->ctl, ctx->sel_part, ctx->grid_select, ctx->sc_part,
                                                         ctx->grid_scatter, ctx->log);
@@ -283,6 +349,7 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
     return DI_ERR_CONTRACTION;
   }
   TRY(choose_hot_window(ctx));
+  TRY(setup_far(ctx));
   ctx->cap_low = hc.n_low;
   ctx->cap_mid = hc.n_mid;
   ctx->cap_hub = hc.n_hub;
@@ -430,7 +497,7 @@ extern "C" di_status di_run(di_ctx *ctx, double target) {
       const long long pass_before = h->pass;
       CK(cudaGraphLaunch(ctx->graph_exec, ctx->stream));
       ctx->graph_launches += 1;
-      ctx->kernel_launches += (ctx->cap_hub > 0 ? 4LL : 3LL) * ctx->check_interval;
+      ctx->kernel_launches += (3LL + (ctx->cap_hub > 0) + (ctx->far.on ? 1 : 0)) * ctx->check_interval;
       TRY(read_ctl(ctx));
       if (ctx->opt.profile) {
         const long long active = std::min<long long>(h->pass - pass_before, ctx->check_interval);

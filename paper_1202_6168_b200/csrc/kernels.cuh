@@ -29,6 +29,8 @@ __device__ __forceinline__ void reset_tickets(Ctl *ctl) {
   ctl->sc_next = 0u;
 #pragma unroll
   for (int k = 0; k < kStripes; ++k) ctl->tickets[32 * k] = 0u;
+#pragma unroll 8
+  for (int k = 0; k < kMaxBins; ++k) ctl->far_cnt[32 * k] = 0u;
 }
 
 // ---------------------------------------------------------------- K1 select --
@@ -175,16 +177,66 @@ __device__ __forceinline__ void push_range(const Graph &g, const Sink &s, long l
   if (e < end) push(s, ld_row(g.row_idx + e), SIGNED ? w * ld_val(g.vals + e) : w);
 }
 
+constexpr int kGroupUnroll = 4;
+
+// Far push (see Far in types.cuh).  Lanes with the same bin are aggregated by
+// __match_any_sync; the lowest lane of each bin group appends the group to this
+// warp's open chunk of that bin (st[b] = chunk id or -1, st[kMaxBins + b] = its
+// fill, warp-private shared memory), closing it and opening a new one with one
+// atomic when the group does not fit.  A bin whose chunks ran out (impossible by
+// the capacity bound) falls back to a direct RED.
+__device__ __forceinline__ void emit_far(const Far &far, Ctl *ctl, const Sink &s, int *st, bool is_far, int row,
+                                         double v) {
+  const unsigned lane = lane_id();
+  const int b = is_far ? (row >> far.shift) : -1;
+  const unsigned peers = __match_any_sync(0xffffffffu, b);
+  const int leader = __ffs(peers) - 1;
+  long long chunk = -1;
+  int f0 = 0;
+  if (is_far && (int)lane == leader) {
+    const int cnt = __popc(peers);
+    int c = st[b];
+    f0 = st[kMaxBins + b];
+    if (c < 0 || f0 + cnt > kFarChunk) {
+      if (c >= 0) far.fill[far.coff[b] + c] = f0;                 // close the full chunk
+      const unsigned k = atomicAdd(&ctl->far_cnt[32 * b], 1u);
+      c = ((long long)k < far.coff[b + 1] - far.coff[b]) ? (int)k : -1;
+      f0 = 0;
+    }
+    st[b] = c;
+    st[kMaxBins + b] = f0 + cnt;
+    chunk = c < 0 ? -1 : far.coff[b] + c;
+  }
+  chunk = __shfl_sync(0xffffffffu, chunk, leader);
+  f0 = __shfl_sync(0xffffffffu, f0, leader);
+  if (is_far) {
+    if (chunk >= 0) {
+      const long long slot = chunk * kFarChunk + f0 + __popc(peers & ((1u << lane) - 1u));
+      far.rows[slot] = row;
+      far.vals[slot] = v;
+    } else {
+      push(s, row, v);
+    }
+  }
+}
+
+// End of the scatter: the warp closes its open chunks (fill counts for k_apply_far).
+__device__ __forceinline__ void close_far(const Far &far, const int *st) {
+  for (int b = (int)lane_id(); b < far.n_bins; b += 32)
+    if (st[b] >= 0) far.fill[far.coff[b] + st[b]] = st[kMaxBins + b];
+}
+
 // One group of up to 32 selected nodes held one per lane (b0, deg, w): the warp
 // scans the degrees, then lane l takes edges l, l+32, ... of the group's
 // concatenated edge list (edge-balanced inside the warp; consecutive lanes read
 // consecutive row indices within a column, and adjacent columns of consecutive
 // ids are adjacent in row_idx).  The owner lane of an edge is found by a 5-step
-// shuffle binary search over the exclusive degree prefix.
-constexpr int kGroupUnroll = 4;
-
+// shuffle binary search over the exclusive degree prefix.  [nlo, nhi] is the
+// group's near window (its columns +- kNear): with far pushes on, a push outside
+// it, the hot window and the warm range becomes a far record.
 template <bool SIGNED>
-__device__ __forceinline__ void push_group(const Graph &g, const Sink &s, long long b0, int deg, double w) {
+__device__ __forceinline__ void push_group(const Graph &g, const Sink &s, Ctl *ctl, int *st, long long b0, int deg,
+                                           double w, int nlo, int nhi) {
   const unsigned lane = lane_id();
   int incl = deg;
 #pragma unroll
@@ -214,9 +266,20 @@ __device__ __forceinline__ void push_group(const Graph &g, const Sink &s, long l
       rows[u] = ok ? ld_row(g.row_idx + ei) : -1;
       vals[u] = ok ? (SIGNED ? ow * ld_val(g.vals + ei) : ow) : 0.0;
     }
+    if (!g.far.on) {
 #pragma unroll
-    for (int u = 0; u < kGroupUnroll; ++u)
-      if (rows[u] >= 0) push(s, rows[u], vals[u]);
+      for (int u = 0; u < kGroupUnroll; ++u)
+        if (rows[u] >= 0) push(s, rows[u], vals[u]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < kGroupUnroll; ++u) {
+        const int row = rows[u];
+        const bool is_far = row >= 0 && (unsigned)(row - s.hot_lo) >= (unsigned)kHot &&
+                            (unsigned)(row - g.far.warm_lo) >= g.far.warm_len && (row < nlo || row > nhi);
+        if (row >= 0 && !is_far) push(s, row, vals[u]);
+        if (__any_sync(0xffffffffu, is_far)) emit_far(g.far, ctl, s, st, is_far, row, vals[u]);
+      }
+    }
   }
 }
 
@@ -292,7 +355,7 @@ __device__ __forceinline__ int find_segment(const int *s_goff, int n_seg, int q)
 
 template <bool SIGNED>
 __device__ __forceinline__ void scatter_group(const Graph &g, const Sink &s, const Frontier &fr, Ctl *ctl,
-                                              const int *s_goff, int q, int &seg, ScAcc &acc) {
+                                              const int *s_goff, int *st, int q, int &seg, ScAcc &acc) {
   // a warp's groups mostly ascend within one segment: walk forward from the
   // last segment, search only after a jump
   if (q < s_goff[seg] || q >= s_goff[seg + 4 < fr.n_seg ? seg + 4 : fr.n_seg]) seg = find_segment(s_goff, fr.n_seg, q);
@@ -331,13 +394,20 @@ __device__ __forceinline__ void scatter_group(const Graph &g, const Sink &s, con
       }
     }
   }
-  push_group<SIGNED>(g, s, b0, deg_eff, w);
+  // near window of the group: its first and last column (ids ascend within a segment)
+  const int n_here = min(32, cnt - 32 * (q - s_goff[lo]));
+  const int i_first = __shfl_sync(0xffffffffu, i, 0) + (int)g.lo;
+  const int i_last = __shfl_sync(0xffffffffu, i, n_here - 1) + (int)g.lo;
+  push_group<SIGNED>(g, s, ctl, st, b0, deg_eff, w, i_first - kNear, i_last + kNear);
 }
 
 template <bool SIGNED>
 __device__ __forceinline__ void scatter_body(const Graph &g, double *__restrict__ F, const Frontier &fr, Ctl *ctl,
                                              ScPartial *__restrict__ part, double *s_hot, int *s_goff) {
   for (int t = threadIdx.x; t < kHot; t += blockDim.x) s_hot[t] = 0.0;
+  __shared__ int s_far[kScatterThreads / 32][2 * kMaxBins];     // per-warp open far chunks
+  int *st = s_far[threadIdx.x >> 5];
+  for (int b = (int)lane_id(); b < kMaxBins; b += 32) { st[b] = -1; st[kMaxBins + b] = 0; }
   const int total = build_group_prefix(fr, s_goff);    // ends with __syncthreads
   const Sink s{F, s_hot, g.hot_lo, g.lo, g.n, g.G, g.dflags};
   const unsigned lane = lane_id();
@@ -354,12 +424,12 @@ __device__ __forceinline__ void scatter_body(const Graph &g, double *__restrict_
     const int t_static = (int)(((long long)n_tiles * 3 / 4) / gridDim.x) * gridDim.x;
     q_static = t_static * kTileGroups;
     for (int t = blockIdx.x; t < t_static; t += gridDim.x)
-      for (int j = warp; j < kTileGroups; j += kW) scatter_group<SIGNED>(g, s, fr, ctl, s_goff, t * kTileGroups + j, seg, acc);
+      for (int j = warp; j < kTileGroups; j += kW) scatter_group<SIGNED>(g, s, fr, ctl, s_goff, st, t * kTileGroups + j, seg, acc);
   } else if (fr.sched == 2) {
     // static warp-interleaved groups; dynamic tail below
     const int gwarp = blockIdx.x * kW + warp;
     q_static = (int)(((long long)total * 3 / 4) / nwarps) * nwarps;
-    for (int q = gwarp; q < q_static; q += nwarps) scatter_group<SIGNED>(g, s, fr, ctl, s_goff, q, seg, acc);
+    for (int q = gwarp; q < q_static; q += nwarps) scatter_group<SIGNED>(g, s, fr, ctl, s_goff, st, q, seg, acc);
   }
   // Dynamic: each warp grabs runs of consecutive groups in ascending order (one
   // atomic per run, no block barrier).  The grid's working set stays a narrow
@@ -375,18 +445,19 @@ __device__ __forceinline__ void scatter_body(const Graph &g, double *__restrict_
   const int gw = blockIdx.x * kW + warp;
   const int ns = fr.stripes;
   for (int k = 0; k < ns; ++k) {
-    const int st = (gw + k) % ns;
-    const int s0 = q_static + (int)((long long)rest * st / ns);
-    const int s1 = q_static + (int)((long long)rest * (st + 1) / ns);
+    const int sp = (gw + k) % ns;
+    const int s0 = q_static + (int)((long long)rest * sp / ns);
+    const int s1 = q_static + (int)((long long)rest * (sp + 1) / ns);
     for (;;) {
       unsigned q0 = 0;
-      if (lane == 0) q0 = atomicAdd(&ctl->tickets[32 * st], (unsigned)run);
+      if (lane == 0) q0 = atomicAdd(&ctl->tickets[32 * sp], (unsigned)run);
       q0 = __shfl_sync(0xffffffffu, q0, 0);
       if ((long long)q0 >= (long long)(s1 - s0)) break;
       const int q1 = min(s1, s0 + (int)q0 + run);
-      for (int q = s0 + (int)q0; q < q1; ++q) scatter_group<SIGNED>(g, s, fr, ctl, s_goff, q, seg, acc);
+      for (int q = s0 + (int)q0; q < q1; ++q) scatter_group<SIGNED>(g, s, fr, ctl, s_goff, st, q, seg, acc);
     }
   }
+  if (g.far.on) close_far(g.far, st);
   // flush the hot window: one RED per touched row per CTA
   __syncthreads();
   for (int t = threadIdx.x; t < kHot; t += blockDim.x) {
@@ -452,6 +523,48 @@ k_scatter_hubs(Graph g, double *__restrict__ F, Frontier fr, const Ctl *ctl) {
   hubs_body<SIGNED>(g, F, fr, ctl);
 }
 
+// ------------------------------------------------------- K4b far-push apply --
+// Opened chunks of every bin, bins in ascending order (prefix of the chunk
+// counters); CTAs take two chunks at a time round-robin, so the grid works on one
+// or two bins at a time and each bin's slice of F (2^shift rows) stays
+// L2-resident while its records land.  Streaming record reads (12 B) replace the
+// random DRAM sector read-modify-write the push would have cost.
+constexpr int kApplyThreads = 256;
+
+__device__ __forceinline__ void apply_far_body(double *__restrict__ F, const Far &far, long long lo, const Ctl *ctl) {
+  __shared__ long long s_pre[kMaxBins + 1];   // prefix of opened chunks over the bins
+  if (threadIdx.x == 0) {
+    long long acc = 0;
+    for (int b = 0; b < far.n_bins; ++b) {
+      s_pre[b] = acc;
+      const long long c = *(volatile const unsigned *)&ctl->far_cnt[32 * b];
+      acc += min(c, far.coff[b + 1] - far.coff[b]);
+    }
+    s_pre[far.n_bins] = acc;
+  }
+  __syncthreads();
+  const long long total = s_pre[far.n_bins];
+  constexpr int kPer = kApplyThreads / kFarChunk;            // chunks per CTA step
+  const int k = threadIdx.x % kFarChunk;
+  int b = 0;
+  for (long long c = (long long)blockIdx.x * kPer + threadIdx.x / kFarChunk; c < total;
+       c += (long long)gridDim.x * kPer) {
+    while (s_pre[b + 1] <= c) ++b;
+    const long long chunk = far.coff[b] + (c - s_pre[b]);
+    if (k < far.fill[chunk]) {
+      const long long slot = chunk * kFarChunk + k;
+      red_add(F + (__ldcs(far.rows + slot) - lo), __ldcs(far.vals + slot));
+    }
+  }
+  __syncthreads();   // s_pre is reused by the next pass of a persistent caller
+}
+
+__global__ void __launch_bounds__(kApplyThreads)
+k_apply_far(double *__restrict__ F, Far far, long long lo, const Ctl *ctl) {
+  if (ctl->done) return;
+  apply_far_body(F, far, lo, ctl);
+}
+
 // -------------------------------------------------------------- K5 finalize --
 // Pass totals as doubles (integers < 2^53 are exact), so a distributed context
 // can all-reduce them in one call: r, loss, |S_p|, E_p, dangling, low, mid, hub.
@@ -475,7 +588,8 @@ __device__ __forceinline__ void reduce_partials(const SelPartial *__restrict__ s
   __syncthreads();
   if (threadIdx.x < kSums) {
     double t = 0.0;
-    for (int k = 0; k < W; ++k) t += s_v[threadIdx.x][k];
+    const int nw = (int)(blockDim.x >> 5);   // the fused kernel calls this with 256 threads
+    for (int k = 0; k < nw; ++k) t += s_v[threadIdx.x][k];
     out[threadIdx.x] = t;
   }
 }
@@ -679,6 +793,30 @@ __global__ void k_hot_sample(const int *row_idx, long long nnz, int stride, unsi
   const long long step = (long long)gridDim.x * blockDim.x * stride;
   for (long long e = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * stride; e < nnz; e += step)
     atomicAdd(&blk[row_idx[e] >> 10], 1u);
+}
+
+// Far-push bin capacities (setup): per bin, the edges whose row can be far --
+// outside the hot window and the warm range, and more than kNear rows from the
+// column (a group's near window always contains its columns +- kNear).
+__global__ void k_far_census(const long long *col_ptr, long long n, const int *row_idx, long long lo, int hot_lo,
+                             int warm_lo, unsigned warm_len, int shift, unsigned long long *cap) {
+  __shared__ unsigned long long s_cap[kMaxBins];
+  for (int b = threadIdx.x; b < kMaxBins; b += blockDim.x) s_cap[b] = 0ull;
+  __syncthreads();
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const long long src = i + lo;
+    for (long long e = col_ptr[i]; e < col_ptr[i + 1]; ++e) {
+      const int row = row_idx[e];
+      const long long dd = (long long)row - src;
+      if ((unsigned)(row - hot_lo) >= (unsigned)kHot && (unsigned)(row - warm_lo) >= warm_len &&
+          (dd > kNear || dd < -kNear))
+        atomicAdd(&s_cap[row >> shift], 1ull);
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < kMaxBins; b += blockDim.x)
+    if (s_cap[b]) atomicAdd(&cap[b], s_cap[b]);
 }
 
 // Start-of-run control update (no host->device memcpy inside di_run's timed path).

@@ -20,6 +20,9 @@ constexpr int kFinalizeThreads = 512;
 constexpr int kSelectCtasPerSm = 2;                  // 16 select warps/SM x 16 x 256 B loads in flight
 constexpr int kMaxSegments = 4096;                   // select warps (= frontier segments) per launch
 constexpr int kStripes = 32;                         // max scatter ticket counters (contiguous group stripes)
+constexpr int kMaxBins = 64;                         // far-push destination bins (propagation blocking)
+constexpr int kNear = 2048;                          // pushes within +-kNear rows of the group are "near"
+constexpr int kFarChunk = 128;                       // far-record slots per warp-owned chunk
 
 // Device-resident control block of one context.
 struct Ctl {
@@ -45,6 +48,8 @@ struct Ctl {
   // scatter tickets: one counter per stripe of the frontier groups, each on its
   // own 128-byte line (reset per pass with sc_next)
   alignas(128) unsigned tickets[kStripes * 32];
+  // far-push chunks opened per destination bin this pass, one counter per 128-byte line
+  alignas(128) unsigned far_cnt[kMaxBins * 32];
 };
 
 // k_select partials (one per CTA): r_p and |S_p|.
@@ -60,6 +65,29 @@ struct ScPartial {
   int dang, n_low, n_mid, n_hub;
 };
 
+// Far pushes (propagation blocking).  A push whose row lies outside the shared-
+// memory hot window, outside the L2-resident "warm" row range [warm_lo, warm_lo +
+// warm_len) and more than kNear rows away from its group's columns would miss L2
+// (a random DRAM sector read-modify-write); it is appended instead as a (row,
+// value) record to the bin of its row (row >> shift), and k_apply_far adds the
+// records bin by bin, each bin's slice of F staying L2-resident while it is
+// applied.  Records go to kFarChunk-slot chunks: each scatter warp owns one open
+// chunk per bin (state in shared memory) and takes a new one with a single atomic
+// on the bin's chunk counter; a closed chunk stores its fill count.  Bin b owns
+// chunks [coff[b], coff[b+1]) (capacity from an exact census at create plus the
+// per-warp waste bound), records at slot chunk * kFarChunk + k.
+struct Far {
+  int on;
+  int warm_lo;
+  unsigned warm_len;
+  int shift;                 // bin = row >> shift
+  int n_bins;
+  int *rows;                 // [n_chunks * kFarChunk]
+  double *vals;
+  int *fill;                 // [n_chunks] records in each closed chunk
+  const long long *coff;     // [n_bins + 1] first chunk of each bin
+};
+
 struct Graph {
   const long long *col_ptr;  // [n+1] owned columns, local (starting at 0)
   const int *row_idx;        // [nnz] GLOBAL row ids
@@ -70,6 +98,7 @@ struct Graph {
   long long lo;              // first owned global id (0 on one GPU)
   double *G;                 // remote outbox over global ids, or nullptr on one GPU
   unsigned char *dflags;     // dirty flag per 32-row block of G
+  Far far;
 };
 
 // Frontier of one pass, compacted per select warp: warp w scans the owned nodes

@@ -9,9 +9,11 @@ ap.add_argument("--config", default="C4")
 ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--max-passes", type=int, default=40)
 ap.add_argument("--policy", default="hybrid")
+ap.add_argument("--opt", action="append", default=[])
 a = ap.parse_args()
 p = gen.config(a.config, 1, n=a.n)
-opts = di.default_options(max_passes=a.max_passes, check_interval=8, pass_kernel=1,
+kw = {k: int(v) for k, v in (o.split("=") for o in a.opt)}
+opts = di.default_options(max_passes=a.max_passes, check_interval=8, pass_kernel=1, **kw,
                           policy=di.DI_POLICY_GEOM if a.policy == "geom" else di.DI_POLICY_HYBRID)
 ctx = di.di_create(p.n, p.col_ptr, p.row_idx, p.values, p.b, p.d, opts)
 t = time.perf_counter()

@@ -24,9 +24,12 @@ import paper_1202_6168_b200 as di
 pytestmark = pytest.mark.gpu
 
 
+ALPHA, FRAC = 2.0, 0.15      # bench.py's --alpha / --hybrid-frac defaults
+
+
 def _bench_opts(policy):
     # bench.py's launch configuration (profile=1: per-kernel CUDA events in the graph)
-    return di.default_options(policy=policy, profile=1)
+    return di.default_options(policy=policy, profile=1, alpha=ALPHA, hybrid_frac=FRAC)
 
 
 def _sampled_identity(n, cp, ri, H, F, b, d, rows):
@@ -84,13 +87,13 @@ def _full_scale_case(p, policy, n_oracle_passes):
     assert r / (1 - p.d) <= 1e-8 * bn
     # first passes against the oracle on the same input (tie-aware, reading R8)
     P = oracle.Problem(n, cp, ri, None, None, p.d)
-    st = P.init()
+    st = P.init(ALPHA)
     near = []
     for _ in range(n_oracle_passes):
         T = st.T
         a = np.abs(st.F)
         near.append(int((np.abs(a - T) <= 1e-12 * T).sum()))
-        P.snapshot(st, p.stop, policy, max_passes=1)
+        P.snapshot(st, p.stop, policy, ALPHA, FRAC, max_passes=1)
     k = n_oracle_passes
     first_tie = next((q for q in range(k) if near[q] > 0), k)
     o = np.array([l[3] for l in st.log[:k]])

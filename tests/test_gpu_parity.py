@@ -177,6 +177,7 @@ VARIANTS = {
     "interleave": {"scatter_kernel": 2},               # static warp interleave + dynamic tail
     "runs": {"scatter_run": 7, "scatter_stripes": 3},  # other grab run / stripe counts
     "nohot": {"hot_window": -1},                       # every push an L2 RED
+    "far": {"far_push": 1, "far_warm_log2": 16},       # far-push bins forced on (auto: F > 64 MB)
 }
 
 
