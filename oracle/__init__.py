@@ -20,6 +20,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 
 GEOM, HYBRID = 0, 1
+KEY_RAW, KEY_EDGE, KEY_PAPER = 0, 1, 2
 OK, ERR_ARG, ERR_OOM, ERR_NOT_CONVERGED, ERR_SINGULAR = 0, 1, 2, 3, 4
 
 
@@ -59,6 +60,11 @@ def _L():
         lib.orc_init.restype = f64
         lib.orc_dit_snapshot.argtypes = [i64, vp, vp, vp, f64, f64, i32, f64, f64, i64,
                                          vp, vp, vp, vp, vp, i64, vp]
+        lib.orc_key_weights.argtypes = [i64, vp, vp, i32, vp]
+        lib.orc_init_key.argtypes = [i64, vp, f64, vp, vp, vp]
+        lib.orc_init_key.restype = f64
+        lib.orc_dit_snapshot_key.argtypes = [i64, vp, vp, vp, f64, f64, i32, f64, f64, i64, vp,
+                                             vp, vp, vp, vp, vp, i64, vp]
         lib.orc_dit_sequential.argtypes = [i64, vp, vp, vp, f64, f64, f64, i64, vp, vp, vp, vp]
         lib.orc_jacobi.argtypes = [i64, vp, vp, vp, f64, vp, f64, i64, vp, vp]
         lib.orc_dense_solve.argtypes = [i64, vp, vp, vp, f64, vp, vp]
@@ -120,16 +126,29 @@ class State:
     log: list = field(default_factory=list)
 
 
-class Problem:
-    """Marshalled (P, B, d): CSC column j = out-edges of j."""
+def key_weights(n, col_ptr, row_idx, key: int):
+    """fp32 selection-key weights w_i (orc_key_weights)."""
+    w = np.empty(int(n), dtype=np.float32)
+    cp = _c(col_ptr, np.int64)
+    ri = _c(row_idx, np.int32) if len(row_idx) else np.zeros(1, np.int32)
+    if _L().orc_key_weights(int(n), _p(cp), _p(ri), int(key), _p(w)):
+        raise ValueError("bad key args")
+    return w
 
-    def __init__(self, n, col_ptr, row_idx, values=None, b=None, d=0.85):
+
+class Problem:
+    """Marshalled (P, B, d): CSC column j = out-edges of j.  `key`
+    selects the selection key of init/snapshot/solve (KEY_RAW default)."""
+
+    def __init__(self, n, col_ptr, row_idx, values=None, b=None, d=0.85, key: int = KEY_RAW):
         self.n = int(n)
         self.col_ptr = _c(col_ptr, np.int64)
         self.row_idx = _c(row_idx, np.int32) if len(row_idx) else np.zeros(1, np.int32)
         self.values = _c(values, np.float64)
         self.d = float(d)
         self.b = _c(b, np.float64) if b is not None else np.full(self.n, (1.0 - self.d) / self.n)
+        self.key = int(key)
+        self.kw = None if self.key == KEY_RAW else key_weights(self.n, self.col_ptr, self.row_idx, self.key)
 
     def _args(self):
         return (self.n, _p(self.col_ptr), _p(self.row_idx), _p(self.values), self.d)
@@ -137,7 +156,7 @@ class Problem:
     def init(self, alpha: float = 1.5) -> State:
         F = np.empty(self.n)
         H = np.empty(self.n)
-        T = _L().orc_init(self.n, _p(self.b), alpha, _p(F), _p(H))
+        T = _L().orc_init_key(self.n, _p(self.b), alpha, _p(self.kw), _p(F), _p(H))
         return State(F, H, T)
 
     def snapshot(self, st: State, target: float, policy: int = HYBRID, alpha: float = 1.5,
@@ -150,9 +169,9 @@ class Problem:
         p = ctypes.c_int64(0)              # log indices relative to this call
         e = ctypes.c_int64(st.edges)
         n, cpp, rip, vp, d = self._args()
-        rc = _L().orc_dit_snapshot(n, cpp, rip, vp, d, target, policy, alpha, hybrid_frac,
-                                   max_passes, _p(st.F), _p(st.H), ctypes.byref(T), ctypes.byref(p),
-                                   log, cap, ctypes.byref(e))
+        rc = _L().orc_dit_snapshot_key(n, cpp, rip, vp, d, target, policy, alpha, hybrid_frac,
+                                       max_passes, _p(self.kw), _p(st.F), _p(st.H), ctypes.byref(T),
+                                       ctypes.byref(p), log, cap, ctypes.byref(e))
         for k in range(min(p.value, cap)):
             L = log[k]
             st.log.append((p0 + k, L.T, L.r, L.frontier, L.edges, L.dangling))

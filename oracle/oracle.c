@@ -135,17 +135,56 @@ double orc_l1(int64_t n, const double *v) {
   return r;
 }
 
-/* Initialisation: H := 0, F := B.  T_0 = max_i |B_i| / alpha
+/* ------------------------------------------------------------------------ *
+ * Selection key weights.  The paper picks                        *
+ *   i_n = argmax_i (F_{n-1})_i / ((#in_i + 1) x (#out_i + 1))                 *
+ * and approximates the argmax by a threshold on the same quantity (P:213-   *
+ * 216).  key_i = |F_i| * w_i with                                            *
+ *   ORC_KEY_RAW   w_i = 1                       (BASELINE north_star, R3)    *
+ *   ORC_KEY_EDGE  w_i = 1 / (#out_i + 1)         *
+ *   ORC_KEY_PAPER w_i = 1 / ((#in_i + 1)(#out_i + 1))   (f1 (i))      *
+ * #out_i = stored entries of column i, #in_i = stored entries of row i      *
+ * ("number of incoming (resp. outgoing) links").  w_i is computed  *
+ * in fp64 and rounded once to fp32 (reading R20: the GPU keeps 4 B/node);    *
+ * the test is |F_i| * (double)w_i > T in fp64.                               *
+ * ------------------------------------------------------------------------ */
+int orc_key_weights(int64_t n, const int64_t *col_ptr, const int32_t *row_idx, int32_t key, float *w) {
+  if (n < 1 || key < ORC_KEY_RAW || key > ORC_KEY_PAPER) return ORC_ERR_ARG;
+  int64_t *in = (int64_t *)calloc((size_t)n, sizeof(int64_t));
+  if (!in) return ORC_ERR_OOM;
+  for (int64_t e = 0; e < col_ptr[n]; ++e) in[row_idx[e]] += 1;
+  for (int64_t i = 0; i < n; ++i) {
+    const double out = (double)(col_ptr[i + 1] - col_ptr[i]);
+    double x = 1.0;
+    if (key == ORC_KEY_EDGE) x = 1.0 / (out + 1.0);
+    else if (key == ORC_KEY_PAPER) x = 1.0 / (((double)in[i] + 1.0) * (out + 1.0));
+    w[i] = (float)x;
+  }
+  free(in);
+  return ORC_OK;
+}
+
+static inline double sel_key(const double *F, const float *kw, int64_t i) {
+  return kw ? fabs(F[i]) * (double)kw[i] : fabs(F[i]);
+}
+
+/* Initialisation: H := 0, F := B.  T_0 = max_i key_i(B) / alpha
  * (reading §8c-Q5: the paper gives no T_0; with strict ">" the first pass
- * then selects every node of a uniform B). */
-double orc_init(int64_t n, const double *b, double alpha, double *F, double *H) {
+ * then selects every node of maximal key, e.g. every node of a uniform B
+ * under the raw key).  kw = NULL is the raw key. */
+double orc_init_key(int64_t n, const double *b, double alpha, const float *kw, double *F, double *H) {
   double mx = 0.0;
   for (int64_t i = 0; i < n; ++i) {
     F[i] = b[i];
     H[i] = 0.0;
-    if (fabs(b[i]) > mx) mx = fabs(b[i]);
+    const double k = sel_key(b, kw, i);
+    if (k > mx) mx = k;
   }
   return mx / alpha;
+}
+
+double orc_init(int64_t n, const double *b, double alpha, double *F, double *H) {
+  return orc_init_key(n, b, alpha, NULL, F, H);
 }
 
 /* ------------------------------------------------------------------------ *
@@ -154,8 +193,9 @@ double orc_init(int64_t n, const double *b, double alpha, double *F, double *H) 
  *   1. r_p = sum_i |F_i|  (|.| for signed P, reading §8c-Q9)    *
  *   2. stop if r_p < target (P:124 stops on r/(1-d) <= Target; BASELINE.json  *
  *      states the target on |F|_1 directly)                                  *
- *   3. S_p = [ i ascending : |F_i| > T_p ]  ("all i such that (F_n)_i *
- *      is above a threshold T_k are chosen"; strict, reading §8c-Q7)          *
+ *   3. S_p = [ i ascending : key_i > T_p ]  ("all i such that (F_n)_i *
+ *      is above a threshold T_k are chosen"; strict, reading §8c-Q7; key_i =   *
+ *      |F_i| w_i, see orc_key_weights; raw key |F_i| when kw = NULL)          *
  *   4. for i in S_p: s_i = F_i; F_i = 0; H_i += s_i                           *
  *   5. for i in S_p ascending, for each child j: F_j += s_i * p_ji            *
  *      (this is eq. defF with J_S = sum_{i in S_p} J_i, a valid D-iteration by  *
@@ -166,11 +206,11 @@ double orc_init(int64_t n, const double *b, double alpha, double *F, double *H) 
  * The log records (p, T_p, r_p, |S_p|, E_p = sum_{i in S_p} #out_i, dangling   *
  * takes).  E_p counts elementary diffusions.                     *
  * ------------------------------------------------------------------------ */
-int orc_dit_snapshot(int64_t n, const int64_t *col_ptr, const int32_t *row_idx,
-                     const double *vals, double d, double target, int32_t policy,
-                     double alpha, double hybrid_frac, int64_t max_passes,
-                     double *F, double *H, double *T_io, int64_t *pass_io,
-                     orc_pass_log *log, int64_t log_cap, int64_t *edges_io) {
+int orc_dit_snapshot_key(int64_t n, const int64_t *col_ptr, const int32_t *row_idx,
+                         const double *vals, double d, double target, int32_t policy,
+                         double alpha, double hybrid_frac, int64_t max_passes, const float *kw,
+                         double *F, double *H, double *T_io, int64_t *pass_io,
+                         orc_pass_log *log, int64_t log_cap, int64_t *edges_io) {
   if (n < 1 || !(alpha > 1.0) || !(d > 0.0 && d < 1.0)) return ORC_ERR_ARG;
   int32_t *S = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
   double *s = (double *)malloc(sizeof(double) * (size_t)n);
@@ -186,7 +226,7 @@ int orc_dit_snapshot(int64_t n, const int64_t *col_ptr, const int32_t *row_idx,
     /* 3. selection */
     int64_t cnt = 0, E = 0, dang = 0;
     for (int64_t i = 0; i < n; ++i)
-      if (fabs(F[i]) > T) S[cnt++] = (int32_t)i;
+      if (sel_key(F, kw, i) > T) S[cnt++] = (int32_t)i;
     /* 4. take */
     for (int64_t k = 0; k < cnt; ++k) {
       int64_t i = S[k];
@@ -218,6 +258,15 @@ int orc_dit_snapshot(int64_t n, const int64_t *col_ptr, const int32_t *row_idx,
   *pass_io = p;
   free(S); free(s);
   return rc;
+}
+
+int orc_dit_snapshot(int64_t n, const int64_t *col_ptr, const int32_t *row_idx,
+                     const double *vals, double d, double target, int32_t policy,
+                     double alpha, double hybrid_frac, int64_t max_passes,
+                     double *F, double *H, double *T_io, int64_t *pass_io,
+                     orc_pass_log *log, int64_t log_cap, int64_t *edges_io) {
+  return orc_dit_snapshot_key(n, col_ptr, row_idx, vals, d, target, policy, alpha, hybrid_frac,
+                              max_passes, NULL, F, H, T_io, pass_io, log, log_cap, edges_io);
 }
 
 /* ------------------------------------------------------------------------ *

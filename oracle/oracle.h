@@ -7,6 +7,7 @@
 
 enum { ORC_OK = 0, ORC_ERR_ARG = 1, ORC_ERR_OOM = 2, ORC_ERR_NOT_CONVERGED = 3, ORC_ERR_SINGULAR = 4 };
 enum { ORC_GEOM = 0, ORC_HYBRID = 1 };
+enum { ORC_KEY_RAW = 0, ORC_KEY_EDGE = 1, ORC_KEY_PAPER = 2 };
 
 typedef struct {
   int64_t pass;      /* p */
@@ -25,6 +26,13 @@ int64_t orc_diffuse_node(int64_t n, const int64_t *col_ptr, const int32_t *row_i
                          const double *vals, double d, int64_t i, double *F, double *H);
 double orc_l1(int64_t n, const double *v);
 double orc_init(int64_t n, const double *b, double alpha, double *F, double *H);
+int orc_key_weights(int64_t n, const int64_t *col_ptr, const int32_t *row_idx, int32_t key, float *w);
+double orc_init_key(int64_t n, const double *b, double alpha, const float *kw, double *F, double *H);
+int orc_dit_snapshot_key(int64_t n, const int64_t *col_ptr, const int32_t *row_idx,
+                         const double *vals, double d, double target, int32_t policy,
+                         double alpha, double hybrid_frac, int64_t max_passes, const float *kw,
+                         double *F, double *H, double *T_io, int64_t *pass_io,
+                         orc_pass_log *log, int64_t log_cap, int64_t *edges_io);
 int orc_dit_snapshot(int64_t n, const int64_t *col_ptr, const int32_t *row_idx,
                      const double *vals, double d, double target, int32_t policy,
                      double alpha, double hybrid_frac, int64_t max_passes,

@@ -408,3 +408,86 @@ def test_partition_equal_degrees_is_uniform():
     for n, K in [(12, 3), (100, 4), (64, 8)]:
         cost = np.arange(n + 1, dtype=np.int64) * 5
         np.testing.assert_array_equal(oracle.partition_cb(cost, K), oracle.partition_uniform(n, K))
+
+
+# ----------------------------------------------------- selection key (f1) ---
+# i_n = argmax F_i / ((#in_i + 1)(#out_i + 1)), approximated by a
+# threshold; per-edge variant 1/(#out_i + 1).
+
+KEY_GRAPH = (3, [(0, 1), (0, 2), (1, 2), (2, 0)])   # edges j -> i; #out = 2,1,1; #in = 1,1,2
+
+
+def test_key_weights_hand():
+    """Hand values: #out = (2,1,1), #in = (1,1,2) -> per-edge 1/3, 1/2, 1/2;
+    paper 1/(2*3), 1/(2*2), 1/(3*2); each rounded once to fp32 (reading R20)."""
+    n, edges = KEY_GRAPH
+    cp, ri = csc_from_edges(n, edges)
+    np.testing.assert_array_equal(oracle.key_weights(n, cp, ri, oracle.KEY_RAW), np.ones(3, np.float32))
+    np.testing.assert_array_equal(oracle.key_weights(n, cp, ri, oracle.KEY_EDGE),
+                                  np.array([1 / 3, 1 / 2, 1 / 2], np.float32))
+    np.testing.assert_array_equal(oracle.key_weights(n, cp, ri, oracle.KEY_PAPER),
+                                  np.array([1 / 6, 1 / 4, 1 / 6], np.float32))
+
+
+@pytest.mark.parametrize("key,expect", [(oracle.KEY_RAW, 3), (oracle.KEY_EDGE, 2), (oracle.KEY_PAPER, 1)])
+def test_key_first_pass_hand(key, expect):
+    """Uniform B = b, alpha = 1.2.  raw: T0 = b/1.2 < b = every key -> 3 nodes.
+    per-edge: keys b/3, b/2, b/2, T0 = (b/2)/1.2 = b/2.4 -> nodes 1, 2.
+    paper: keys b/6, b/4, b/6, T0 = (b/4)/1.2 = b/4.8 -> node 1 only."""
+    n, edges = KEY_GRAPH
+    cp, ri = csc_from_edges(n, edges)
+    P = oracle.Problem(n, cp, ri, key=key)
+    st = P.init(1.2)
+    P.snapshot(st, 0.0, oracle.GEOM, 1.2, max_passes=1)
+    assert st.log[0][3] == expect
+    sel = np.flatnonzero(st.H > 0)
+    assert list(sel) == {3: [0, 1, 2], 2: [1, 2], 1: [1]}[expect]
+
+
+@pytest.mark.parametrize("key", [oracle.KEY_EDGE, oracle.KEY_PAPER])
+@pytest.mark.parametrize("policy", [oracle.GEOM, oracle.HYBRID])
+def test_key_same_fixed_point(key, policy):
+    """Any selection order converges to the same X: the keyed run
+    reaches LAPACK's solution on a random graph with dangling nodes."""
+    n = 300
+    cp, ri = gen.web_graph(n, 5, window=50, max_deg=40)
+    X = np.linalg.solve(np.eye(n) - p_matrix(n, cp, ri).toarray(), np.full(n, (1 - D) / n))
+    P = oracle.Problem(n, cp, ri, key=key)
+    st = P.init()
+    assert P.snapshot(st, 1e-15, policy) == oracle.OK
+    assert np.abs(st.H - X).sum() <= 1e-13
+
+
+@pytest.mark.parametrize("key,wv", [(oracle.KEY_EDGE, 0.5), (oracle.KEY_PAPER, 0.25)])
+def test_key_on_cycle_equals_raw(key, wv):
+    """Directed cycle: #in = #out = 1, so w = 1/2 (per-edge) or 1/4 (paper) on every
+    node, exact in fp32: keyed selection is the raw selection with T scaled by w,
+    so the logs (frontier, edges) coincide pass for pass."""
+    n = 50
+    cp, ri = csc_from_edges(n, [(j, (j + 1) % n) for j in range(n)])
+    rng = np.random.default_rng(3)
+    b = rng.random(n) * 0.15 / n
+    np.testing.assert_array_equal(oracle.key_weights(n, cp, ri, key), np.full(n, wv, np.float32))
+    logs = []
+    for k in (oracle.KEY_RAW, key):
+        P = oracle.Problem(n, cp, ri, b=b, key=k)
+        st = P.init()
+        P.snapshot(st, 1e-12, oracle.HYBRID)
+        logs.append([(l[3], l[4]) for l in st.log])
+    assert logs[0] == logs[1]
+
+
+def test_key_reduces_work_weblike():
+    """The degree-weighted key is the paper's heuristic for cheaper convergence
+    (P:208-212); on a web-like graph (N = 2e5, HYBRID) the per-edge and paper keys
+    need fewer elementary diffusions than the raw key (18.9 ->
+    13.9 / 12.7 normalized iterations)."""
+    p = gen.config("C2", 1, n=200_000)
+    work = {}
+    for k in (oracle.KEY_RAW, oracle.KEY_EDGE, oracle.KEY_PAPER):
+        P = oracle.Problem(p.n, p.col_ptr, p.row_idx, key=k)
+        st = P.init()
+        assert P.snapshot(st, 1e-9 * 0.15, oracle.HYBRID) == oracle.OK
+        work[k] = st.edges / p.nnz
+    assert work[oracle.KEY_EDGE] < 0.9 * work[oracle.KEY_RAW]
+    assert work[oracle.KEY_PAPER] < 0.9 * work[oracle.KEY_RAW]
