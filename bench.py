@@ -48,6 +48,19 @@ WORKLOADS = {
 }
 L2_BYTES = 126 * 2 ** 20
 
+# Launch configuration per workload: (policy, alpha, hybrid_frac, select_key) with
+# policy 0 = GEOM / 1 = HYBRID (reading R4) and key 0 = raw |F_i|, 1 = per-edge
+# |F_i|/(#out_i+1).  Tuned on B200 within the paper's
+# alpha range [1.2, 2]; DESIGN.md §7 has the sweep.  Every choice is
+# the same method (any order converges to the same X).
+SCHEDULES = {
+    "C1": (1, 1.5, 0.05, 0),
+    "C2": (1, 2.0, 0.30, 1),
+    "C3": (1, 2.0, 0.15, 1),
+    "C4": (1, 2.0, 0.50, 1),
+    "C5": (1, 2.0, 0.15, 0),
+}
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -59,11 +72,11 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--policy", default=None, choices=[None, "geom", "hybrid"])
     # threshold schedule T_k <- T_k / alpha (alpha in [1.2, 2], results "not
-    # sensitive"); HYBRID lowers T only when |S_p| <= f N (reading R4).  alpha = 2 and
-    # f = 0.15 trade fewer passes (each a full scan of F) for a few % more edges: C4
-    # 360 -> 317 ms vs the paper's default 1.5 / 0.05.
-    ap.add_argument("--alpha", type=float, default=2.0)
-    ap.add_argument("--hybrid-frac", type=float, default=0.15)
+    # sensitive"); HYBRID lowers T only when |S_p| <= f N (reading R4); see SCHEDULES
+    ap.add_argument("--alpha", type=float, default=None, help="default: SCHEDULES[config]")
+    ap.add_argument("--hybrid-frac", type=float, default=None, help="default: SCHEDULES[config]")
+    ap.add_argument("--key", type=int, default=None, choices=[0, 1, 2],
+                    help="selection key 0 raw / 1 per-edge / 2 paper; default: SCHEDULES[config]")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="bound on the oracle sample for cpu_baseline / reference steps")
     ap.add_argument("--no-e2e", action="store_true")
@@ -104,13 +117,19 @@ def load_problem(args):
 
 
 def policy_of(args):
-    import paper_1202_6168_b200 as di
+    """Fill args.alpha / hybrid_frac / key from SCHEDULES where not given; return the policy."""
+    pol, alpha, frac, key = SCHEDULES[args.config]
+    if args.alpha is None:
+        args.alpha = alpha
+    if args.hybrid_frac is None:
+        args.hybrid_frac = frac
+    if args.key is None:
+        args.key = key
     if args.policy == "geom":
-        return di.DI_POLICY_GEOM
+        return 0
     if args.policy == "hybrid":
-        return di.DI_POLICY_HYBRID
-    # SURVEY §8c-Q4 / DESIGN R4: HYBRID on web-like and signed, GEOM on R-MAT
-    return di.DI_POLICY_GEOM if args.config == "C3" else di.DI_POLICY_HYBRID
+        return 1
+    return pol
 
 
 # ------------------------------------------------------------------ clocks --
@@ -176,11 +195,16 @@ class ClockSampler:
 
 # ------------------------------------------------------------ cpu baseline --
 
-def oracle_sample(p, policy_geom: bool, seconds: float, state=None, alpha=1.5, hybrid_frac=0.05):
+_ORACLE_PROBLEM = {}
+
+
+def oracle_sample(p, policy_geom: bool, seconds: float, state=None, alpha=1.5, hybrid_frac=0.05, key=0):
     """Time the CPU oracle (as it stands, 1 thread) on snapshot passes of the same
     solve until `seconds` elapse; returns (edges, secs, passes, state)."""
     import oracle
-    P = oracle.Problem(p.n, p.col_ptr, p.row_idx, p.values, p.b, p.d)
+    if key not in _ORACLE_PROBLEM:        # key weights are setup, not timed (like di_create)
+        _ORACLE_PROBLEM[key] = oracle.Problem(p.n, p.col_ptr, p.row_idx, p.values, p.b, p.d, key=key)
+    P = _ORACLE_PROBLEM[key]
     st = state or P.init(alpha)
     pol = oracle.GEOM if policy_geom else oracle.HYBRID
     e0, p0 = st.edges, st.passes
@@ -228,10 +252,10 @@ def run_reference(args, rank, world):
     per = max(1.0, args.cpu_seconds / max(1, args.steps + args.warmup))
     st = None
     for _ in range(args.warmup):
-        _, _, _, st = oracle_sample(p, geom, per, st, args.alpha, args.hybrid_frac)
+        _, _, _, st = oracle_sample(p, geom, per, st, args.alpha, args.hybrid_frac, args.key)
     edges, secs, passes = 0, 0.0, 0
     for _ in range(args.steps):
-        e, dt, np_, st = oracle_sample(p, geom, per, st, args.alpha, args.hybrid_frac)
+        e, dt, np_, st = oracle_sample(p, geom, per, st, args.alpha, args.hybrid_frac, args.key)
         edges += e
         secs += dt
         passes += np_
@@ -243,7 +267,8 @@ def run_reference(args, rank, world):
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic",
            "config": {"workload": WORKLOADS[args.config], "n": p.n, "nnz": p.nnz,
-                      "alpha": args.alpha, "hybrid_frac": args.hybrid_frac},
+                      "alpha": args.alpha, "hybrid_frac": args.hybrid_frac,
+                      "select_key": ["raw", "per-edge", "paper"][args.key]},
            "cpu_baseline": {"value": v, "unit": "edges/s", "cores": 1, "kind": "oracle",
                             "sample": sample},
            "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -273,7 +298,7 @@ def run_ours(args, rank, world, local_rank):
     pol = policy_of(args)
     mode = di.DI_EXCHANGE_SYNC if args.exchange == "sync" else di.DI_EXCHANGE_ASYNC
     opts = di.default_options(policy=pol, device=local_rank, profile=1, exchange_mode=mode,
-                              alpha=args.alpha, hybrid_frac=args.hybrid_frac)
+                              alpha=args.alpha, hybrid_frac=args.hybrid_frac, select_key=args.key)
     comm_id, bounds, shard = None, None, None
     if dist:
         bounds = dd.partition_bounds(p.col_ptr, world, cost=args.partition, row_idx=p.row_idx)
@@ -359,7 +384,7 @@ def run_ours(args, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         e, dt, npass, st = oracle_sample(p, pol == di.DI_POLICY_GEOM, args.cpu_seconds, None,
-                                         args.alpha, args.hybrid_frac)
+                                         args.alpha, args.hybrid_frac, args.key)
         cpu = {"value": e / dt if dt > 0 else None, "unit": "edges/s", "cores": 1, "kind": "oracle",
                "sample": f"first {npass} snapshot passes ({e} edges) of the same {args.config} solve "
                          f"on the full graph, {dt:.1f}s on 1 host core"}
@@ -373,6 +398,7 @@ def run_ours(args, rank, world, local_rank):
            "config": {"workload": WORKLOADS[args.config], "n": p.n, "nnz": p.nnz,
                       "stop": p.stop, "policy": "geom" if pol == 0 else "hybrid", "seed": args.seed,
                       "alpha": args.alpha, "hybrid_frac": args.hybrid_frac,
+                      "select_key": ["raw", "per-edge", "paper"][args.key],
                       "parallelism": par,
                       "l2": ("flushed between steps (252 MB write)" if flush is not None else
                              f"inputs ({resident / 1e9:.1f} GB resident per GPU) larger than L2 (126 MB)")},

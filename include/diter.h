@@ -34,6 +34,7 @@
 #ifndef DITER_H
 #define DITER_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -64,6 +65,16 @@ typedef enum {
 enum {
   DI_POLICY_GEOM = 0,      /* T <- T/alpha after every pass (literal "scale down progressively") */
   DI_POLICY_HYBRID = 1     /* T <- T/alpha iff |S_p| <= hybrid_frac * N, else T unchanged */
+};
+
+/* Selection keys (readings R3, R20).  Pass p selects
+   {i : |F_i| w_i > T_p} with fp32 weights w_i computed once at create in fp64 and
+   rounded to nearest fp32; T_0 = max_i |B_i| w_i / alpha. */
+enum {
+  DI_KEY_RAW = 0,          /* w_i = 1 (BASELINE north_star "above a per-pass threshold") */
+  DI_KEY_EDGE = 1,         /* w_i = 1 / (#out_i + 1): per-edge key, out-degree only */
+  DI_KEY_PAPER = 2         /* w_i = 1 / ((#in_i + 1)(#out_i + 1)): the paper's argmax key
+                              (PAPER.md:210); one GPU only (needs global in-degrees) */
 };
 
 /* Exchange modes of distributed contexts. */
@@ -98,6 +109,8 @@ typedef struct {
                               removes; on a pure Zipf-over-id graph it wins, 18.2 -> 13.8 ms/pass);
                               -1 = off */
   int32_t far_warm_log2;   /* log2 of the warm row range kept on direct L2 REDs; 0 = default (21) */
+  int32_t select_key;      /* DI_KEY_*; default DI_KEY_RAW */
+  int32_t reserved[7];
 } di_options;
 
 /* One record per executed pass (device-logged, read with di_get_pass_log). */
@@ -139,6 +152,11 @@ typedef struct {
 
 /* Fill *opt with the defaults above. */
 DI_API void di_default_options(di_options *opt);
+
+/* sizeof of the ABI structs as compiled into the library (which: 0 = di_options,
+ * 1 = di_stats, 2 = di_pass_log; anything else returns 0), so a binding can check
+ * its own layout against the library's. */
+DI_API size_t di_struct_size(int32_t which);
 
 /* Single-GPU context.  n nodes; col_ptr[n+1] (int64, col_ptr[0] = 0,
  * non-decreasing, col_ptr[n] = nnz); row_idx[nnz] (int32 in [0,n)).

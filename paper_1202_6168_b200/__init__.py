@@ -25,13 +25,14 @@ DI_OK, DI_ERR_INVALID_ARG, DI_ERR_CONTRACTION, DI_ERR_OOM, DI_ERR_CUDA, DI_ERR_N
     DI_ERR_NOT_CONVERGED, DI_ERR_STATE, DI_ERR_UNSUPPORTED = range(9)
 DI_POLICY_GEOM, DI_POLICY_HYBRID = 0, 1
 DI_EXCHANGE_SYNC, DI_EXCHANGE_ASYNC = 0, 1
+DI_KEY_RAW, DI_KEY_EDGE, DI_KEY_PAPER = 0, 1, 2
 
 STATUS_NAMES = {0: "DI_OK", 1: "DI_ERR_INVALID_ARG", 2: "DI_ERR_CONTRACTION", 3: "DI_ERR_OOM",
                 4: "DI_ERR_CUDA", 5: "DI_ERR_NCCL", 6: "DI_ERR_NOT_CONVERGED", 7: "DI_ERR_STATE",
                 8: "DI_ERR_UNSUPPORTED"}
 
 # every symbol include/diter.h declares (checked by tests/test_abi.py)
-EXPORTS = ["di_default_options", "di_create", "di_create_dist", "di_get_unique_id", "di_reset", "di_run",
+EXPORTS = ["di_default_options", "di_struct_size", "di_create", "di_create_dist", "di_get_unique_id", "di_reset", "di_run",
            "di_get_history", "di_get_fluid", "di_get_history_device", "di_get_fluid_device",
            "di_get_residual", "di_get_stats", "di_get_pass_log", "di_last_error", "di_destroy",
            "di_csc_from_coo", "di_partition_cb"]
@@ -51,7 +52,8 @@ class di_options(ctypes.Structure):
                 ("scatter_kernel", ctypes.c_int32), ("profile", ctypes.c_int32),
                 ("pass_kernel", ctypes.c_int32), ("hot_window", ctypes.c_int32),
                 ("scatter_run", ctypes.c_int32), ("scatter_stripes", ctypes.c_int32),
-                ("far_push", ctypes.c_int32), ("far_warm_log2", ctypes.c_int32)]
+                ("far_push", ctypes.c_int32), ("far_warm_log2", ctypes.c_int32),
+                ("select_key", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
 
 
 class di_pass_log(ctypes.Structure):
@@ -92,6 +94,7 @@ def load_library() -> ctypes.CDLL:
     st = ctypes.c_int
     sig = {
         "di_default_options": (None, [ctypes.POINTER(di_options)]),
+        "di_struct_size": (ctypes.c_size_t, [i32]),
         "di_create": (st, [ctypes.POINTER(vp), i64, vp, vp, vp, vp, f64, ctypes.POINTER(di_options)]),
         "di_create_dist": (st, [ctypes.POINTER(vp), i32, i32, vp, vp, i64, vp, vp, vp, vp, f64,
                                 ctypes.POINTER(di_options)]),

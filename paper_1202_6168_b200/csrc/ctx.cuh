@@ -33,6 +33,7 @@ struct di_ctx {
   double *G = nullptr;           // remote outbox over global ids (distributed only)
   unsigned char *dflags = nullptr;  // dirty flag per 32-row block of G
   double *H = nullptr;           // history [n_local]
+  float *kw = nullptr;           // selection-key weights [n_local] (nullptr = raw key |F_i|)
   diter::Frontier fr{};
   diter::Far far{};               // far-push bins (propagation blocking), 1 GPU
   long long *far_off = nullptr;   // [n_bins + 1] first chunk of each bin (device)

@@ -411,7 +411,7 @@ static di_status exchange(di_ctx *ctx, bool send_now) {
 static void launch_pass_kernels(di_ctx *ctx) {
   Graph g = diter_graph(ctx);
   k_select<<<ctx->grid_select, kSelectThreads, 0, ctx->stream>>>(ctx->F, ctx->H, ctx->fr, ctx->n_local, ctx->ctl,
-                                                                ctx->sel_part);
+                                                                ctx->sel_part, ctx->kw);
   if (ctx->vals)
     k_scatter<true><<<ctx->grid_scatter, kScatterThreads, ctx->scatter_smem, ctx->stream>>>(
         g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part);

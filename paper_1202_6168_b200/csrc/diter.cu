@@ -42,6 +42,15 @@ void diter_set_err(di_ctx *ctx, const char *fmt, ...) {
     }                                                                                  \
   } while (0)
 
+extern "C" size_t di_struct_size(int32_t which) {
+  switch (which) {
+    case 0: return sizeof(di_options);
+    case 1: return sizeof(di_stats);
+    case 2: return sizeof(di_pass_log);
+    default: return 0;
+  }
+}
+
 extern "C" void di_default_options(di_options *o) {
   if (!o) return;
   std::memset(o, 0, sizeof(*o));
@@ -80,7 +89,7 @@ static void free_ctx(di_ctx *c) {
     if (e) cudaEventDestroy(e);
   void *ptrs[] = {c->col_ptr, c->row_idx, c->vals, c->d_b, c->F, c->H, c->fr.ids, c->fr.S, c->fr.seg_cnt,
                   c->fr.hub_w, c->fr.hub_b0, c->fr.hub_deg, c->fr.hub_chunk, c->sel_part, c->sc_part,
-                  c->l1_part, c->l1_out, c->ctl, c->log, c->far_off, c->far.rows, c->far.vals, c->far.fill};
+                  c->l1_part, c->l1_out, c->ctl, c->log, c->far_off, c->far.rows, c->far.vals, c->far.fill, c->kw};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
@@ -237,6 +246,34 @@ static di_status setup_far(di_ctx *ctx) {
   return DI_OK;
 }
 
+// Selection-key weights (DI_KEY_*, reading R20).  The paper key needs the global
+// in-degree of every owned row, which a distributed rank does not hold.
+static di_status setup_key(di_ctx *ctx) {
+  const int key = ctx->opt.select_key;
+  if (key == DI_KEY_RAW) return DI_OK;
+  if (key != DI_KEY_EDGE && key != DI_KEY_PAPER) {
+    diter_set_err(ctx, "select_key must be DI_KEY_RAW, DI_KEY_EDGE or DI_KEY_PAPER");
+    return DI_ERR_INVALID_ARG;
+  }
+  if (key == DI_KEY_PAPER && ctx->world > 1) {
+    diter_set_err(ctx, "DI_KEY_PAPER needs global in-degrees: one GPU only (use DI_KEY_EDGE)");
+    return DI_ERR_INVALID_ARG;
+  }
+  const long long n = ctx->n_local;
+  TRY(dalloc(ctx, &ctx->kw, (size_t)n));
+  unsigned *indeg = nullptr;
+  if (key == DI_KEY_PAPER) {
+    TRY(dalloc(ctx, &indeg, (size_t)n));
+    CK(cudaMemsetAsync(indeg, 0, sizeof(unsigned) * n, ctx->stream));
+    k_in_degree<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->row_idx, ctx->nnz_local, indeg);
+  }
+  k_key_weights<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->col_ptr, n, indeg, key, ctx->kw);
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (indeg) cudaFree(indeg);
+  CK(cudaGetLastError());
+  return DI_OK;
+}
+
 Graph diter_graph(const di_ctx *ctx) {
   return Graph{ctx->col_ptr, ctx->row_idx, ctx->vals, ctx->n_local, ctx->d, ctx->hot_lo,
                ctx->lo, ctx->G, ctx->dflags, ctx->far};
@@ -255,7 +292,7 @@ static di_status capture_graph(di_ctx *ctx) {
   for (int k = 0; k < ctx->check_interval; ++k) {
     if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 0], ctx->stream, cudaEventRecordExternal));
     k_select<<<ctx->grid_select, kSelectThreads, 0, ctx->stream>>>(ctx->F, ctx->H, ctx->fr, ctx->n_local,
-                                                                  ctx->ctl, ctx->sel_part);
+                                                                  ctx->ctl, ctx->sel_part, ctx->kw);
     if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 1], ctx->stream, cudaEventRecordExternal));
     if (ctx->vals)
       k_scatter<true><<<ctx->grid_scatter, kScatterThreads, ctx->scatter_smem, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part);
@@ -350,6 +387,7 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
   }
   TRY(choose_hot_window(ctx));
   TRY(setup_far(ctx));
+  TRY(setup_key(ctx));
   ctx->cap_low = hc.n_low;
   ctx->cap_mid = hc.n_mid;
   ctx->cap_hub = hc.n_hub;
@@ -378,7 +416,7 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
   if (!(T0 > 0.0)) {
     double mx = 0.0;
     if (n > 0) {
-      k_max_abs<<<ctx->grid_l1, 256, 0, ctx->stream>>>(ctx->F, n, ctx->l1_part);
+      k_max_abs<<<ctx->grid_l1, 256, 0, ctx->stream>>>(ctx->F, n, ctx->l1_part, ctx->kw);
       std::vector<double> hp(ctx->grid_l1);
       CK(cudaMemcpyAsync(hp.data(), ctx->l1_part, sizeof(double) * ctx->grid_l1, cudaMemcpyDeviceToHost, ctx->stream));
       CK(cudaStreamSynchronize(ctx->stream));
@@ -474,7 +512,7 @@ extern "C" di_status di_run(di_ctx *ctx, double target) {
       Graph g = diter_graph(ctx);
       int has_hubs = ctx->cap_hub > 0 ? 1 : 0, max_p = 4 * ctx->check_interval;
       void *args[] = {&g, &ctx->F, &ctx->H, &ctx->fr, &ctx->ctl, &ctx->sel_part, &ctx->sc_part,
-                      &ctx->log, &has_hubs, &max_p};
+                      &ctx->log, &has_hubs, &max_p, &ctx->kw};
       for (;;) {
         const long long pass_before = h->pass;
         if (ctx->vals)

@@ -45,41 +45,54 @@ __device__ __forceinline__ void reset_tickets(Ctl *ctl) {
 // rank given by the ballot popcounts -- consecutive, coalesced writes instead of
 // scattered 8-byte stores, and the scatter never scans empty ranges.  Per-CTA
 // partials (r_p, |S_p|) in a fixed order make r_p deterministic for given F bytes.
-__device__ __forceinline__ void select_body(double *__restrict__ F, double *__restrict__ H, const Frontier &fr,
-                                            long long n, const double T, SelPartial *__restrict__ part) {
+template <bool KEY>
+__device__ __forceinline__ void select_loop(double *__restrict__ F, double *__restrict__ H, const Frontier &fr,
+                                            long long beg, long long end, const double T, const float *__restrict__ kw,
+                                            double &r, int &cnt) {
   const unsigned lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
-  const int gw = blockIdx.x * (kSelectThreads / 32) + (threadIdx.x >> 5);
-  const long long beg = (long long)gw * fr.seg_len;
-  const long long end = min(n, beg + fr.seg_len);
-  int* __restrict__ ids = fr.ids + beg;
-  double* __restrict__ sv = fr.S + beg;
-  double r = 0.0;
-  int cnt = 0;                                   // warp-uniform running count
+  int *__restrict__ ids = fr.ids + beg;
+  double *__restrict__ sv = fr.S + beg;
   for (long long base = beg; base < end; base += kSelectSpan) {
     double f[kSelectItems];
+    float w[KEY ? kSelectItems : 1];
 #pragma unroll
     for (int k = 0; k < kSelectItems; ++k) {
       const long long i = base + 32 * k + lane;
       f[k] = (i < end) ? F[i] : 0.0;
+      if (KEY) w[k] = (i < end) ? __ldcs(kw + i) : 0.0f;
     }
 #pragma unroll
     for (int k = 0; k < kSelectItems; ++k) {
       const long long i = base + 32 * k + lane;
       const double af = fabs(f[k]);
       r += af;
-      const bool sel = af > T;                   // f = 0 beyond `end`, never selected
+      // key_i = |F_i| w_i (reading R20); f = 0 beyond `end`, never selected
+      const bool sel = (KEY ? af * (double)w[k] : af) > T;
       const unsigned m = __ballot_sync(0xffffffffu, sel);
       if (sel) {
         const int pos = cnt + __popc(m & lt);
         F[i] = 0.0;            // F_i := 0
         red_add(H + i, f[k]);  // H_i += sent
-        ids[pos] = (int)(i);   // node and sent value, for the scatter
+        ids[pos] = (int)(i);        // node and sent value, for the scatter
         sv[pos] = f[k];
       }
       cnt += __popc(m);
     }
   }
+}
+
+__device__ __forceinline__ void select_body(double *__restrict__ F, double *__restrict__ H, const Frontier &fr,
+                                            long long n, const double T, SelPartial *__restrict__ part,
+                                            const float *__restrict__ kw) {
+  const unsigned lane = lane_id();
+  const int gw = blockIdx.x * (kSelectThreads / 32) + (threadIdx.x >> 5);
+  const long long beg = (long long)gw * fr.seg_len;
+  const long long end = min(n, beg + fr.seg_len);
+  double r = 0.0;
+  int cnt = 0;                                   // warp-uniform running count
+  if (kw) select_loop<true>(F, H, fr, beg, end, T, kw, r, cnt);
+  else select_loop<false>(F, H, fr, beg, end, T, kw, r, cnt);
   if (gw < fr.n_seg && lane == 0) fr.seg_cnt[gw] = cnt;
   r = warp_sum(r);
   __shared__ double s_r[kSelectThreads / 32];
@@ -95,9 +108,9 @@ __device__ __forceinline__ void select_body(double *__restrict__ F, double *__re
 
 __global__ void __launch_bounds__(kSelectThreads, kSelectCtasPerSm)
 k_select(double *__restrict__ F, double *__restrict__ H, Frontier fr, long long n, const Ctl *ctl,
-         SelPartial *__restrict__ part) {
+         SelPartial *__restrict__ part, const float *__restrict__ kw) {
   if (ctl->done) return;
-  select_body(F, H, fr, n, ctl->T, part);
+  select_body(F, H, fr, n, ctl->T, part, kw);
 }
 
 // ------------------------------------------------------------ K2-K4 scatter --
@@ -664,7 +677,7 @@ template <bool SIGNED>
 __global__ void __launch_bounds__(kScatterThreads)
 k_pass_fused(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ctl *ctl,
              SelPartial *__restrict__ sp, ScPartial *__restrict__ cp, di_pass_log *log,
-             int has_hubs, int max_passes) {
+             int has_hubs, int max_passes, const float *__restrict__ kw) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double s_hot[kHot];
   extern __shared__ int s_goff[];
@@ -673,7 +686,7 @@ k_pass_fused(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier f
     if (*(volatile int *)&ctl->done) break;          // written by CTA 0 before the last barrier
     unsigned long long t0 = 0, t1 = 0, t2 = 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) t0 = globaltimer_ns();
-    select_body(F, H, fr, g.n, *(volatile double *)&ctl->T, sp);
+    select_body(F, H, fr, g.n, *(volatile double *)&ctl->T, sp, kw);
     grid.sync();
     if (blockIdx.x == 0 && threadIdx.x == 0) t1 = globaltimer_ns();
     scatter_body<SIGNED>(g, F, fr, ctl, cp, s_hot, s_goff);
@@ -771,11 +784,12 @@ __global__ void k_census(const long long *col_ptr, long long n, const int *row_i
   if (bc) atomicAdd(&c->bad_contraction, bc);
 }
 
-__global__ void k_max_abs(const double *b, long long n, double *part) {
+// max_i |b_i| w_i (w = 1 without a key): T_0 = this / alpha (reading R5)
+__global__ void k_max_abs(const double *b, long long n, double *part, const float *kw) {
   double m = 0.0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    m = fmax(m, fabs(b[i]));
+    m = fmax(m, kw ? fabs(b[i]) * (double)kw[i] : fabs(b[i]));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   __shared__ double s[32];
@@ -817,6 +831,26 @@ __global__ void k_far_census(const long long *col_ptr, long long n, const int *r
   __syncthreads();
   for (int b = threadIdx.x; b < kMaxBins; b += blockDim.x)
     if (s_cap[b]) atomicAdd(&cap[b], s_cap[b]);
+}
+
+// Selection-key weights (setup, reading R20): in-degree by
+// counting stored entries per row, then w_i = fp32(1 / (#out_i + 1)) or
+// fp32(1 / ((#in_i + 1)(#out_i + 1))), each computed in fp64 and rounded once.
+__global__ void k_in_degree(const int *row_idx, long long nnz, unsigned *indeg) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += stride)
+    atomicAdd(indeg + row_idx[e], 1u);
+}
+
+__global__ void k_key_weights(const long long *col_ptr, long long n, const unsigned *indeg, int key, float *w) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double out = (double)(col_ptr[i + 1] - col_ptr[i]);
+    double x = 1.0;
+    if (key == DI_KEY_EDGE) x = 1.0 / (out + 1.0);
+    else if (key == DI_KEY_PAPER) x = 1.0 / (((double)indeg[i] + 1.0) * (out + 1.0));
+    w[i] = __double2float_rn(x);
+  }
 }
 
 // Start-of-run control update (no host->device memcpy inside di_run's timed path).

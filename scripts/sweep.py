@@ -20,12 +20,17 @@ ap.add_argument("--variants", default="")
 ap.add_argument("--policy", default="hybrid")
 a = ap.parse_args()
 p = gen.config(a.config, 1, n=a.n)
+if a.config == "C3":
+    src, dst = gen.rmat_coo(24, 1)
+    p.col_ptr, p.row_idx = di.di_csc_from_coo(p.n, src, dst)
+    del src, dst
 for v in [x for x in a.variants.split(";")] or [""]:
     kw = {}
     for item in filter(None, v.split(",")):
         k, val = item.split("=")
         kw[k.strip()] = float(val) if "." in val else int(val)
     kw.setdefault("policy", di.DI_POLICY_GEOM if a.policy == "geom" else di.DI_POLICY_HYBRID)
+    kw["policy"] = int(kw["policy"])
     ctx = di.di_create(p.n, p.col_ptr, p.row_idx, p.values, p.b, p.d, di.default_options(**kw))
     ts = []
     for _ in range(a.reps + 1):

@@ -24,12 +24,13 @@ import paper_1202_6168_b200 as di
 pytestmark = pytest.mark.gpu
 
 
-ALPHA, FRAC = 2.0, 0.15      # bench.py's --alpha / --hybrid-frac defaults
+import bench                 # bench.SCHEDULES: the launch configuration bench.py times
 
 
-def _bench_opts(policy):
+def _bench_opts(cfg):
     # bench.py's launch configuration (profile=1: per-kernel CUDA events in the graph)
-    return di.default_options(policy=policy, profile=1, alpha=ALPHA, hybrid_frac=FRAC)
+    pol, alpha, frac, key = bench.SCHEDULES[cfg]
+    return di.default_options(policy=pol, profile=1, alpha=alpha, hybrid_frac=frac, select_key=key)
 
 
 def _sampled_identity(n, cp, ri, H, F, b, d, rows):
@@ -56,9 +57,10 @@ def _sampled_identity(n, cp, ri, H, F, b, d, rows):
     return float(np.max(np.abs(F[rows] - pred) / scale))
 
 
-def _full_scale_case(p, policy, n_oracle_passes):
+def _full_scale_case(p, cfg, n_oracle_passes):
     n, cp, ri = p.n, p.col_ptr, p.row_idx
-    ctx = di.di_create(n, cp, ri, None, None, p.d, _bench_opts(policy))
+    policy, ALPHA, FRAC, key = bench.SCHEDULES[cfg]
+    ctx = di.di_create(n, cp, ri, None, None, p.d, _bench_opts(cfg))
     di.di_run(ctx, p.stop)                         # metric target (bench)
     r_metric = di.di_get_residual(ctx)
     di.di_run(ctx, p.parity_stop)                  # resumed to the parity target (reading R1)
@@ -86,7 +88,7 @@ def _full_scale_case(p, policy, n_oracle_passes):
     # bound: ||X - H||_1 <= r / (1 - d) <= 1e-8 |B|_1 (north_star tolerance)
     assert r / (1 - p.d) <= 1e-8 * bn
     # first passes against the oracle on the same input (tie-aware, reading R8)
-    P = oracle.Problem(n, cp, ri, None, None, p.d)
+    P = oracle.Problem(n, cp, ri, None, None, p.d, key=key)
     st = P.init(ALPHA)
     near = []
     for _ in range(n_oracle_passes):
@@ -103,15 +105,15 @@ def _full_scale_case(p, policy, n_oracle_passes):
 
 
 def test_c4_full_scale_parity():
-    """configs[3]: N=1e8 web-like PageRank, HYBRID (bench default)."""
+    """configs[3]: N=1e8 web-like PageRank, bench's schedule (HYBRID, per-edge key)."""
     p = gen.config("C4", 1)
-    _full_scale_case(p, di.DI_POLICY_HYBRID, 3)
+    _full_scale_case(p, "C4", 3)
 
 
 def test_c3_full_scale_parity():
-    """configs[2]: R-MAT scale 24, CSC built on the GPU (K8), GEOM (reading R4)."""
+    """configs[2]: R-MAT scale 24, CSC built on the GPU (K8), bench's schedule."""
     p = gen.config("C3", 1)
     src, dst = gen.rmat_coo(24, 1)
     p.col_ptr, p.row_idx = di.di_csc_from_coo(p.n, src, dst)
     del src, dst
-    _full_scale_case(p, di.DI_POLICY_GEOM, 3)
+    _full_scale_case(p, "C3", 3)

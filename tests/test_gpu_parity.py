@@ -156,18 +156,18 @@ def test_c2_full_parity(seed):
 _ORACLE_CACHE = {}
 
 
-def _c2_random_b_oracle(policy):
-    """Oracle run (memoised per policy) on the configs[1] graph with a random B."""
-    if policy not in _ORACLE_CACHE:
+def _c2_random_b_oracle(policy, key=0):
+    """Oracle run (memoised per policy and key) on the configs[1] graph with a random B."""
+    if (policy, key) not in _ORACLE_CACHE:
         p = gen.config("C2", 3)
         rng = np.random.default_rng(7)
         b = rng.random(p.n) + 0.5
         b *= 0.15 / b.sum()
         target = 1e-9 * 0.15
-        P = oracle.Problem(p.n, p.col_ptr, p.row_idx, None, b)
+        P = oracle.Problem(p.n, p.col_ptr, p.row_idx, None, b, key=key)
         st, near = _oracle_passes_with_ties(P, target, policy)
-        _ORACLE_CACHE[policy] = (p, b, target, st, near)
-    return _ORACLE_CACHE[policy]
+        _ORACLE_CACHE[(policy, key)] = (p, b, target, st, near)
+    return _ORACLE_CACHE[(policy, key)]
 
 
 VARIANTS = {
@@ -177,7 +177,10 @@ VARIANTS = {
     "interleave": {"scatter_kernel": 2},               # static warp interleave + dynamic tail
     "runs": {"scatter_run": 7, "scatter_stripes": 3},  # other grab run / stripe counts
     "nohot": {"hot_window": -1},                       # every push an L2 RED
-    "far": {"far_push": 1, "far_warm_log2": 16},       # far-push bins forced on (auto: F > 64 MB)
+    "far": {"far_push": 1, "far_warm_log2": 16},       # far-push bins forced on (auto: off)
+    "key_edge": {"select_key": di.DI_KEY_EDGE},        # per-edge key 1/(#out+1)
+    "key_paper": {"select_key": di.DI_KEY_PAPER},      # paper key 1/((#in+1)(#out+1))
+    "key_paper_fused": {"select_key": di.DI_KEY_PAPER, "pass_kernel": 2},
 }
 
 
@@ -187,7 +190,7 @@ def test_c2_graph_random_b_logs_exact(policy, variant):
     """configs[1] graph with a seeded random positive B: no exact-arithmetic ties with
     T_p, so frontier sizes, edges and dangling counts match the oracle pass for pass --
     for every pass-kernel / scatter-schedule option."""
-    p, b, target, st, near = _c2_random_b_oracle(policy)
+    p, b, target, st, near = _c2_random_b_oracle(policy, VARIANTS[variant].get("select_key", 0))
     H, F, log, r, stats = _gpu(p.n, p.col_ptr, p.row_idx, target, b=b, policy=policy, **VARIANTS[variant])
     assert sum(near) == 0
     _compare_logs(log, st.log)
