@@ -147,7 +147,8 @@ typedef struct {
   double kt_scatter_ms;    /* profile=1: summed device time of k_scatter over executed passes */
   double kt_finalize_ms;   /* profile=1: summed device time of k_finalize over executed passes */
   int64_t kt_passes;       /* profile=1: executed passes those sums cover */
-  int64_t scatter_bytes;   /* algorithmic bytes of the scatter kernel since create: 20 E (28 E signed) */
+  int64_t scatter_bytes;   /* algorithmic bytes of the scatter kernel since create: 20 E (28 E signed)
+                              + 16 per diffused node (its col_ptr pair) */
 } di_stats;
 
 /* Fill *opt with the defaults above. */

@@ -654,7 +654,7 @@ extern "C" di_status di_get_stats(const di_ctx *ctx, di_stats *s) {
   s->kt_scatter_ms = ctx->kt_ms[1];
   s->kt_finalize_ms = ctx->kt_ms[2];
   s->kt_passes = ctx->kt_passes;
-  s->scatter_bytes = (ctx->vals ? 28LL : 20LL) * ctx->edges;
+  s->scatter_bytes = (ctx->vals ? 28LL : 20LL) * ctx->edges + 16LL * ctx->nodes;
   return DI_OK;
 }
 
