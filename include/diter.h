@@ -204,6 +204,14 @@ DI_API di_status di_get_fluid(const di_ctx *ctx, double *f_out);
 /* Device-to-device variants: d_out is a device pointer on the context's device. */
 DI_API di_status di_get_history_device(const di_ctx *ctx, double *d_out);
 DI_API di_status di_get_fluid_device(const di_ctx *ctx, double *d_out);
+/* Completed PageRank ("one may complete by 1/N"):
+ * with dangling fluid leaving, the completed solution is X' = X / |X|_1, so this
+ * writes H_i / |H|_1 (|H|_1 by a deterministic reduction, global if distributed;
+ * collective then) into the caller's host buffer (n, or hi-lo when distributed).
+ * Meaningful for PageRank contexts (values == NULL); H approximates X within
+ * |F|_1/(1-d).  The device variant writes a device pointer. */
+DI_API di_status di_get_pagerank(di_ctx *ctx, double *x_out);
+DI_API di_status di_get_pagerank_device(di_ctx *ctx, double *d_out);
 /* Exact |F|_1 by a deterministic two-level reduction (global if distributed;
  * collective then).  Also refreshes stats.residual. */
 DI_API di_status di_get_residual(di_ctx *ctx, double *r_out);

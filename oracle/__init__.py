@@ -68,6 +68,7 @@ def _L():
         lib.orc_dit_sequential.argtypes = [i64, vp, vp, vp, f64, f64, f64, i64, vp, vp, vp, vp]
         lib.orc_jacobi.argtypes = [i64, vp, vp, vp, f64, vp, f64, i64, vp, vp]
         lib.orc_dense_solve.argtypes = [i64, vp, vp, vp, f64, vp, vp]
+        lib.orc_completed_pagerank_dense.argtypes = [i64, vp, vp, f64, vp]
         _lib = lib
     return _lib
 
@@ -210,6 +211,14 @@ class Problem:
         rc = _L().orc_dense_solve(n, cpp, rip, vp, d, _p(self.b), _p(X))
         if rc:
             raise RuntimeError(f"orc_dense_solve rc={rc}")
+        return X
+
+    def completed_pagerank_dense(self):
+        """X' of the completed (dangling -> 1/N) PageRank system, dense."""
+        X = np.empty(self.n)
+        rc = _L().orc_completed_pagerank_dense(self.n, _p(self.col_ptr), _p(self.row_idx), self.d, _p(X))
+        if rc:
+            raise RuntimeError(f"orc_completed_pagerank_dense rc={rc}")
         return X
 
     def solve(self, target: float, policy: int = HYBRID, alpha: float = 1.5,

@@ -332,23 +332,14 @@ int orc_jacobi(int64_t n, const int64_t *col_ptr, const int32_t *row_idx, const 
  * Dense solve of (I - P) X = B by Gaussian elimination with        *
  * partial pivoting (textbook; tiny N only).  A is built densely from CSC.    *
  * ------------------------------------------------------------------------ */
-int orc_dense_solve(int64_t n, const int64_t *col_ptr, const int32_t *row_idx,
-                    const double *vals, double d, const double *b, double *X) {
-  if (n < 1 || n > 4096) return ORC_ERR_ARG;
-  double *A = (double *)calloc((size_t)(n * n), sizeof(double));
-  double *y = (double *)malloc(sizeof(double) * (size_t)n);
-  if (!A || !y) { free(A); free(y); return ORC_ERR_OOM; }
-  for (int64_t i = 0; i < n; ++i) { A[i * n + i] = 1.0; y[i] = b[i]; }
-  for (int64_t j = 0; j < n; ++j) {
-    double w = vals ? 0.0 : pagerank_w(col_ptr, j, d);
-    for (int64_t e = col_ptr[j]; e < col_ptr[j + 1]; ++e)
-      A[(int64_t)row_idx[e] * n + j] -= (vals ? vals[e] : w);
-  }
+/* Gaussian elimination with partial pivoting on the dense n x n system A X = y
+ * (A and y are overwritten). */
+static int gauss_solve(int64_t n, double *A, double *y, double *X) {
   for (int64_t k = 0; k < n; ++k) {
     int64_t piv = k;
     for (int64_t i = k + 1; i < n; ++i)
       if (fabs(A[i * n + k]) > fabs(A[piv * n + k])) piv = i;
-    if (A[piv * n + k] == 0.0) { free(A); free(y); return ORC_ERR_SINGULAR; }
+    if (A[piv * n + k] == 0.0) return ORC_ERR_SINGULAR;
     if (piv != k) {
       for (int64_t c = 0; c < n; ++c) { double t = A[k * n + c]; A[k * n + c] = A[piv * n + c]; A[piv * n + c] = t; }
       double t = y[k]; y[k] = y[piv]; y[piv] = t;
@@ -365,6 +356,48 @@ int orc_dense_solve(int64_t n, const int64_t *col_ptr, const int32_t *row_idx,
     for (int64_t c = i + 1; c < n; ++c) acc -= A[i * n + c] * X[c];
     X[i] = acc / A[i * n + i];
   }
-  free(A); free(y);
   return ORC_OK;
+}
+
+int orc_dense_solve(int64_t n, const int64_t *col_ptr, const int32_t *row_idx,
+                    const double *vals, double d, const double *b, double *X) {
+  if (n < 1 || n > 4096) return ORC_ERR_ARG;
+  double *A = (double *)calloc((size_t)(n * n), sizeof(double));
+  double *y = (double *)malloc(sizeof(double) * (size_t)n);
+  if (!A || !y) { free(A); free(y); return ORC_ERR_OOM; }
+  for (int64_t i = 0; i < n; ++i) { A[i * n + i] = 1.0; y[i] = b[i]; }
+  for (int64_t j = 0; j < n; ++j) {
+    double w = vals ? 0.0 : pagerank_w(col_ptr, j, d);
+    for (int64_t e = col_ptr[j]; e < col_ptr[j + 1]; ++e)
+      A[(int64_t)row_idx[e] * n + j] -= (vals ? vals[e] : w);
+  }
+  int rc = gauss_solve(n, A, y, X);
+  free(A); free(y);
+  return rc;
+}
+
+/* Completed PageRank: the paper's "one may complete by 1/N" for a
+ * node without out-link makes Q stochastic, Q' = Q + (1/N) 1 a^T (a marks the
+ * dangling columns), and X' = d Q' X' + (1-d)/N 1 (eq. pr2 with V = 1/N).  Solved
+ * here densely from that definition (n <= 4096); SURVEY App. A.4 shows
+ * X' = X / |X|_1 for the fluid-leaves X the D-iteration computes. */
+int orc_completed_pagerank_dense(int64_t n, const int64_t *col_ptr, const int32_t *row_idx, double d,
+                                 double *X) {
+  if (n < 1 || n > 4096 || !(d > 0.0 && d < 1.0)) return ORC_ERR_ARG;
+  double *A = (double *)calloc((size_t)(n * n), sizeof(double));
+  double *y = (double *)malloc(sizeof(double) * (size_t)n);
+  if (!A || !y) { free(A); free(y); return ORC_ERR_OOM; }
+  for (int64_t i = 0; i < n; ++i) { A[i * n + i] = 1.0; y[i] = (1.0 - d) / (double)n; }
+  for (int64_t j = 0; j < n; ++j) {
+    const int64_t deg = col_ptr[j + 1] - col_ptr[j];
+    if (deg == 0) {
+      for (int64_t i = 0; i < n; ++i) A[i * n + j] -= d / (double)n;     /* completion 1/N */
+    } else {
+      for (int64_t e = col_ptr[j]; e < col_ptr[j + 1]; ++e)
+        A[(int64_t)row_idx[e] * n + j] -= d / (double)deg;
+    }
+  }
+  int rc = gauss_solve(n, A, y, X);
+  free(A); free(y);
+  return rc;
 }

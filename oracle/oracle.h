@@ -47,4 +47,6 @@ int orc_jacobi(int64_t n, const int64_t *col_ptr, const int32_t *row_idx, const 
                int64_t *iters_out);
 int orc_dense_solve(int64_t n, const int64_t *col_ptr, const int32_t *row_idx,
                     const double *vals, double d, const double *b, double *X);
+int orc_completed_pagerank_dense(int64_t n, const int64_t *col_ptr, const int32_t *row_idx, double d,
+                                 double *X);
 #endif

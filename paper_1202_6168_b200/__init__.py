@@ -34,6 +34,7 @@ STATUS_NAMES = {0: "DI_OK", 1: "DI_ERR_INVALID_ARG", 2: "DI_ERR_CONTRACTION", 3:
 # every symbol include/diter.h declares (checked by tests/test_abi.py)
 EXPORTS = ["di_default_options", "di_struct_size", "di_create", "di_create_dist", "di_get_unique_id", "di_reset", "di_run",
            "di_get_history", "di_get_fluid", "di_get_history_device", "di_get_fluid_device",
+           "di_get_pagerank", "di_get_pagerank_device",
            "di_get_residual", "di_get_stats", "di_get_pass_log", "di_last_error", "di_destroy",
            "di_csc_from_coo", "di_partition_cb"]
 
@@ -104,6 +105,8 @@ def load_library() -> ctypes.CDLL:
         "di_get_history": (st, [vp, vp]),
         "di_get_fluid": (st, [vp, vp]),
         "di_get_history_device": (st, [vp, vp]),
+        "di_get_pagerank": (st, [vp, vp]),
+        "di_get_pagerank_device": (st, [vp, vp]),
         "di_get_fluid_device": (st, [vp, vp]),
         "di_get_residual": (st, [vp, ctypes.POINTER(f64)]),
         "di_get_stats": (st, [vp, ctypes.POINTER(di_stats)]),
@@ -249,6 +252,15 @@ def di_get_history_device(ctx: Context, out):
 
 def di_get_fluid_device(ctx: Context, out):
     return _get_vec(load_library().di_get_fluid_device, ctx, out)
+
+
+def di_get_pagerank(ctx: Context, out=None):
+    """Completed PageRank H / |H|_1."""
+    return _get_vec(load_library().di_get_pagerank, ctx, out)
+
+
+def di_get_pagerank_device(ctx: Context, out):
+    return _get_vec(load_library().di_get_pagerank_device, ctx, out)
 
 
 def di_get_residual(ctx: Context) -> float:

@@ -31,7 +31,21 @@ def _deps():
 
 
 def _nccl_flags():
-    """NCCL for the multi-GPU exchange: the system header + library, else none."""
+    """NCCL for the multi-GPU exchange.  Prefer the NCCL wheel torch itself loads
+    (nvidia/nccl in site-packages, with an rpath to it): both libraries then resolve
+    the one libnccl.so.2 whichever is loaded first -- linking the older system copy
+    let libditer pull it in before torch, whose libtorch_cuda then misses newer NCCL
+    symbols.  Else the system header + library, else none."""
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+        for root in (spec.submodule_search_locations or []) if spec else []:
+            inc, lib = os.path.join(root, "include"), os.path.join(root, "lib")
+            if os.path.exists(os.path.join(inc, "nccl.h")) and os.path.exists(os.path.join(lib, "libnccl.so.2")):
+                return (["-DDITER_WITH_NCCL=1", "-I", inc],
+                        ["-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib])
+    except Exception:
+        pass
     inc = "/usr/include/nccl.h"
     lib = "/usr/lib/x86_64-linux-gnu/libnccl.so"
     if os.path.exists(inc) and os.path.exists(lib):

@@ -78,6 +78,7 @@ void diter_set_err(di_ctx *ctx, const char *fmt, ...);
 di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_idx,
                       const double *values, const double *b, const di_options *opt);
 di_status diter_l1_launch(di_ctx *ctx);
+di_status diter_l1_launch_of(di_ctx *ctx, const double *v);
 diter::Graph diter_graph(const di_ctx *ctx);
 
 // distributed hooks (dist.cu); identities / no-ops on single-GPU contexts

@@ -583,6 +583,10 @@ extern "C" di_status di_create_dist(di_ctx **out, int32_t rank, int32_t world, c
     diter_set_err(nullptr, "%s", e.c_str());
     return s;
   };
+  if (opt && opt->select_key == DI_KEY_PAPER) {     // before any collective step
+    diter_set_err(ctx, "DI_KEY_PAPER needs global in-degrees: one GPU only (use DI_KEY_EDGE)");
+    return fail(DI_ERR_INVALID_ARG);
+  }
   DistState *ds = new DistState();
   ctx->dist = ds;
   ds->bounds.assign(bounds, bounds + world + 1);

@@ -475,8 +475,11 @@ extern "C" di_status di_create(di_ctx **out, int64_t n, const int64_t *col_ptr, 
 }
 
 // Exact |F|_1 of this context's slice into ctx->l1_out (device), deterministic.
-di_status diter_l1_launch(di_ctx *ctx) {
-  k_l1_partial<<<ctx->grid_l1, kSelectThreads, 0, ctx->stream>>>(ctx->F, ctx->n_local, ctx->l1_part);
+di_status diter_l1_launch(di_ctx *ctx) { return diter_l1_launch_of(ctx, ctx->F); }
+
+// Deterministic |v|_1 of a local vector into ctx->l1_out (device).
+di_status diter_l1_launch_of(di_ctx *ctx, const double *v) {
+  k_l1_partial<<<ctx->grid_l1, kSelectThreads, 0, ctx->stream>>>(v, ctx->n_local, ctx->l1_part);
   k_l1_final<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->l1_part, ctx->grid_l1, ctx->l1_out);
   ctx->kernel_launches += 2;
   CK(cudaGetLastError());
@@ -618,6 +621,27 @@ extern "C" di_status di_get_history_device(const di_ctx *ctx, double *h) {
 extern "C" di_status di_get_fluid_device(const di_ctx *ctx, double *f) {
   return copy_out(ctx, ctx ? ctx->F : nullptr, f, cudaMemcpyDeviceToDevice);
 }
+
+// Completed PageRank H / |H|_1 (App. A.4), into d_dst (device) or h_dst (host,
+// staged in the frontier value buffer, which di_run rewrites every pass).
+static di_status pagerank_out(di_ctx *ctx, double *d_dst, double *h_dst) {
+  if (!ctx || (!d_dst && !h_dst)) { diter_set_err(ctx, "NULL argument"); return DI_ERR_INVALID_ARG; }
+  CK(cudaSetDevice(ctx->device));
+  TRY(diter_l1_launch_of(ctx, ctx->H));
+  double sh = 0.0;
+  CK(cudaMemcpyAsync(&sh, ctx->l1_out, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  sh = diter_dist_sum(ctx, sh);
+  if (!(sh > 0.0)) { diter_set_err(ctx, "|H|_1 = 0: run the solver first"); return DI_ERR_STATE; }
+  double *dst = d_dst ? d_dst : ctx->fr.S;
+  k_div<<<ctx->grid_l1, 256, 0, ctx->stream>>>(dst, ctx->H, sh, ctx->n_local);
+  ctx->kernel_launches += 1;
+  if (h_dst) CK(cudaMemcpyAsync(h_dst, dst, sizeof(double) * ctx->n_local, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return DI_OK;
+}
+extern "C" di_status di_get_pagerank(di_ctx *ctx, double *x) { return pagerank_out(ctx, nullptr, x); }
+extern "C" di_status di_get_pagerank_device(di_ctx *ctx, double *d) { return pagerank_out(ctx, d, nullptr); }
 
 extern "C" di_status di_get_residual(di_ctx *ctx, double *r_out) {
   if (!ctx || !r_out) { diter_set_err(ctx, "NULL argument"); return DI_ERR_INVALID_ARG; }

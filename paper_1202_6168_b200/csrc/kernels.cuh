@@ -745,6 +745,12 @@ k_l1_final(const double *__restrict__ part, int n_part, double *out) {
   }
 }
 
+// out_i = in_i / s  (completed PageRank H / |H|_1, App. A.4)
+__global__ void k_div(double *__restrict__ out, const double *__restrict__ in, double s, long long n) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = in[i] / s;
+}
+
 // -------------------------------------------------------------- setup kernels --
 // F = B (or (1-d)/n), H = 0
 __global__ void k_init_state(double *F, double *H, const double *b, double b_uniform, long long n) {

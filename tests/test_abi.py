@@ -62,3 +62,15 @@ def test_partition_cb_edge_cases():
     np.testing.assert_array_equal(di.di_partition_cb(cost, 5), [0, 1, 2, 3, 4, 5])
     with pytest.raises(di.DiError):
         di.di_partition_cb(cost, 6)
+
+
+def test_library_then_torch_import_order():
+    """libditer links the NCCL torch loads (rpath to the nvidia-nccl wheel): loading
+    libditer first must not break a later `import torch` (an older system libnccl
+    loaded first left libtorch_cuda without ncclDevCommCreate)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r); import paper_1202_6168_b200 as di; "
+            "di.load_library(); import torch; print('ok')") % ROOT
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]

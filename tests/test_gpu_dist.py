@@ -30,7 +30,8 @@ def run_ranks(K, n, cp, ri, vals, b, d, target, bounds, mode, key, **opts):
             ctx = di.di_create_dist(r, K, cid, bounds, n, lcp, lri, lv, lb, d, o)
             di.di_run(ctx, target)
             out[r] = (di.di_get_history(ctx), di.di_get_fluid(ctx), di.di_get_pass_log(ctx),
-                      di.di_get_stats(ctx), di.di_get_residual(ctx))
+                      di.di_get_stats(ctx), di.di_get_residual(ctx),
+                      di.di_get_pagerank(ctx) if vals is None else None)
             di.di_destroy(ctx)
         except Exception as e:          # surfaced below
             err[r] = e
@@ -48,19 +49,22 @@ def run_ranks(K, n, cp, ri, vals, b, d, target, bounds, mode, key, **opts):
     return H, F, out
 
 
-@pytest.mark.parametrize("K", [2, 4])
-def test_sync_matches_single_gpu_passes(K):
+@pytest.mark.parametrize("K,key", [(2, di.DI_KEY_RAW), (4, di.DI_KEY_RAW), (3, di.DI_KEY_EDGE)])
+def test_sync_matches_single_gpu_passes(K, key):
     """SYNC mode is the single-GPU snapshot pass: same per-pass frontier sizes,
-    edges and thresholds (random B: no exact-arithmetic ties), same fixed point."""
+    edges and thresholds (random B: no exact-arithmetic ties), same fixed point --
+    with the raw and the per-edge selection key (per-edge weights need only local
+    out-degrees)."""
     n = 200_000
     cp, ri = gen.web_graph(n, 5)
     rng = np.random.default_rng(3)
     b = rng.random(n) + 0.5
     b *= 0.15 / b.sum()
     target = 1e-9 * 0.15
-    H1, _, log1 = di.solve(n, cp, ri, target, b=b)
+    H1, _, log1 = di.solve(n, cp, ri, target, b=b, select_key=key)
     bounds = dist.partition_bounds(cp, K)
-    H, F, outs = run_ranks(K, n, cp, ri, None, b, 0.85, target, bounds, di.DI_EXCHANGE_SYNC, f"sync{K}")
+    H, F, outs = run_ranks(K, n, cp, ri, None, b, 0.85, target, bounds, di.DI_EXCHANGE_SYNC, f"sync{K}k{key}",
+                           select_key=key)
     for o in outs:        # every rank logs the same global pass records
         lg = o[2]
         np.testing.assert_array_equal(lg["frontier"], log1["frontier"])
@@ -87,6 +91,20 @@ def test_async_parity(K, cost):
     ledger = np.abs(F).sum() + 0.15 * H.sum() + 0.85 * H[deg == 0].sum()
     assert abs(ledger - bn) <= 1e-12 * bn          # no mass lost or duplicated in flight
     assert all(o[4] < p.parity_stop for o in outs)  # global residual on every rank
+    Xp = np.concatenate([o[5] for o in outs])       # completed PageRank, global |H|_1 (f4)
+    assert abs(Xp.sum() - 1.0) <= 1e-12
+    assert np.abs(Xp - X / X.sum()).sum() <= 2e-8
+
+
+def test_paper_key_rejected_on_distributed():
+    """DI_KEY_PAPER needs global in-degrees, which a rank does not hold."""
+    n = 1000
+    cp, ri = gen.uniform_graph(n, 1)
+    bounds = dist.partition_bounds(cp, 2)
+    with pytest.raises(di.DiError) as e:
+        run_ranks(2, n, cp, ri, None, None, 0.85, 1e-9, bounds, di.DI_EXCHANGE_SYNC, "paperkey",
+                  select_key=di.DI_KEY_PAPER)
+    assert e.value.status == di.DI_ERR_INVALID_ARG
 
 
 def test_async_signed():

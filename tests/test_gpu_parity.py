@@ -350,3 +350,25 @@ def test_device_getters():
     torch.cuda.synchronize()
     np.testing.assert_array_equal(h.cpu().numpy(), di.di_get_history(ctx))
     di.di_destroy(ctx)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_completed_pagerank_output(seed):
+    """NEXT f4 (completed PageRank): di_get_pagerank = H/|H|_1 against the
+    oracle's dense completed system (N = 1500 web-like graph with dangling nodes), and
+    the device variant byte-for-byte."""
+    import torch
+    n = 1500
+    cp, ri = gen.web_graph(n, seed, window=100, max_deg=200)
+    assert (np.diff(cp) == 0).sum() > 50
+    Xc = oracle.Problem(n, cp, ri).completed_pagerank_dense()
+    ctx = di.di_create(n, cp, ri)
+    di.di_run(ctx, 1e-14)
+    x = di.di_get_pagerank(ctx)
+    d = torch.empty(n, dtype=torch.float64, device="cuda")
+    di.di_get_pagerank_device(ctx, d)
+    torch.cuda.synchronize()
+    di.di_destroy(ctx)
+    assert abs(x.sum() - 1.0) <= 1e-12
+    assert np.abs(x - Xc).sum() <= 1e-11
+    np.testing.assert_array_equal(d.cpu().numpy(), x)

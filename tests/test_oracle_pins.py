@@ -491,3 +491,34 @@ def test_key_reduces_work_weblike():
         work[k] = st.edges / p.nnz
     assert work[oracle.KEY_EDGE] < 0.9 * work[oracle.KEY_RAW]
     assert work[oracle.KEY_PAPER] < 0.9 * work[oracle.KEY_RAW]
+
+
+# ------------------------------------------- completed PageRank (f4, App. A.4) ---
+
+def test_completed_pagerank_two_nodes_closed_form():
+    """0 -> 1, node 1 dangling.  Completed Q' = [[0, 1/2], [1, 1/2]]; with x0 + x1 = 1,
+    x0 = d x1 / 2 + (1-d)/2  =>  x0 = 1/(2+d), x1 = (1+d)/(2+d)."""
+    cp, ri = csc_from_edges(2, [(0, 1)])
+    X = oracle.Problem(2, cp, ri).completed_pagerank_dense()
+    np.testing.assert_allclose(X, [1 / (2 + D), (1 + D) / (2 + D)], rtol=1e-15)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_completed_pagerank_is_normalised_fluid_leaves_solution(seed):
+    """App. A.4: the completed solution sums to 1 (Q' stochastic) and equals X/|X|_1 of
+    the fluid-leaves system, here from LAPACK; and power iteration on the completed
+    Google matrix (an independent route) converges to it."""
+    n = 400
+    cp, ri = gen.web_graph(n, seed, window=30, max_deg=60)
+    assert (np.diff(cp) == 0).sum() > 20
+    Xc = oracle.Problem(n, cp, ri).completed_pagerank_dense()
+    assert abs(Xc.sum() - 1.0) <= 1e-13
+    X = lapack_solve(n, cp, ri)
+    np.testing.assert_allclose(Xc, X / X.sum(), rtol=1e-11, atol=1e-16)
+    deg = np.diff(cp)
+    G = p_matrix(n, cp, ri, d=1.0).toarray()
+    G[:, deg == 0] = 1.0 / n
+    x = np.full(n, 1.0 / n)
+    for _ in range(400):
+        x = D * G @ x + (1 - D) / n
+    np.testing.assert_allclose(Xc, x, rtol=1e-12, atol=1e-16)
