@@ -56,7 +56,7 @@ L2_BYTES = 126 * 2 ** 20
 SCHEDULES = {
     "C1": (1, 1.5, 0.05, 0),
     "C2": (1, 2.0, 0.30, 1),
-    "C3": (1, 2.0, 0.15, 1),
+    "C3": (1, 1.5, 0.05, 1),
     "C4": (1, 2.0, 0.50, 1),
     "C5": (1, 2.0, 0.15, 0),
 }

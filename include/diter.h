@@ -92,9 +92,8 @@ typedef struct {
   int64_t max_passes;      /* guard -> DI_ERR_NOT_CONVERGED; default 1000000 */
   int32_t exchange_mode;   /* DI_EXCHANGE_*; distributed only; default ASYNC */
   int32_t device;          /* CUDA device ordinal; -1 = current device (default) */
-  int32_t scatter_kernel;  /* scatter schedule over frontier groups (32 selected nodes): 0 = dynamic
-                              runs grabbed per warp in ascending order (default), 1 = static CTA
-                              tiles + dynamic tail, 2 = static warp interleave + dynamic tail */
+  int32_t scatter_kernel;  /* reserved (0): the scatter grabs runs of frontier groups dynamically;
+                              static CTA-tile and warp-interleave schedules measured 30 % slower */
   int32_t profile;         /* 1: time each kernel of each executed pass with CUDA events
                               recorded inside the captured graph (di_stats.kt_*); default 0 */
   int32_t pass_kernel;     /* 0 = auto (= 1), 1 = one kernel per phase, check_interval passes per captured
@@ -102,7 +101,7 @@ typedef struct {
                               passes (grid barriers between phases; 1-GPU only) */
   int32_t hot_window;      /* 0 = stage the 2048 rows of largest in-degree in shared memory (default),
                               -1 = off (every push is an L2 RED) */
-  int32_t scatter_run;     /* groups per dynamic grab of schedule 0; 0 = default (2) */
+  int32_t scatter_run;     /* groups per dynamic grab of the scatter; 0 = default (2) */
   int32_t scatter_stripes; /* ticket stripes of the dynamic schedule, 1..32; 0 = default (8) */
   int32_t far_push;        /* far-push bins (propagation blocking, one GPU): 1 = on; 0 = auto (= off:
                               on C4 the record emission costs more than the L2-missing REDs it

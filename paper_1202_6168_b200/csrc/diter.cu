@@ -133,7 +133,6 @@ static di_status setup_geometry(di_ctx *ctx) {
   const long long per = (n + ctx->fr.n_seg - 1) / ctx->fr.n_seg;
   ctx->fr.seg_len = std::max<long long>(kSelectSpan, (per + kSelectSpan - 1) / kSelectSpan * kSelectSpan);
   ctx->scatter_smem = sizeof(int) * (size_t)(ctx->fr.n_seg + 1);
-  ctx->fr.sched = (ctx->opt.scatter_kernel >= 0 && ctx->opt.scatter_kernel <= 2) ? ctx->opt.scatter_kernel : 0;
   ctx->fr.run = ctx->opt.scatter_run > 0 ? ctx->opt.scatter_run : 2;
   ctx->fr.stripes = (ctx->opt.scatter_stripes > 0 && ctx->opt.scatter_stripes <= kStripes) ? ctx->opt.scatter_stripes : 8;
   int occ_sc = 0;

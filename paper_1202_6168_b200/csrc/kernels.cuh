@@ -428,33 +428,15 @@ __device__ __forceinline__ void scatter_body(const Graph &g, double *__restrict_
   constexpr int kW = kScatterThreads / 32;
   const int nwarps = gridDim.x * kW;
   const int warp = threadIdx.x >> 5;
-  int q_static = 0, seg = 0;
-  if (fr.sched == 1) {
-    // static CTA tiles of kTileGroups consecutive groups dealt round-robin to the
-    // CTAs, the CTA's warps interleaved inside the tile; dynamic tail below
-    constexpr int kTileGroups = 64;
-    const int n_tiles = total / kTileGroups;
-    const int t_static = (int)(((long long)n_tiles * 3 / 4) / gridDim.x) * gridDim.x;
-    q_static = t_static * kTileGroups;
-    for (int t = blockIdx.x; t < t_static; t += gridDim.x)
-      for (int j = warp; j < kTileGroups; j += kW) scatter_group<SIGNED>(g, s, fr, ctl, s_goff, st, t * kTileGroups + j, seg, acc);
-  } else if (fr.sched == 2) {
-    // static warp-interleaved groups; dynamic tail below
-    const int gwarp = blockIdx.x * kW + warp;
-    q_static = (int)(((long long)total * 3 / 4) / nwarps) * nwarps;
-    for (int q = gwarp; q < q_static; q += nwarps) scatter_group<SIGNED>(g, s, fr, ctl, s_goff, st, q, seg, acc);
-  }
+  const int q_static = 0;
+  int seg = 0;
+  const int rest = total - q_static;
   // Dynamic: each warp grabs runs of consecutive groups in ascending order (one
   // atomic per run, no block barrier).  The grid's working set stays a narrow
-  // window of consecutive columns, so the ±1000-local pushes of neighbouring
-  // columns meet their F lines in L2 before eviction; a static split lets CTAs
-  // drift apart and widens that window past L2.
-  // The groups left are split into `stripes` contiguous stripes with one ticket
-  // counter each (less same-address contention, so runs can stay short, and each
-  // stripe's working window is narrow); a warp starts on stripe (warp id mod
-  // stripes) and moves on when it is drained.
-  const int rest = total - q_static;
-  const int run = fr.sched == 0 ? max(1, min(fr.run, rest / (2 * nwarps))) : max(1, rest / (4 * nwarps));
+  // window of consecutive columns, so the +-1000-local pushes of neighbouring
+  // columns meet their F lines in L2 before eviction; static CTA-tile or
+  // warp-interleave splits let CTAs drift apart and measured 30 % slower on C4.
+  const int run = max(1, min(fr.run, rest / (2 * nwarps)));
   const int gw = blockIdx.x * kW + warp;
   const int ns = fr.stripes;
   for (int k = 0; k < ns; ++k) {
@@ -499,7 +481,7 @@ __device__ __forceinline__ void scatter_body(const Graph &g, double *__restrict_
 
 // dynamic shared memory: the group prefix s_goff[n_seg + 1]
 template <bool SIGNED>
-__global__ void __launch_bounds__(kScatterThreads)
+__global__ void __launch_bounds__(kScatterThreads, kScatterMinBlocks)
 k_scatter(Graph g, double *__restrict__ F, Frontier fr, Ctl *ctl, ScPartial *__restrict__ part) {
   if (ctl->done) return;
   __shared__ double s_hot[kHot];

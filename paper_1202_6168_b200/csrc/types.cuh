@@ -16,6 +16,10 @@ constexpr int kSelectThreads = 256;
 constexpr int kSelectItems = 16;                     // 32-node words per warp iteration
 constexpr int kSelectSpan = 32 * kSelectItems;       // nodes per warp iteration (segment granule)
 constexpr int kScatterThreads = 256;
+#ifndef DITER_SCATTER_MIN_BLOCKS
+#define DITER_SCATTER_MIN_BLOCKS 1
+#endif
+constexpr int kScatterMinBlocks = DITER_SCATTER_MIN_BLOCKS;   // __launch_bounds__ min CTAs/SM of k_scatter
 constexpr int kFinalizeThreads = 512;
 constexpr int kSelectCtasPerSm = 2;                  // 16 select warps/SM x 16 x 256 B loads in flight
 constexpr int kMaxSegments = 4096;                   // select warps (= frontier segments) per launch
@@ -111,8 +115,7 @@ struct Frontier {
   int *seg_cnt;          // [n_seg] selected nodes per segment
   long long seg_len;     // nodes per segment, a multiple of kSelectSpan
   int n_seg;             // select grid x warps per CTA (<= kMaxSegments)
-  int sched;             // scatter schedule: 0 dynamic warp runs (default), 1 static CTA tiles, 2 static warp interleave
-  int run;               // groups per dynamic grab (schedule 0)
+  int run;               // groups per dynamic grab of the scatter
   int stripes;           // ticket stripes in use (<= kStripes)
   double *hub_w;         // push value per edge of the hub (s d/#out or s)
   long long *hub_b0;

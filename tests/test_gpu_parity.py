@@ -173,8 +173,6 @@ def _c2_random_b_oracle(policy, key=0):
 VARIANTS = {
     "default": {},
     "fused": {"pass_kernel": 2},                       # cooperative persistent pass kernel
-    "tiles": {"scatter_kernel": 1},                    # static CTA tiles + dynamic tail
-    "interleave": {"scatter_kernel": 2},               # static warp interleave + dynamic tail
     "runs": {"scatter_run": 7, "scatter_stripes": 3},  # other grab run / stripe counts
     "nohot": {"hot_window": -1},                       # every push an L2 RED
     "far": {"far_push": 1, "far_warm_log2": 16},       # far-push bins forced on (auto: off)
