@@ -86,6 +86,9 @@ def parse():
     ap.add_argument("--pass-csv", default=None, help="write the last solve's per-pass log here")
     ap.add_argument("--exchange", default="async", choices=["sync", "async"],
                     help="multi-GPU exchange mode (DESIGN.md: SYNC = per-pass rounds, ASYNC = paper's send rule)")
+    ap.add_argument("--round-passes", type=int, default=4, help="N > 1, ASYNC: local passes per exchange round")
+    ap.add_argument("--remote-push", type=int, default=1, choices=[0, 1],
+                    help="N > 1: 0 per diffusion, 1 H increments at rounds (NEXT f2)")
     ap.add_argument("--partition", default="inout", choices=["out", "inout"],
                     help="edge-balanced contiguous ranges by out-edges or in+out edges")
     return ap.parse_args()
@@ -297,8 +300,12 @@ def run_ours(args, rank, world, local_rank):
     p = load_problem(args)
     pol = policy_of(args)
     mode = di.DI_EXCHANGE_SYNC if args.exchange == "sync" else di.DI_EXCHANGE_ASYNC
+    # N > 1 (ASYNC): exchange rounds every 4 passes, remote edges pushed as H
+    # increments at the rounds (NEXT f2), receive-side T rescale --
+    # DESIGN.md §6 "Multi-GPU" has the loopback measurements behind these choices
+    dist_kw = dict(check_interval=args.round_passes, remote_push=args.remote_push) if world > 1 else {}
     opts = di.default_options(policy=pol, device=local_rank, profile=1, exchange_mode=mode,
-                              alpha=args.alpha, hybrid_frac=args.hybrid_frac, select_key=args.key)
+                              alpha=args.alpha, hybrid_frac=args.hybrid_frac, select_key=args.key, **dist_kw)
     comm_id, bounds, shard = None, None, None
     if dist:
         bounds = dd.partition_bounds(p.col_ptr, world, cost=args.partition, row_idx=p.row_idx)
@@ -390,7 +397,9 @@ def run_ours(args, rank, world, local_rank):
                          f"on the full graph, {dt:.1f}s on 1 host core"}
     clocks = clk.summary()
     di.di_destroy(ctx)
-    par = "dp1" if world == 1 else f"node-partition x{world} ({args.partition}-balanced ranges, {args.exchange} exchange)"
+    par = "dp1" if world == 1 else (f"node-partition x{world} ({args.partition}-balanced ranges, {args.exchange} exchange, "
+                                    f"rounds every {args.round_passes} passes, remote edges "
+                                    f"{'as H increments' if args.remote_push else 'per diffusion'})")
     out = {"metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot["run_ms"] / args.steps,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",

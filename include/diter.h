@@ -77,6 +77,15 @@ enum {
                               (PAPER.md:210); one GPU only (needs global in-degrees) */
 };
 
+/* How a distributed rank pushes fluid along edges to rows it does not own. */
+enum {
+  DI_REMOTE_PER_DIFFUSION = 0,  /* every diffusion pushes its remote edges into the outbox
+                                   (continuous s_k, PAPER.md:227 first bullet) */
+  DI_REMOTE_INCREMENT = 1       /* the scatter pushes local edges only; at an exchange round
+                                   the remote edges get (H - H_old) p_ji and H_old := H
+                                   (the paper's preferred variant) */
+};
+
 /* Exchange modes of distributed contexts. */
 enum {
   DI_EXCHANGE_SYNC = 0,    /* exchange + merge after every pass (reproduces the 1-GPU passes) */
@@ -109,7 +118,10 @@ typedef struct {
                               -1 = off */
   int32_t far_warm_log2;   /* log2 of the warm row range kept on direct L2 REDs; 0 = default (21) */
   int32_t select_key;      /* DI_KEY_*; default DI_KEY_RAW */
-  int32_t reserved[7];
+  int32_t remote_push;     /* DI_REMOTE_*; distributed only; default DI_REMOTE_PER_DIFFUSION */
+  int32_t receive_rescale; /* ASYNC only: after merging received fluid R, T_k <- T_k (r_k + R) / r_k
+                              (reading R13); 1 = on (default), 0 = off */
+  int32_t reserved[5];
 } di_options;
 
 /* One record per executed pass (device-logged, read with di_get_pass_log). */
@@ -148,6 +160,9 @@ typedef struct {
   int64_t kt_passes;       /* profile=1: executed passes those sums cover */
   int64_t scatter_bytes;   /* algorithmic bytes of the scatter kernel since create: 20 E (28 E signed)
                               + 16 per diffused node (its col_ptr pair) */
+  int64_t remote_pushes;   /* distributed: pushes into the remote outbox since create (one RED per
+                              remote edge per diffusion, or per column increment with
+                              DI_REMOTE_INCREMENT) */
 } di_stats;
 
 /* Fill *opt with the defaults above. */

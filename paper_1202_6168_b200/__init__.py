@@ -26,6 +26,7 @@ DI_OK, DI_ERR_INVALID_ARG, DI_ERR_CONTRACTION, DI_ERR_OOM, DI_ERR_CUDA, DI_ERR_N
 DI_POLICY_GEOM, DI_POLICY_HYBRID = 0, 1
 DI_EXCHANGE_SYNC, DI_EXCHANGE_ASYNC = 0, 1
 DI_KEY_RAW, DI_KEY_EDGE, DI_KEY_PAPER = 0, 1, 2
+DI_REMOTE_PER_DIFFUSION, DI_REMOTE_INCREMENT = 0, 1
 
 STATUS_NAMES = {0: "DI_OK", 1: "DI_ERR_INVALID_ARG", 2: "DI_ERR_CONTRACTION", 3: "DI_ERR_OOM",
                 4: "DI_ERR_CUDA", 5: "DI_ERR_NCCL", 6: "DI_ERR_NOT_CONVERGED", 7: "DI_ERR_STATE",
@@ -54,7 +55,8 @@ class di_options(ctypes.Structure):
                 ("pass_kernel", ctypes.c_int32), ("hot_window", ctypes.c_int32),
                 ("scatter_run", ctypes.c_int32), ("scatter_stripes", ctypes.c_int32),
                 ("far_push", ctypes.c_int32), ("far_warm_log2", ctypes.c_int32),
-                ("select_key", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+                ("select_key", ctypes.c_int32), ("remote_push", ctypes.c_int32),
+                ("receive_rescale", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
 
 
 class di_pass_log(ctypes.Structure):
@@ -74,7 +76,8 @@ class di_stats(ctypes.Structure):
                 ("nnz_local", ctypes.c_int64), ("graph_launches", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("kt_select_ms", ctypes.c_double),
                 ("kt_scatter_ms", ctypes.c_double), ("kt_finalize_ms", ctypes.c_double),
-                ("kt_passes", ctypes.c_int64), ("scatter_bytes", ctypes.c_int64)]
+                ("kt_passes", ctypes.c_int64), ("scatter_bytes", ctypes.c_int64),
+                ("remote_pushes", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

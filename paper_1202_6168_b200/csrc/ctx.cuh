@@ -34,6 +34,9 @@ struct di_ctx {
   unsigned char *dflags = nullptr;  // dirty flag per 32-row block of G
   double *H = nullptr;           // history [n_local]
   float *kw = nullptr;           // selection-key weights [n_local] (nullptr = raw key |F_i|)
+  int *nloc = nullptr;           // distributed: local (owned-row) edges per column, stored first
+  double *H_old = nullptr;       // DI_REMOTE_INCREMENT: H at the last push of the remote edges
+  long long remote_pushes = 0;   // pushes into the outbox since create
   diter::Frontier fr{};
   diter::Far far{};               // far-push bins (propagation blocking), 1 GPU
   long long *far_off = nullptr;   // [n_bins + 1] first chunk of each bin (device)

@@ -295,12 +295,99 @@ __global__ void k_outbox_mass(const double *__restrict__ G, const unsigned char 
 
 // Merge received records: F[row] += val ("add them to existing
 // fluids, node per node").
-__global__ void k_merge(double *__restrict__ F, const Rec *__restrict__ recv, long long n) {
+__global__ void k_merge(double *__restrict__ F, const Rec *__restrict__ recv, long long n, double *recv_mass) {
   const long long stride = (long long)gridDim.x * blockDim.x;
+  double m = 0.0;
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
     const Rec r = recv[k];
     red_add(F + r.row, r.val);
+    m += fabs(r.val);
   }
+  m = warp_sum(m);
+  if (lane_id() == 0 && m != 0.0) atomicAdd(recv_mass, m);
+}
+
+// Receive-side threshold rescale ("update the threshold T_k,
+// rescaling up by a factor ... proportional to min((r_k + received)/r_k,
+// received)"; reading R13): T_k <- T_k (r_k + R) / r_k with R the fluid mass just
+// merged and r_k the local residual before the merge (r_k = 0: unchanged).
+__global__ void k_rescale_T(Ctl *ctl, const double *recv_mass, double r_k) {
+  const double R = *recv_mass;
+  if (r_k > 0.0 && R > 0.0) ctl->T = ctl->T * ((r_k + R) / r_k);
+}
+
+// Setup: stable partition of every owned column into local rows (owned by this
+// rank) then remote rows, into new arrays; nloc[i] = local edges of column i.
+// Push order within a column is immaterial (sums), so this only reorders storage.
+__global__ void k_partition_columns(const long long *__restrict__ col_ptr, long long n, const int *__restrict__ ri,
+                                    const double *__restrict__ v, long long lo, long long hi, int *__restrict__ ri2,
+                                    double *__restrict__ v2, int *__restrict__ nloc) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const long long b = col_ptr[i], e = col_ptr[i + 1];
+    long long w = b;
+    for (long long k = b; k < e; ++k) {
+      const int r = ri[k];
+      if (r >= lo && r < hi) { ri2[w] = r; if (v) v2[w] = v[k]; ++w; }
+    }
+    nloc[i] = (int)(w - b);
+    for (long long k = b; k < e; ++k) {
+      const int r = ri[k];
+      if (!(r >= lo && r < hi)) { ri2[w] = r; if (v) v2[w] = v[k]; ++w; }
+    }
+  }
+}
+
+// DI_REMOTE_INCREMENT: pending remote mass
+// s_k = sum_i |H_i - H_old_i| sum_{remote e of i} |p_e| -- the fluid the remote
+// edges owe since the last push (p = d/#out, or |vals| signed).
+__global__ void k_pending_mass(const long long *__restrict__ col_ptr, const int *__restrict__ nloc,
+                               const double *__restrict__ vals, double d, const double *__restrict__ H,
+                               const double *__restrict__ H_old, long long n, double *out) {
+  double m = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const long long b = col_ptr[i], e = col_ptr[i + 1];
+    const long long nl = nloc[i];
+    if (nl == e - b) continue;
+    const double dh = H[i] - H_old[i];
+    if (dh == 0.0) continue;
+    double c = 0.0;
+    if (vals) { for (long long k = b + nl; k < e; ++k) c += fabs(vals[k]); }
+    else c = d * (double)(e - b - nl) / (double)(e - b);
+    m += fabs(dh) * c;
+  }
+  m = warp_sum(m);
+  if (lane_id() == 0 && m != 0.0) atomicAdd(out, m);
+}
+
+// DI_REMOTE_INCREMENT push: for every column with H_i != H_old_i, its remote edges
+// get (H_i - H_old_i) p_ji in the outbox (dirty-flagged), then H_old_i := H_i.
+// One warp per column, lanes over its remote edges.
+__global__ void k_push_increment(const long long *__restrict__ col_ptr, const int *__restrict__ nloc,
+                                 const int *__restrict__ ri, const double *__restrict__ vals, double d,
+                                 const double *__restrict__ H, double *__restrict__ H_old, long long n,
+                                 double *__restrict__ G, unsigned char *__restrict__ dflags,
+                                 unsigned long long *pushes) {
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  const unsigned lane = lane_id();
+  long long cnt = 0;
+  for (long long i = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
+    const long long b = col_ptr[i], e = col_ptr[i + 1];
+    const long long nl = nloc[i];
+    if (nl == e - b) continue;
+    const double h = H[i];
+    const double dh = h - H_old[i];
+    if (dh == 0.0) continue;
+    const double w = vals ? dh : dh * (d / (double)(e - b));
+    for (long long k = b + nl + lane; k < e; k += 32) {
+      const int r = ri[k];
+      red_add(G + r, vals ? w * vals[k] : w);
+      dflags[r >> 5] = 1;
+    }
+    if (lane == 0) { H_old[i] = h; cnt += e - b - nl; }
+  }
+  if (lane == 0 && cnt) atomicAdd(pushes, (unsigned long long)cnt);
 }
 
 __global__ void k_set_target(Ctl *ctl, double target, long long max_pass, int done) {
@@ -345,9 +432,18 @@ di_status diter_dist_reset(di_ctx *ctx) {
   if (!ctx->dist) return DI_OK;
   CKD(cudaMemsetAsync(ctx->G, 0, sizeof(double) * ctx->n_rows, ctx->stream));
   CKD(cudaMemsetAsync(ctx->dflags, 0, (size_t)((ctx->n_rows + 31) >> 5), ctx->stream));
+  if (ctx->H_old) CKD(cudaMemsetAsync(ctx->H_old, 0, sizeof(double) * ctx->n_local, ctx->stream));
   CKD(cudaStreamSynchronize(ctx->stream));
   ctx->dist->s_k = 0.0;
   return DI_OK;
+}
+
+// DI_REMOTE_INCREMENT: push H - H_old along the remote edges into the outbox.
+static void push_increment(di_ctx *ctx) {
+  k_push_increment<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->col_ptr, ctx->nloc, ctx->row_idx, ctx->vals,
+                                                              ctx->d, ctx->H, ctx->H_old, ctx->n_local, ctx->G,
+                                                              ctx->dflags, &ctx->ctl->remote_pushes);
+  ctx->kernel_launches += 1;
 }
 
 // exact global |F|_1 (+ s_k outbox mass when `with_outbox`)
@@ -371,6 +467,7 @@ static di_status exchange(di_ctx *ctx, bool send_now) {
   DistState *ds = ctx->dist;
   const int W = ctx->world;
   CKD(cudaMemsetAsync(ds->d_scnt, 0, sizeof(long long) * W, ctx->stream));
+  CKD(cudaMemsetAsync(ds->d_sums + kSums + 1, 0, sizeof(double), ctx->stream));   // received mass
   if (send_now) {
     long long *d_soff = reinterpret_cast<long long *>(ds->d_sums + kSums + 2);
     CKD(cudaMemcpyAsync(d_soff, ds->soff.data(), sizeof(long long) * W, cudaMemcpyHostToDevice, ctx->stream));
@@ -396,7 +493,7 @@ static di_status exchange(di_ctx *ctx, bool send_now) {
   TRYD(ds->fabric->alltoallv(ctx, ds->send, ds->soff.data(), ds->scnt.data(), ds->recv, ds->roff.data(),
                              ds->rcnt.data()));
   if (tot > 0) {
-    k_merge<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->F, ds->recv, tot);
+    k_merge<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->F, ds->recv, tot, ds->d_sums + kSums + 1);
     ctx->kernel_launches += 1;
   }
   if (sent > 0) {
@@ -433,6 +530,7 @@ di_status diter_dist_run(di_ctx *ctx, double target) {
   CKD(cudaEventRecord(ctx->ev0, ctx->stream));
   const long long max_pass_abs = ctx->passes_done + ctx->opt.max_passes;
   const bool sync_mode = ctx->opt.exchange_mode == DI_EXCHANGE_SYNC;
+  const bool incr = ctx->H_old != nullptr;   // DI_REMOTE_INCREMENT
   Ctl *h = reinterpret_cast<Ctl *>(ctx->h_ctl);
   di_status st = DI_OK;
   double R = 0.0;
@@ -448,6 +546,7 @@ di_status diter_dist_run(di_ctx *ctx, double target) {
       k_reduce_partials<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->ctl, ctx->sel_part, ctx->grid_select,
                                                                   ctx->sc_part, ctx->grid_scatter, ds->d_sums);
       TRYD(ds->fabric->allreduce_sum(ctx, ds->d_sums, kSums));
+      if (incr) push_increment(ctx);
       TRYD(exchange(ctx, true));
       k_apply_pass<<<1, 1, 0, ctx->stream>>>(ctx->ctl, ds->d_sums, ctx->log);
       ctx->kernel_launches += 2;
@@ -472,10 +571,15 @@ di_status diter_dist_run(di_ctx *ctx, double target) {
                                                             ctx->grid_scatter, ctx->log);
         ctx->kernel_launches += 1;
       }
-      // round: s_k (outbox mass) and r_k decide the send (eq. send)
+      // round: s_k (outbox mass, or the pending increment mass) and r_k decide the
+      // send (eq. send)
       CKD(cudaMemsetAsync(ds->d_sums, 0, sizeof(double), ctx->stream));
-      k_outbox_mass<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->G, ctx->dflags, ctx->n_rows, ctx->lo,
-                                                               ctx->lo + ctx->n_local, ds->d_sums);
+      if (incr)
+        k_pending_mass<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->col_ptr, ctx->nloc, ctx->vals, ctx->d, ctx->H,
+                                                                  ctx->H_old, ctx->n_local, ds->d_sums);
+      else
+        k_outbox_mass<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->G, ctx->dflags, ctx->n_rows, ctx->lo,
+                                                                 ctx->lo + ctx->n_local, ds->d_sums);
       TRYD(diter_l1_launch(ctx));
       double hs[2];
       CKD(cudaMemcpyAsync(&hs[0], ds->d_sums, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -485,7 +589,12 @@ di_status diter_dist_run(di_ctx *ctx, double target) {
       ds->s_k = hs[0];
       const double r_k = hs[1];
       const bool send_now = (ds->s_k > r_k / ctx->world) || (r_k == 0.0 && ds->s_k > 0.0);
+      if (incr && send_now) push_increment(ctx);
       TRYD(exchange(ctx, send_now));
+      if (ctx->opt.receive_rescale) {
+        k_rescale_T<<<1, 1, 0, ctx->stream>>>(ctx->ctl, ds->d_sums + kSums + 1, r_k);
+        ctx->kernel_launches += 1;
+      }
       ctx->passes_done = h->pass;
       TRYD(global_residual(ctx, ds->s_k, &R));
       ctx->residual = R;
@@ -493,6 +602,7 @@ di_status diter_dist_run(di_ctx *ctx, double target) {
       if (stop || out_of_passes) {
         // deliver what is left in the outboxes, so that on return F (with H) is
         // the whole state: F = B - (I-P)H on every rank, nothing in flight
+        if (incr) push_increment(ctx);
         TRYD(exchange(ctx, true));
         if (!stop) st = DI_ERR_NOT_CONVERGED;
         break;
@@ -514,6 +624,7 @@ out:
   ctx->edges = h->edges;
   ctx->nodes = h->nodes;
   ctx->threshold = h->T;
+  ctx->remote_pushes = (long long)h->remote_pushes;
   if (st == DI_ERR_NOT_CONVERGED) diter_set_err(ctx, "max_passes reached before |F|_1 < %g", target);
   return st;
 }
@@ -635,6 +746,37 @@ extern "C" di_status di_create_dist(di_ctx **out, int32_t rank, int32_t world, c
   }
   di_status s = diter_setup(ctx, col_ptr_local, row_idx_local, values_local, b_local, opt);
   if (s != DI_OK) return fail(s);
+  // local rows first in every column (nloc), in place via a scratch copy
+  {
+    const long long n = ctx->n_local, nnz = ctx->nnz_local;
+    int *ri2 = nullptr;
+    double *v2 = nullptr;
+    if (cudaMalloc(&ctx->nloc, sizeof(int) * std::max(1LL, n)) != cudaSuccess ||
+        cudaMalloc(&ri2, sizeof(int) * std::max(1LL, nnz)) != cudaSuccess ||
+        (ctx->vals && cudaMalloc(&v2, sizeof(double) * std::max(1LL, nnz)) != cudaSuccess)) {
+      if (ri2) cudaFree(ri2);
+      diter_set_err(ctx, "cudaMalloc (column partition) failed");
+      return fail(DI_ERR_OOM);
+    }
+    k_partition_columns<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->col_ptr, n, ctx->row_idx, ctx->vals, lo,
+                                                                   lo + n, ri2, v2, ctx->nloc);
+    cudaMemcpyAsync(ctx->row_idx, ri2, sizeof(int) * nnz, cudaMemcpyDeviceToDevice, ctx->stream);
+    if (v2) cudaMemcpyAsync(ctx->vals, v2, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, ctx->stream);
+    const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(ri2);
+    if (v2) cudaFree(v2);
+    if (e != cudaSuccess) { diter_set_err(ctx, "column partition failed: %s", cudaGetErrorString(e)); return fail(DI_ERR_CUDA); }
+    if (ctx->opt.remote_push == DI_REMOTE_INCREMENT) {
+      if (cudaMalloc(&ctx->H_old, sizeof(double) * std::max(1LL, n)) != cudaSuccess) {
+        diter_set_err(ctx, "cudaMalloc (H_old) failed");
+        return fail(DI_ERR_OOM);
+      }
+      cudaMemsetAsync(ctx->H_old, 0, sizeof(double) * std::max(1LL, n), ctx->stream);
+    } else if (ctx->opt.remote_push != DI_REMOTE_PER_DIFFUSION) {
+      diter_set_err(ctx, "remote_push must be DI_REMOTE_PER_DIFFUSION or DI_REMOTE_INCREMENT");
+      return fail(DI_ERR_INVALID_ARG);
+    }
+  }
   // outbox, flags, exchange buffers
   {
     const long long nb = (n_global + 31) >> 5;

@@ -65,6 +65,7 @@ extern "C" void di_default_options(di_options *o) {
   o->scatter_kernel = 0;
   o->profile = 0;
   o->pass_kernel = 0;
+  o->receive_rescale = 1;
 }
 
 template <typename T>
@@ -89,7 +90,7 @@ static void free_ctx(di_ctx *c) {
     if (e) cudaEventDestroy(e);
   void *ptrs[] = {c->col_ptr, c->row_idx, c->vals, c->d_b, c->F, c->H, c->fr.ids, c->fr.S, c->fr.seg_cnt,
                   c->fr.hub_w, c->fr.hub_b0, c->fr.hub_deg, c->fr.hub_chunk, c->sel_part, c->sc_part,
-                  c->l1_part, c->l1_out, c->ctl, c->log, c->far_off, c->far.rows, c->far.vals, c->far.fill, c->kw};
+                  c->l1_part, c->l1_out, c->ctl, c->log, c->far_off, c->far.rows, c->far.vals, c->far.fill, c->kw, c->nloc, c->H_old};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
@@ -275,7 +276,8 @@ static di_status setup_key(di_ctx *ctx) {
 
 Graph diter_graph(const di_ctx *ctx) {
   return Graph{ctx->col_ptr, ctx->row_idx, ctx->vals, ctx->n_local, ctx->d, ctx->hot_lo,
-               ctx->lo, ctx->G, ctx->dflags, ctx->far};
+               ctx->lo, ctx->G, ctx->dflags, ctx->far, ctx->nloc,
+               ctx->opt.remote_push == DI_REMOTE_INCREMENT ? 1 : 0};
 }
 
 // Capture check_interval passes of (select, scatter, finalize) once.
@@ -678,6 +680,7 @@ extern "C" di_status di_get_stats(const di_ctx *ctx, di_stats *s) {
   s->kt_finalize_ms = ctx->kt_ms[2];
   s->kt_passes = ctx->kt_passes;
   s->scatter_bytes = (ctx->vals ? 28LL : 20LL) * ctx->edges + 16LL * ctx->nodes;
+  s->remote_pushes = ctx->remote_pushes;
   return DI_OK;
 }
 

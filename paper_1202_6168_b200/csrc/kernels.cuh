@@ -299,6 +299,7 @@ __device__ __forceinline__ void push_group(const Graph &g, const Sink &s, Ctl *c
 struct ScAcc {
   double loss = 0.0;
   long long edges = 0;
+  long long remote = 0;   // distributed, per-diffusion mode: pushes into the outbox
   int dang = 0, lo = 0, mi = 0, hu = 0;
 };
 
@@ -386,6 +387,14 @@ __device__ __forceinline__ void scatter_group(const Graph &g, const Sink &s, con
   if (k < cnt) {
     b0 = __ldg(g.col_ptr + i);
     const long long deg = __ldg(g.col_ptr + i + 1) - b0;
+    // edges this scatter pushes: all, or (DI_REMOTE_INCREMENT) the local ones, which
+    // a distributed context stores first in each column
+    long long dpush = deg;
+    if (g.nloc) {
+      const long long nl = __ldg(g.nloc + i);
+      if (g.local_only) dpush = nl;
+      else acc.remote += deg - nl;
+    }
     const double asv = fabs(sv);
     acc.loss += (deg > 0) ? (1.0 - g.d) * asv : asv;
     acc.edges += deg;
@@ -393,16 +402,18 @@ __device__ __forceinline__ void scatter_group(const Graph &g, const Sink &s, con
       acc.dang += 1;
     } else {
       w = SIGNED ? sv : sv * (g.d / (double)deg);
-      if (deg <= kLowMax) { acc.lo += 1; deg_eff = (int)deg; }
-      else if (deg <= kMidMax) { acc.mi += 1; deg_eff = (int)deg; }
-      else {
+      if (deg <= kLowMax) acc.lo += 1;
+      else if (deg <= kMidMax) acc.mi += 1;
+      else acc.hu += 1;
+      if (dpush <= kMidMax) {
+        deg_eff = (int)dpush;
+      } else {
         // one 64-bit atomic hands out the slot AND the first chunk id, so
         // hub_chunk[] is sorted by slot and k_scatter_hubs can binary-search it
-        acc.hu += 1;
-        const unsigned long long nch = (unsigned long long)((deg + kHubChunk - 1) / kHubChunk);
+        const unsigned long long nch = (unsigned long long)((dpush + kHubChunk - 1) / kHubChunk);
         const unsigned long long old = atomicAdd(&ctl->hub_packed, (1ull << 32) | nch);
         const unsigned sl = (unsigned)(old >> 32);
-        fr.hub_w[sl] = w; fr.hub_b0[sl] = b0; fr.hub_deg[sl] = deg;
+        fr.hub_w[sl] = w; fr.hub_b0[sl] = b0; fr.hub_deg[sl] = dpush;
         fr.hub_chunk[sl] = (unsigned)(old & 0xffffffffull);
       }
     }
@@ -466,15 +477,19 @@ __device__ __forceinline__ void scatter_body(const Graph &g, double *__restrict_
   acc.lo = warp_sum(acc.lo);
   acc.mi = warp_sum(acc.mi);
   acc.hu = warp_sum(acc.hu);
+  acc.remote = warp_sum(acc.remote);
   __shared__ ScAcc s_acc[kScatterThreads / 32];
   if (lane == 0) s_acc[threadIdx.x >> 5] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
     ScPartial p{0.0, 0, 0, 0, 0, 0};
+    long long remote = 0;
     for (int k = 0; k < kScatterThreads / 32; ++k) {
       p.loss += s_acc[k].loss; p.edges += s_acc[k].edges; p.dang += s_acc[k].dang;
       p.n_low += s_acc[k].lo; p.n_mid += s_acc[k].mi; p.n_hub += s_acc[k].hu;
+      remote += s_acc[k].remote;
     }
+    if (remote) atomicAdd(&ctl->remote_pushes, (unsigned long long)remote);
     part[blockIdx.x] = p;
   }
 }

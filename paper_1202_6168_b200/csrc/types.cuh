@@ -47,6 +47,7 @@ struct Ctl {
   long long log_cap;
   unsigned sc_next;    // next frontier group of the scatter's dynamic tail (reset per pass)
   int _pad;
+  unsigned long long remote_pushes;   // distributed: pushes into the outbox (one atomic per CTA per pass)
   double t_sel_us;     // fused kernel: accumulated select / scatter phase time (%globaltimer)
   double t_sc_us;
   // scatter tickets: one counter per stripe of the frontier groups, each on its
@@ -103,6 +104,8 @@ struct Graph {
   double *G;                 // remote outbox over global ids, or nullptr on one GPU
   unsigned char *dflags;     // dirty flag per 32-row block of G
   Far far;
+  const int *nloc;           // distributed: local edges of each column (stored first), else nullptr
+  int local_only;            // DI_REMOTE_INCREMENT: the scatter pushes [b0, b0 + nloc) only
 };
 
 // Frontier of one pass, compacted per select warp: warp w scans the owned nodes

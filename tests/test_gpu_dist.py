@@ -49,12 +49,15 @@ def run_ranks(K, n, cp, ri, vals, b, d, target, bounds, mode, key, **opts):
     return H, F, out
 
 
-@pytest.mark.parametrize("K,key", [(2, di.DI_KEY_RAW), (4, di.DI_KEY_RAW), (3, di.DI_KEY_EDGE)])
-def test_sync_matches_single_gpu_passes(K, key):
+@pytest.mark.parametrize("K,key,remote", [(2, di.DI_KEY_RAW, 0), (4, di.DI_KEY_RAW, 0), (3, di.DI_KEY_EDGE, 0),
+                                          (2, di.DI_KEY_RAW, 1), (3, di.DI_KEY_EDGE, 1)])
+def test_sync_matches_single_gpu_passes(K, key, remote):
     """SYNC mode is the single-GPU snapshot pass: same per-pass frontier sizes,
     edges and thresholds (random B: no exact-arithmetic ties), same fixed point --
     with the raw and the per-edge selection key (per-edge weights need only local
-    out-degrees)."""
+    out-degrees), and with remote edges pushed per diffusion or as H increments at
+    each exchange (NEXT f2: the same fluid reaches the same rows
+    before the next selection)."""
     n = 200_000
     cp, ri = gen.web_graph(n, 5)
     rng = np.random.default_rng(3)
@@ -63,8 +66,8 @@ def test_sync_matches_single_gpu_passes(K, key):
     target = 1e-9 * 0.15
     H1, _, log1 = di.solve(n, cp, ri, target, b=b, select_key=key)
     bounds = dist.partition_bounds(cp, K)
-    H, F, outs = run_ranks(K, n, cp, ri, None, b, 0.85, target, bounds, di.DI_EXCHANGE_SYNC, f"sync{K}k{key}",
-                           select_key=key)
+    H, F, outs = run_ranks(K, n, cp, ri, None, b, 0.85, target, bounds, di.DI_EXCHANGE_SYNC,
+                           f"sync{K}k{key}r{remote}", select_key=key, remote_push=remote)
     for o in outs:        # every rank logs the same global pass records
         lg = o[2]
         np.testing.assert_array_equal(lg["frontier"], log1["frontier"])
@@ -94,6 +97,40 @@ def test_async_parity(K, cost):
     Xp = np.concatenate([o[5] for o in outs])       # completed PageRank, global |H|_1 (f4)
     assert abs(Xp.sum() - 1.0) <= 1e-12
     assert np.abs(Xp - X / X.sum()).sum() <= 2e-8
+
+
+@pytest.mark.parametrize("K", [2, 4])
+def test_async_remote_increments(K):
+    """NEXT f2: remote edges pushed from H - H_old at exchange
+    rounds instead of at every diffusion.  Parity with the oracle, a closed ledger,
+    the completed PageRank, and fewer pushes into the outbox than per-diffusion
+    pushing on the same problem (nodes re-diffuse between rounds)."""
+    p = gen.config("C2", 2, n=300_000)
+    bn = 0.15
+    bounds = dist.partition_bounds(p.col_ptr, K, cost="inout", row_idx=p.row_idx)
+    X = oracle.Problem(p.n, p.col_ptr, p.row_idx).solve(1e-12 * bn * 0.15).H
+    deg = np.diff(p.col_ptr)
+    pushes = {}
+    for remote in (di.DI_REMOTE_PER_DIFFUSION, di.DI_REMOTE_INCREMENT):
+        H, F, outs = run_ranks(K, p.n, p.col_ptr, p.row_idx, None, None, 0.85, p.parity_stop, bounds,
+                               di.DI_EXCHANGE_ASYNC, f"incr{K}r{remote}", check_interval=8, remote_push=remote)
+        assert np.abs(H - X).sum() <= 1e-8 * bn
+        ledger = np.abs(F).sum() + 0.15 * H.sum() + 0.85 * H[deg == 0].sum()
+        assert abs(ledger - bn) <= 1e-12 * bn
+        assert all(o[4] < p.parity_stop for o in outs)
+        pushes[remote] = sum(o[3]["remote_pushes"] for o in outs)
+    assert 0 < pushes[di.DI_REMOTE_INCREMENT] < pushes[di.DI_REMOTE_PER_DIFFUSION]
+
+
+def test_async_remote_increments_signed():
+    n = 100_000
+    cp, ri, v, b = gen.signed_system(n, 3)
+    bn = np.abs(b).sum()
+    bounds = dist.partition_bounds(cp, 3)
+    H, F, outs = run_ranks(3, n, cp, ri, v, b, 0.9, 5e-10 * bn, bounds, di.DI_EXCHANGE_ASYNC, "signedincr",
+                           remote_push=di.DI_REMOTE_INCREMENT)
+    X, _ = oracle.Problem(n, cp, ri, v, b, 0.9).jacobi(1e-13 * bn)
+    assert np.abs(H - X).sum() <= 1e-8 * bn
 
 
 def test_paper_key_rejected_on_distributed():
