@@ -81,9 +81,13 @@ enum {
 enum {
   DI_REMOTE_PER_DIFFUSION = 0,  /* every diffusion pushes its remote edges into the outbox
                                    (continuous s_k, PAPER.md:227 first bullet) */
-  DI_REMOTE_INCREMENT = 1       /* the scatter pushes local edges only; at an exchange round
+  DI_REMOTE_INCREMENT = 1,      /* the scatter pushes local edges only; at an exchange round
                                    the remote edges get (H - H_old) p_ji and H_old := H
                                    (the paper's preferred variant) */
+  DI_REMOTE_RECEIVER = 2        /* receiver computes: ship (j, H_j - H_old_j)
+                                   once per peer owning rows of column j; receivers keep the
+                                   remote in-edges of their rows (one setup all-to-all) and
+                                   apply p_ij themselves; at most 64 ranks */
 };
 
 /* Exchange modes of distributed contexts. */

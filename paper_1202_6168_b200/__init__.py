@@ -26,7 +26,7 @@ DI_OK, DI_ERR_INVALID_ARG, DI_ERR_CONTRACTION, DI_ERR_OOM, DI_ERR_CUDA, DI_ERR_N
 DI_POLICY_GEOM, DI_POLICY_HYBRID = 0, 1
 DI_EXCHANGE_SYNC, DI_EXCHANGE_ASYNC = 0, 1
 DI_KEY_RAW, DI_KEY_EDGE, DI_KEY_PAPER = 0, 1, 2
-DI_REMOTE_PER_DIFFUSION, DI_REMOTE_INCREMENT = 0, 1
+DI_REMOTE_PER_DIFFUSION, DI_REMOTE_INCREMENT, DI_REMOTE_RECEIVER = 0, 1, 2
 
 STATUS_NAMES = {0: "DI_OK", 1: "DI_ERR_INVALID_ARG", 2: "DI_ERR_CONTRACTION", 3: "DI_ERR_OOM",
                 4: "DI_ERR_CUDA", 5: "DI_ERR_NCCL", 6: "DI_ERR_NOT_CONVERGED", 7: "DI_ERR_STATE",

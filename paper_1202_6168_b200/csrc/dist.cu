@@ -33,6 +33,8 @@
 #include <string>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "../../include/diter.h"
 #include "ctx.cuh"
 #include "kernels.cuh"
@@ -235,6 +237,18 @@ struct DistState {
   double *d_sums = nullptr;            // [kSums + 2]
   std::vector<long long> soff, scnt, roff, rcnt;
   double s_k = 0.0;                    // outbox mass (ASYNC)
+  // DI_REMOTE_RECEIVER (NEXT f3).  Sender: per peer q the local
+  // columns with at least one row in Omega_q, cols[pair_off[q] ..).  Receiver: the
+  // remote in-edges of the owned rows grouped by source column: ric_src sorted
+  // global source ids, edges [ric_off[k], ric_off[k+1]) of (ric_row local row,
+  // ric_p weight p_ij).
+  int *cols = nullptr;
+  long long *d_pair_off = nullptr;     // [world + 1]
+  std::vector<long long> pair_off;
+  long long *ric_src = nullptr, *ric_off = nullptr;
+  int *ric_row = nullptr;
+  double *ric_p = nullptr;
+  long long ric_n = 0, ric_e = 0;
 };
 
 // ----------------------------------------------------------------- kernels --
@@ -317,23 +331,25 @@ __global__ void k_rescale_T(Ctl *ctl, const double *recv_mass, double r_k) {
 }
 
 // Setup: stable partition of every owned column into local rows (owned by this
-// rank) then remote rows, into new arrays; nloc[i] = local edges of column i.
-// Push order within a column is immaterial (sums), so this only reorders storage.
+// rank), then the remote rows grouped by owning peer in rank order, into new
+// arrays; nloc[i] = local edges of column i.  Push order within a column is
+// immaterial (sums), so this only reorders storage; the peer grouping lets the
+// receiver-computes exchange treat a column's rows of one peer as one range.
 __global__ void k_partition_columns(const long long *__restrict__ col_ptr, long long n, const int *__restrict__ ri,
-                                    const double *__restrict__ v, long long lo, long long hi, int *__restrict__ ri2,
-                                    double *__restrict__ v2, int *__restrict__ nloc) {
+                                    const double *__restrict__ v, const long long *bounds, int world, int rank,
+                                    int *__restrict__ ri2, double *__restrict__ v2, int *__restrict__ nloc) {
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const long long b = col_ptr[i], e = col_ptr[i + 1];
     long long w = b;
-    for (long long k = b; k < e; ++k) {
-      const int r = ri[k];
-      if (r >= lo && r < hi) { ri2[w] = r; if (v) v2[w] = v[k]; ++w; }
-    }
-    nloc[i] = (int)(w - b);
-    for (long long k = b; k < e; ++k) {
-      const int r = ri[k];
-      if (!(r >= lo && r < hi)) { ri2[w] = r; if (v) v2[w] = v[k]; ++w; }
+    for (int step = 0; step < world; ++step) {
+      const int q = step == 0 ? rank : (step <= rank ? step - 1 : step);   // own rows first, then peers
+      const long long a = bounds[q], z = bounds[q + 1];
+      for (long long k = b; k < e; ++k) {
+        const int r = ri[k];
+        if (r >= a && r < z) { ri2[w] = r; if (v) v2[w] = v[k]; ++w; }
+      }
+      if (step == 0) nloc[i] = (int)(w - b);
     }
   }
 }
@@ -390,6 +406,159 @@ __global__ void k_push_increment(const long long *__restrict__ col_ptr, const in
   if (lane == 0 && cnt) atomicAdd(pushes, (unsigned long long)cnt);
 }
 
+// ---- DI_REMOTE_RECEIVER (receiver computes, NEXT f3) -------------------------
+__device__ __forceinline__ int owner_of(const long long *bounds, int world, long long row) {
+  int q = 0;
+  while (q + 1 < world && bounds[q + 1] <= row) ++q;
+  return q;
+}
+constexpr int kMaxWorld = 64;   // per-peer shared-memory counters of the setup census
+
+// Setup pass 1: per peer, the (column, peer) pairs and remote edges of the owned
+// columns (remote rows are stored after the local ones, ascending, so a column's
+// rows of one peer are contiguous).  Block-local counters, then global adds.
+__global__ void k_ric_census(const long long *__restrict__ col_ptr, const int *__restrict__ nloc, long long n,
+                             const int *__restrict__ ri, const long long *bounds, int world,
+                             unsigned long long *pairs, unsigned long long *edges) {
+  __shared__ unsigned long long s_p[kMaxWorld], s_e[kMaxWorld];
+  for (int q = threadIdx.x; q < kMaxWorld; q += blockDim.x) { s_p[q] = 0; s_e[q] = 0; }
+  __syncthreads();
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const long long e = col_ptr[i + 1];
+    long long k = col_ptr[i] + nloc[i];
+    while (k < e) {
+      const int q = owner_of(bounds, world, ri[k]);
+      long long k2 = k;
+      while (k2 < e && ri[k2] >= bounds[q] && ri[k2] < bounds[q + 1]) ++k2;
+      atomicAdd(&s_p[q], 1ull);
+      atomicAdd(&s_e[q], (unsigned long long)(k2 - k));
+      k = k2;
+    }
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < world; q += blockDim.x) {
+    if (s_p[q]) atomicAdd(&pairs[q], s_p[q]);
+    if (s_e[q]) atomicAdd(&edges[q], s_e[q]);
+  }
+}
+
+// Setup pass 2: the column lists per peer and the edge records shipped once to
+// each receiver: key = (global source column << 32) | local row at the receiver,
+// value = p_ij (d/#out_j, or vals).
+__global__ void k_ric_fill(const long long *__restrict__ col_ptr, const int *__restrict__ nloc, long long n,
+                           const int *__restrict__ ri, const double *__restrict__ vals, double d, long long lo,
+                           const long long *bounds, int world, const long long *pair_off, unsigned long long *pair_cur,
+                           int *cols, const long long *edge_off, unsigned long long *edge_cur, Rec *erec) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const long long b = col_ptr[i], e = col_ptr[i + 1];
+    long long k = b + nloc[i];
+    const double w = d / (double)(e - b);
+    while (k < e) {
+      const int q = owner_of(bounds, world, ri[k]);
+      long long k2 = k;
+      while (k2 < e && ri[k2] >= bounds[q] && ri[k2] < bounds[q + 1]) ++k2;
+      const unsigned long long ps = atomicAdd(&pair_cur[q], 1ull);
+      cols[pair_off[q] + (long long)ps] = (int)i;
+      const unsigned long long es = atomicAdd(&edge_cur[q], (unsigned long long)(k2 - k));
+      for (long long t = k; t < k2; ++t) {
+        const long long slot = edge_off[q] + (long long)es + (t - k);
+        erec[slot] = Rec{(long long)(((unsigned long long)(i + lo) << 32) | (unsigned long long)(ri[t] - bounds[q])),
+                         vals ? vals[t] : w};
+      }
+      k = k2;
+    }
+  }
+}
+
+__global__ void k_unpack_recs(const Rec *__restrict__ r, long long m, unsigned long long *key, double *val) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += stride) {
+    key[k] = (unsigned long long)r[k].row;
+    val[k] = r[k].val;
+  }
+}
+
+// Receiver setup: the sorted keys (by source column, then row) become the
+// remote-in CSR: unique sources, offsets, rows, weights.
+__global__ void k_ric_build(const unsigned long long *__restrict__ key, long long m, const long long *__restrict__ pos,
+                            long long *src, long long *off, int *row) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += stride) {
+    const unsigned long long kk = key[k];
+    row[k] = (int)(kk & 0xffffffffull);
+    if (k == 0 || (key[k - 1] >> 32) != (kk >> 32)) {
+      src[pos[k]] = (long long)(kk >> 32);
+      off[pos[k]] = k;
+    }
+  }
+}
+__global__ void k_ric_flags(const unsigned long long *__restrict__ key, long long m, long long *flag) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += stride)
+    flag[k] = (k == 0 || (key[k - 1] >> 32) != (key[k] >> 32)) ? 1 : 0;
+}
+
+// Round, sender: for every (column j, peer q) pair with H_j != H_old_j, the record
+// (global j, H_j - H_old_j) for q.  H_old := H afterwards (a copy).
+__global__ void k_send_increments(const int *__restrict__ cols, const long long *__restrict__ pair_off, int world,
+                                  int rank, const double *__restrict__ H, const double *__restrict__ H_old,
+                                  long long lo, Rec *__restrict__ send, const long long *soff,
+                                  long long *scnt) {
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  for (int q = 0; q < world; ++q) {
+    if (q == rank) continue;
+    const long long a = pair_off[q], b = pair_off[q + 1];
+    for (long long t0 = a + gw * 32; t0 < b; t0 += warps * 32) {
+      const long long t = t0 + lane_id();
+      double dh = 0.0;
+      int j = 0;
+      if (t < b) { j = cols[t]; dh = H[j] - H_old[j]; }
+      const bool keep = dh != 0.0;
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (!m) continue;
+      unsigned long long base = 0;
+      if (lane_id() == 0) base = atomicAdd((unsigned long long *)&scnt[q], (unsigned long long)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (keep) send[soff[q] + (long long)base + __popc(m & lanemask_lt())] = Rec{(long long)j + lo, dh};
+    }
+  }
+}
+
+// Round, receiver: F_i += dh_j p_ij over the remote in-edges of source j (binary
+// search of j in ric_src), warp per record; received mass for the T rescale.
+__global__ void k_apply_remote_in(double *__restrict__ F, const Rec *__restrict__ recv, long long n_rec,
+                                  const long long *__restrict__ src, const long long *__restrict__ off, long long ric_n,
+                                  const int *__restrict__ row, const double *__restrict__ p, double *recv_mass,
+                                  unsigned long long *pushes) {
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  double m = 0.0;
+  long long cnt = 0;
+  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rec; r += warps) {
+    const Rec rc = recv[r];
+    long long lo = 0, hi = ric_n - 1;
+    while (lo < hi) {
+      const long long mid = (lo + hi + 1) >> 1;
+      if (src[mid] <= rc.row) lo = mid; else hi = mid - 1;
+    }
+    if (src[lo] != rc.row) continue;                 // cannot happen: senders ship only listed pairs
+    const long long b = off[lo], e = off[lo + 1];
+    for (long long k = b + lane_id(); k < e; k += 32) {
+      const double v = rc.val * p[k];
+      red_add(F + row[k], v);
+      m += fabs(v);
+    }
+    cnt += e - b;
+  }
+  m = warp_sum(m);
+  if (lane_id() == 0) {
+    if (m != 0.0) atomicAdd(recv_mass, m);
+    if (cnt) atomicAdd(pushes, (unsigned long long)cnt);
+  }
+}
+
 __global__ void k_set_target(Ctl *ctl, double target, long long max_pass, int done) {
   ctl->target = target;
   ctl->max_pass = max_pass;
@@ -402,7 +571,8 @@ __global__ void k_set_target(Ctl *ctl, double target, long long max_pass, int do
 void diter_dist_free(di_ctx *ctx) {
   if (!ctx || !ctx->dist) return;
   DistState *ds = ctx->dist;
-  void *ptrs[] = {ds->d_bounds, ds->send, ds->recv, ds->d_scnt, ds->d_sums};
+  void *ptrs[] = {ds->d_bounds, ds->send, ds->recv, ds->d_scnt, ds->d_sums, ds->cols, ds->d_pair_off,
+                  ds->ric_src, ds->ric_off, ds->ric_row, ds->ric_p};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (ctx->G) cudaFree(ctx->G);
@@ -505,6 +675,172 @@ static di_status exchange(di_ctx *ctx, bool send_now) {
   return DI_OK;
 }
 
+// DI_REMOTE_RECEIVER setup (collective): the receivers get, once, the remote
+// in-edges of their rows -- (P)_{i in Omega_k, j in Omega} of PAPER.md:268-272 --
+// and the senders their per-peer column lists.
+#define CKR(call)                                                                      \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess) {                                                           \
+      diter_set_err(ctx, "%s failed: %s", #call, cudaGetErrorString(e_));             \
+      st = e_ == cudaErrorMemoryAllocation ? DI_ERR_OOM : DI_ERR_CUDA;                 \
+      goto done;                                                                       \
+    }                                                                                  \
+  } while (0)
+
+static di_status setup_receiver(di_ctx *ctx) {
+  DistState *ds = ctx->dist;
+  const int W = ctx->world;
+  di_status st = DI_OK;
+  unsigned long long *d_cnt = nullptr;   // [4 W]: pairs, edges, pair cursor, edge cursor
+  long long *d_eoff = nullptr, *d_flag = nullptr, *d_pos = nullptr;
+  Rec *erec = nullptr, *rrec = nullptr;
+  unsigned long long *k1 = nullptr, *k2 = nullptr;
+  double *v1 = nullptr;
+  void *tmp = nullptr;
+  std::vector<unsigned long long> h(2 * W);
+  std::vector<long long> eoff(W + 1, 0), ecnt(W), rcnt(W), roff(W + 1, 0);
+  long long R = 0;
+  const int grid = ctx->num_sms * 8;
+  if (W > kMaxWorld) { diter_set_err(ctx, "DI_REMOTE_RECEIVER supports at most %d ranks", kMaxWorld); return DI_ERR_INVALID_ARG; }
+  CKR(cudaMalloc(&d_cnt, sizeof(unsigned long long) * 4 * W));
+  CKR(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * 4 * W, ctx->stream));
+  k_ric_census<<<grid, 256, 0, ctx->stream>>>(ctx->col_ptr, ctx->nloc, ctx->n_local, ctx->row_idx, ds->d_bounds, W,
+                                             d_cnt, d_cnt + W);
+  CKR(cudaMemcpyAsync(h.data(), d_cnt, sizeof(unsigned long long) * 2 * W, cudaMemcpyDeviceToHost, ctx->stream));
+  CKR(cudaStreamSynchronize(ctx->stream));
+  ds->pair_off.assign(W + 1, 0);
+  for (int q = 0; q < W; ++q) {
+    ds->pair_off[q + 1] = ds->pair_off[q] + (long long)h[q];
+    ecnt[q] = (long long)h[W + q];
+    eoff[q + 1] = eoff[q] + ecnt[q];
+  }
+  CKR(cudaMalloc(&ds->cols, sizeof(int) * std::max(1LL, ds->pair_off[W])));
+  CKR(cudaMalloc(&ds->d_pair_off, sizeof(long long) * (W + 1)));
+  CKR(cudaMalloc(&d_eoff, sizeof(long long) * (W + 1)));
+  CKR(cudaMalloc(&erec, sizeof(Rec) * std::max(1LL, eoff[W])));
+  CKR(cudaMemcpyAsync(ds->d_pair_off, ds->pair_off.data(), sizeof(long long) * (W + 1), cudaMemcpyHostToDevice, ctx->stream));
+  CKR(cudaMemcpyAsync(d_eoff, eoff.data(), sizeof(long long) * (W + 1), cudaMemcpyHostToDevice, ctx->stream));
+  k_ric_fill<<<grid, 256, 0, ctx->stream>>>(ctx->col_ptr, ctx->nloc, ctx->n_local, ctx->row_idx, ctx->vals, ctx->d,
+                                           ctx->lo, ds->d_bounds, W, ds->d_pair_off, d_cnt + 2 * W, ds->cols, d_eoff,
+                                           d_cnt + 3 * W, erec);
+  CKR(cudaStreamSynchronize(ctx->stream));
+  // ship every edge record to its receiver once
+  st = ds->fabric->alltoall_counts(ctx, ecnt.data(), rcnt.data());
+  if (st != DI_OK) goto done;
+  for (int q = 0; q < W; ++q) roff[q + 1] = roff[q] + rcnt[q];
+  R = roff[W];
+  CKR(cudaMalloc(&rrec, sizeof(Rec) * std::max(1LL, R)));
+  st = ds->fabric->alltoallv(ctx, erec, eoff.data(), ecnt.data(), rrec, roff.data(), rcnt.data());
+  if (st != DI_OK) goto done;
+  ctx->exchanged_bytes += (long long)sizeof(Rec) * eoff[W];
+  // sort by (source column, row) and build the remote-in CSR
+  ds->ric_e = R;
+  CKR(cudaMalloc(&ds->ric_row, sizeof(int) * std::max(1LL, R)));
+  CKR(cudaMalloc(&ds->ric_p, sizeof(double) * std::max(1LL, R)));
+  if (R > 0) {
+    CKR(cudaMalloc(&k1, sizeof(unsigned long long) * R));
+    CKR(cudaMalloc(&k2, sizeof(unsigned long long) * R));
+    CKR(cudaMalloc(&v1, sizeof(double) * R));
+    CKR(cudaMalloc(&d_flag, sizeof(long long) * R));
+    CKR(cudaMalloc(&d_pos, sizeof(long long) * R));
+    k_unpack_recs<<<grid, 256, 0, ctx->stream>>>(rrec, R, k1, v1);
+    size_t t1 = 0, t2 = 0;
+    CKR(cub::DeviceRadixSort::SortPairs(nullptr, t1, k1, k2, v1, ds->ric_p, (int64_t)R, 0, 64, ctx->stream));
+    CKR(cub::DeviceScan::ExclusiveSum(nullptr, t2, d_flag, d_pos, (int64_t)R, ctx->stream));
+    CKR(cudaMalloc(&tmp, std::max(t1, t2)));
+    CKR(cub::DeviceRadixSort::SortPairs(tmp, t1, k1, k2, v1, ds->ric_p, (int64_t)R, 0, 64, ctx->stream));
+    k_ric_flags<<<grid, 256, 0, ctx->stream>>>(k2, R, d_flag);
+    CKR(cub::DeviceScan::ExclusiveSum(tmp, t2, d_flag, d_pos, (int64_t)R, ctx->stream));
+    long long last_pos = 0, last_flag = 0;
+    CKR(cudaMemcpyAsync(&last_pos, d_pos + R - 1, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+    CKR(cudaMemcpyAsync(&last_flag, d_flag + R - 1, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+    CKR(cudaStreamSynchronize(ctx->stream));
+    ds->ric_n = last_pos + last_flag;
+  }
+  CKR(cudaMalloc(&ds->ric_src, sizeof(long long) * std::max(1LL, ds->ric_n)));
+  CKR(cudaMalloc(&ds->ric_off, sizeof(long long) * (ds->ric_n + 1)));
+  if (R > 0) {
+    k_ric_build<<<grid, 256, 0, ctx->stream>>>(k2, R, d_pos, ds->ric_src, ds->ric_off, ds->ric_row);
+    CKR(cudaMemcpyAsync(ds->ric_off + ds->ric_n, &ds->ric_e, sizeof(long long), cudaMemcpyHostToDevice, ctx->stream));
+  }
+  // round buffers: at most one record per (column, peer) pair out, per source column in
+  {
+    const long long scap = std::max(1LL, ds->pair_off[W]), rcap = std::max(1LL, ds->ric_n);
+    if (scap > ds->send_cap) {
+      cudaFree(ds->send);
+      ds->send = nullptr;
+      CKR(cudaMalloc(&ds->send, sizeof(Rec) * scap));
+      ds->send_cap = scap;
+    }
+    if (rcap > ds->recv_cap) {
+      cudaFree(ds->recv);
+      ds->recv = nullptr;
+      CKR(cudaMalloc(&ds->recv, sizeof(Rec) * rcap));
+      ds->recv_cap = rcap;
+    }
+    for (int q = 0; q < W; ++q) ds->soff[q] = ds->pair_off[q];
+  }
+  CKR(cudaStreamSynchronize(ctx->stream));
+done:
+  void *fr_[] = {d_cnt, d_eoff, d_flag, d_pos, erec, rrec, k1, k2, v1, tmp};
+  for (void *x : fr_)
+    if (x) cudaFree(x);
+  return st;
+}
+
+// Receiver-computes round (collective): ship (j, H_j - H_old_j) per listed pair,
+// H_old := H, exchange, receivers apply their in-edges.
+static di_status exchange_receiver(di_ctx *ctx, bool send_now) {
+  DistState *ds = ctx->dist;
+  const int W = ctx->world;
+  CKD(cudaMemsetAsync(ds->d_scnt, 0, sizeof(long long) * W, ctx->stream));
+  CKD(cudaMemsetAsync(ds->d_sums + kSums + 1, 0, sizeof(double), ctx->stream));   // received mass
+  if (send_now) {
+    long long *d_soff = reinterpret_cast<long long *>(ds->d_sums + kSums + 2);
+    CKD(cudaMemcpyAsync(d_soff, ds->soff.data(), sizeof(long long) * W, cudaMemcpyHostToDevice, ctx->stream));
+    k_send_increments<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ds->cols, ds->d_pair_off, W, ctx->rank, ctx->H,
+                                                                 ctx->H_old, ctx->lo, ds->send, d_soff, ds->d_scnt);
+    CKD(cudaMemcpyAsync(ctx->H_old, ctx->H, sizeof(double) * ctx->n_local, cudaMemcpyDeviceToDevice, ctx->stream));
+    ctx->kernel_launches += 1;
+  }
+  CKD(cudaMemcpyAsync(ds->scnt.data(), ds->d_scnt, sizeof(long long) * W, cudaMemcpyDeviceToHost, ctx->stream));
+  CKD(cudaStreamSynchronize(ctx->stream));
+  TRYD(ds->fabric->alltoall_counts(ctx, ds->scnt.data(), ds->rcnt.data()));
+  long long tot = 0, sent = 0;
+  for (int q = 0; q < W; ++q) {
+    ds->roff[q] = tot;
+    tot += ds->rcnt[q];
+    sent += ds->scnt[q];
+  }
+  if (tot > ds->recv_cap) {
+    diter_set_err(ctx, "receive overflow (%lld > %lld)", tot, ds->recv_cap);
+    return DI_ERR_STATE;
+  }
+  TRYD(ds->fabric->alltoallv(ctx, ds->send, ds->soff.data(), ds->scnt.data(), ds->recv, ds->roff.data(),
+                             ds->rcnt.data()));
+  if (tot > 0) {
+    k_apply_remote_in<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->F, ds->recv, tot, ds->ric_src, ds->ric_off,
+                                                                 ds->ric_n, ds->ric_row, ds->ric_p,
+                                                                 ds->d_sums + kSums + 1, &ctx->ctl->remote_pushes);
+    ctx->kernel_launches += 1;
+  }
+  if (sent > 0) {
+    ctx->exchanged_bytes += (long long)sizeof(Rec) * sent;
+    ctx->alg_bytes_exchange += 12LL * sent + 20LL * tot;
+    ctx->exchanges += 1;
+  }
+  if (send_now) ds->s_k = 0.0;
+  return DI_OK;
+}
+
+// One exchange round in the context's remote-push mode (collective).
+static di_status round_exchange(di_ctx *ctx, bool send_now) {
+  if (ctx->opt.remote_push == DI_REMOTE_RECEIVER) return exchange_receiver(ctx, send_now);
+  if (ctx->opt.remote_push == DI_REMOTE_INCREMENT && send_now) push_increment(ctx);
+  return exchange(ctx, send_now);
+}
+
 static void launch_pass_kernels(di_ctx *ctx) {
   Graph g = diter_graph(ctx);
   k_select<<<ctx->grid_select, kSelectThreads, 0, ctx->stream>>>(ctx->F, ctx->H, ctx->fr, ctx->n_local, ctx->ctl,
@@ -546,8 +882,7 @@ di_status diter_dist_run(di_ctx *ctx, double target) {
       k_reduce_partials<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->ctl, ctx->sel_part, ctx->grid_select,
                                                                   ctx->sc_part, ctx->grid_scatter, ds->d_sums);
       TRYD(ds->fabric->allreduce_sum(ctx, ds->d_sums, kSums));
-      if (incr) push_increment(ctx);
-      TRYD(exchange(ctx, true));
+      TRYD(round_exchange(ctx, true));
       k_apply_pass<<<1, 1, 0, ctx->stream>>>(ctx->ctl, ds->d_sums, ctx->log);
       ctx->kernel_launches += 2;
       CKD(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
@@ -589,8 +924,7 @@ di_status diter_dist_run(di_ctx *ctx, double target) {
       ds->s_k = hs[0];
       const double r_k = hs[1];
       const bool send_now = (ds->s_k > r_k / ctx->world) || (r_k == 0.0 && ds->s_k > 0.0);
-      if (incr && send_now) push_increment(ctx);
-      TRYD(exchange(ctx, send_now));
+      TRYD(round_exchange(ctx, send_now));
       if (ctx->opt.receive_rescale) {
         k_rescale_T<<<1, 1, 0, ctx->stream>>>(ctx->ctl, ds->d_sums + kSums + 1, r_k);
         ctx->kernel_launches += 1;
@@ -602,8 +936,7 @@ di_status diter_dist_run(di_ctx *ctx, double target) {
       if (stop || out_of_passes) {
         // deliver what is left in the outboxes, so that on return F (with H) is
         // the whole state: F = B - (I-P)H on every rank, nothing in flight
-        if (incr) push_increment(ctx);
-        TRYD(exchange(ctx, true));
+        TRYD(round_exchange(ctx, true));
         if (!stop) st = DI_ERR_NOT_CONVERGED;
         break;
       }
@@ -758,22 +1091,31 @@ extern "C" di_status di_create_dist(di_ctx **out, int32_t rank, int32_t world, c
       diter_set_err(ctx, "cudaMalloc (column partition) failed");
       return fail(DI_ERR_OOM);
     }
-    k_partition_columns<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->col_ptr, n, ctx->row_idx, ctx->vals, lo,
-                                                                   lo + n, ri2, v2, ctx->nloc);
+    long long *d_b = nullptr;
+    if (cudaMalloc(&d_b, sizeof(long long) * (world + 1)) != cudaSuccess) {
+      cudaFree(ri2);
+      if (v2) cudaFree(v2);
+      diter_set_err(ctx, "cudaMalloc failed");
+      return fail(DI_ERR_OOM);
+    }
+    cudaMemcpyAsync(d_b, bounds, sizeof(long long) * (world + 1), cudaMemcpyHostToDevice, ctx->stream);
+    k_partition_columns<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->col_ptr, n, ctx->row_idx, ctx->vals, d_b,
+                                                                   world, rank, ri2, v2, ctx->nloc);
     cudaMemcpyAsync(ctx->row_idx, ri2, sizeof(int) * nnz, cudaMemcpyDeviceToDevice, ctx->stream);
     if (v2) cudaMemcpyAsync(ctx->vals, v2, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, ctx->stream);
     const cudaError_t e = cudaStreamSynchronize(ctx->stream);
     cudaFree(ri2);
+    cudaFree(d_b);
     if (v2) cudaFree(v2);
     if (e != cudaSuccess) { diter_set_err(ctx, "column partition failed: %s", cudaGetErrorString(e)); return fail(DI_ERR_CUDA); }
-    if (ctx->opt.remote_push == DI_REMOTE_INCREMENT) {
+    if (ctx->opt.remote_push == DI_REMOTE_INCREMENT || ctx->opt.remote_push == DI_REMOTE_RECEIVER) {
       if (cudaMalloc(&ctx->H_old, sizeof(double) * std::max(1LL, n)) != cudaSuccess) {
         diter_set_err(ctx, "cudaMalloc (H_old) failed");
         return fail(DI_ERR_OOM);
       }
       cudaMemsetAsync(ctx->H_old, 0, sizeof(double) * std::max(1LL, n), ctx->stream);
     } else if (ctx->opt.remote_push != DI_REMOTE_PER_DIFFUSION) {
-      diter_set_err(ctx, "remote_push must be DI_REMOTE_PER_DIFFUSION or DI_REMOTE_INCREMENT");
+      diter_set_err(ctx, "remote_push must be DI_REMOTE_PER_DIFFUSION, DI_REMOTE_INCREMENT or DI_REMOTE_RECEIVER");
       return fail(DI_ERR_INVALID_ARG);
     }
   }
@@ -808,6 +1150,10 @@ extern "C" di_status di_create_dist(di_ctx **out, int32_t rank, int32_t world, c
     cudaMemcpyAsync(ds->d_bounds, bounds, sizeof(long long) * (world + 1), cudaMemcpyHostToDevice, ctx->stream);
     s = diter_dist_reset(ctx);
     if (s != DI_OK) return fail(s);
+    if (ctx->opt.remote_push == DI_REMOTE_RECEIVER) {
+      s = setup_receiver(ctx);
+      if (s != DI_OK) return fail(s);
+    }
   }
   // The threshold schedule is global: T_0 = max over ranks |B_i| / alpha (done in
   // setup through diter_dist_max); SYNC applies the HYBRID rule to the global |S_p|

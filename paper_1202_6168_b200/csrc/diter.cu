@@ -277,7 +277,7 @@ static di_status setup_key(di_ctx *ctx) {
 Graph diter_graph(const di_ctx *ctx) {
   return Graph{ctx->col_ptr, ctx->row_idx, ctx->vals, ctx->n_local, ctx->d, ctx->hot_lo,
                ctx->lo, ctx->G, ctx->dflags, ctx->far, ctx->nloc,
-               ctx->opt.remote_push == DI_REMOTE_INCREMENT ? 1 : 0};
+               ctx->opt.remote_push != DI_REMOTE_PER_DIFFUSION ? 1 : 0};
 }
 
 // Capture check_interval passes of (select, scatter, finalize) once.

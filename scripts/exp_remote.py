@@ -1,5 +1,5 @@
 """Remote-push modes on K loopback ranks (one GPU): outbox pushes, exchanged bytes,
-passes, for per-diffusion vs H-increment remote pushes (NEXT f2).  Experiment."""
+passes -- per-diffusion, H increments (NEXT f2), receiver computes (NEXT f3).  Experiment."""
 import os, sys, threading
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -11,8 +11,8 @@ n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 1_000_000
 p = gen.config("C2", 1, n=n)
 for K in (2, 4, 8):
     bounds = dist.partition_bounds(p.col_ptr, K, cost="inout", row_idx=p.row_idx)
-    for remote in (1,):
-        for ci, rr in ((1, 1), (2, 1), (4, 1), (8, 1)):
+    for remote in (0, 1, 2):
+        for ci, rr in ((4, 1),):
             st = [None] * K
             cid = dist.loopback_comm_id(f"x{K}{remote}{ci}{rr}")
 
@@ -27,6 +27,6 @@ for K in (2, 4, 8):
             th = [threading.Thread(target=w, args=(r,)) for r in range(K)]
             [t.start() for t in th]
             [t.join() for t in th]
-            print(f"K={K} remote={'incr' if remote else 'diff'} ci={ci} rescale={rr}: outbox pushes={sum(s['remote_pushes'] for s in st):.4e} "
+            print(f"K={K} remote={['diff', 'incr', 'recv'][remote]} ci={ci} rescale={rr}: outbox pushes={sum(s['remote_pushes'] for s in st):.4e} "
                   f"exchanged={sum(s['exchanged_bytes'] for s in st) / 1e6:.1f} MB edges={sum(s['edges'] for s in st):.4e} "
                   f"passes(max)={max(s['passes'] for s in st)}", flush=True)

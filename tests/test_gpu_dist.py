@@ -50,14 +50,16 @@ def run_ranks(K, n, cp, ri, vals, b, d, target, bounds, mode, key, **opts):
 
 
 @pytest.mark.parametrize("K,key,remote", [(2, di.DI_KEY_RAW, 0), (4, di.DI_KEY_RAW, 0), (3, di.DI_KEY_EDGE, 0),
-                                          (2, di.DI_KEY_RAW, 1), (3, di.DI_KEY_EDGE, 1)])
+                                          (2, di.DI_KEY_RAW, 1), (3, di.DI_KEY_EDGE, 1),
+                                          (2, di.DI_KEY_RAW, 2), (4, di.DI_KEY_EDGE, 2)])
 def test_sync_matches_single_gpu_passes(K, key, remote):
     """SYNC mode is the single-GPU snapshot pass: same per-pass frontier sizes,
     edges and thresholds (random B: no exact-arithmetic ties), same fixed point --
     with the raw and the per-edge selection key (per-edge weights need only local
-    out-degrees), and with remote edges pushed per diffusion or as H increments at
-    each exchange (NEXT f2: the same fluid reaches the same rows
-    before the next selection)."""
+    out-degrees), and with remote edges pushed per diffusion, as H increments at
+    each exchange (NEXT f2) or applied by the receivers from the
+    shipped increments (NEXT f3): the same fluid reaches the same
+    rows before the next selection."""
     n = 200_000
     cp, ri = gen.web_graph(n, 5)
     rng = np.random.default_rng(3)
@@ -120,6 +122,45 @@ def test_async_remote_increments(K):
         assert all(o[4] < p.parity_stop for o in outs)
         pushes[remote] = sum(o[3]["remote_pushes"] for o in outs)
     assert 0 < pushes[di.DI_REMOTE_INCREMENT] < pushes[di.DI_REMOTE_PER_DIFFUSION]
+
+
+@pytest.mark.parametrize("K,cost", [(2, "out"), (4, "inout")])
+def test_async_receiver_computes(K, cost):
+    """NEXT f3: senders ship (column, H increment) once per peer
+    owning rows of the column; receivers apply their stored in-edges.  Parity, a
+    closed ledger, the completed PageRank; the receivers do the remote pushes."""
+    p = gen.config("C2", 2, n=300_000)
+    bn = 0.15
+    bounds = dist.partition_bounds(p.col_ptr, K, cost=cost, row_idx=p.row_idx)
+    H, F, outs = run_ranks(K, p.n, p.col_ptr, p.row_idx, None, None, 0.85, p.parity_stop, bounds,
+                           di.DI_EXCHANGE_ASYNC, f"recv{K}{cost}", check_interval=4, remote_push=di.DI_REMOTE_RECEIVER)
+    X = oracle.Problem(p.n, p.col_ptr, p.row_idx).solve(1e-12 * bn * 0.15).H
+    assert np.abs(H - X).sum() <= 1e-8 * bn
+    deg = np.diff(p.col_ptr)
+    ledger = np.abs(F).sum() + 0.15 * H.sum() + 0.85 * H[deg == 0].sum()
+    assert abs(ledger - bn) <= 1e-12 * bn
+    assert all(o[4] < p.parity_stop for o in outs)
+    Xp = np.concatenate([o[5] for o in outs])
+    assert np.abs(Xp - X / X.sum()).sum() <= 2e-8
+    assert sum(o[3]["remote_pushes"] for o in outs) > 0 and all(o[3]["exchanged_bytes"] > 0 for o in outs)
+
+
+def test_async_receiver_computes_signed_unsorted_rows():
+    """Signed P with each column's rows in reverse (unsorted) order: the create-time
+    partition groups remote rows by peer, so receiver-computes stays exact."""
+    n = 60_000
+    cp, ri, v, b = gen.signed_system(n, 4)
+    ri2, v2 = ri.copy(), v.copy()
+    for j in range(n):
+        a, z = cp[j], cp[j + 1]
+        ri2[a:z] = ri[a:z][::-1]
+        v2[a:z] = v[a:z][::-1]
+    bn = np.abs(b).sum()
+    bounds = dist.partition_bounds(cp, 3)
+    H, F, outs = run_ranks(3, n, cp, ri2, v2, b, 0.9, 5e-10 * bn, bounds, di.DI_EXCHANGE_ASYNC, "recvsigned",
+                           remote_push=di.DI_REMOTE_RECEIVER)
+    X, _ = oracle.Problem(n, cp, ri, v, b, 0.9).jacobi(1e-13 * bn)
+    assert np.abs(H - X).sum() <= 1e-8 * bn
 
 
 def test_async_remote_increments_signed():
