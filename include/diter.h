@@ -125,7 +125,11 @@ typedef struct {
   int32_t remote_push;     /* DI_REMOTE_*; distributed only; default DI_REMOTE_PER_DIFFUSION */
   int32_t receive_rescale; /* ASYNC only: after merging received fluid R, T_k <- T_k (r_k + R) / r_k
                               (reading R13); 1 = on (default), 0 = off */
-  int32_t reserved[5];
+  int32_t adapt_rounds;    /* ASYNC only: every adapt_rounds exchange rounds apply the paper's
+                              partition adaptation (reading R22) -- a boundary
+                              moves by 10 % of the busier side when its residual is > 2x and its
+                              work since the last check > 1.2x the neighbour's; 0 = off (default) */
+  int32_t reserved[4];
 } di_options;
 
 /* One record per executed pass (device-logged, read with di_get_pass_log). */
@@ -166,7 +170,9 @@ typedef struct {
                               + 16 per diffused node (its col_ptr pair) */
   int64_t remote_pushes;   /* distributed: pushes into the remote outbox since create (one RED per
                               remote edge per diffusion, or per column increment with
-                              DI_REMOTE_INCREMENT) */
+                              DI_REMOTE_INCREMENT; the receiver's in-edge adds with
+                              DI_REMOTE_RECEIVER) */
+  int64_t rebalances;      /* distributed: ownership changes (di_rebalance / adapt_rounds) */
 } di_stats;
 
 /* Fill *opt with the defaults above. */
@@ -234,6 +240,16 @@ DI_API di_status di_get_pagerank_device(di_ctx *ctx, double *d_out);
  * collective then).  Also refreshes stats.residual. */
 DI_API di_status di_get_residual(di_ctx *ctx, double *r_out);
 DI_API di_status di_get_stats(const di_ctx *ctx, di_stats *s);
+/* Distributed: move node ownership to new_bounds[world+1] (0 = b_0 < ... < b_world = N,
+ * the same array on every rank; collective).  Everything in flight is delivered
+ * first; each moved node's column (rows, values), F, H and B travel to its new owner,
+ * which rebuilds its device state over the new range and keeps T, the pass counters
+ * and the statistics ("we just need to transmit the information F_n
+ * and H_n of the candidate nodes").  Call between di_run calls, or let di_run do it
+ * with options.adapt_rounds. */
+DI_API di_status di_rebalance(di_ctx *ctx, const int64_t *new_bounds);
+/* Current ownership bounds: world+1 entries (distributed) or {0, N}. */
+DI_API di_status di_get_bounds(const di_ctx *ctx, int64_t *out);
 /* Copy pass records [first, first+count) into out; *n_copied receives the
  * number copied (passes beyond the log capacity are not recorded). */
 DI_API di_status di_get_pass_log(const di_ctx *ctx, int64_t first, int64_t count, di_pass_log *out,

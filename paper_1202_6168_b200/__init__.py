@@ -35,7 +35,7 @@ STATUS_NAMES = {0: "DI_OK", 1: "DI_ERR_INVALID_ARG", 2: "DI_ERR_CONTRACTION", 3:
 # every symbol include/diter.h declares (checked by tests/test_abi.py)
 EXPORTS = ["di_default_options", "di_struct_size", "di_create", "di_create_dist", "di_get_unique_id", "di_reset", "di_run",
            "di_get_history", "di_get_fluid", "di_get_history_device", "di_get_fluid_device",
-           "di_get_pagerank", "di_get_pagerank_device",
+           "di_get_pagerank", "di_get_pagerank_device", "di_rebalance", "di_get_bounds",
            "di_get_residual", "di_get_stats", "di_get_pass_log", "di_last_error", "di_destroy",
            "di_csc_from_coo", "di_partition_cb"]
 
@@ -56,7 +56,8 @@ class di_options(ctypes.Structure):
                 ("scatter_run", ctypes.c_int32), ("scatter_stripes", ctypes.c_int32),
                 ("far_push", ctypes.c_int32), ("far_warm_log2", ctypes.c_int32),
                 ("select_key", ctypes.c_int32), ("remote_push", ctypes.c_int32),
-                ("receive_rescale", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+                ("receive_rescale", ctypes.c_int32), ("adapt_rounds", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 4)]
 
 
 class di_pass_log(ctypes.Structure):
@@ -77,7 +78,7 @@ class di_stats(ctypes.Structure):
                 ("kernel_launches", ctypes.c_int64), ("kt_select_ms", ctypes.c_double),
                 ("kt_scatter_ms", ctypes.c_double), ("kt_finalize_ms", ctypes.c_double),
                 ("kt_passes", ctypes.c_int64), ("scatter_bytes", ctypes.c_int64),
-                ("remote_pushes", ctypes.c_int64)]
+                ("remote_pushes", ctypes.c_int64), ("rebalances", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -109,6 +110,8 @@ def load_library() -> ctypes.CDLL:
         "di_get_fluid": (st, [vp, vp]),
         "di_get_history_device": (st, [vp, vp]),
         "di_get_pagerank": (st, [vp, vp]),
+        "di_rebalance": (st, [vp, vp]),
+        "di_get_bounds": (st, [vp, vp]),
         "di_get_pagerank_device": (st, [vp, vp]),
         "di_get_fluid_device": (st, [vp, vp]),
         "di_get_residual": (st, [vp, ctypes.POINTER(f64)]),
@@ -207,7 +210,9 @@ def di_create_dist(rank, world, comm_id: bytes, bounds, n_global, col_ptr_local,
     s = lib.di_create_dist(ctypes.byref(h), int(rank), int(world), idbuf, _p(bnd), int(n_global),
                            pc, pr, pv, pb, float(d), ctypes.byref(opt))
     _check(s)
-    return Context(h, int(bnd[rank + 1] - bnd[rank]))
+    ctx = Context(h, int(bnd[rank + 1] - bnd[rank]))
+    ctx.world = int(world)
+    return ctx
 
 
 def di_get_unique_id() -> bytes:
@@ -218,6 +223,8 @@ def di_get_unique_id() -> bytes:
 
 def di_run(ctx: Context, residual_target: float, raise_on_not_converged: bool = True) -> int:
     s = load_library().di_run(ctx.handle, float(residual_target))
+    if getattr(ctx, "world", 1) > 1:          # options.adapt_rounds may move ownership
+        ctx.n_local = int(di_get_stats(ctx)["n_local"])
     if s == DI_ERR_NOT_CONVERGED and not raise_on_not_converged:
         return s
     _check(s, ctx.handle)
@@ -264,6 +271,19 @@ def di_get_pagerank(ctx: Context, out=None):
 
 def di_get_pagerank_device(ctx: Context, out):
     return _get_vec(load_library().di_get_pagerank_device, ctx, out)
+
+
+def di_rebalance(ctx: Context, new_bounds):
+    """Collective: move ownership to new_bounds (world + 1 int64, same on every rank)."""
+    nb = np.ascontiguousarray(new_bounds, dtype=np.int64)
+    _check(load_library().di_rebalance(ctx.handle, _p(nb)), ctx.handle)
+    ctx.n_local = int(di_get_stats(ctx)["n_local"])
+
+
+def di_get_bounds(ctx: Context):
+    out = np.zeros(max(2, getattr(ctx, "world", 1) + 1), dtype=np.int64)
+    _check(load_library().di_get_bounds(ctx.handle, _p(out)), ctx.handle)
+    return out
 
 
 def di_get_residual(ctx: Context) -> float:

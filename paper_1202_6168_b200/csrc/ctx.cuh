@@ -37,6 +37,7 @@ struct di_ctx {
   int *nloc = nullptr;           // distributed: local (owned-row) edges per column, stored first
   double *H_old = nullptr;       // DI_REMOTE_INCREMENT: H at the last push of the remote edges
   long long remote_pushes = 0;   // pushes into the outbox since create
+  long long rebalances = 0;      // di_rebalance calls that moved ownership (distributed)
   diter::Frontier fr{};
   diter::Far far{};               // far-push bins (propagation blocking), 1 GPU
   long long *far_off = nullptr;   // [n_bins + 1] first chunk of each bin (device)

@@ -860,6 +860,42 @@ static void launch_pass_kernels(di_ctx *ctx) {
   ctx->kernel_launches += ctx->cap_hub > 0 ? 3 : 2;
 }
 
+// Partition adaptation rule (reading R22): for each boundary
+// omega_k between ranks a = k-1 and b = k, if one side has > 2x the other's
+// residual and has done > 1.2x its work (edges) since the last check, 10 % of the
+// busier side's nodes move across.  Inputs are gathered from every rank, so all
+// ranks compute the same bounds; *nb stays empty when nothing moves.
+extern "C" di_status di_rebalance(di_ctx *ctx, const int64_t *nb);
+static di_status adapt_bounds(di_ctx *ctx, double r_k, long long work, std::vector<long long> *nb) {
+  DistState *ds = ctx->dist;
+  const int W = ctx->world;
+  std::vector<long long> send(W), rr(W), ww(W);
+  long long rbits;
+  std::memcpy(&rbits, &r_k, sizeof(double));
+  std::fill(send.begin(), send.end(), rbits);
+  TRYD(ds->fabric->alltoall_counts(ctx, send.data(), rr.data()));
+  std::fill(send.begin(), send.end(), work);
+  TRYD(ds->fabric->alltoall_counts(ctx, send.data(), ww.data()));
+  std::vector<double> r(W);
+  for (int q = 0; q < W; ++q) std::memcpy(&r[q], &rr[q], sizeof(double));
+  std::vector<long long> b = ds->bounds;
+  bool moved = false;
+  for (int k = 1; k < W; ++k) {
+    const int a = k - 1, c = k;
+    if (r[a] > 2.0 * r[c] && (double)ww[a] > 1.2 * (double)ww[c]) {
+      const long long m = std::max(1LL, (b[k] - b[k - 1]) / 10);
+      const long long nk = std::max(b[k - 1] + 1, b[k] - m);
+      if (nk != b[k]) { b[k] = nk; moved = true; }
+    } else if (r[c] > 2.0 * r[a] && (double)ww[c] > 1.2 * (double)ww[a]) {
+      const long long m = std::max(1LL, (b[k + 1] - b[k]) / 10);
+      const long long nk = std::min(b[k + 1] - 1, b[k] + m);
+      if (nk != b[k]) { b[k] = nk; moved = true; }
+    }
+  }
+  if (moved) *nb = b;
+  return DI_OK;
+}
+
 di_status diter_dist_run(di_ctx *ctx, double target) {
   DistState *ds = ctx->dist;
   CKD(cudaSetDevice(ctx->device));
@@ -897,6 +933,7 @@ di_status diter_dist_run(di_ctx *ctx, double target) {
     }
   } else {
     // -------- ASYNC: local passes, exchange rounds every check_interval ------
+    long long rounds = 0, edges_mark = h->edges;
     for (;;) {
       // local passes: no target (never "done" locally), local threshold policy
       k_set_target<<<1, 1, 0, ctx->stream>>>(ctx->ctl, 0.0, max_pass_abs, 0);
@@ -940,6 +977,19 @@ di_status diter_dist_run(di_ctx *ctx, double target) {
         if (!stop) st = DI_ERR_NOT_CONVERGED;
         break;
       }
+      // partition adaptation (NEXT f4, reading R22) every adapt_rounds rounds
+      if (ctx->opt.adapt_rounds > 0 && ++rounds % ctx->opt.adapt_rounds == 0) {
+        std::vector<long long> nb;
+        TRYD(adapt_bounds(ctx, r_k, h->edges - edges_mark, &nb));
+        if (!nb.empty()) {
+          TRYD(di_rebalance(ctx, reinterpret_cast<const int64_t *>(nb.data())));
+          ds = ctx->dist;                              // the context was rebuilt
+          h = reinterpret_cast<Ctl *>(ctx->h_ctl);
+          CKD(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+          CKD(cudaStreamSynchronize(ctx->stream));
+        }
+        edges_mark = h->edges;
+      }
     }
   }
 out:
@@ -963,6 +1013,211 @@ out:
 }
 
 // ----------------------------------------------------------------- create --
+
+static di_status dist_build(di_ctx *ctx, const int64_t *col_ptr_local, const int32_t *row_idx_local,
+                            const double *values_local, const double *b_local, const di_options *opt);
+
+// ---------------------------------------------------------- rebalance (f4) --
+// PAPER.md:178-184 remark + P:523-543: "an idle PID could take nodes from the
+// busiest PID ... we just need to transmit the information F_n and H_n of the
+// candidate nodes".  Ranks here hold only their own columns, so the moved
+// columns travel too.  Collective: deliver everything in flight, ship each
+// node's column (degree, rows, values), F, H and B to its owner under the new
+// bounds, rebuild the context on its new range (same fabric, stream, events),
+// restore F, H, the control block and the counters.
+namespace {
+template <typename T>
+void put(std::vector<unsigned char> &b, const T *p, size_t n) {
+  const size_t o = b.size();
+  b.resize(o + sizeof(T) * n);
+  if (n) std::memcpy(b.data() + o, p, sizeof(T) * n);
+  b.resize((b.size() + 7) & ~size_t(7));
+}
+template <typename T>
+const unsigned char *get(const unsigned char *c, T *p, size_t n) {
+  if (n) std::memcpy(p, c, sizeof(T) * n);
+  return c + ((sizeof(T) * n + 7) & ~size_t(7));
+}
+}  // namespace
+
+extern "C" di_status di_rebalance(di_ctx *ctx, const int64_t *nb) {
+  if (!ctx || !nb) { diter_set_err(ctx, "NULL argument"); return DI_ERR_INVALID_ARG; }
+  if (!ctx->dist || ctx->world < 2) { diter_set_err(ctx, "di_rebalance: distributed contexts only"); return DI_ERR_INVALID_ARG; }
+  const int W = ctx->world, rank = ctx->rank;
+  if (nb[0] != 0 || nb[W] != ctx->n_rows) { diter_set_err(ctx, "bounds must start at 0 and end at N"); return DI_ERR_INVALID_ARG; }
+  for (int k = 0; k < W; ++k)
+    if (nb[k + 1] <= nb[k]) { diter_set_err(ctx, "bounds must be strictly increasing"); return DI_ERR_INVALID_ARG; }
+  CKD(cudaSetDevice(ctx->device));
+  DistState *ds = ctx->dist;
+  TRYD(round_exchange(ctx, true));                 // nothing in flight from here on
+  const long long n = ctx->n_local, nnz = ctx->nnz_local, lo = ctx->lo;
+  std::vector<long long> cp(n + 1);
+  std::vector<int> ri(nnz);
+  std::vector<double> vv(ctx->vals ? nnz : 0), F(n), H(n), B(ctx->d_b ? n : 0);
+  Ctl c;
+  CKD(cudaMemcpyAsync(cp.data(), ctx->col_ptr, sizeof(long long) * (n + 1), cudaMemcpyDeviceToHost, ctx->stream));
+  if (nnz) CKD(cudaMemcpyAsync(ri.data(), ctx->row_idx, sizeof(int) * nnz, cudaMemcpyDeviceToHost, ctx->stream));
+  if (ctx->vals && nnz) CKD(cudaMemcpyAsync(vv.data(), ctx->vals, sizeof(double) * nnz, cudaMemcpyDeviceToHost, ctx->stream));
+  CKD(cudaMemcpyAsync(F.data(), ctx->F, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CKD(cudaMemcpyAsync(H.data(), ctx->H, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (ctx->d_b) CKD(cudaMemcpyAsync(B.data(), ctx->d_b, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CKD(cudaMemcpyAsync(&c, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+  CKD(cudaStreamSynchronize(ctx->stream));
+  // pack, per new owner q, my nodes [a, z) in its new range
+  std::vector<std::vector<unsigned char>> pk(W);
+  for (int q = 0; q < W; ++q) {
+    const long long a = std::max<long long>(lo, nb[q]), z = std::min<long long>(lo + n, nb[q + 1]);
+    if (z <= a) continue;
+    const long long m = z - a, e0 = cp[a - lo], e1 = cp[z - lo];
+    std::vector<long long> deg(m);
+    for (long long i = 0; i < m; ++i) deg[i] = cp[a - lo + i + 1] - cp[a - lo + i];
+    const long long hdr[3] = {a, m, e1 - e0};
+    put(pk[q], hdr, 3);
+    put(pk[q], deg.data(), m);
+    put(pk[q], ri.data() + e0, e1 - e0);
+    if (ctx->vals) put(pk[q], vv.data() + e0, e1 - e0);
+    put(pk[q], F.data() + (a - lo), m);
+    put(pk[q], H.data() + (a - lo), m);
+    if (ctx->d_b) put(pk[q], B.data() + (a - lo), m);
+    pk[q].resize((pk[q].size() + sizeof(Rec) - 1) / sizeof(Rec) * sizeof(Rec));
+  }
+  std::vector<long long> soff(W, 0), scnt(W, 0), roff(W, 0), rcnt(W, 0);
+  long long stot = 0;
+  for (int q = 0; q < W; ++q) {
+    soff[q] = stot;
+    scnt[q] = q == rank ? 0 : (long long)(pk[q].size() / sizeof(Rec));
+    stot += scnt[q];
+  }
+  TRYD(ds->fabric->alltoall_counts(ctx, scnt.data(), rcnt.data()));
+  long long rtot = 0;
+  for (int q = 0; q < W; ++q) { roff[q] = rtot; rtot += q == rank ? 0 : rcnt[q]; }
+  std::vector<unsigned char> hs(std::max<long long>(1, stot) * sizeof(Rec)), hr(std::max<long long>(1, rtot) * sizeof(Rec));
+  for (int q = 0; q < W; ++q)
+    if (scnt[q]) std::memcpy(hs.data() + soff[q] * sizeof(Rec), pk[q].data(), pk[q].size());
+  Rec *dsend = nullptr, *drecv = nullptr;
+  CKD(cudaMalloc(&dsend, hs.size()));
+  CKD(cudaMalloc(&drecv, hr.size()));
+  CKD(cudaMemcpyAsync(dsend, hs.data(), hs.size(), cudaMemcpyHostToDevice, ctx->stream));
+  di_status st = ds->fabric->alltoallv(ctx, dsend, soff.data(), scnt.data(), drecv, roff.data(), rcnt.data());
+  if (st == DI_OK && cudaMemcpyAsync(hr.data(), drecv, hr.size(), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess)
+    st = DI_ERR_CUDA;
+  cudaStreamSynchronize(ctx->stream);
+  cudaFree(dsend);
+  cudaFree(drecv);
+  if (st != DI_OK) return st;
+  // unpack in source-rank order: the pieces of [nb[rank], nb[rank+1]) ascend
+  const long long lo2 = nb[rank], n2 = nb[rank + 1] - nb[rank];
+  std::vector<long long> cp2(n2 + 1, 0);
+  std::vector<int> ri2;
+  std::vector<double> vv2, F2(n2), H2(n2), B2(ctx->d_b ? n2 : 0);
+  long long next = lo2;
+  for (int q = 0; q < W; ++q) {
+    const bool self = q == rank;
+    if ((self ? (long long)pk[q].size() : rcnt[q]) == 0) continue;
+    const unsigned char *cur = self ? pk[q].data() : hr.data() + roff[q] * sizeof(Rec);
+    long long hdr[3];
+    cur = get(cur, hdr, 3);
+    const long long a = hdr[0], m = hdr[1], e = hdr[2];
+    if (a != next || a + m > lo2 + n2) {
+      diter_set_err(ctx, "di_rebalance: pieces do not tile the new range (rank %d, piece %lld+%lld)", rank, a, m);
+      return DI_ERR_STATE;
+    }
+    std::vector<long long> deg(m);
+    cur = get(cur, deg.data(), m);
+    const long long i0 = a - lo2, e_base = (long long)ri2.size();
+    for (long long i = 0; i < m; ++i) cp2[i0 + i + 1] = cp2[i0 + i] + deg[i];
+    if (cp2[i0 + m] - cp2[i0] != e || cp2[i0] != e_base) { diter_set_err(ctx, "di_rebalance: corrupt piece"); return DI_ERR_STATE; }
+    ri2.resize(e_base + e);
+    cur = get(cur, ri2.data() + e_base, e);
+    if (ctx->vals) { vv2.resize(e_base + e); cur = get(cur, vv2.data() + e_base, e); }
+    cur = get(cur, F2.data() + i0, m);
+    cur = get(cur, H2.data() + i0, m);
+    if (ctx->d_b) cur = get(cur, B2.data() + i0, m);
+    next = a + m;
+  }
+  if (next != lo2 + n2) { diter_set_err(ctx, "di_rebalance: new range not covered"); return DI_ERR_STATE; }
+  // rebuild on the new range with the same fabric
+  di_ctx *nc = new (std::nothrow) di_ctx();
+  if (!nc) { diter_set_err(ctx, "host OOM"); return DI_ERR_OOM; }
+  nc->n_rows = ctx->n_rows;
+  nc->n_local = n2;
+  nc->nnz_local = cp2[n2];
+  nc->lo = lo2;
+  nc->d = ctx->d;
+  nc->rank = rank;
+  nc->world = W;
+  nc->dist = new DistState();
+  nc->dist->fabric = std::move(ds->fabric);
+  nc->dist->bounds.assign(nb, nb + W + 1);
+  di_options o = ctx->opt;
+  o.device = ctx->device;
+  st = dist_build(nc, reinterpret_cast<const int64_t *>(cp2.data()), ri2.empty() ? nullptr : ri2.data(), ctx->vals ? vv2.data() : nullptr,
+                  ctx->d_b ? B2.data() : nullptr, &o);
+  if (st != DI_OK) {
+    ds->fabric = std::move(nc->dist->fabric);   // the old context stays usable
+    diter_set_err(ctx, "di_rebalance: rebuild failed: %s", nc->err.c_str());
+    di_destroy(nc);
+    return st;
+  }
+  // restore the state: F, H (H_old = H: nothing is pending after the flush), the
+  // control block (T, pass, counters; per-pass scratch cleared), the pass log
+  CKD(cudaMemcpyAsync(nc->F, F2.data(), sizeof(double) * n2, cudaMemcpyHostToDevice, nc->stream));
+  CKD(cudaMemcpyAsync(nc->H, H2.data(), sizeof(double) * n2, cudaMemcpyHostToDevice, nc->stream));
+  if (nc->H_old) CKD(cudaMemcpyAsync(nc->H_old, H2.data(), sizeof(double) * n2, cudaMemcpyHostToDevice, nc->stream));
+  Ctl c2 = c;
+  c2.n_total = nc->ctl_init.n_total;
+  c2.hub_packed = 0ull;
+  c2.sc_next = 0u;
+  std::memset(c2.tickets, 0, sizeof(c2.tickets));
+  std::memset(c2.far_cnt, 0, sizeof(c2.far_cnt));
+  CKD(cudaMemcpyAsync(nc->ctl, &c2, sizeof(Ctl), cudaMemcpyHostToDevice, nc->stream));
+  CKD(cudaMemcpyAsync(nc->log, ctx->log, sizeof(di_pass_log) * std::min(nc->log_cap, ctx->log_cap),
+                      cudaMemcpyDeviceToDevice, nc->stream));
+  CKD(cudaStreamSynchronize(nc->stream));
+  Ctl ci = ctx->ctl_init;                       // di_reset keeps the original T_0
+  ci.n_total = nc->ctl_init.n_total;
+  nc->ctl_init = ci;
+  // the caller's stream and timing events stay with the handle
+  cudaEventDestroy(nc->ev0);
+  cudaEventDestroy(nc->ev1);
+  cudaStreamDestroy(nc->stream);
+  nc->stream = ctx->stream;
+  nc->ev0 = ctx->ev0;
+  nc->ev1 = ctx->ev1;
+  ctx->stream = nullptr;
+  ctx->ev0 = ctx->ev1 = nullptr;
+  nc->passes_done = ctx->passes_done;
+  nc->edges = ctx->edges;
+  nc->nodes = ctx->nodes;
+  nc->graph_launches = ctx->graph_launches;
+  nc->kernel_launches += ctx->kernel_launches;
+  nc->exchanged_bytes = ctx->exchanged_bytes + stot * (long long)sizeof(Rec);
+  nc->exchanges = ctx->exchanges;
+  nc->alg_bytes_exchange = ctx->alg_bytes_exchange;
+  nc->residual = ctx->residual;
+  nc->threshold = ctx->threshold;
+  nc->run_ms = ctx->run_ms;
+  nc->run_ms_total = ctx->run_ms_total;
+  nc->kt_passes = ctx->kt_passes;
+  for (int k = 0; k < 3; ++k) nc->kt_ms[k] = ctx->kt_ms[k];
+  nc->remote_pushes = ctx->remote_pushes;
+  nc->rebalances = ctx->rebalances + 1;
+  std::swap(*ctx, *nc);
+  di_destroy(nc);                               // the old device state (its fabric moved out)
+  return DI_OK;
+}
+
+extern "C" di_status di_get_bounds(const di_ctx *ctx, int64_t *out) {
+  if (!ctx || !out) { diter_set_err(nullptr, "NULL argument"); return DI_ERR_INVALID_ARG; }
+  if (ctx->dist) {
+    for (int k = 0; k <= ctx->world; ++k) out[k] = ctx->dist->bounds[k];
+  } else {
+    out[0] = 0;
+    out[1] = ctx->n_rows;
+  }
+  return DI_OK;
+}
+
 extern "C" di_status di_get_unique_id(void *comm_id_out) {
   if (!comm_id_out) {
     diter_set_err(nullptr, "NULL argument");
@@ -985,6 +1240,104 @@ extern "C" di_status di_get_unique_id(void *comm_id_out) {
 }
 
 static const char kLoopTag[8] = {'D', 'I', 'L', 'O', 'O', 'P', '0', '1'};
+
+// Everything of a distributed context after its fabric exists (ds->bounds set,
+// ctx->lo / n_local / nnz_local describing this rank's columns): device setup,
+// column partition, outbox and exchange buffers, receiver structures.  Shared by
+// di_create_dist and di_rebalance.  Collective.
+static di_status dist_build(di_ctx *ctx, const int64_t *col_ptr_local, const int32_t *row_idx_local,
+                            const double *values_local, const double *b_local, const di_options *opt) {
+  DistState *ds = ctx->dist;
+  const int world = ctx->world, rank = ctx->rank;
+  const long long n_global = ctx->n_rows, nl = ctx->n_local;
+  di_status s = diter_setup(ctx, col_ptr_local, row_idx_local, values_local, b_local, opt);
+  if (s != DI_OK) return s;
+  // local rows first in every column (nloc), in place via a scratch copy
+  {
+    const long long n = ctx->n_local, nnz = ctx->nnz_local;
+    int *ri2 = nullptr;
+    double *v2 = nullptr;
+    if (cudaMalloc(&ctx->nloc, sizeof(int) * std::max(1LL, n)) != cudaSuccess ||
+        cudaMalloc(&ri2, sizeof(int) * std::max(1LL, nnz)) != cudaSuccess ||
+        (ctx->vals && cudaMalloc(&v2, sizeof(double) * std::max(1LL, nnz)) != cudaSuccess)) {
+      if (ri2) cudaFree(ri2);
+      diter_set_err(ctx, "cudaMalloc (column partition) failed");
+      return (DI_ERR_OOM);
+    }
+    long long *d_b = nullptr;
+    if (cudaMalloc(&d_b, sizeof(long long) * (world + 1)) != cudaSuccess) {
+      cudaFree(ri2);
+      if (v2) cudaFree(v2);
+      diter_set_err(ctx, "cudaMalloc failed");
+      return (DI_ERR_OOM);
+    }
+    cudaMemcpyAsync(d_b, ds->bounds.data(), sizeof(long long) * (world + 1), cudaMemcpyHostToDevice, ctx->stream);
+    k_partition_columns<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->col_ptr, n, ctx->row_idx, ctx->vals, d_b,
+                                                                   world, rank, ri2, v2, ctx->nloc);
+    cudaMemcpyAsync(ctx->row_idx, ri2, sizeof(int) * nnz, cudaMemcpyDeviceToDevice, ctx->stream);
+    if (v2) cudaMemcpyAsync(ctx->vals, v2, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, ctx->stream);
+    const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(ri2);
+    cudaFree(d_b);
+    if (v2) cudaFree(v2);
+    if (e != cudaSuccess) { diter_set_err(ctx, "column partition failed: %s", cudaGetErrorString(e)); return (DI_ERR_CUDA); }
+    if (ctx->opt.remote_push == DI_REMOTE_INCREMENT || ctx->opt.remote_push == DI_REMOTE_RECEIVER) {
+      if (cudaMalloc(&ctx->H_old, sizeof(double) * std::max(1LL, n)) != cudaSuccess) {
+        diter_set_err(ctx, "cudaMalloc (H_old) failed");
+        return (DI_ERR_OOM);
+      }
+      cudaMemsetAsync(ctx->H_old, 0, sizeof(double) * std::max(1LL, n), ctx->stream);
+    } else if (ctx->opt.remote_push != DI_REMOTE_PER_DIFFUSION) {
+      diter_set_err(ctx, "remote_push must be DI_REMOTE_PER_DIFFUSION, DI_REMOTE_INCREMENT or DI_REMOTE_RECEIVER");
+      return (DI_ERR_INVALID_ARG);
+    }
+  }
+  // outbox, flags, exchange buffers
+  {
+    const long long nb = (n_global + 31) >> 5;
+    if (cudaMalloc(&ctx->G, sizeof(double) * n_global) != cudaSuccess ||
+        cudaMalloc(&ctx->dflags, (size_t)nb) != cudaSuccess) {
+      diter_set_err(ctx, "cudaMalloc (outbox) failed");
+      return (DI_ERR_OOM);
+    }
+    // records to peer q: at most |Omega_q| (one per row); from peers: at most (K-1) |Omega_k|
+    ds->soff.assign(world, 0);
+    ds->scnt.assign(world, 0);
+    ds->roff.assign(world, 0);
+    ds->rcnt.assign(world, 0);
+    long long cap = 0;
+    for (int q = 0; q < world; ++q) {
+      ds->soff[q] = cap;
+      if (q != rank) cap += ds->bounds[q + 1] - ds->bounds[q];
+    }
+    ds->send_cap = std::max(1LL, cap);
+    ds->recv_cap = std::max(1LL, (long long)(world - 1) * nl);
+    if (cudaMalloc(&ds->send, sizeof(Rec) * ds->send_cap) != cudaSuccess ||
+        cudaMalloc(&ds->recv, sizeof(Rec) * ds->recv_cap) != cudaSuccess ||
+        cudaMalloc(&ds->d_bounds, sizeof(long long) * (world + 1)) != cudaSuccess ||
+        cudaMalloc(&ds->d_scnt, sizeof(long long) * world) != cudaSuccess ||
+        cudaMalloc(&ds->d_sums, sizeof(double) * (kSums + 2) + sizeof(long long) * world) != cudaSuccess) {
+      diter_set_err(ctx, "cudaMalloc (exchange buffers) failed");
+      return (DI_ERR_OOM);
+    }
+    cudaMemcpyAsync(ds->d_bounds, ds->bounds.data(), sizeof(long long) * (world + 1), cudaMemcpyHostToDevice, ctx->stream);
+    s = diter_dist_reset(ctx);
+    if (s != DI_OK) return (s);
+    if (ctx->opt.remote_push == DI_REMOTE_RECEIVER) {
+      s = setup_receiver(ctx);
+      if (s != DI_OK) return (s);
+    }
+  }
+  // The threshold schedule is global: T_0 = max over ranks |B_i| / alpha (done in
+  // setup through diter_dist_max); SYNC applies the HYBRID rule to the global |S_p|
+  // and N; ASYNC applies it per rank to |S_p^k| and |Omega_k| (SURVEY §8e).
+  if (ctx->opt.exchange_mode == DI_EXCHANGE_ASYNC) {
+    ctx->ctl_init.n_total = (double)nl;
+    cudaMemcpyAsync(ctx->ctl, &ctx->ctl_init, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+  }
+  return DI_OK;
+}
 
 extern "C" di_status di_create_dist(di_ctx **out, int32_t rank, int32_t world, const void *comm_id,
                                     const int64_t *bounds, int64_t n_global, const int64_t *col_ptr_local,
@@ -1077,92 +1430,8 @@ extern "C" di_status di_create_dist(di_ctx **out, int32_t rank, int32_t world, c
     return fail(DI_ERR_UNSUPPORTED);
 #endif
   }
-  di_status s = diter_setup(ctx, col_ptr_local, row_idx_local, values_local, b_local, opt);
+  di_status s = dist_build(ctx, col_ptr_local, row_idx_local, values_local, b_local, opt);
   if (s != DI_OK) return fail(s);
-  // local rows first in every column (nloc), in place via a scratch copy
-  {
-    const long long n = ctx->n_local, nnz = ctx->nnz_local;
-    int *ri2 = nullptr;
-    double *v2 = nullptr;
-    if (cudaMalloc(&ctx->nloc, sizeof(int) * std::max(1LL, n)) != cudaSuccess ||
-        cudaMalloc(&ri2, sizeof(int) * std::max(1LL, nnz)) != cudaSuccess ||
-        (ctx->vals && cudaMalloc(&v2, sizeof(double) * std::max(1LL, nnz)) != cudaSuccess)) {
-      if (ri2) cudaFree(ri2);
-      diter_set_err(ctx, "cudaMalloc (column partition) failed");
-      return fail(DI_ERR_OOM);
-    }
-    long long *d_b = nullptr;
-    if (cudaMalloc(&d_b, sizeof(long long) * (world + 1)) != cudaSuccess) {
-      cudaFree(ri2);
-      if (v2) cudaFree(v2);
-      diter_set_err(ctx, "cudaMalloc failed");
-      return fail(DI_ERR_OOM);
-    }
-    cudaMemcpyAsync(d_b, bounds, sizeof(long long) * (world + 1), cudaMemcpyHostToDevice, ctx->stream);
-    k_partition_columns<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->col_ptr, n, ctx->row_idx, ctx->vals, d_b,
-                                                                   world, rank, ri2, v2, ctx->nloc);
-    cudaMemcpyAsync(ctx->row_idx, ri2, sizeof(int) * nnz, cudaMemcpyDeviceToDevice, ctx->stream);
-    if (v2) cudaMemcpyAsync(ctx->vals, v2, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, ctx->stream);
-    const cudaError_t e = cudaStreamSynchronize(ctx->stream);
-    cudaFree(ri2);
-    cudaFree(d_b);
-    if (v2) cudaFree(v2);
-    if (e != cudaSuccess) { diter_set_err(ctx, "column partition failed: %s", cudaGetErrorString(e)); return fail(DI_ERR_CUDA); }
-    if (ctx->opt.remote_push == DI_REMOTE_INCREMENT || ctx->opt.remote_push == DI_REMOTE_RECEIVER) {
-      if (cudaMalloc(&ctx->H_old, sizeof(double) * std::max(1LL, n)) != cudaSuccess) {
-        diter_set_err(ctx, "cudaMalloc (H_old) failed");
-        return fail(DI_ERR_OOM);
-      }
-      cudaMemsetAsync(ctx->H_old, 0, sizeof(double) * std::max(1LL, n), ctx->stream);
-    } else if (ctx->opt.remote_push != DI_REMOTE_PER_DIFFUSION) {
-      diter_set_err(ctx, "remote_push must be DI_REMOTE_PER_DIFFUSION, DI_REMOTE_INCREMENT or DI_REMOTE_RECEIVER");
-      return fail(DI_ERR_INVALID_ARG);
-    }
-  }
-  // outbox, flags, exchange buffers
-  {
-    const long long nb = (n_global + 31) >> 5;
-    if (cudaMalloc(&ctx->G, sizeof(double) * n_global) != cudaSuccess ||
-        cudaMalloc(&ctx->dflags, (size_t)nb) != cudaSuccess) {
-      diter_set_err(ctx, "cudaMalloc (outbox) failed");
-      return fail(DI_ERR_OOM);
-    }
-    // records to peer q: at most |Omega_q| (one per row); from peers: at most (K-1) |Omega_k|
-    ds->soff.assign(world, 0);
-    ds->scnt.assign(world, 0);
-    ds->roff.assign(world, 0);
-    ds->rcnt.assign(world, 0);
-    long long cap = 0;
-    for (int q = 0; q < world; ++q) {
-      ds->soff[q] = cap;
-      if (q != rank) cap += bounds[q + 1] - bounds[q];
-    }
-    ds->send_cap = std::max(1LL, cap);
-    ds->recv_cap = std::max(1LL, (long long)(world - 1) * nl);
-    if (cudaMalloc(&ds->send, sizeof(Rec) * ds->send_cap) != cudaSuccess ||
-        cudaMalloc(&ds->recv, sizeof(Rec) * ds->recv_cap) != cudaSuccess ||
-        cudaMalloc(&ds->d_bounds, sizeof(long long) * (world + 1)) != cudaSuccess ||
-        cudaMalloc(&ds->d_scnt, sizeof(long long) * world) != cudaSuccess ||
-        cudaMalloc(&ds->d_sums, sizeof(double) * (kSums + 2) + sizeof(long long) * world) != cudaSuccess) {
-      diter_set_err(ctx, "cudaMalloc (exchange buffers) failed");
-      return fail(DI_ERR_OOM);
-    }
-    cudaMemcpyAsync(ds->d_bounds, bounds, sizeof(long long) * (world + 1), cudaMemcpyHostToDevice, ctx->stream);
-    s = diter_dist_reset(ctx);
-    if (s != DI_OK) return fail(s);
-    if (ctx->opt.remote_push == DI_REMOTE_RECEIVER) {
-      s = setup_receiver(ctx);
-      if (s != DI_OK) return fail(s);
-    }
-  }
-  // The threshold schedule is global: T_0 = max over ranks |B_i| / alpha (done in
-  // setup through diter_dist_max); SYNC applies the HYBRID rule to the global |S_p|
-  // and N; ASYNC applies it per rank to |S_p^k| and |Omega_k| (SURVEY §8e).
-  if (ctx->opt.exchange_mode == DI_EXCHANGE_ASYNC) {
-    ctx->ctl_init.n_total = (double)nl;
-    cudaMemcpyAsync(ctx->ctl, &ctx->ctl_init, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream);
-    cudaStreamSynchronize(ctx->stream);
-  }
   *out = ctx;
   return DI_OK;
 }

@@ -681,6 +681,7 @@ extern "C" di_status di_get_stats(const di_ctx *ctx, di_stats *s) {
   s->kt_passes = ctx->kt_passes;
   s->scatter_bytes = (ctx->vals ? 28LL : 20LL) * ctx->edges + 16LL * ctx->nodes;
   s->remote_pushes = ctx->remote_pushes;
+  s->rebalances = ctx->rebalances;
   return DI_OK;
 }
 

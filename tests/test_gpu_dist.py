@@ -174,6 +174,104 @@ def test_async_remote_increments_signed():
     assert np.abs(H - X).sum() <= 1e-8 * bn
 
 
+def _run_ranks_fn(K, key, fn):
+    """K loopback ranks, each running fn(rank, comm_id) in its own thread."""
+    cid = dist.loopback_comm_id(key)
+    out, err = [None] * K, [None] * K
+
+    def worker(r):
+        try:
+            out[r] = fn(r, cid)
+        except Exception as e:
+            err[r] = e
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(K)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for e in err:
+        if e is not None:
+            raise e
+    return out
+
+
+@pytest.mark.parametrize("remote", [0, 1, 2])
+def test_rebalance_moves_state_and_keeps_parity(remote):
+    """NEXT f4: di_rebalance ships columns, F, H (and B) of moved
+    nodes mid-solve; the run resumes on the new ranges and reaches the same X with a
+    closed ledger.  Random positive B exercises the B transfer (di_reset after it)."""
+    K = 3
+    p = gen.config("C2", 2, n=200_000)
+    rng = np.random.default_rng(2)
+    b = rng.random(p.n) + 0.5
+    b *= 0.15 / b.sum()
+    bn = 0.15
+    bounds = dist.partition_bounds(p.col_ptr, K)
+    nb = bounds.copy()
+    nb[1] = int(bounds[1] * 0.8)                   # rank 0 gives nodes to rank 1
+    nb[2] = int(bounds[2] + (p.n - bounds[2]) * 0.25)   # rank 1 takes nodes from rank 2
+
+    def fn(r, cid):
+        lcp, lri, lv, lb = dist.shard_csc(p.col_ptr, p.row_idx, None, b, bounds, r)
+        o = di.default_options(exchange_mode=di.DI_EXCHANGE_ASYNC, check_interval=4, remote_push=remote)
+        ctx = di.di_create_dist(r, K, cid, bounds, p.n, lcp, lri, lv, lb, p.d, o)
+        di.di_run(ctx, 1e-4)
+        h0 = di.di_get_history(ctx).sum()
+        di.di_rebalance(ctx, nb)
+        got = di.di_get_bounds(ctx)
+        res = (list(got), ctx.n_local, h0)
+        di.di_run(ctx, p.parity_stop)
+        H, F, st = di.di_get_history(ctx), di.di_get_fluid(ctx), di.di_get_stats(ctx)
+        di.di_reset(ctx)                           # F = B over the new range
+        Fr = di.di_get_fluid(ctx)
+        di.di_destroy(ctx)
+        return res, H, F, st, Fr
+    outs = _run_ranks_fn(K, f"rebal{remote}", fn)
+    for r, o in enumerate(outs):
+        assert o[0][0] == list(nb) and o[0][1] == nb[r + 1] - nb[r]
+        assert o[3]["rebalances"] == 1
+    H = np.concatenate([o[1] for o in outs])
+    F = np.concatenate([o[2] for o in outs])
+    X = oracle.Problem(p.n, p.col_ptr, p.row_idx, None, b).solve(1e-12 * bn * 0.15).H
+    assert np.abs(H - X).sum() <= 1e-8 * bn
+    deg = np.diff(p.col_ptr)
+    ledger = np.abs(F).sum() + 0.15 * H.sum() + 0.85 * H[deg == 0].sum()
+    assert abs(ledger - bn) <= 1e-12 * bn
+    np.testing.assert_array_equal(np.concatenate([o[4] for o in outs]), b)
+
+
+def test_adaptation_moves_boundaries_on_skewed_partition():
+    """options.adapt_rounds: on the out-edge-balanced partition of a Zipf-over-id
+    graph rank 0 holds most of the residual and work, so the rule moves omega_1
+    down; the solve stays exact."""
+    K = 2
+    p = gen.config("C2", 1, n=300_000)
+    bn = 0.15
+    bounds = dist.partition_bounds(p.col_ptr, K, cost="out")
+
+    def fn(r, cid):
+        lcp, lri, lv, lb = dist.shard_csc(p.col_ptr, p.row_idx, None, None, bounds, r)
+        o = di.default_options(exchange_mode=di.DI_EXCHANGE_ASYNC, check_interval=4, adapt_rounds=1,
+                               remote_push=di.DI_REMOTE_INCREMENT)
+        ctx = di.di_create_dist(r, K, cid, bounds, p.n, lcp, lri, lv, lb, p.d, o)
+        di.di_run(ctx, p.parity_stop)
+        out = (di.di_get_bounds(ctx), ctx.n_local, di.di_get_history(ctx), di.di_get_fluid(ctx), di.di_get_stats(ctx))
+        di.di_destroy(ctx)
+        return out
+    outs = _run_ranks_fn(K, "adapt", fn)
+    nb = outs[0][0]
+    assert list(nb) == list(outs[1][0])
+    assert outs[0][4]["rebalances"] > 0 and nb[1] < bounds[1]
+    H = np.concatenate([o[2] for o in outs])
+    F = np.concatenate([o[3] for o in outs])
+    assert len(H) == p.n
+    X = oracle.Problem(p.n, p.col_ptr, p.row_idx).solve(1e-12 * bn * 0.15).H
+    assert np.abs(H - X).sum() <= 1e-8 * bn
+    deg = np.diff(p.col_ptr)
+    ledger = np.abs(F).sum() + 0.15 * H.sum() + 0.85 * H[deg == 0].sum()
+    assert abs(ledger - bn) <= 1e-12 * bn
+
+
 def test_paper_key_rejected_on_distributed():
     """DI_KEY_PAPER needs global in-degrees, which a rank does not hold."""
     n = 1000
