@@ -122,7 +122,10 @@ def load_library() -> ctypes.CDLL:
         "di_csc_from_coo": (st, [i64, i64, vp, vp, vp, vp, ctypes.POINTER(i64)]),
         "di_partition_cb": (st, [i64, vp, i32, vp]),
     }
+    partial = bool(os.environ.get("DITER_LIB_PARTIAL"))   # experiments: an older build of the library
     for name, (res, args) in sig.items():
+        if partial and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

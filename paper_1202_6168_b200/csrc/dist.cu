@@ -846,10 +846,10 @@ static void launch_pass_kernels(di_ctx *ctx) {
   k_select<<<ctx->grid_select, kSelectThreads, 0, ctx->stream>>>(ctx->F, ctx->H, ctx->fr, ctx->n_local, ctx->ctl,
                                                                 ctx->sel_part, ctx->kw);
   if (ctx->vals)
-    k_scatter<true><<<ctx->grid_scatter, kScatterThreads, ctx->scatter_smem, ctx->stream>>>(
+    k_scatter<true, true><<<ctx->grid_scatter, kScatterThreads, ctx->scatter_smem, ctx->stream>>>(
         g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part);
   else
-    k_scatter<false><<<ctx->grid_scatter, kScatterThreads, ctx->scatter_smem, ctx->stream>>>(
+    k_scatter<false, true><<<ctx->grid_scatter, kScatterThreads, ctx->scatter_smem, ctx->stream>>>(
         g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part);
   if (ctx->cap_hub > 0) {
     if (ctx->vals)

@@ -10,6 +10,9 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -326,6 +329,20 @@ static di_status capture_graph(di_ctx *ctx) {
   return DI_OK;
 }
 
+// DITER_TRACE=1: stream-synchronised phase times of the setup on stderr.
+struct SetupTrace {
+  bool on = std::getenv("DITER_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(cudaStream_t s, const char *what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[diter setup] %-22s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+
 // Shared by di_create and di_create_dist: upload, validate, allocate, init.
 di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_idx,
                       const double *values, const double *b, const di_options *opt) {
@@ -344,15 +361,18 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
   } else {
     CK(cudaGetDevice(&ctx->device));
   }
+  SetupTrace tr;
   CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
   CK(cudaEventCreate(&ctx->ev0));
   CK(cudaEventCreate(&ctx->ev1));
+  tr.mark(ctx->stream, "stream/events");
   const long long n = ctx->n_local, nnz = ctx->nnz_local;
   TRY(dalloc(ctx, &ctx->col_ptr, (size_t)n + 1));
   TRY(dalloc(ctx, &ctx->row_idx, (size_t)nnz));
   if (values) TRY(dalloc(ctx, &ctx->vals, (size_t)nnz));
   TRY(dalloc(ctx, &ctx->F, (size_t)n));
   TRY(dalloc(ctx, &ctx->H, (size_t)n));
+  tr.mark(ctx->stream, "malloc graph+F+H");
   CK(cudaMemcpyAsync(ctx->col_ptr, col_ptr, sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, ctx->stream));
   if (nnz)
     CK(cudaMemcpyAsync(ctx->row_idx, row_idx, sizeof(int) * nnz, cudaMemcpyHostToDevice, ctx->stream));
@@ -362,6 +382,7 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
     TRY(dalloc(ctx, &ctx->d_b, (size_t)n));
     CK(cudaMemcpyAsync(ctx->d_b, b, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
   }
+  tr.mark(ctx->stream, "H2D graph (+B)");
   TRY(setup_geometry(ctx));
   // validation + bin census on the device
   Census *d_c = nullptr;
@@ -386,9 +407,12 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
     diter_set_err(ctx, "%llu columns have sum |p_ij| > d = %g (not contractive)", hc.bad_contraction, ctx->d);
     return DI_ERR_CONTRACTION;
   }
+  tr.mark(ctx->stream, "census/validate");
   TRY(choose_hot_window(ctx));
+  tr.mark(ctx->stream, "hot window");
   TRY(setup_far(ctx));
   TRY(setup_key(ctx));
+  tr.mark(ctx->stream, "far bins + key weights");
   ctx->cap_low = hc.n_low;
   ctx->cap_mid = hc.n_mid;
   ctx->cap_hub = hc.n_hub;
@@ -408,6 +432,7 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
   TRY(dalloc(ctx, &ctx->ctl, 1));
   ctx->log_cap = 1 << 18;  // passes logged since create/reset (di_run is resumable)
   TRY(dalloc(ctx, &ctx->log, (size_t)ctx->log_cap));
+  tr.mark(ctx->stream, "malloc frontier etc");
   CK(cudaHostAlloc((void **)&ctx->h_ctl, sizeof(Ctl), cudaHostAllocDefault));
   // state: F = B, H = 0
   ctx->b_uniform = (1.0 - ctx->d) / (double)ctx->n_rows;
@@ -441,7 +466,9 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
   CK(cudaMemcpyAsync(ctx->ctl, &ctx->ctl_init, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->threshold = T0;
+  tr.mark(ctx->stream, "init F,H,T0");
   TRY(capture_graph(ctx));
+  tr.mark(ctx->stream, "graph capture");
   return DI_OK;
 }
 

@@ -367,7 +367,7 @@ __device__ __forceinline__ int find_segment(const int *s_goff, int n_seg, int q)
   return lo;
 }
 
-template <bool SIGNED>
+template <bool SIGNED, bool DIST>
 __device__ __forceinline__ void scatter_group(const Graph &g, const Sink &s, const Frontier &fr, Ctl *ctl,
                                               const int *s_goff, int *st, int q, int &seg, ScAcc &acc) {
   // a warp's groups mostly ascend within one segment: walk forward from the
@@ -387,14 +387,6 @@ __device__ __forceinline__ void scatter_group(const Graph &g, const Sink &s, con
   if (k < cnt) {
     b0 = __ldg(g.col_ptr + i);
     const long long deg = __ldg(g.col_ptr + i + 1) - b0;
-    // edges this scatter pushes: all, or (DI_REMOTE_INCREMENT) the local ones, which
-    // a distributed context stores first in each column
-    long long dpush = deg;
-    if (g.nloc) {
-      const long long nl = __ldg(g.nloc + i);
-      if (g.local_only) dpush = nl;
-      else acc.remote += deg - nl;
-    }
     const double asv = fabs(sv);
     acc.loss += (deg > 0) ? (1.0 - g.d) * asv : asv;
     acc.edges += deg;
@@ -402,12 +394,19 @@ __device__ __forceinline__ void scatter_group(const Graph &g, const Sink &s, con
       acc.dang += 1;
     } else {
       w = SIGNED ? sv : sv * (g.d / (double)deg);
-      if (deg <= kLowMax) acc.lo += 1;
-      else if (deg <= kMidMax) acc.mi += 1;
+      // edges this scatter pushes: all, or on a distributed context with
+      // DI_REMOTE_INCREMENT / _RECEIVER the local ones, stored first in each column
+      long long dpush = deg;
+      if (DIST) {
+        const long long nl = __ldg(g.nloc + i);
+        if (g.local_only) dpush = nl;
+        else acc.remote += deg - nl;
+      }
+      if (deg <= kLowMax) { acc.lo += 1; if (!DIST) deg_eff = (int)deg; }
+      else if (deg <= kMidMax) { acc.mi += 1; if (!DIST) deg_eff = (int)deg; }
       else acc.hu += 1;
-      if (dpush <= kMidMax) {
-        deg_eff = (int)dpush;
-      } else {
+      if (DIST && dpush <= kMidMax) deg_eff = (int)dpush;
+      if (dpush > kMidMax) {
         // one 64-bit atomic hands out the slot AND the first chunk id, so
         // hub_chunk[] is sorted by slot and k_scatter_hubs can binary-search it
         const unsigned long long nch = (unsigned long long)((dpush + kHubChunk - 1) / kHubChunk);
@@ -425,7 +424,7 @@ __device__ __forceinline__ void scatter_group(const Graph &g, const Sink &s, con
   push_group<SIGNED>(g, s, ctl, st, b0, deg_eff, w, i_first - kNear, i_last + kNear);
 }
 
-template <bool SIGNED>
+template <bool SIGNED, bool DIST>
 __device__ __forceinline__ void scatter_body(const Graph &g, double *__restrict__ F, const Frontier &fr, Ctl *ctl,
                                              ScPartial *__restrict__ part, double *s_hot, int *s_goff) {
   for (int t = threadIdx.x; t < kHot; t += blockDim.x) s_hot[t] = 0.0;
@@ -460,7 +459,7 @@ __device__ __forceinline__ void scatter_body(const Graph &g, double *__restrict_
       q0 = __shfl_sync(0xffffffffu, q0, 0);
       if ((long long)q0 >= (long long)(s1 - s0)) break;
       const int q1 = min(s1, s0 + (int)q0 + run);
-      for (int q = s0 + (int)q0; q < q1; ++q) scatter_group<SIGNED>(g, s, fr, ctl, s_goff, st, q, seg, acc);
+      for (int q = s0 + (int)q0; q < q1; ++q) scatter_group<SIGNED, DIST>(g, s, fr, ctl, s_goff, st, q, seg, acc);
     }
   }
   if (g.far.on) close_far(g.far, st);
@@ -477,7 +476,7 @@ __device__ __forceinline__ void scatter_body(const Graph &g, double *__restrict_
   acc.lo = warp_sum(acc.lo);
   acc.mi = warp_sum(acc.mi);
   acc.hu = warp_sum(acc.hu);
-  acc.remote = warp_sum(acc.remote);
+  if (DIST) acc.remote = warp_sum(acc.remote);
   __shared__ ScAcc s_acc[kScatterThreads / 32];
   if (lane == 0) s_acc[threadIdx.x >> 5] = acc;
   __syncthreads();
@@ -489,19 +488,19 @@ __device__ __forceinline__ void scatter_body(const Graph &g, double *__restrict_
       p.n_low += s_acc[k].lo; p.n_mid += s_acc[k].mi; p.n_hub += s_acc[k].hu;
       remote += s_acc[k].remote;
     }
-    if (remote) atomicAdd(&ctl->remote_pushes, (unsigned long long)remote);
+    if (DIST && remote) atomicAdd(&ctl->remote_pushes, (unsigned long long)remote);
     part[blockIdx.x] = p;
   }
 }
 
 // dynamic shared memory: the group prefix s_goff[n_seg + 1]
-template <bool SIGNED>
+template <bool SIGNED, bool DIST = false>
 __global__ void __launch_bounds__(kScatterThreads, kScatterMinBlocks)
 k_scatter(Graph g, double *__restrict__ F, Frontier fr, Ctl *ctl, ScPartial *__restrict__ part) {
   if (ctl->done) return;
   __shared__ double s_hot[kHot];
   extern __shared__ int s_goff[];
-  scatter_body<SIGNED>(g, F, fr, ctl, part, s_hot, s_goff);
+  scatter_body<SIGNED, DIST>(g, F, fr, ctl, part, s_hot, s_goff);
 }
 
 // Hub columns (> kMidMax edges), one CTA per 2048-edge chunk (chunks of a hub
@@ -686,7 +685,7 @@ k_pass_fused(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier f
     select_body(F, H, fr, g.n, *(volatile double *)&ctl->T, sp, kw);
     grid.sync();
     if (blockIdx.x == 0 && threadIdx.x == 0) t1 = globaltimer_ns();
-    scatter_body<SIGNED>(g, F, fr, ctl, cp, s_hot, s_goff);
+    scatter_body<SIGNED, false>(g, F, fr, ctl, cp, s_hot, s_goff);
     grid.sync();
     if (has_hubs) {
       hubs_body<SIGNED>(g, F, fr, ctl);
