@@ -119,6 +119,28 @@ def load_problem(args):
     return p
 
 
+def graph_residency(p):
+    """(bytes resident per GPU at N = 1, whether bench flushes L2 between steps)."""
+    graph_bytes = 8 * (p.n + 1) + 4 * p.nnz + (8 * p.nnz if p.values is not None else 0)
+    resident = graph_bytes + 16 * p.n
+    return resident, resident < 4 * L2_BYTES
+
+
+def bench_config(args, p, pol, world, resident, flushed):
+    """The workload description both arms print (the reference arm times the oracle on
+    this same configuration)."""
+    par = "dp1" if world == 1 else (f"node-partition x{world} ({args.partition}-balanced ranges, {args.exchange} exchange, "
+                                    f"rounds every {args.round_passes} passes, remote edges "
+                                    f"{'as H increments' if args.remote_push else 'per diffusion'})")
+    return {"workload": WORKLOADS[args.config], "n": p.n, "nnz": p.nnz,
+            "stop": p.stop, "policy": "geom" if pol == 0 else "hybrid", "seed": args.seed,
+            "alpha": args.alpha, "hybrid_frac": args.hybrid_frac,
+            "select_key": ["raw", "per-edge", "paper"][args.key],
+            "parallelism": par,
+            "l2": ("flushed between steps (252 MB write)" if flushed else
+                   f"inputs ({resident / 1e9:.1f} GB resident per GPU) larger than L2 (126 MB)")}
+
+
 def policy_of(args):
     """Fill args.alpha / hybrid_frac / key from SCHEDULES where not given; return the policy."""
     pol, alpha, frac, key = SCHEDULES[args.config]
@@ -269,9 +291,7 @@ def run_reference(args, rank, world):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3 / args.steps,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic",
-           "config": {"workload": WORKLOADS[args.config], "n": p.n, "nnz": p.nnz,
-                      "alpha": args.alpha, "hybrid_frac": args.hybrid_frac,
-                      "select_key": ["raw", "per-edge", "paper"][args.key]},
+           "config": bench_config(args, p, policy_of(args), 1, *graph_residency(p)),
            "cpu_baseline": {"value": v, "unit": "edges/s", "cores": 1, "kind": "oracle",
                             "sample": sample},
            "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -397,20 +417,11 @@ def run_ours(args, rank, world, local_rank):
                          f"on the full graph, {dt:.1f}s on 1 host core"}
     clocks = clk.summary()
     di.di_destroy(ctx)
-    par = "dp1" if world == 1 else (f"node-partition x{world} ({args.partition}-balanced ranges, {args.exchange} exchange, "
-                                    f"rounds every {args.round_passes} passes, remote edges "
-                                    f"{'as H increments' if args.remote_push else 'per diffusion'})")
     out = {"metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot["run_ms"] / args.steps,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic",
-           "config": {"workload": WORKLOADS[args.config], "n": p.n, "nnz": p.nnz,
-                      "stop": p.stop, "policy": "geom" if pol == 0 else "hybrid", "seed": args.seed,
-                      "alpha": args.alpha, "hybrid_frac": args.hybrid_frac,
-                      "select_key": ["raw", "per-edge", "paper"][args.key],
-                      "parallelism": par,
-                      "l2": ("flushed between steps (252 MB write)" if flush is not None else
-                             f"inputs ({resident / 1e9:.1f} GB resident per GPU) larger than L2 (126 MB)")},
+           "config": bench_config(args, p, pol, world, resident, flush is not None),
            "time_to_target_ms": tot["run_ms"] / args.steps,
            "passes_per_solve": tot["passes"] / args.steps,
            "normalized_iterations": edges_all / args.steps / p.nnz,
