@@ -451,7 +451,13 @@ def run_e2e(args, p, opts, di, torch, rank=0, world=1, comm_id=None, bounds=None
     o2.profile = 0
 
     def one():
-        ctx = make_ctx(args, p, o2, di, rank, world, comm_id, bounds, pin)
+        # an ncclUniqueId initialises one communicator only: every distributed
+        # context gets a fresh one (collective over the torch process group)
+        cid = comm_id
+        if world > 1:
+            from paper_1202_6168_b200 import dist as dd
+            cid = dd.nccl_comm_id()
+        ctx = make_ctx(args, p, o2, di, rank, world, cid, bounds, pin)
         di.di_run(ctx, p.stop)
         di.di_get_history(ctx, H)
         e = di.di_get_stats(ctx)["edges"]
