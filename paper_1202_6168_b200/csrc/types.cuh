@@ -10,7 +10,10 @@ constexpr int kLowMax = 32;      // 1..32     : "low"  (statistics only; same wa
 constexpr int kMidMax = 8192;    // 33..8192  : "mid"  -- both: 32 selected nodes per warp,
                                  //             lanes over the group's concatenated edges
 constexpr int kHubChunk = 2048;  // > 8192    : "hub"  -- one CTA per 2048-edge chunk
-constexpr int kHot = 2048;       // rows staged in shared memory by each scatter CTA
+#ifndef DITER_HOT_ROWS
+#define DITER_HOT_ROWS 2048
+#endif
+constexpr int kHot = DITER_HOT_ROWS;        // rows staged in shared memory by each scatter CTA
 
 constexpr int kSelectThreads = 256;
 constexpr int kSelectItems = 16;                     // 32-node words per warp iteration
