@@ -91,7 +91,7 @@ static void free_ctx(di_ctx *c) {
   if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
   for (cudaEvent_t e : c->prof_ev)
     if (e) cudaEventDestroy(e);
-  void *ptrs[] = {c->col_ptr, c->row_idx, c->vals, c->d_b, c->F, c->H, c->fr.ids, c->fr.S, c->fr.seg_cnt,
+  void *ptrs[] = {c->col_ptr, c->row_idx, c->vals, c->d_b, c->F, c->H, c->fr.ids, c->fr.S, c->fr.seg_cnt, const_cast<unsigned *>(c->fr.dang_bits),
                   c->fr.hub_w, c->fr.hub_b0, c->fr.hub_deg, c->fr.hub_chunk, c->sel_part, c->sc_part,
                   c->l1_part, c->l1_out, c->ctl, c->log, c->far_off, c->far.rows, c->far.vals, c->far.fill, c->kw, c->nloc, c->H_old};
   for (void *p : ptrs)
@@ -420,6 +420,13 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
   TRY(dalloc(ctx, &ctx->fr.ids, fr_cap));
   TRY(dalloc(ctx, &ctx->fr.S, fr_cap));
   TRY(dalloc(ctx, &ctx->fr.seg_cnt, (size_t)ctx->fr.n_seg));
+  {
+    unsigned *db = nullptr;
+    TRY(dalloc(ctx, &db, (size_t)((n + 31) >> 5) + kSelectItems));   // + a pad word per item of the last span
+    CK(cudaMemsetAsync(db, 0, sizeof(unsigned) * (((n + 31) >> 5) + kSelectItems), ctx->stream));
+    k_dangling_bits<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->col_ptr, n, db);
+    ctx->fr.dang_bits = db;
+  }
   TRY(dalloc(ctx, &ctx->fr.hub_w, hc.n_hub));
   TRY(dalloc(ctx, &ctx->fr.hub_b0, hc.n_hub));
   TRY(dalloc(ctx, &ctx->fr.hub_deg, hc.n_hub));

@@ -45,10 +45,13 @@ __device__ __forceinline__ void reset_tickets(Ctl *ctl) {
 // rank given by the ballot popcounts -- consecutive, coalesced writes instead of
 // scattered 8-byte stores, and the scatter never scans empty ranges.  Per-CTA
 // partials (r_p, |S_p|) in a fixed order make r_p deterministic for given F bytes.
+// A selected dangling node (no out-edge, bit in fr.dang_bits) is taken here and
+// its fluid counted as leaving (App. A.2: c_i = 0); it never enters the frontier
+// list, so the scatter does no work for it.
 template <bool KEY>
 __device__ __forceinline__ void select_loop(double *__restrict__ F, double *__restrict__ H, const Frontier &fr,
                                             long long beg, long long end, const double T, const float *__restrict__ kw,
-                                            double &r, int &cnt) {
+                                            double &r, int &cnt, int &sel_all, double &dloss) {
   const unsigned lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
   int *__restrict__ ids = fr.ids + beg;
@@ -62,6 +65,9 @@ __device__ __forceinline__ void select_loop(double *__restrict__ F, double *__re
       f[k] = (i < end) ? F[i] : 0.0;
       if (KEY) w[k] = (i < end) ? __ldcs(kw + i) : 0.0f;
     }
+    // lane k < 16 holds the dangling word of item k (32 nodes, base is 512-aligned)
+    const long long wi = (base >> 5) + lane;
+    const unsigned dword = ((int)lane < kSelectItems && (wi << 5) < end) ? __ldg(fr.dang_bits + wi) : 0u;
 #pragma unroll
     for (int k = 0; k < kSelectItems; ++k) {
       const long long i = base + 32 * k + lane;
@@ -69,15 +75,21 @@ __device__ __forceinline__ void select_loop(double *__restrict__ F, double *__re
       r += af;
       // key_i = |F_i| w_i (reading R20); f = 0 beyond `end`, never selected
       const bool sel = (KEY ? af * (double)w[k] : af) > T;
-      const unsigned m = __ballot_sync(0xffffffffu, sel);
+      const bool dang = (__shfl_sync(0xffffffffu, dword, k) >> lane) & 1u;
+      const unsigned m = __ballot_sync(0xffffffffu, sel && !dang);
       if (sel) {
-        const int pos = cnt + __popc(m & lt);
         F[i] = 0.0;            // F_i := 0
         red_add(H + i, f[k]);  // H_i += sent
-        ids[pos] = (int)(i);        // node and sent value, for the scatter
-        sv[pos] = f[k];
+        if (dang) {
+          dloss += af;
+        } else {
+          const int pos = cnt + __popc(m & lt);
+          ids[pos] = (int)(i);        // node and sent value, for the scatter
+          sv[pos] = f[k];
+        }
       }
       cnt += __popc(m);
+      sel_all += __popc(__ballot_sync(0xffffffffu, sel));
     }
   }
 }
@@ -89,19 +101,25 @@ __device__ __forceinline__ void select_body(double *__restrict__ F, double *__re
   const int gw = blockIdx.x * (kSelectThreads / 32) + (threadIdx.x >> 5);
   const long long beg = (long long)gw * fr.seg_len;
   const long long end = min(n, beg + fr.seg_len);
-  double r = 0.0;
-  int cnt = 0;                                   // warp-uniform running count
-  if (kw) select_loop<true>(F, H, fr, beg, end, T, kw, r, cnt);
-  else select_loop<false>(F, H, fr, beg, end, T, kw, r, cnt);
+  double r = 0.0, dloss = 0.0;
+  int cnt = 0, sel_all = 0;                      // warp-uniform running counts
+  if (kw) select_loop<true>(F, H, fr, beg, end, T, kw, r, cnt, sel_all, dloss);
+  else select_loop<false>(F, H, fr, beg, end, T, kw, r, cnt, sel_all, dloss);
   if (gw < fr.n_seg && lane == 0) fr.seg_cnt[gw] = cnt;
   r = warp_sum(r);
-  __shared__ double s_r[kSelectThreads / 32];
-  __shared__ int s_c[kSelectThreads / 32];
-  if (lane == 0) { s_r[threadIdx.x >> 5] = r; s_c[threadIdx.x >> 5] = cnt; }
+  dloss = warp_sum(dloss);
+  __shared__ double s_r[kSelectThreads / 32], s_l[kSelectThreads / 32];
+  __shared__ int s_c[kSelectThreads / 32], s_d[kSelectThreads / 32];
+  if (lane == 0) {
+    s_r[threadIdx.x >> 5] = r; s_l[threadIdx.x >> 5] = dloss;
+    s_c[threadIdx.x >> 5] = sel_all; s_d[threadIdx.x >> 5] = sel_all - cnt;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    SelPartial p{0.0, 0};
-    for (int k = 0; k < kSelectThreads / 32; ++k) { p.r += s_r[k]; p.cnt += s_c[k]; }
+    SelPartial p{0.0, 0, 0.0, 0};
+    for (int k = 0; k < kSelectThreads / 32; ++k) {
+      p.r += s_r[k]; p.cnt += s_c[k]; p.loss += s_l[k]; p.dang += s_d[k];
+    }
     part[blockIdx.x] = p;
   }
 }
@@ -582,7 +600,9 @@ constexpr int kSums = 8;
 __device__ __forceinline__ void reduce_partials(const SelPartial *__restrict__ sp, int n_sp,
                                                 const ScPartial *__restrict__ cp, int n_cp, double *out) {
   double v[kSums] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int k = threadIdx.x; k < n_sp; k += blockDim.x) { v[0] += sp[k].r; v[2] += (double)sp[k].cnt; }
+  for (int k = threadIdx.x; k < n_sp; k += blockDim.x) {
+    v[0] += sp[k].r; v[2] += (double)sp[k].cnt; v[1] += sp[k].loss; v[4] += (double)sp[k].dang;
+  }
   for (int k = threadIdx.x; k < n_cp; k += blockDim.x) {
     const ScPartial p = cp[k];
     v[1] += p.loss; v[3] += (double)p.edges; v[4] += p.dang; v[5] += p.n_low; v[6] += p.n_mid; v[7] += p.n_hub;
@@ -852,6 +872,20 @@ __global__ void k_key_weights(const long long *col_ptr, long long n, const unsig
     if (key == DI_KEY_EDGE) x = 1.0 / (out + 1.0);
     else if (key == DI_KEY_PAPER) x = 1.0 / (((double)indeg[i] + 1.0) * (out + 1.0));
     w[i] = __double2float_rn(x);
+  }
+}
+
+// Dangling bitmap (setup): bit i%32 of word i/32 set when column i has no out-edge.
+__global__ void k_dangling_bits(const long long *col_ptr, long long n, unsigned *bits) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long nw = (n + 31) >> 5;
+  for (long long wdx = (long long)blockIdx.x * blockDim.x + threadIdx.x; wdx < nw; wdx += stride) {
+    unsigned w = 0u;
+    for (int b = 0; b < 32; ++b) {
+      const long long i = (wdx << 5) + b;
+      if (i < n && col_ptr[i + 1] == col_ptr[i]) w |= 1u << b;
+    }
+    bits[wdx] = w;
   }
 }
 

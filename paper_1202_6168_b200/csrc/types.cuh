@@ -63,7 +63,9 @@ struct Ctl {
 // k_select partials (one per CTA): r_p and |S_p|.
 struct SelPartial {
   double r;
-  long long cnt;
+  long long cnt;      // |S_p|, dangling nodes included
+  double loss;        // sum |s_i| over the dangling nodes taken (their fluid leaves, App. A.2)
+  long long dang;     // dangling nodes taken (they never reach the scatter)
 };
 
 // k_scatter partials (one per CTA): guaranteed |F|_1 drop and frontier census.
@@ -118,7 +120,8 @@ struct Graph {
 struct Frontier {
   int *ids;              // [n_seg * seg_len] local node ids
   double *S;             // [n_seg * seg_len] taken values s_i
-  int *seg_cnt;          // [n_seg] selected nodes per segment
+  int *seg_cnt;          // [n_seg] selected nodes per segment (dangling ones excluded)
+  const unsigned *dang_bits;   // [ceil(n/32)] bit i%32 of word i/32: column i has no out-edge
   long long seg_len;     // nodes per segment, a multiple of kSelectSpan
   int n_seg;             // select grid x warps per CTA (<= kMaxSegments)
   int run;               // groups per dynamic grab of the scatter
