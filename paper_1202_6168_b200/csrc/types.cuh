@@ -16,7 +16,13 @@ constexpr int kHubChunk = 2048;  // > 8192    : "hub"  -- one CTA per 2048-edge 
 constexpr int kHot = DITER_HOT_ROWS;        // rows staged in shared memory by each scatter CTA
 
 constexpr int kSelectThreads = 256;
-constexpr int kSelectItems = 16;                     // 32-node words per warp iteration
+#ifndef DITER_SELECT_ITEMS
+#define DITER_SELECT_ITEMS 16
+#endif
+#ifndef DITER_SELECT_CTAS
+#define DITER_SELECT_CTAS 2
+#endif
+constexpr int kSelectItems = DITER_SELECT_ITEMS;     // 32-node words per warp iteration
 constexpr int kSelectSpan = 32 * kSelectItems;       // nodes per warp iteration (segment granule)
 constexpr int kScatterThreads = 256;
 #ifndef DITER_SCATTER_MIN_BLOCKS
@@ -24,8 +30,8 @@ constexpr int kScatterThreads = 256;
 #endif
 constexpr int kScatterMinBlocks = DITER_SCATTER_MIN_BLOCKS;   // __launch_bounds__ min CTAs/SM of k_scatter
 constexpr int kFinalizeThreads = 512;
-constexpr int kSelectCtasPerSm = 2;                  // 16 select warps/SM x 16 x 256 B loads in flight
-constexpr int kMaxSegments = 4096;                   // select warps (= frontier segments) per launch
+constexpr int kSelectCtasPerSm = DITER_SELECT_CTAS;  // 16 select warps/SM x 16 x 256 B loads in flight
+constexpr int kMaxSegments = 8192;                   // select warps (= frontier segments) per launch
 constexpr int kStripes = 32;                         // max scatter ticket counters (contiguous group stripes)
 constexpr int kMaxBins = 64;                         // far-push destination bins (propagation blocking)
 constexpr int kNear = 2048;                          // pushes within +-kNear rows of the group are "near"
