@@ -291,3 +291,33 @@ def test_async_signed():
     H, F, outs = run_ranks(2, n, cp, ri, v, b, 0.9, 5e-10 * bn, bounds, di.DI_EXCHANGE_ASYNC, "signed")
     X, _ = oracle.Problem(n, cp, ri, v, b, 0.9).jacobi(1e-13 * bn)
     assert np.abs(H - X).sum() <= 1e-8 * bn
+
+
+def test_rebalance_rejects_bad_bounds_and_keeps_state():
+    """Invalid new bounds are rejected on every rank before any collective step; the
+    contexts stay usable and still reach parity."""
+    K = 2
+    p = gen.config("C2", 3, n=100_000)
+    bounds = dist.partition_bounds(p.col_ptr, K)
+
+    def fn(r, cid):
+        lcp, lri, lv, lb = dist.shard_csc(p.col_ptr, p.row_idx, None, None, bounds, r)
+        ctx = di.di_create_dist(r, K, cid, bounds, p.n, lcp, lri, lv, lb, p.d,
+                                di.default_options(exchange_mode=di.DI_EXCHANGE_ASYNC))
+        bad = []
+        for nb in ([0, bounds[1], p.n - 1], [0, 0, p.n], [0, p.n, p.n]):
+            try:
+                di.di_rebalance(ctx, nb)
+            except di.DiError as e:
+                bad.append(e.status)
+        di.di_run(ctx, p.parity_stop)
+        out = (bad, di.di_get_history(ctx), di.di_get_bounds(ctx))
+        di.di_destroy(ctx)
+        return out
+    outs = _run_ranks_fn(K, "badbounds", fn)
+    for o in outs:
+        assert o[0] == [di.DI_ERR_INVALID_ARG] * 3
+        np.testing.assert_array_equal(o[2], bounds)
+    H = np.concatenate([o[1] for o in outs])
+    X = oracle.Problem(p.n, p.col_ptr, p.row_idx).solve(1e-12 * 0.15 * 0.15).H
+    assert np.abs(H - X).sum() <= 1e-8 * 0.15

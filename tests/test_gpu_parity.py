@@ -370,3 +370,31 @@ def test_completed_pagerank_output(seed):
     assert abs(x.sum() - 1.0) <= 1e-12
     assert np.abs(x - Xc).sum() <= 1e-11
     np.testing.assert_array_equal(d.cpu().numpy(), x)
+
+
+@pytest.mark.parametrize("opts", [{"far_push": 1, "far_warm_log2": 12}, {"pass_kernel": 2},
+                                  {"select_key": di.DI_KEY_EDGE}])
+def test_signed_variants(opts):
+    """configs[4] shape (signed P) through the far-push bins, the fused persistent
+    kernel and the per-edge key: parity with the Jacobi fixed point and the exact
+    identity F = B - (I-P)H."""
+    n = 200_000
+    cp, ri, v, b = gen.signed_system(n, 2)
+    bn = np.abs(b).sum()
+    X, _ = oracle.Problem(n, cp, ri, v, b, 0.9).jacobi(1e-13 * bn)
+    H, F, log, r, stats = _gpu(n, cp, ri, 5e-10 * bn, v, b, 0.9, **opts)
+    assert np.abs(H - X).sum() <= TOL * bn
+    _check_state(n, cp, ri, v, b, 0.9, H, F, r, 5e-10 * bn)
+
+
+def test_bounds_and_rebalance_on_one_gpu():
+    """A single-GPU context owns [0, n); di_rebalance needs a distributed context."""
+    cp, ri = gen.uniform_graph(1000, 3)
+    ctx = di.di_create(1000, cp, ri)
+    np.testing.assert_array_equal(di.di_get_bounds(ctx), [0, 1000])
+    with pytest.raises(di.DiError) as e:
+        di.di_rebalance(ctx, [0, 500, 1000])
+    assert e.value.status == di.DI_ERR_INVALID_ARG
+    di.di_run(ctx, 1e-12)                     # the context is still usable
+    assert di.di_get_residual(ctx) < 1e-12
+    di.di_destroy(ctx)
