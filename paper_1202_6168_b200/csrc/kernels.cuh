@@ -2,11 +2,14 @@
 //
 // One pass p, snapshot semantics:
 //   k_select        (K1) stream F once: r_p = sum |F_i| (warp-shuffle reduction),
-//                   S_p = {i : |F_i| > T_p}; take every i in S_p (s_i = F_i,
-//                   F_i = 0, H_i += s_i); selection bitmap + s_i for the scatter.
-//   k_scatter       (K2/K3) F_j += p_ji s_i for every edge of every selected node of
-//                   degree <= kMidMax: 32 selected nodes per warp, lanes spread over
-//                   the group's concatenated out-edges (edge-balanced, coalesced).
+//                   S_p = {i : |F_i| w_i > T_p} (w = selection-key weight, 1 for the
+//                   raw key); take every i in S_p (s_i = F_i, F_i = 0, H_i += s_i);
+//                   dangling i are finished here, the others appended as (i, s_i)
+//                   to the select warp's compacted frontier segment.
+//   k_scatter       (K2/K3) F_j += p_ji s_i for every edge of every listed node of
+//                   degree <= kMidMax: groups of 32 list entries per warp, grabbed in
+//                   ascending runs, lanes spread over the group's concatenated
+//                   out-edges (edge-balanced, coalesced).
 //   k_scatter_hubs  (K4) selected columns of > kMidMax edges, one CTA per 2048-edge chunk.
 //   k_finalize      (K5) deterministic second-level reduction, pass log, T_{p+1},
 //                   stop flag.
@@ -325,10 +328,9 @@ struct ScAcc {
 // a2-a4).  Every CTA first builds, in shared memory, the exclusive prefix of
 // ceil(seg_cnt/32) over the n_seg segments (s_goff[n_seg] = total groups), so a
 // global group index maps to (segment, group) by a binary search in shared
-// memory.  Schedule: the first 3/4 of the groups are dealt round-robin to the
-// grid's warps (no atomics; consecutive groups run side by side, so the ±1000
-// local pushes of neighbouring columns meet in L2), the rest are grabbed
-// dynamically in small runs (one atomic per run) to absorb the degree skew.
+// memory.  Schedule: warps grab short runs of consecutive groups from striped
+// ticket counters (scatter_body), so the grid works on narrow ascending windows
+// of columns.
 // For a group, lane t loads its entry (id, s) (coalesced), gathers
 // col_ptr[id..id+1], derives the push value s_i * (d / #out_i) (PageRank weights
 // are never stored, BASELINE north_star; the oracle's two roundings), and the
