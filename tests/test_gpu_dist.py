@@ -81,7 +81,7 @@ def test_sync_matches_single_gpu_passes(K, key, remote):
     assert np.abs(F).sum() < target
 
 
-@pytest.mark.parametrize("K,cost", [(2, "out"), (3, "inout"), (4, "out")])
+@pytest.mark.parametrize("K,cost", [(2, "out"), (3, "inout"), (4, "out"), (8, "inout")])
 def test_async_parity(K, cost):
     """ASYNC mode (send when s_k > r_k/K, rounds every check_interval passes):
     parity with the oracle and a closed mass ledger."""

@@ -117,3 +117,15 @@ def test_c3_full_scale_parity():
     p.col_ptr, p.row_idx = di.di_csc_from_coo(p.n, src, dst)
     del src, dst
     _full_scale_case(p, "C3", 3)
+
+
+def test_more_than_2_31_edges():
+    """Maximum-size edge case: a web-like graph with nnz > 2^31 (64-bit edge offsets
+    through create/validation, hot-window sampling, scatter and hub chunks), in C4's
+    launch configuration; the same properties as above (oracle first passes too)."""
+    n = 55_000_000
+    cp, ri = gen.web_graph(n, 2, 10.0)
+    assert cp[-1] > 2 ** 31, cp[-1]
+    p = gen.config("C4", 2, n=1000)               # for d, stop, parity_stop only
+    p.n, p.col_ptr, p.row_idx = n, cp, ri
+    _full_scale_case(p, "C4", 2)
