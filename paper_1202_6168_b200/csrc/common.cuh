@@ -9,8 +9,6 @@
 
 namespace diter {
 
-constexpr int kWarp = 32;
-
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -30,85 +28,6 @@ __device__ __forceinline__ T warp_sum(T v) {
 // diffusion F_j += p_ji * sent.
 __device__ __forceinline__ void red_add(double *addr, double v) {
   atomicAdd(addr, v);  // result unused -> RED (no return trip, no ordering with loads)
-}
-
-// Streaming 16-byte load of 4 row indices that bypasses L1 allocation
-// (each row index is read once per diffusion of its column).
-__device__ __forceinline__ int4 ld_stream_i4(const int4 *p) {
-  int4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-
-__device__ __forceinline__ int ld_stream_i1(const int *p) {
-  int r;
-  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
-  return r;
-}
-
-__device__ __forceinline__ double2 ld_stream_d2(const double2 *p) {
-  double2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
-               : "=d"(r.x), "=d"(r.y)
-               : "l"(p));
-  return r;
-}
-
-__device__ __forceinline__ double ld_stream_d1(const double *p) {
-  double r;
-  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
-  return r;
-}
-
-// ---- TMA bulk copies (cp.async.bulk) + mbarrier, sm_90+/sm_100a ----
-__device__ __forceinline__ unsigned smem_u32(const void *p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long *bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-// 1-D bulk copy global -> shared (TMA engine, UBLKCP in SASS); bytes % 16 == 0.
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// Warp-aggregated append: every lane of the warp calls it (uniform control
-// flow); lanes with pred get consecutive slots of *counter.
-__device__ __forceinline__ unsigned warp_append(unsigned *counter, bool pred) {
-  const unsigned mask = __ballot_sync(0xffffffffu, pred);
-  if (mask == 0u) return 0u;
-  const int leader = __ffs(mask) - 1;
-  unsigned base = 0u;
-  if ((int)lane_id() == leader) base = atomicAdd(counter, (unsigned)__popc(mask));
-  base = __shfl_sync(0xffffffffu, base, leader);
-  return base + (unsigned)__popc(mask & lanemask_lt());
 }
 
 }  // namespace diter
