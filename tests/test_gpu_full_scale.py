@@ -129,3 +129,27 @@ def test_more_than_2_31_edges():
     p = gen.config("C4", 2, n=1000)               # for d, stop, parity_stop only
     p.n, p.col_ptr, p.row_idx = n, cp, ri
     _full_scale_case(p, "C4", 2)
+
+
+def test_max_nodes_cycle_closed_form():
+    """Maximum-size edge case for node ids: n = 2^31 - 1 (the ABI's limit) on the
+    directed N-cycle, whose fixed point is X_i = 1/N.  Every pass
+    diffuses every node (uniform F), so the solve also streams ~17 GB of F per pass.
+    Checks |X - H|_1 <= |F|_1 / (1 - d) against the closed form and that |F|_1 is exact."""
+    n = 2 ** 31 - 1
+    cp = np.arange(n + 1, dtype=np.int64)
+    ri = np.arange(1, n + 1, dtype=np.int64)
+    ri[-1] = 0
+    ri = ri.astype(np.int32)
+    ctx = di.di_create(n, cp, ri, None, None, 0.85, di.default_options(policy=di.DI_POLICY_GEOM))
+    del cp, ri
+    target = 1e-6
+    di.di_run(ctx, target)
+    r = di.di_get_residual(ctx)
+    H = di.di_get_history(ctx)
+    st = di.di_get_stats(ctx)
+    di.di_destroy(ctx)
+    assert r < target and st["passes"] > 50
+    err = float(np.abs(H - 1.0 / n).sum())
+    assert err <= r / 0.15 * (1 + 1e-9), (err, r / 0.15)
+    assert H.min() > 0.0 and abs(float(H.sum()) - (1.0 - r / 0.15)) <= 1e-9
