@@ -74,7 +74,8 @@ enum {
   DI_KEY_RAW = 0,          /* w_i = 1 (BASELINE north_star "above a per-pass threshold") */
   DI_KEY_EDGE = 1,         /* w_i = 1 / (#out_i + 1): per-edge key, out-degree only */
   DI_KEY_PAPER = 2         /* w_i = 1 / ((#in_i + 1)(#out_i + 1)): the paper's argmax key
-                              (PAPER.md:210); one GPU only (needs global in-degrees) */
+                              (PAPER.md:210); distributed ranks get the global in-degrees of
+                              their rows by a reduce-scatter at create */
 };
 
 /* How a distributed rank pushes fluid along edges to rows it does not own. */

@@ -89,5 +89,6 @@ diter::Graph diter_graph(const di_ctx *ctx);
 void diter_dist_free(di_ctx *ctx);
 double diter_dist_max(di_ctx *ctx, double v);
 double diter_dist_sum(di_ctx *ctx, double v);
+di_status diter_dist_indegree(di_ctx *ctx, unsigned *indeg_local);   // DI_KEY_PAPER, collective
 di_status diter_dist_run(di_ctx *ctx, double target);
 di_status diter_dist_reset(di_ctx *ctx);

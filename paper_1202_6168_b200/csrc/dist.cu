@@ -583,6 +583,73 @@ void diter_dist_free(di_ctx *ctx) {
   ctx->dist = nullptr;
 }
 
+__global__ void k_indeg_all(const int *__restrict__ row_idx, long long nnz, unsigned *cnt) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += stride)
+    atomicAdd(cnt + row_idx[e], 1u);
+}
+__global__ void k_indeg_sum(const unsigned *__restrict__ own, const unsigned *__restrict__ recv, int nblk,
+                            long long blk_stride, long long n, unsigned *out) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    unsigned c = own[i];
+    for (int q = 0; q < nblk; ++q) c += recv[q * blk_stride + i];
+    out[i] = c;
+  }
+}
+
+// Global in-degree of the owned rows (DI_KEY_PAPER on a distributed context,
+// PAPER.md:210): count this rank's edges into every global row, then a dense
+// reduce-scatter through the fabric -- rank k receives every peer's counts for
+// Omega_k (blocks padded to 16-byte records) and adds them to its own.  Setup only.
+di_status diter_dist_indegree(di_ctx *ctx, unsigned *indeg_local) {
+  DistState *ds = ctx->dist;
+  const int W = ctx->world, rank = ctx->rank;
+  const std::vector<long long> &b = ds->bounds;
+  auto pad4 = [](long long x) { return (x + 3) / 4 * 4; };
+  std::vector<long long> boff(W + 1, 0), soff(W), scnt(W), roff(W), rcnt(W);
+  for (int q = 0; q < W; ++q) boff[q + 1] = boff[q] + pad4(b[q + 1] - b[q]);
+  const long long my_blk = pad4(b[rank + 1] - b[rank]);
+  unsigned *all = nullptr, *send = nullptr, *recv = nullptr;
+  di_status st = DI_OK;
+  const long long nr = ctx->n_rows;
+  if (cudaMalloc(&all, sizeof(unsigned) * std::max(1LL, nr)) != cudaSuccess ||
+      cudaMalloc(&send, sizeof(unsigned) * std::max(4LL, boff[W])) != cudaSuccess ||
+      cudaMalloc(&recv, sizeof(unsigned) * std::max(4LL, my_blk * W)) != cudaSuccess) {
+    diter_set_err(ctx, "cudaMalloc (in-degree exchange) failed");
+    st = DI_ERR_OOM;
+  }
+  if (st == DI_OK) {
+    cudaMemsetAsync(all, 0, sizeof(unsigned) * nr, ctx->stream);
+    cudaMemsetAsync(send, 0, sizeof(unsigned) * boff[W], ctx->stream);
+    k_indeg_all<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->row_idx, ctx->nnz_local, all);
+    for (int q = 0; q < W; ++q)
+      cudaMemcpyAsync(send + boff[q], all + b[q], sizeof(unsigned) * (b[q + 1] - b[q]), cudaMemcpyDeviceToDevice,
+                      ctx->stream);
+    for (int q = 0; q < W; ++q) {
+      soff[q] = boff[q] / 4;
+      scnt[q] = q == rank ? 0 : pad4(b[q + 1] - b[q]) / 4;
+      roff[q] = q * my_blk / 4;
+      rcnt[q] = q == rank ? 0 : my_blk / 4;
+    }
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) st = DI_ERR_CUDA;
+  }
+  if (st == DI_OK)
+    st = ds->fabric->alltoallv(ctx, reinterpret_cast<const Rec *>(send), soff.data(), scnt.data(),
+                               reinterpret_cast<Rec *>(recv), roff.data(), rcnt.data());
+  if (st == DI_OK) {
+    // own block: my rows' counts from my own edges; peers' blocks in recv (own slot unused)
+    cudaMemsetAsync(recv + rank * my_blk, 0, sizeof(unsigned) * my_blk, ctx->stream);
+    k_indeg_sum<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(all + b[rank], recv, W, my_blk, b[rank + 1] - b[rank],
+                                                            indeg_local);
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) st = DI_ERR_CUDA;
+  }
+  cudaFree(all);
+  cudaFree(send);
+  cudaFree(recv);
+  return st;
+}
+
 double diter_dist_max(di_ctx *ctx, double v) {
   if (!ctx->dist) return v;
   return ctx->dist->fabric->host_max(ctx, v);
@@ -1380,10 +1447,6 @@ extern "C" di_status di_create_dist(di_ctx **out, int32_t rank, int32_t world, c
     diter_set_err(nullptr, "%s", e.c_str());
     return s;
   };
-  if (opt && opt->select_key == DI_KEY_PAPER) {     // before any collective step
-    diter_set_err(ctx, "DI_KEY_PAPER needs global in-degrees: one GPU only (use DI_KEY_EDGE)");
-    return fail(DI_ERR_INVALID_ARG);
-  }
   DistState *ds = new DistState();
   ctx->dist = ds;
   ds->bounds.assign(bounds, bounds + world + 1);

@@ -250,7 +250,7 @@ static di_status setup_far(di_ctx *ctx) {
 }
 
 // Selection-key weights (DI_KEY_*, reading R20).  The paper key needs the global
-// in-degree of every owned row, which a distributed rank does not hold.
+// in-degree of every owned row: a distributed rank gets it by a reduce-scatter.
 static di_status setup_key(di_ctx *ctx) {
   const int key = ctx->opt.select_key;
   if (key == DI_KEY_RAW) return DI_OK;
@@ -258,17 +258,17 @@ static di_status setup_key(di_ctx *ctx) {
     diter_set_err(ctx, "select_key must be DI_KEY_RAW, DI_KEY_EDGE or DI_KEY_PAPER");
     return DI_ERR_INVALID_ARG;
   }
-  if (key == DI_KEY_PAPER && ctx->world > 1) {
-    diter_set_err(ctx, "DI_KEY_PAPER needs global in-degrees: one GPU only (use DI_KEY_EDGE)");
-    return DI_ERR_INVALID_ARG;
-  }
   const long long n = ctx->n_local;
   TRY(dalloc(ctx, &ctx->kw, (size_t)n));
   unsigned *indeg = nullptr;
   if (key == DI_KEY_PAPER) {
     TRY(dalloc(ctx, &indeg, (size_t)n));
-    CK(cudaMemsetAsync(indeg, 0, sizeof(unsigned) * n, ctx->stream));
-    k_in_degree<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->row_idx, ctx->nnz_local, indeg);
+    if (ctx->world > 1) {
+      TRY(diter_dist_indegree(ctx, indeg));   // global in-degrees of the owned rows (collective)
+    } else {
+      CK(cudaMemsetAsync(indeg, 0, sizeof(unsigned) * n, ctx->stream));
+      k_in_degree<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->row_idx, ctx->nnz_local, indeg);
+    }
   }
   k_key_weights<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->col_ptr, n, indeg, key, ctx->kw);
   CK(cudaStreamSynchronize(ctx->stream));

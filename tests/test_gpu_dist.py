@@ -51,12 +51,14 @@ def run_ranks(K, n, cp, ri, vals, b, d, target, bounds, mode, key, **opts):
 
 @pytest.mark.parametrize("K,key,remote", [(2, di.DI_KEY_RAW, 0), (4, di.DI_KEY_RAW, 0), (3, di.DI_KEY_EDGE, 0),
                                           (2, di.DI_KEY_RAW, 1), (3, di.DI_KEY_EDGE, 1),
-                                          (2, di.DI_KEY_RAW, 2), (4, di.DI_KEY_EDGE, 2)])
+                                          (2, di.DI_KEY_RAW, 2), (4, di.DI_KEY_EDGE, 2),
+                                          (3, di.DI_KEY_PAPER, 0), (2, di.DI_KEY_PAPER, 1)])
 def test_sync_matches_single_gpu_passes(K, key, remote):
     """SYNC mode is the single-GPU snapshot pass: same per-pass frontier sizes,
     edges and thresholds (random B: no exact-arithmetic ties), same fixed point --
     with the raw and the per-edge selection key (per-edge weights need only local
-    out-degrees), and with remote edges pushed per diffusion, as H increments at
+    out-degrees) and the paper key (global in-degrees by a reduce-scatter at create),
+    and with remote edges pushed per diffusion, as H increments at
     each exchange (NEXT f2) or applied by the receivers from the
     shipped increments (NEXT f3): the same fluid reaches the same
     rows before the next selection."""
@@ -270,17 +272,6 @@ def test_adaptation_moves_boundaries_on_skewed_partition():
     deg = np.diff(p.col_ptr)
     ledger = np.abs(F).sum() + 0.15 * H.sum() + 0.85 * H[deg == 0].sum()
     assert abs(ledger - bn) <= 1e-12 * bn
-
-
-def test_paper_key_rejected_on_distributed():
-    """DI_KEY_PAPER needs global in-degrees, which a rank does not hold."""
-    n = 1000
-    cp, ri = gen.uniform_graph(n, 1)
-    bounds = dist.partition_bounds(cp, 2)
-    with pytest.raises(di.DiError) as e:
-        run_ranks(2, n, cp, ri, None, None, 0.85, 1e-9, bounds, di.DI_EXCHANGE_SYNC, "paperkey",
-                  select_key=di.DI_KEY_PAPER)
-    assert e.value.status == di.DI_ERR_INVALID_ARG
 
 
 def test_async_signed():
