@@ -130,6 +130,9 @@ static di_status setup_geometry(di_ctx *ctx) {
     if (ctx->vals) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, k_pass_fused<true>, kScatterThreads, dyn));
     else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, k_pass_fused<false>, kScatterThreads, dyn));
     ctx->grid_fused = ctx->num_sms * std::max(1, std::min(occ_f, 4));
+    // a small graph gets a small grid: the three grid barriers per pass then span few
+    // CTAs (1 CTA for configs[0]); one CTA per 4096 nodes
+    ctx->grid_fused = (int)std::max(1LL, std::min<long long>(ctx->grid_fused, (n + 4095) / 4096));
     gs = std::min<long long>(ctx->grid_fused, kMaxSegments / kWarps);
   }
   ctx->grid_select = (int)gs;
