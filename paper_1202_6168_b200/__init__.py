@@ -19,7 +19,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libditer.so")
+# DITER_LIB: another build of this library (A/B experiments, scripts/build_variant.py)
+LIB_PATH = os.environ.get("DITER_LIB") or os.path.join(_HERE, "libditer.so")
 
 DI_OK, DI_ERR_INVALID_ARG, DI_ERR_CONTRACTION, DI_ERR_OOM, DI_ERR_CUDA, DI_ERR_NCCL, \
     DI_ERR_NOT_CONVERGED, DI_ERR_STATE, DI_ERR_UNSUPPORTED = range(9)
