@@ -7,7 +7,7 @@ import os, subprocess, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1202_6168_b200 import build as b
 
-out, defs = sys.argv[1], sys.argv[2:]
+out, defs = os.path.abspath(sys.argv[1]), sys.argv[2:]
 cflags, lflags = b._nccl_flags()
 cmd = [b.NVCC, *b.ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
        "-Xcompiler", "-fvisibility=hidden", "-Xptxas", "-v", "--expt-relaxed-constexpr",
