@@ -216,6 +216,14 @@ DI_API di_status di_get_unique_id(void *comm_id_out);
  * the next di_run solves from scratch.  Collective for distributed contexts. */
 DI_API di_status di_reset(di_ctx *ctx);
 
+/* Switch per-kernel timing on (1) or off (0) for the following di_run calls:
+ * with it on, CUDA events recorded between the pass kernels give the select /
+ * scatter / finalize durations in di_stats (kt_*_ms) and the pass log, at a cost
+ * of ~25 us of device time per pass (the events split the captured pass graph);
+ * the single-GPU pass graph is re-captured.  Same as options.profile at create.
+ * Not collective. */
+DI_API di_status di_set_profile(di_ctx *ctx, int32_t on);
+
 /* Run passes until |F|_1 < residual_target (absolute; global if distributed).
  * Resumable: call again with a smaller target to continue from (F, H).
  * Collective for distributed contexts.  Returns DI_OK when the target is met,

@@ -34,7 +34,7 @@ STATUS_NAMES = {0: "DI_OK", 1: "DI_ERR_INVALID_ARG", 2: "DI_ERR_CONTRACTION", 3:
                 8: "DI_ERR_UNSUPPORTED"}
 
 # every symbol include/diter.h declares (checked by tests/test_abi.py)
-EXPORTS = ["di_default_options", "di_struct_size", "di_create", "di_create_dist", "di_get_unique_id", "di_reset", "di_run",
+EXPORTS = ["di_default_options", "di_struct_size", "di_create", "di_create_dist", "di_get_unique_id", "di_reset", "di_set_profile", "di_run",
            "di_get_history", "di_get_fluid", "di_get_history_device", "di_get_fluid_device",
            "di_get_pagerank", "di_get_pagerank_device", "di_rebalance", "di_get_bounds",
            "di_get_residual", "di_get_stats", "di_get_pass_log", "di_last_error", "di_destroy",
@@ -106,6 +106,7 @@ def load_library() -> ctypes.CDLL:
                                 ctypes.POINTER(di_options)]),
         "di_get_unique_id": (st, [vp]),
         "di_reset": (st, [vp]),
+        "di_set_profile": (st, [vp, i32]),
         "di_run": (st, [vp, f64]),
         "di_get_history": (st, [vp, vp]),
         "di_get_fluid": (st, [vp, vp]),
@@ -237,6 +238,10 @@ def di_run(ctx: Context, residual_target: float, raise_on_not_converged: bool = 
 
 def di_reset(ctx: Context):
     _check(load_library().di_reset(ctx.handle), ctx.handle)
+
+
+def di_set_profile(ctx: Context, on: bool):
+    _check(load_library().di_set_profile(ctx.handle, 1 if on else 0), ctx.handle)
 
 
 def _get_vec(fn, ctx: Context, out=None):

@@ -908,10 +908,32 @@ static di_status round_exchange(di_ctx *ctx, bool send_now) {
   return exchange(ctx, send_now);
 }
 
-static void launch_pass_kernels(di_ctx *ctx) {
+// profile=1: events around the select and the scatter of local pass `slot` of a
+// round (slot < check_interval), read back after the round's host sync
+static void prof_mark(di_ctx *ctx, int slot, int q) {
+  if (ctx->opt.profile && !ctx->prof_ev.empty()) cudaEventRecord(ctx->prof_ev[4 * slot + q], ctx->stream);
+}
+
+static di_status prof_collect(di_ctx *ctx, int npasses) {
+  if (!ctx->opt.profile || ctx->prof_ev.empty()) return DI_OK;
+  for (int k = 0; k < npasses; ++k) {
+    float a = 0.f, b = 0.f;
+    CKD(cudaEventElapsedTime(&a, ctx->prof_ev[4 * k + 0], ctx->prof_ev[4 * k + 1]));
+    CKD(cudaEventElapsedTime(&b, ctx->prof_ev[4 * k + 1], ctx->prof_ev[4 * k + 2]));
+    ctx->kt_ms[0] += a;
+    ctx->kt_ms[1] += b;
+    ctx->pass_us.push_back({a * 1e3, b * 1e3});
+  }
+  ctx->kt_passes += npasses;
+  return DI_OK;
+}
+
+static void launch_pass_kernels(di_ctx *ctx, int slot) {
   Graph g = diter_graph(ctx);
+  prof_mark(ctx, slot, 0);
   k_select<<<ctx->grid_select, kSelectThreads, 0, ctx->stream>>>(ctx->F, ctx->H, ctx->fr, ctx->n_local, ctx->ctl,
                                                                 ctx->sel_part, ctx->kw);
+  prof_mark(ctx, slot, 1);
   if (ctx->vals)
     k_scatter<true, true><<<ctx->grid_scatter, kScatterThreads, ctx->scatter_smem, ctx->stream>>>(
         g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part);
@@ -924,6 +946,7 @@ static void launch_pass_kernels(di_ctx *ctx) {
     else
       k_scatter_hubs<false><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
   }
+  prof_mark(ctx, slot, 2);
   ctx->kernel_launches += ctx->cap_hub > 0 ? 3 : 2;
 }
 
@@ -981,7 +1004,7 @@ di_status diter_dist_run(di_ctx *ctx, double target) {
     // -------- SYNC: one exchange per pass, pass totals all-reduced ----------
     k_set_target<<<1, 1, 0, ctx->stream>>>(ctx->ctl, target, max_pass_abs, 0);
     for (;;) {
-      launch_pass_kernels(ctx);
+      launch_pass_kernels(ctx, 0);
       k_reduce_partials<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->ctl, ctx->sel_part, ctx->grid_select,
                                                                   ctx->sc_part, ctx->grid_scatter, ds->d_sums);
       TRYD(ds->fabric->allreduce_sum(ctx, ds->d_sums, kSums));
@@ -990,6 +1013,7 @@ di_status diter_dist_run(di_ctx *ctx, double target) {
       ctx->kernel_launches += 2;
       CKD(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
       CKD(cudaStreamSynchronize(ctx->stream));
+      TRYD(prof_collect(ctx, 1));
       if (!h->done) continue;
       ctx->passes_done = h->pass;
       TRYD(global_residual(ctx, 0.0, &R));
@@ -1005,7 +1029,7 @@ di_status diter_dist_run(di_ctx *ctx, double target) {
       // local passes: no target (never "done" locally), local threshold policy
       k_set_target<<<1, 1, 0, ctx->stream>>>(ctx->ctl, 0.0, max_pass_abs, 0);
       for (int k = 0; k < ctx->check_interval; ++k) {
-        launch_pass_kernels(ctx);
+        launch_pass_kernels(ctx, k);
         k_finalize<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->ctl, ctx->sel_part, ctx->grid_select, ctx->sc_part,
                                                             ctx->grid_scatter, ctx->log);
         ctx->kernel_launches += 1;
@@ -1025,6 +1049,7 @@ di_status diter_dist_run(di_ctx *ctx, double target) {
       CKD(cudaMemcpyAsync(&hs[1], ctx->l1_out, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
       CKD(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
       CKD(cudaStreamSynchronize(ctx->stream));
+      TRYD(prof_collect(ctx, ctx->check_interval));
       ds->s_k = hs[0];
       const double r_k = hs[1];
       const bool send_now = (ds->s_k > r_k / ctx->world) || (r_k == 0.0 && ds->s_k > 0.0);

@@ -618,6 +618,23 @@ extern "C" di_status di_run(di_ctx *ctx, double target) {
   return st;
 }
 
+extern "C" di_status di_set_profile(di_ctx *ctx, int32_t on) {
+  if (!ctx) { diter_set_err(nullptr, "ctx is NULL"); return DI_ERR_INVALID_ARG; }
+  CK(cudaSetDevice(ctx->device));
+  if ((ctx->opt.profile != 0) == (on != 0)) return DI_OK;
+  ctx->opt.profile = on ? 1 : 0;
+  if (on && ctx->prof_ev.empty()) {
+    ctx->prof_ev.assign(4 * ctx->check_interval, nullptr);
+    for (auto &e : ctx->prof_ev) CK(cudaEventCreate(&e));
+  }
+  if (ctx->graph_exec) {
+    CK(cudaGraphExecDestroy(ctx->graph_exec));
+    ctx->graph_exec = nullptr;
+  }
+  if (ctx->world == 1 && !ctx->fused) TRY(capture_graph(ctx));
+  return DI_OK;
+}
+
 extern "C" di_status di_reset(di_ctx *ctx) {
   if (!ctx) { diter_set_err(nullptr, "ctx is NULL"); return DI_ERR_INVALID_ARG; }
   CK(cudaSetDevice(ctx->device));

@@ -19,7 +19,7 @@ ap.add_argument("--config", default="C4")
 ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--variants", default="")
-ap.add_argument("--policy", default="hybrid")
+ap.add_argument("--policy", default="bench")
 a = ap.parse_args()
 p = gen.config(a.config, 1, n=a.n)
 if a.config == "C3":
@@ -31,6 +31,11 @@ for v in [x for x in a.variants.split(";")] or [""]:
     for item in filter(None, v.split(",")):
         k, val = item.split("=")
         kw[k.strip()] = float(val) if "." in val else int(val)
+    if a.policy == "bench":      # the bench's launch configuration
+        import bench
+        pol, alpha, frac, key = bench.SCHEDULES[a.config]
+        for k_, v_ in (("policy", pol), ("alpha", alpha), ("hybrid_frac", frac), ("select_key", key)):
+            kw.setdefault(k_, v_)
     kw.setdefault("policy", di.DI_POLICY_GEOM if a.policy == "geom" else di.DI_POLICY_HYBRID)
     kw["policy"] = int(kw["policy"])
     ctx = di.di_create(p.n, p.col_ptr, p.row_idx, p.values, p.b, p.d, di.default_options(**kw))

@@ -312,3 +312,17 @@ def test_rebalance_rejects_bad_bounds_and_keeps_state():
     H = np.concatenate([o[1] for o in outs])
     X = oracle.Problem(p.n, p.col_ptr, p.row_idx).solve(1e-12 * 0.15 * 0.15).H
     assert np.abs(H - X).sum() <= 1e-8 * 0.15
+
+
+@pytest.mark.parametrize("mode", [di.DI_EXCHANGE_SYNC, di.DI_EXCHANGE_ASYNC])
+def test_dist_profile_kernel_times(mode):
+    """profile=1 on distributed contexts: events around each local pass's select and
+    scatter, read back at the round's host sync (bench.py's roofline at N > 1)."""
+    p = gen.config("C2", 1, n=200_000)
+    bounds = dist.partition_bounds(p.col_ptr, 2)
+    _, _, out = run_ranks(2, p.n, p.col_ptr, p.row_idx, None, None, 0.85, p.stop, bounds, mode,
+                          "prof%d" % mode, profile=1)
+    for o in out:
+        s = o[3]
+        assert s["kt_scatter_ms"] > 0 and s["kt_select_ms"] > 0
+        assert s["kt_passes"] == s["passes"]

@@ -398,3 +398,28 @@ def test_bounds_and_rebalance_on_one_gpu():
     di.di_run(ctx, 1e-12)                     # the context is still usable
     assert di.di_get_residual(ctx) < 1e-12
     di.di_destroy(ctx)
+
+
+def test_set_profile_same_solve_and_kernel_times():
+    """di_set_profile re-captures the pass graph with events between the kernels:
+    the solve is the same up to the order of the fp64 REDs (which differs between
+    any two runs) and the kernel times fill."""
+    p = gen.config("C2", 1)
+    ctx = di.di_create(p.n, p.col_ptr, p.row_idx, None, None, 0.85, di.default_options())
+    out = []
+    for on in (False, True, False):
+        di.di_set_profile(ctx, on)
+        di.di_reset(ctx)
+        di.di_run(ctx, p.stop)
+        s = di.di_get_stats(ctx)
+        out.append((di.di_get_history(ctx), s))
+        if on:
+            assert s["kt_scatter_ms"] > 0 and s["kt_select_ms"] > 0 and s["kt_passes"] == s["passes"]
+            lg = di.di_get_pass_log(ctx)
+            assert np.all(lg["t_scatter_us"] > 0)
+        else:
+            assert s["kt_scatter_ms"] == 0
+    di.di_destroy(ctx)
+    for k in (1, 2):
+        assert np.abs(out[k][0] - out[0][0]).sum() <= 1e-12 * out[0][0].sum()
+        assert abs(out[k][1]["passes"] - out[0][1]["passes"]) <= 1
