@@ -87,6 +87,9 @@ diter::Graph diter_graph(const di_ctx *ctx);
 
 // distributed hooks (dist.cu); identities / no-ops on single-GPU contexts
 void diter_dist_free(di_ctx *ctx);
+// context device memory (per-device stream-ordered pool, ordered on ctx->stream)
+di_status diter_alloc(di_ctx *ctx, void **p, size_t bytes);
+void diter_free(di_ctx *ctx, void *p);
 double diter_dist_max(di_ctx *ctx, double v);
 double diter_dist_sum(di_ctx *ctx, double v);
 di_status diter_dist_indegree(di_ctx *ctx, unsigned *indeg_local);   // DI_KEY_PAPER, collective

@@ -575,8 +575,8 @@ void diter_dist_free(di_ctx *ctx) {
                   ds->ric_src, ds->ric_off, ds->ric_row, ds->ric_p};
   for (void *p : ptrs)
     if (p) cudaFree(p);
-  if (ctx->G) cudaFree(ctx->G);
-  if (ctx->dflags) cudaFree(ctx->dflags);
+  diter_free(ctx, ctx->G);
+  diter_free(ctx, ctx->dflags);
   ctx->G = nullptr;
   ctx->dflags = nullptr;
   delete ds;
@@ -1349,7 +1349,7 @@ static di_status dist_build(di_ctx *ctx, const int64_t *col_ptr_local, const int
     const long long n = ctx->n_local, nnz = ctx->nnz_local;
     int *ri2 = nullptr;
     double *v2 = nullptr;
-    if (cudaMalloc(&ctx->nloc, sizeof(int) * std::max(1LL, n)) != cudaSuccess ||
+    if (diter_alloc(ctx, (void **)&ctx->nloc, sizeof(int) * std::max(1LL, n)) != DI_OK ||
         cudaMalloc(&ri2, sizeof(int) * std::max(1LL, nnz)) != cudaSuccess ||
         (ctx->vals && cudaMalloc(&v2, sizeof(double) * std::max(1LL, nnz)) != cudaSuccess)) {
       if (ri2) cudaFree(ri2);
@@ -1374,7 +1374,7 @@ static di_status dist_build(di_ctx *ctx, const int64_t *col_ptr_local, const int
     if (v2) cudaFree(v2);
     if (e != cudaSuccess) { diter_set_err(ctx, "column partition failed: %s", cudaGetErrorString(e)); return (DI_ERR_CUDA); }
     if (ctx->opt.remote_push == DI_REMOTE_INCREMENT || ctx->opt.remote_push == DI_REMOTE_RECEIVER) {
-      if (cudaMalloc(&ctx->H_old, sizeof(double) * std::max(1LL, n)) != cudaSuccess) {
+      if (diter_alloc(ctx, (void **)&ctx->H_old, sizeof(double) * std::max(1LL, n)) != DI_OK) {
         diter_set_err(ctx, "cudaMalloc (H_old) failed");
         return (DI_ERR_OOM);
       }
@@ -1387,8 +1387,8 @@ static di_status dist_build(di_ctx *ctx, const int64_t *col_ptr_local, const int
   // outbox, flags, exchange buffers
   {
     const long long nb = (n_global + 31) >> 5;
-    if (cudaMalloc(&ctx->G, sizeof(double) * n_global) != cudaSuccess ||
-        cudaMalloc(&ctx->dflags, (size_t)nb) != cudaSuccess) {
+    if (diter_alloc(ctx, (void **)&ctx->G, sizeof(double) * n_global) != DI_OK ||
+        diter_alloc(ctx, (void **)&ctx->dflags, (size_t)nb) != DI_OK) {
       diter_set_err(ctx, "cudaMalloc (outbox) failed");
       return (DI_ERR_OOM);
     }

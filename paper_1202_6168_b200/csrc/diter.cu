@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "../../include/diter.h"
@@ -71,12 +72,47 @@ extern "C" void di_default_options(di_options *o) {
   o->receive_rescale = 1;
 }
 
+// Device memory of a context comes from one stream-ordered pool per device that
+// keeps what contexts free (release threshold = max): the ~11 GB of a C4 context
+// is mapped once per process, and create/destroy cycles (bench e2e) no longer pay
+// cudaMalloc / cudaFree of multi-GB buffers (measured: usually ~10 ms, sporadically
+// 300-400 ms per call).
+static cudaMemPool_t device_pool(int dev) {
+  static std::mutex mu;
+  static std::vector<cudaMemPool_t> pools;
+  std::lock_guard<std::mutex> g(mu);
+  if ((int)pools.size() <= dev) pools.resize(dev + 1, nullptr);
+  if (!pools[dev]) {
+    cudaMemPoolProps pr = {};
+    pr.allocType = cudaMemAllocationTypePinned;
+    pr.location.type = cudaMemLocationTypeDevice;
+    pr.location.id = dev;
+    cudaMemPool_t mp = nullptr;
+    if (cudaMemPoolCreate(&mp, &pr) != cudaSuccess) return nullptr;
+    unsigned long long keep = ~0ull;
+    cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep);
+    pools[dev] = mp;
+  }
+  return pools[dev];
+}
+
+di_status diter_alloc(di_ctx *ctx, void **p, size_t bytes) {
+  *p = nullptr;
+  cudaMemPool_t mp = device_pool(ctx->device);
+  if (!mp) { diter_set_err(ctx, "cudaMemPoolCreate failed on device %d", ctx->device); return DI_ERR_CUDA; }
+  CK(cudaMallocFromPoolAsync(p, bytes ? bytes : 1, mp, ctx->stream));
+  return DI_OK;
+}
+
+// ctx->stream may be null (a context whose stream moved to its rebuilt successor):
+// its work is complete, the legacy stream orders the free
+void diter_free(di_ctx *ctx, void *p) {
+  if (p) cudaFreeAsync(p, ctx->stream);
+}
+
 template <typename T>
 static di_status dalloc(di_ctx *ctx, T **p, size_t count) {
-  *p = nullptr;
-  if (count == 0) count = 1;
-  CK(cudaMalloc((void **)p, count * sizeof(T)));
-  return DI_OK;
+  return diter_alloc(ctx, (void **)p, (count ? count : 1) * sizeof(T));
 }
 
 #define TRY(x)                      \
@@ -94,13 +130,14 @@ static void free_ctx(di_ctx *c) {
   void *ptrs[] = {c->col_ptr, c->row_idx, c->vals, c->d_b, c->F, c->H, c->fr.ids, c->fr.S, c->fr.seg_cnt, const_cast<unsigned *>(c->fr.dang_bits),
                   c->fr.hub_w, c->fr.hub_b0, c->fr.hub_deg, c->fr.hub_chunk, c->sel_part, c->sc_part,
                   c->l1_part, c->l1_out, c->ctl, c->log, c->far_off, c->far.rows, c->far.vals, c->far.fill, c->kw, c->nloc, c->H_old};
-  for (void *p : ptrs)
-    if (p) cudaFree(p);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (void *p : ptrs) diter_free(c, p);
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
-  if (c->stream) cudaStreamDestroy(c->stream);
   diter_dist_free(c);
+  cudaStreamSynchronize(c->stream);            // the frees above are stream-ordered
+  if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
 
@@ -178,7 +215,7 @@ static di_status choose_hot_window(di_ctx *ctx) {
   ctx->blk_stride = stride;
   CK(cudaMemcpyAsync(h.data(), blk, sizeof(unsigned) * nb, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  cudaFree(blk);
+  diter_free(ctx, blk);
   long long best = ctx->lo >> 10, best_mass = -1;
   const long long hi = ctx->lo + ctx->n_local;
   for (long long b = 0; b + 1 < nb; ++b) {
@@ -228,7 +265,7 @@ static di_status setup_far(di_ctx *ctx) {
   std::vector<unsigned long long> cap(kMaxBins);
   CK(cudaMemcpyAsync(cap.data(), d_cap, sizeof(unsigned long long) * kMaxBins, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  cudaFree(d_cap);
+  diter_free(ctx, d_cap);
   // chunks per bin: every chunk closed before the end of a pass holds > kFarChunk - 32
   // records, and each scatter warp leaves at most one partial chunk per bin
   const long long warps = (long long)ctx->grid_scatter * (kScatterThreads / 32);
@@ -275,7 +312,7 @@ static di_status setup_key(di_ctx *ctx) {
   }
   k_key_weights<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->col_ptr, n, indeg, key, ctx->kw);
   CK(cudaStreamSynchronize(ctx->stream));
-  if (indeg) cudaFree(indeg);
+  if (indeg) diter_free(ctx, indeg);
   CK(cudaGetLastError());
   return DI_OK;
 }
@@ -396,7 +433,7 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
   Census hc;
   CK(cudaMemcpyAsync(&hc, d_c, sizeof(Census), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  cudaFree(d_c);
+  diter_free(ctx, d_c);
   CK(cudaGetLastError());
   if (hc.bad_ptr) {
     diter_set_err(ctx, "col_ptr is not non-decreasing (%llu columns)", hc.bad_ptr);
