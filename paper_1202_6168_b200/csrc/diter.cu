@@ -123,21 +123,35 @@ static di_status dalloc(di_ctx *ctx, T **p, size_t count) {
 
 static void free_ctx(di_ctx *c) {
   if (!c) return;
+  const bool tr = std::getenv("DITER_TRACE") != nullptr;
+  auto t = std::chrono::steady_clock::now();
+  auto mark = [&](const char *what) {
+    if (!tr) return;
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[diter destroy] %-16s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  };
   if (c->device >= 0) cudaSetDevice(c->device);
   if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+  mark("graph exec");
   for (cudaEvent_t e : c->prof_ev)
     if (e) cudaEventDestroy(e);
   void *ptrs[] = {c->col_ptr, c->row_idx, c->vals, c->d_b, c->F, c->H, c->fr.ids, c->fr.S, c->fr.seg_cnt, const_cast<unsigned *>(c->fr.dang_bits),
                   c->fr.hub_w, c->fr.hub_b0, c->fr.hub_deg, c->fr.hub_chunk, c->sel_part, c->sc_part,
                   c->l1_part, c->l1_out, c->ctl, c->log, c->far_off, c->far.rows, c->far.vals, c->far.fill, c->kw, c->nloc, c->H_old};
   if (c->stream) cudaStreamSynchronize(c->stream);
+  mark("sync");
   for (void *p : ptrs) diter_free(c, p);
+  mark("frees");
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
+  mark("free host");
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   diter_dist_free(c);
   cudaStreamSynchronize(c->stream);            // the frees above are stream-ordered
+  mark("sync frees");
   if (c->stream) cudaStreamDestroy(c->stream);
+  mark("stream");
   delete c;
 }
 
@@ -146,9 +160,8 @@ static void free_ctx(di_ctx *c) {
 // warp owning seg_len consecutive nodes (a multiple of 256); the scatter keeps
 // the prefix over segments in (n_seg + 1) ints of dynamic shared memory.
 static di_status setup_geometry(di_ctx *ctx) {
-  cudaDeviceProp prop;
-  CK(cudaGetDeviceProperties(&prop, ctx->device));
-  ctx->num_sms = prop.multiProcessorCount;
+  // one attribute query (cudaGetDeviceProperties fills ~100 fields, 3-20 ms)
+  CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
   const long long n = ctx->n_local;
   constexpr int kWarps = kSelectThreads / 32;
   int occ_sel = 0;
@@ -369,6 +382,24 @@ static di_status capture_graph(di_ctx *ctx) {
   return DI_OK;
 }
 
+// T_0 = max |B_i| w_i / alpha (reading R5) unless options.t0 > 0; needs F = B and
+// the key weights.  The max is global on a distributed context (collective).
+static di_status initial_threshold(di_ctx *ctx, double *T0) {
+  if (*T0 > 0.0) return DI_OK;
+  const long long n = ctx->n_local;
+  double mx = 0.0;
+  if (n > 0) {
+    k_max_abs<<<ctx->grid_l1, 256, 0, ctx->stream>>>(ctx->F, n, ctx->l1_part, ctx->kw);
+    std::vector<double> hp(ctx->grid_l1);
+    CK(cudaMemcpyAsync(hp.data(), ctx->l1_part, sizeof(double) * ctx->grid_l1, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (double v : hp) mx = std::max(mx, v);
+  }
+  mx = diter_dist_max(ctx, mx);   // global max over ranks (identity when not distributed)
+  *T0 = mx / ctx->opt.alpha;
+  return DI_OK;
+}
+
 // DITER_TRACE=1: stream-synchronised phase times of the setup on stderr.
 struct SetupTrace {
   bool on = std::getenv("DITER_TRACE") != nullptr;
@@ -412,19 +443,60 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
   if (values) TRY(dalloc(ctx, &ctx->vals, (size_t)nnz));
   TRY(dalloc(ctx, &ctx->F, (size_t)n));
   TRY(dalloc(ctx, &ctx->H, (size_t)n));
+  if (b) TRY(dalloc(ctx, &ctx->d_b, (size_t)n));
   tr.mark(ctx->stream, "malloc graph+F+H");
+  // Upload: col_ptr and B on the context stream, row_idx / values on a copy stream.
+  // Everything that needs only col_ptr and B (geometry, frontier buffers, dangling
+  // bits, edge-key weights, F/H init, T_0) then runs while the row indices are still
+  // crossing the host link (~115 ms of a C4 create); the census, which validates
+  // both, and whatever reads row_idx wait for the copy stream.
   CK(cudaMemcpyAsync(ctx->col_ptr, col_ptr, sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, ctx->stream));
-  if (nnz)
-    CK(cudaMemcpyAsync(ctx->row_idx, row_idx, sizeof(int) * nnz, cudaMemcpyHostToDevice, ctx->stream));
-  if (values && nnz)
-    CK(cudaMemcpyAsync(ctx->vals, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, ctx->stream));
-  if (b) {
-    TRY(dalloc(ctx, &ctx->d_b, (size_t)n));
-    CK(cudaMemcpyAsync(ctx->d_b, b, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
-  }
-  tr.mark(ctx->stream, "H2D graph (+B)");
+  if (b) CK(cudaMemcpyAsync(ctx->d_b, b, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  cudaStream_t cs = nullptr;
+  cudaEvent_t rows_in = nullptr;
+  CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  struct CopyStream {
+    cudaStream_t &s; cudaEvent_t &e;
+    ~CopyStream() { if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); } if (e) cudaEventDestroy(e); }
+  } cs_guard{cs, rows_in};
+  CK(cudaEventCreateWithFlags(&rows_in, cudaEventDisableTiming));
+  CK(cudaEventRecord(ctx->ev1, ctx->stream));    // the pool allocations are ordered on ctx->stream
+  CK(cudaStreamWaitEvent(cs, ctx->ev1, 0));
+  if (nnz) CK(cudaMemcpyAsync(ctx->row_idx, row_idx, sizeof(int) * nnz, cudaMemcpyHostToDevice, cs));
+  if (values && nnz) CK(cudaMemcpyAsync(ctx->vals, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, cs));
+  CK(cudaEventRecord(rows_in, cs));
   TRY(setup_geometry(ctx));
-  // validation + bin census on the device
+  // frontier and per-pass buffers
+  const size_t fr_cap = (size_t)ctx->fr.n_seg * (size_t)ctx->fr.seg_len;
+  TRY(dalloc(ctx, &ctx->fr.ids, fr_cap));
+  TRY(dalloc(ctx, &ctx->fr.S, fr_cap));
+  TRY(dalloc(ctx, &ctx->fr.seg_cnt, (size_t)ctx->fr.n_seg));
+  {
+    unsigned *db = nullptr;
+    TRY(dalloc(ctx, &db, (size_t)((n + 31) >> 5) + kSelectItems));   // + a pad word per item of the last span
+    CK(cudaMemsetAsync(db, 0, sizeof(unsigned) * (((n + 31) >> 5) + kSelectItems), ctx->stream));
+    k_dangling_bits<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->col_ptr, n, db);
+    ctx->fr.dang_bits = db;
+  }
+  TRY(dalloc(ctx, &ctx->sel_part, (size_t)std::max(ctx->grid_select, ctx->grid_fused)));
+  TRY(dalloc(ctx, &ctx->sc_part, (size_t)ctx->grid_scatter));
+  TRY(dalloc(ctx, &ctx->l1_part, (size_t)ctx->grid_l1));
+  TRY(dalloc(ctx, &ctx->l1_out, 1));
+  TRY(dalloc(ctx, &ctx->ctl, 1));
+  ctx->log_cap = 1 << 18;  // passes logged since create/reset (di_run is resumable)
+  TRY(dalloc(ctx, &ctx->log, (size_t)ctx->log_cap));
+  CK(cudaHostAlloc((void **)&ctx->h_ctl, sizeof(Ctl), cudaHostAllocDefault));
+  // state: F = B, H = 0
+  ctx->b_uniform = (1.0 - ctx->d) / (double)ctx->n_rows;
+  k_init_state<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->F, ctx->H, ctx->d_b, ctx->b_uniform, n);
+  // selection-key weights: the paper key needs in-degrees (row_idx), after the census
+  const bool key_early = o.select_key != DI_KEY_PAPER;
+  if (key_early) TRY(setup_key(ctx));
+  double T0 = o.t0;
+  if (key_early) TRY(initial_threshold(ctx, &T0));
+  tr.mark(ctx->stream, "col_ptr-only setup");
+  // validation + bin census on the device, once the rows are in
+  CK(cudaStreamWaitEvent(ctx->stream, rows_in, 0));
   Census *d_c = nullptr;
   TRY(dalloc(ctx, &d_c, 1));
   CK(cudaMemsetAsync(d_c, 0, sizeof(Census), ctx->stream));
@@ -435,6 +507,7 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
   CK(cudaStreamSynchronize(ctx->stream));
   diter_free(ctx, d_c);
   CK(cudaGetLastError());
+  tr.mark(ctx->stream, "H2D rows + census");
   if (hc.bad_ptr) {
     diter_set_err(ctx, "col_ptr is not non-decreasing (%llu columns)", hc.bad_ptr);
     return DI_ERR_INVALID_ARG;
@@ -447,57 +520,19 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
     diter_set_err(ctx, "%llu columns have sum |p_ij| > d = %g (not contractive)", hc.bad_contraction, ctx->d);
     return DI_ERR_CONTRACTION;
   }
-  tr.mark(ctx->stream, "census/validate");
   TRY(choose_hot_window(ctx));
   tr.mark(ctx->stream, "hot window");
   TRY(setup_far(ctx));
-  TRY(setup_key(ctx));
-  tr.mark(ctx->stream, "far bins + key weights");
+  if (!key_early) TRY(setup_key(ctx));
+  if (!key_early) TRY(initial_threshold(ctx, &T0));
+  tr.mark(ctx->stream, "far bins + paper key");
   ctx->cap_low = hc.n_low;
   ctx->cap_mid = hc.n_mid;
   ctx->cap_hub = hc.n_hub;
-  const size_t fr_cap = (size_t)ctx->fr.n_seg * (size_t)ctx->fr.seg_len;
-  TRY(dalloc(ctx, &ctx->fr.ids, fr_cap));
-  TRY(dalloc(ctx, &ctx->fr.S, fr_cap));
-  TRY(dalloc(ctx, &ctx->fr.seg_cnt, (size_t)ctx->fr.n_seg));
-  {
-    unsigned *db = nullptr;
-    TRY(dalloc(ctx, &db, (size_t)((n + 31) >> 5) + kSelectItems));   // + a pad word per item of the last span
-    CK(cudaMemsetAsync(db, 0, sizeof(unsigned) * (((n + 31) >> 5) + kSelectItems), ctx->stream));
-    k_dangling_bits<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->col_ptr, n, db);
-    ctx->fr.dang_bits = db;
-  }
   TRY(dalloc(ctx, &ctx->fr.hub_w, hc.n_hub));
   TRY(dalloc(ctx, &ctx->fr.hub_b0, hc.n_hub));
   TRY(dalloc(ctx, &ctx->fr.hub_deg, hc.n_hub));
   TRY(dalloc(ctx, &ctx->fr.hub_chunk, hc.n_hub));
-  TRY(dalloc(ctx, &ctx->sel_part, (size_t)std::max(ctx->grid_select, ctx->grid_fused)));
-  TRY(dalloc(ctx, &ctx->sc_part, (size_t)ctx->grid_scatter));
-
-  TRY(dalloc(ctx, &ctx->l1_part, (size_t)ctx->grid_l1));
-  TRY(dalloc(ctx, &ctx->l1_out, 1));
-  TRY(dalloc(ctx, &ctx->ctl, 1));
-  ctx->log_cap = 1 << 18;  // passes logged since create/reset (di_run is resumable)
-  TRY(dalloc(ctx, &ctx->log, (size_t)ctx->log_cap));
-  tr.mark(ctx->stream, "malloc frontier etc");
-  CK(cudaHostAlloc((void **)&ctx->h_ctl, sizeof(Ctl), cudaHostAllocDefault));
-  // state: F = B, H = 0
-  ctx->b_uniform = (1.0 - ctx->d) / (double)ctx->n_rows;
-  k_init_state<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->F, ctx->H, ctx->d_b, ctx->b_uniform, n);
-  // T_0 = max |B_i| / alpha (reading R5) unless given
-  double T0 = o.t0;
-  if (!(T0 > 0.0)) {
-    double mx = 0.0;
-    if (n > 0) {
-      k_max_abs<<<ctx->grid_l1, 256, 0, ctx->stream>>>(ctx->F, n, ctx->l1_part, ctx->kw);
-      std::vector<double> hp(ctx->grid_l1);
-      CK(cudaMemcpyAsync(hp.data(), ctx->l1_part, sizeof(double) * ctx->grid_l1, cudaMemcpyDeviceToHost, ctx->stream));
-      CK(cudaStreamSynchronize(ctx->stream));
-      for (double v : hp) mx = std::max(mx, v);
-    }
-    mx = diter_dist_max(ctx, mx);   // global max over ranks (identity when not distributed)
-    T0 = mx / o.alpha;
-  }
   Ctl hc0;
   std::memset(&hc0, 0, sizeof(hc0));
   hc0.T = T0;
@@ -513,7 +548,7 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
   CK(cudaMemcpyAsync(ctx->ctl, &ctx->ctl_init, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->threshold = T0;
-  tr.mark(ctx->stream, "init F,H,T0");
+  tr.mark(ctx->stream, "init ctl");
   TRY(capture_graph(ctx));
   tr.mark(ctx->stream, "graph capture");
   return DI_OK;

@@ -802,11 +802,19 @@ __global__ void k_census(const long long *col_ptr, long long n, const int *row_i
       if (s > d * (1.0 + 1e-12)) ++bc;
     }
   }
+  // row range check: 16-byte loads, four in flight per thread (row_idx is a pool
+  // allocation, 256-byte aligned)
   unsigned long long br = 0;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += stride) {
-    const int r = row_idx[e];
-    if (r < 0 || (long long)r >= n_rows) ++br;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nv = nnz >> 2;
+  const int4 *r4 = reinterpret_cast<const int4 *>(row_idx);
+  auto bad = [n_rows](int r) -> unsigned { return (r < 0 || (long long)r >= n_rows) ? 1u : 0u; };
+#pragma unroll 4
+  for (long long v = tid; v < nv; v += stride) {
+    const int4 q = __ldcs(r4 + v);
+    br += bad(q.x) + bad(q.y) + bad(q.z) + bad(q.w);
   }
+  for (long long e = (nv << 2) + tid; e < nnz; e += stride) br += bad(row_idx[e]);
   if (bp) atomicAdd(&c->bad_ptr, bp);
   if (br) atomicAdd(&c->bad_row, br);
   if (lo) atomicAdd(&c->n_low, lo);
@@ -835,10 +843,18 @@ __global__ void k_max_abs(const double *b, long long n, double *part, const floa
 }
 
 // Hot-window census (setup): sampled in-degree per 1024-row block.
+// Sampled in-degree per 1024-row block (every stride-th edge).  Lanes of a warp
+// that sample the same block add once (match + popc): on Zipf-over-id graphs most
+// samples land in the first blocks and per-sample atomics serialised there.
 __global__ void k_hot_sample(const int *row_idx, long long nnz, int stride, unsigned *blk) {
   const long long step = (long long)gridDim.x * blockDim.x * stride;
-  for (long long e = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * stride; e < nnz; e += step)
-    atomicAdd(&blk[row_idx[e] >> 10], 1u);
+  const long long w0 = ((long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) * stride;
+  for (long long base = w0; base < nnz; base += step) {        // warp-uniform trip count
+    const long long e = base + (long long)lane_id() * stride;
+    const int b = e < nnz ? (row_idx[e] >> 10) : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, b);
+    if (b >= 0 && (int)lane_id() == __ffs(peers) - 1) atomicAdd(&blk[b], (unsigned)__popc(peers));
+  }
 }
 
 // Far-push bin capacities (setup): per bin, the edges whose row can be far --

@@ -14,7 +14,7 @@ pol, alpha, frac, key = bench.SCHEDULES[cfg]
 o = di.default_options(policy=pol, alpha=alpha, hybrid_frac=frac, select_key=key)
 pin = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in (p.col_ptr, p.row_idx)]
 H = torch.empty(p.n, dtype=torch.float64).pin_memory()
-for rep in range(4):
+for rep in range(int(os.environ.get("REPS", "4"))):
     t = [time.perf_counter()]
     ctx = di.di_create(p.n, pin[0], pin[1], None, None, p.d, o)
     torch.cuda.synchronize(); t.append(time.perf_counter())
