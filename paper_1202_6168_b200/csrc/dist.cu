@@ -1259,7 +1259,6 @@ extern "C" di_status di_rebalance(di_ctx *ctx, const int64_t *nb) {
   Ctl c2 = c;
   c2.n_total = nc->ctl_init.n_total;
   c2.hub_packed = 0ull;
-  c2.sc_next = 0u;
   std::memset(c2.tickets, 0, sizeof(c2.tickets));
   std::memset(c2.far_cnt, 0, sizeof(c2.far_cnt));
   CKD(cudaMemcpyAsync(nc->ctl, &c2, sizeof(Ctl), cudaMemcpyHostToDevice, nc->stream));

@@ -270,6 +270,17 @@ static di_status setup_far(di_ctx *ctx) {
   ctx->far.warm_len = (unsigned)W;
   ctx->far.shift = shift;
   ctx->far.n_bins = n_bins;
+  {
+    // the far scatter stages records in 24 KB more shared memory per CTA: static +
+    // dynamic then exceed the default 48 KB, which needs the opt-in
+    const int dyn = (int)ctx->scatter_smem;
+    CK(cudaFuncSetAttribute(k_scatter<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    CK(cudaFuncSetAttribute(k_scatter<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    int occ = 0;
+    if (ctx->vals) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scatter<true, false, true>, kScatterThreads, ctx->scatter_smem));
+    else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scatter<false, false, true>, kScatterThreads, ctx->scatter_smem));
+    ctx->grid_scatter = std::min(ctx->grid_scatter, ctx->num_sms * std::max(1, occ));
+  }
   unsigned long long *d_cap = nullptr;
   TRY(dalloc(ctx, &d_cap, (size_t)kMaxBins));
   CK(cudaMemsetAsync(d_cap, 0, sizeof(unsigned long long) * kMaxBins, ctx->stream));
@@ -352,9 +363,11 @@ static di_status capture_graph(di_ctx *ctx) {
                                                                   ctx->ctl, ctx->sel_part, ctx->kw);
     if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 1], ctx->stream, cudaEventRecordExternal));
     if (ctx->vals)
-      k_scatter<true><<<ctx->grid_scatter, kScatterThreads, ctx->scatter_smem, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part);
+      (ctx->far.on ? k_scatter<true, false, true> : k_scatter<true, false, false>)
+          <<<ctx->grid_scatter, kScatterThreads, ctx->scatter_smem, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part);
     else
-      k_scatter<false><<<ctx->grid_scatter, kScatterThreads, ctx->scatter_smem, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part);
+      (ctx->far.on ? k_scatter<false, false, true> : k_scatter<false, false, false>)
+          <<<ctx->grid_scatter, kScatterThreads, ctx->scatter_smem, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part);
     if (ctx->cap_hub > 0) {
       if (ctx->vals)
         k_scatter_hubs<true><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);

@@ -29,7 +29,6 @@ namespace diter {
 namespace {
 
 __device__ __forceinline__ void reset_tickets(Ctl *ctl) {
-  ctl->sc_next = 0u;
 #pragma unroll
   for (int k = 0; k < kStripes; ++k) ctl->tickets[32 * k] = 0u;
 #pragma unroll 8
@@ -268,9 +267,31 @@ __device__ __forceinline__ void close_far(const Far &far, const int *st) {
 // shuffle binary search over the exclusive degree prefix.  [nlo, nhi] is the
 // group's near window (its columns +- kNear): with far pushes on, a push outside
 // it, the hot window and the warm range becomes a far record.
-template <bool SIGNED>
+// Far records are staged per warp in shared memory (a ballot and a store per push
+// round) and binned only when the stage fills (flush_stage), so the match/aggregate
+// work of emit_far runs once per 32 records instead of once per round with any far
+// lane.
+constexpr int kStage = 256;
+struct Stage {
+  int *row;      // this warp's kStage staged rows (shared memory)
+  double *val;
+  int cnt;       // warp-uniform fill
+};
+
+__device__ __noinline__ void flush_stage(const Far far, Ctl *ctl, const Sink s, int *st, const int *srow,
+                                         const double *sval, int cnt) {
+  __syncwarp();
+  for (int k = 0; k < cnt; k += 32) {
+    const int i = k + (int)lane_id();
+    const bool ok = i < cnt;
+    emit_far(far, ctl, s, st, ok, ok ? srow[i] : 0, ok ? sval[i] : 0.0);
+  }
+  __syncwarp();
+}
+
+template <bool SIGNED, bool FAR = false>
 __device__ __forceinline__ void push_group(const Graph &g, const Sink &s, Ctl *ctl, int *st, long long b0, int deg,
-                                           double w, int nlo, int nhi) {
+                                           double w, int nlo, int nhi, Stage &sg) {
   const unsigned lane = lane_id();
   int incl = deg;
 #pragma unroll
@@ -300,7 +321,7 @@ __device__ __forceinline__ void push_group(const Graph &g, const Sink &s, Ctl *c
       rows[u] = ok ? ld_row(g.row_idx + ei) : -1;
       vals[u] = ok ? (SIGNED ? ow * ld_val(g.vals + ei) : ow) : 0.0;
     }
-    if (!g.far.on) {
+    if constexpr (!FAR) {
 #pragma unroll
       for (int u = 0; u < kGroupUnroll; ++u)
         if (rows[u] >= 0) push(s, rows[u], vals[u]);
@@ -311,7 +332,17 @@ __device__ __forceinline__ void push_group(const Graph &g, const Sink &s, Ctl *c
         const bool is_far = row >= 0 && (unsigned)(row - s.hot_lo) >= (unsigned)kHot &&
                             (unsigned)(row - g.far.warm_lo) >= g.far.warm_len && (row < nlo || row > nhi);
         if (row >= 0 && !is_far) push(s, row, vals[u]);
-        if (__any_sync(0xffffffffu, is_far)) emit_far(g.far, ctl, s, st, is_far, row, vals[u]);
+        const unsigned m = __ballot_sync(0xffffffffu, is_far);
+        if (is_far) {
+          const int p = sg.cnt + __popc(m & ((1u << lane) - 1u));
+          sg.row[p] = row;
+          sg.val[p] = vals[u];
+        }
+        sg.cnt += __popc(m);
+      }
+      if (sg.cnt > kStage - 32 * kGroupUnroll) {
+        flush_stage(g.far, ctl, s, st, sg.row, sg.val, sg.cnt);
+        sg.cnt = 0;
       }
     }
   }
@@ -387,9 +418,9 @@ __device__ __forceinline__ int find_segment(const int *s_goff, int n_seg, int q)
   return lo;
 }
 
-template <bool SIGNED, bool DIST>
+template <bool SIGNED, bool DIST, bool FAR>
 __device__ __forceinline__ void scatter_group(const Graph &g, const Sink &s, const Frontier &fr, Ctl *ctl,
-                                              const int *s_goff, int *st, int q, int &seg, ScAcc &acc) {
+                                              const int *s_goff, int *st, int q, int &seg, ScAcc &acc, Stage &sg) {
   // a warp's groups mostly ascend within one segment: walk forward from the
   // last segment, search only after a jump
   if (q < s_goff[seg] || q >= s_goff[seg + 4 < fr.n_seg ? seg + 4 : fr.n_seg]) seg = find_segment(s_goff, fr.n_seg, q);
@@ -441,12 +472,19 @@ __device__ __forceinline__ void scatter_group(const Graph &g, const Sink &s, con
   const int n_here = min(32, cnt - 32 * (q - s_goff[lo]));
   const int i_first = __shfl_sync(0xffffffffu, i, 0) + (int)g.lo;
   const int i_last = __shfl_sync(0xffffffffu, i, n_here - 1) + (int)g.lo;
-  push_group<SIGNED>(g, s, ctl, st, b0, deg_eff, w, i_first - kNear, i_last + kNear);
+  push_group<SIGNED, FAR>(g, s, ctl, st, b0, deg_eff, w, i_first - kNear, i_last + kNear, sg);
 }
 
-template <bool SIGNED, bool DIST>
+template <bool SIGNED, bool DIST, bool FAR = false>
 __device__ __forceinline__ void scatter_body(const Graph &g, double *__restrict__ F, const Frontier &fr, Ctl *ctl,
                                              ScPartial *__restrict__ part, double *s_hot, int *s_goff) {
+  Stage sg{nullptr, nullptr, 0};
+  if constexpr (FAR) {
+    __shared__ int s_srow[kScatterThreads / 32][kStage];
+    __shared__ double s_sval[kScatterThreads / 32][kStage];
+    sg.row = s_srow[threadIdx.x >> 5];
+    sg.val = s_sval[threadIdx.x >> 5];
+  }
   for (int t = threadIdx.x; t < kHot; t += blockDim.x) s_hot[t] = 0.0;
   __shared__ int s_far[kScatterThreads / 32][2 * kMaxBins];     // per-warp open far chunks
   int *st = s_far[threadIdx.x >> 5];
@@ -460,9 +498,8 @@ __device__ __forceinline__ void scatter_body(const Graph &g, double *__restrict_
   constexpr int kW = kScatterThreads / 32;
   const int nwarps = gridDim.x * kW;
   const int warp = threadIdx.x >> 5;
-  const int q_static = 0;
   int seg = 0;
-  const int rest = total - q_static;
+  const int rest = total;
   // Dynamic: each warp grabs runs of consecutive groups in ascending order (one
   // atomic per run, no block barrier).  The grid's working set stays a narrow
   // window of consecutive columns, so the +-1000-local pushes of neighbouring
@@ -473,8 +510,8 @@ __device__ __forceinline__ void scatter_body(const Graph &g, double *__restrict_
   const int ns = fr.stripes;
   for (int k = 0; k < ns; ++k) {
     const int sp = (gw + k) % ns;
-    const int s0 = q_static + (int)((long long)rest * sp / ns);
-    const int s1 = q_static + (int)((long long)rest * (sp + 1) / ns);
+    const int s0 = (int)((long long)rest * sp / ns);
+    const int s1 = (int)((long long)rest * (sp + 1) / ns);
     for (;;) {
       // a stripe one warp of the CTA found exhausted is skipped by the others
       // without a claim: at the end of a pass every warp would otherwise fail one
@@ -487,10 +524,13 @@ __device__ __forceinline__ void scatter_body(const Graph &g, double *__restrict_
         break;
       }
       const int q1 = min(s1, s0 + (int)q0 + run);
-      for (int q = s0 + (int)q0; q < q1; ++q) scatter_group<SIGNED, DIST>(g, s, fr, ctl, s_goff, st, q, seg, acc);
+      for (int q = s0 + (int)q0; q < q1; ++q) scatter_group<SIGNED, DIST, FAR>(g, s, fr, ctl, s_goff, st, q, seg, acc, sg);
     }
   }
-  if (g.far.on) close_far(g.far, st);
+  if constexpr (FAR) {
+    if (sg.cnt > 0) flush_stage(g.far, ctl, s, st, sg.row, sg.val, sg.cnt);
+    close_far(g.far, st);
+  }
   // flush the hot window: one RED per touched row per CTA
   __syncthreads();
   for (int t = threadIdx.x; t < kHot; t += blockDim.x) {
@@ -522,13 +562,13 @@ __device__ __forceinline__ void scatter_body(const Graph &g, double *__restrict_
 }
 
 // dynamic shared memory: the group prefix s_goff[n_seg + 1]
-template <bool SIGNED, bool DIST = false>
-__global__ void __launch_bounds__(kScatterThreads, kScatterMinBlocks)
+template <bool SIGNED, bool DIST = false, bool FAR = false>
+__global__ void __launch_bounds__(kScatterThreads, FAR ? 3 : kScatterMinBlocks)
 k_scatter(Graph g, double *__restrict__ F, Frontier fr, Ctl *ctl, ScPartial *__restrict__ part) {
   if (ctl->done) return;
   __shared__ double s_hot[kHot];
   extern __shared__ int s_goff[];
-  scatter_body<SIGNED, DIST>(g, F, fr, ctl, part, s_hot, s_goff);
+  scatter_body<SIGNED, DIST, FAR>(g, F, fr, ctl, part, s_hot, s_goff);
 }
 
 // Hub columns (> kMidMax edges), one CTA per 2048-edge chunk (chunks of a hub

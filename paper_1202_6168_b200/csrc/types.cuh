@@ -54,13 +54,12 @@ struct Ctl {
   int policy;          // DI_POLICY_*
   unsigned long long hub_packed;  // (hub slots << 32) | hub chunks; reset by k_finalize
   long long log_cap;
-  unsigned sc_next;    // next frontier group of the scatter's dynamic tail (reset per pass)
   int _pad;
   unsigned long long remote_pushes;   // distributed: pushes into the outbox (one atomic per CTA per pass)
   double t_sel_us;     // fused kernel: accumulated select / scatter phase time (%globaltimer)
   double t_sc_us;
   // scatter tickets: one counter per stripe of the frontier groups, each on its
-  // own 128-byte line (reset per pass with sc_next)
+  // own 128-byte line (reset per pass)
   alignas(128) unsigned tickets[kStripes * 32];
   // far-push chunks opened per destination bin this pass, one counter per 128-byte line
   alignas(128) unsigned far_cnt[kMaxBins * 32];

@@ -423,3 +423,16 @@ def test_set_profile_same_solve_and_kernel_times():
     for k in (1, 2):
         assert np.abs(out[k][0] - out[0][0]).sum() <= 1e-12 * out[0][0].sum()
         assert abs(out[k][1]["passes"] - out[0][1]["passes"]) <= 1
+
+
+def test_far_push_large_segment_prefix():
+    """Far-push bins on a 4e6-node web-like graph: the staged far scatter's static (45 KB)
+    plus dynamic (segment prefix, ~9.5 KB) shared memory exceeds the default 48 KB and
+    runs on the opt-in.  Same solution as the plain scatter, exact identity F = B - (I-P)H."""
+    p = gen.config("C2", 3, n=4_000_000)
+    H0, F0, _, r0, s0 = _gpu(p.n, p.col_ptr, p.row_idx, p.stop)
+    H1, F1, _, r1, s1 = _gpu(p.n, p.col_ptr, p.row_idx, p.stop, far_push=1, far_warm_log2=16)
+    bn = 0.15                                      # |B|_1 = (1 - d)
+    _check_state(p.n, p.col_ptr, p.row_idx, None, None, 0.85, H1, F1, r1, p.stop)
+    assert np.abs(H1 - H0).sum() <= 2 * p.stop / 0.15 + 1e-12 * bn
+    assert abs(s1["passes"] - s0["passes"]) <= 1
