@@ -210,7 +210,10 @@ __device__ __forceinline__ void push_range(const Graph &g, const Sink &s, long l
   if (e < end) push(s, ld_row(g.row_idx + e), SIGNED ? w * ld_val(g.vals + e) : w);
 }
 
-constexpr int kGroupUnroll = 4;
+#ifndef DITER_GROUP_UNROLL
+#define DITER_GROUP_UNROLL 7
+#endif
+constexpr int kGroupUnroll = DITER_GROUP_UNROLL;
 
 // Far push (see Far in types.cuh).  Lanes with the same bin are aggregated by
 // __match_any_sync; the lowest lane of each bin group appends the group to this

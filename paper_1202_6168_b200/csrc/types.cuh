@@ -26,7 +26,7 @@ constexpr int kSelectItems = DITER_SELECT_ITEMS;     // 32-node words per warp i
 constexpr int kSelectSpan = 32 * kSelectItems;       // nodes per warp iteration (segment granule)
 constexpr int kScatterThreads = 256;
 #ifndef DITER_SCATTER_MIN_BLOCKS
-#define DITER_SCATTER_MIN_BLOCKS 1
+#define DITER_SCATTER_MIN_BLOCKS 3
 #endif
 constexpr int kScatterMinBlocks = DITER_SCATTER_MIN_BLOCKS;   // __launch_bounds__ min CTAs/SM of k_scatter
 constexpr int kFinalizeThreads = 512;
