@@ -196,6 +196,9 @@ static di_status setup_geometry(di_ctx *ctx) {
   if (ctx->vals) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sc, k_scatter<true>, kScatterThreads, ctx->scatter_smem));
   else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sc, k_scatter<false>, kScatterThreads, ctx->scatter_smem));
   ctx->grid_scatter = ctx->fused ? ctx->grid_fused : ctx->num_sms * std::max(1, occ_sc);
+  // a frontier holds at most n / 32 groups: more than one CTA (8 warps) per 256 nodes
+  // would only zero and flush hot windows (C1: 4 CTAs instead of 444)
+  if (!ctx->fused) ctx->grid_scatter = (int)std::max(1LL, std::min<long long>(ctx->grid_scatter, (n + 255) / 256));
   ctx->grid_l1 = (int)std::min<long long>(ctx->num_sms * 8LL, std::max(1LL, (n + 255) / 256));
   return DI_OK;
 }
