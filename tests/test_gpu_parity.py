@@ -420,8 +420,10 @@ def test_set_profile_same_solve_and_kernel_times():
         else:
             assert s["kt_scatter_ms"] == 0
     di.di_destroy(ctx)
+    # two stopped solves agree to the sum of their bounds r/(1-d), not better:
+    # the RED order moves ties at a threshold and with them the stopping state
     for k in (1, 2):
-        assert np.abs(out[k][0] - out[0][0]).sum() <= 1e-12 * out[0][0].sum()
+        assert np.abs(out[k][0] - out[0][0]).sum() <= 2 * p.stop / 0.15
         assert abs(out[k][1]["passes"] - out[0][1]["passes"]) <= 1
 
 
