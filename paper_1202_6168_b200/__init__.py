@@ -58,7 +58,7 @@ class di_options(ctypes.Structure):
                 ("far_push", ctypes.c_int32), ("far_warm_log2", ctypes.c_int32),
                 ("select_key", ctypes.c_int32), ("remote_push", ctypes.c_int32),
                 ("receive_rescale", ctypes.c_int32), ("adapt_rounds", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 4)]
+                ("l2_persist", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
 
 
 class di_pass_log(ctypes.Structure):

@@ -42,6 +42,7 @@ struct di_ctx {
   diter::Far far{};               // far-push bins (propagation blocking), 1 GPU
   long long *far_off = nullptr;   // [n_bins + 1] first chunk of each bin (device)
   long long far_cap = 0;          // total chunks
+  long long l2_lo = 0, l2_bytes = 0;   // L2 persisting window over F (rows from l2_lo), 0 = none
   std::vector<unsigned> blk_hist; // sampled in-degree per 1024-row block (setup)
   int blk_stride = 1;
   unsigned long long cap_low = 0, cap_mid = 0, cap_hub = 0;
@@ -87,6 +88,8 @@ diter::Graph diter_graph(const di_ctx *ctx);
 
 // distributed hooks (dist.cu); identities / no-ops on single-GPU contexts
 void diter_dist_free(di_ctx *ctx);
+// the context's L2 persisting window (options.l2_persist) as its stream's access policy
+di_status diter_set_l2_window(di_ctx *ctx);
 // context device memory (per-device stream-ordered pool, ordered on ctx->stream)
 di_status diter_alloc(di_ctx *ctx, void **p, size_t bytes);
 void diter_free(di_ctx *ctx, void *p);

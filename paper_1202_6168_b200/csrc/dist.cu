@@ -1277,6 +1277,7 @@ extern "C" di_status di_rebalance(di_ctx *ctx, const int64_t *nb) {
   nc->ev1 = ctx->ev1;
   ctx->stream = nullptr;
   ctx->ev0 = ctx->ev1 = nullptr;
+  (void)diter_set_l2_window(nc);   // a cache hint: the stream now serves the rebuilt context's F
   nc->passes_done = ctx->passes_done;
   nc->edges = ctx->edges;
   nc->nodes = ctx->nodes;

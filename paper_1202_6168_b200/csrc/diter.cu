@@ -121,6 +121,8 @@ static di_status dalloc(di_ctx *ctx, T **p, size_t count) {
     if (s_ != DI_OK) return s_;     \
   } while (0)
 
+static void l2_release(di_ctx *ctx);
+
 static void free_ctx(di_ctx *c) {
   if (!c) return;
   const bool tr = std::getenv("DITER_TRACE") != nullptr;
@@ -132,6 +134,7 @@ static void free_ctx(di_ctx *c) {
     t = n;
   };
   if (c->device >= 0) cudaSetDevice(c->device);
+  l2_release(c);
   if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
   mark("graph exec");
   for (cudaEvent_t e : c->prof_ev)
@@ -240,6 +243,96 @@ static di_status choose_hot_window(di_ctx *ctx) {
     if (m > best_mass) { best_mass = m; best = b; }
   }
   ctx->hot_lo = (int)std::max<long long>(ctx->lo, std::min<long long>(best << 10, hi - kHot));
+  return DI_OK;
+}
+
+// L2 persisting window (options.l2_persist): the set-aside is a device-wide limit,
+// taken by the first context that wants a window and released (with the persisting
+// lines) when the last one is destroyed.
+static std::mutex g_l2_mu;
+static std::vector<int> g_l2_users;
+
+static di_status l2_acquire(di_ctx *ctx, size_t bytes) {
+  std::lock_guard<std::mutex> g(g_l2_mu);
+  if ((int)g_l2_users.size() <= ctx->device) g_l2_users.resize(ctx->device + 1, 0);
+  int maxp = 0;
+  CK(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, ctx->device));
+  size_t cur = 0;
+  CK(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+  const size_t want = std::min(bytes, (size_t)maxp);
+  if (want > cur) CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+  ++g_l2_users[ctx->device];
+  return DI_OK;
+}
+
+static void l2_release(di_ctx *ctx) {
+  if (ctx->l2_bytes == 0) return;
+  std::lock_guard<std::mutex> g(g_l2_mu);
+  if (ctx->device < (int)g_l2_users.size() && --g_l2_users[ctx->device] == 0) {
+    cudaCtxResetPersistingL2Cache();
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+  }
+  ctx->l2_bytes = 0;
+}
+
+// Window rows: the 1024-row-aligned range of the window size with the most sampled
+// pushes among the owned rows.  Auto: off while F fits in 64 MB (it stays L2-resident
+// anyway); else 28 MB when F is at most 2x the L2 and 20 MB above that.  Measured on
+// this B200 (126 MB L2): C3 (F 134 MB, permuted R-MAT -- no hot rows, the window just
+// keeps part of an oversized working set from thrashing) 219 -> 184 ms at 28-30 MB;
+// C4 (F 800 MB, the Zipf-over-id head: 26 % of the pushes in the first 20 MB) 265 ->
+// 250 ms at 20 MB.  Larger set-asides slow the select's streaming (C4 24 MB: +6 ms,
+// C3 >= 32 MB: +5 ms) and 79 MB (the maximum) loses outright.
+static di_status choose_l2_window(di_ctx *ctx) {
+  ctx->l2_lo = 0;
+  ctx->l2_bytes = 0;
+  const int opt = ctx->opt.l2_persist;
+  const long long n = ctx->n_local;
+  if (opt < 0 || ctx->blk_hist.empty() || n == 0) return DI_OK;
+  const long long f_bytes = n * (long long)sizeof(double);
+  if (opt == 0 && f_bytes <= (64LL << 20)) return DI_OK;
+  int l2 = 0;
+  CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device));
+  const long long auto_mb = f_bytes <= 2LL * l2 ? 28 : 20;
+  const long long want_rows = ((opt > 0 ? (long long)opt : auto_mb) << 20) / (long long)sizeof(double);
+  const std::vector<unsigned> &h = ctx->blk_hist;
+  const long long b_lo = ctx->lo >> 10, b_hi = std::min<long long>((long long)h.size(), (ctx->lo + n + 1023) >> 10);
+  const long long wb = std::max(1LL, std::min(want_rows >> 10, b_hi - b_lo));
+  long long tot = 0, win = 0, best = -1, best_b = b_lo;
+  for (long long b = b_lo; b < b_hi; ++b) tot += h[b];
+  for (long long b = b_lo; b < b_hi; ++b) {
+    win += h[b];
+    if (b - b_lo >= wb) win -= h[b - wb];
+    if (b - b_lo + 1 >= wb && win > best) { best = win; best_b = b - wb + 1; }
+  }
+  const long long row0 = std::max(ctx->lo, best_b << 10) - ctx->lo;             // local row
+  const long long rows = std::min(wb << 10, n - row0);
+  if (rows <= 0) return DI_OK;
+  int max_win = 0;
+  CK(cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device));
+  const size_t bytes = std::min((size_t)rows * sizeof(double), (size_t)max_win);
+  TRY(l2_acquire(ctx, bytes));
+  ctx->l2_lo = row0;
+  ctx->l2_bytes = (long long)bytes;
+  if (std::getenv("DITER_TRACE"))
+    std::fprintf(stderr, "[diter setup] L2 window rows [%lld, %lld) %.1f MB, %.1f%% of sampled pushes\n", ctx->lo + row0,
+                 ctx->lo + row0 + rows, bytes / 1048576.0, tot ? 100.0 * (double)best / (double)tot : 0.0);
+  return diter_set_l2_window(ctx);
+}
+
+// The window as the stream's access policy (kernels launched or captured on it
+// afterwards carry it); cleared when the context has none.
+di_status diter_set_l2_window(di_ctx *ctx) {
+  if (!ctx->stream) return DI_OK;
+  cudaStreamAttrValue av = {};
+  if (ctx->l2_bytes > 0) {
+    av.accessPolicyWindow.base_ptr = ctx->F + ctx->l2_lo;
+    av.accessPolicyWindow.num_bytes = (size_t)ctx->l2_bytes;
+    av.accessPolicyWindow.hitRatio = 1.0f;
+    av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  }
+  CK(cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &av));
   return DI_OK;
 }
 
@@ -537,7 +630,8 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
     return DI_ERR_CONTRACTION;
   }
   TRY(choose_hot_window(ctx));
-  tr.mark(ctx->stream, "hot window");
+  TRY(choose_l2_window(ctx));
+  tr.mark(ctx->stream, "hot window + L2 window");
   TRY(setup_far(ctx));
   if (!key_early) TRY(setup_key(ctx));
   if (!key_early) TRY(initial_threshold(ctx, &T0));

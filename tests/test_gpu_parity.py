@@ -438,3 +438,15 @@ def test_far_push_large_segment_prefix():
     _check_state(p.n, p.col_ptr, p.row_idx, None, None, 0.85, H1, F1, r1, p.stop)
     assert np.abs(H1 - H0).sum() <= 2 * p.stop / 0.15 + 1e-12 * bn
     assert abs(s1["passes"] - s0["passes"]) <= 1
+
+
+@pytest.mark.parametrize("mb", [4, 64])
+def test_l2_persist_window_forced(mb):
+    """options.l2_persist > 0 forces a persisting L2 window over F's most-pushed rows (a
+    cache hint only): the solve is unchanged -- exact identity, same passes as without."""
+    p = gen.config("C2", 2)
+    H0, F0, _, r0, s0 = _gpu(p.n, p.col_ptr, p.row_idx, p.stop, l2_persist=-1)
+    H1, F1, _, r1, s1 = _gpu(p.n, p.col_ptr, p.row_idx, p.stop, l2_persist=mb)
+    _check_state(p.n, p.col_ptr, p.row_idx, None, None, 0.85, H1, F1, r1, p.stop)
+    assert np.abs(H1 - H0).sum() <= 2 * p.stop / 0.15
+    assert abs(s1["passes"] - s0["passes"]) <= 1
