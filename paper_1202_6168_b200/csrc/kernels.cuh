@@ -433,14 +433,16 @@ __device__ __forceinline__ void scatter_group(const Graph &g, const Sink &s, con
   const long long e = (long long)lo * fr.seg_len + k;
   // independent loads issued together (entries past the count are never used)
   const int cnt = fr.seg_cnt[lo];
-  const int i = fr.ids[e];
-  const double sv = fr.S[e];
+  // read-once-per-pass data (the entry, its col_ptr pair): evict-first loads, so they do
+  // not displace F lines in L2 (C3 -0.7 %, neutral on C2/C4)
+  const int i = __ldcs(fr.ids + e);
+  const double sv = __ldcs(fr.S + e);
   long long b0 = 0;
   int deg_eff = 0;
   double w = 0.0;
   if (k < cnt) {
-    b0 = __ldg(g.col_ptr + i);
-    const long long deg = __ldg(g.col_ptr + i + 1) - b0;
+    b0 = __ldcs(g.col_ptr + i);
+    const long long deg = __ldcs(g.col_ptr + i + 1) - b0;
     const double asv = fabs(sv);
     acc.loss += (deg > 0) ? (1.0 - g.d) * asv : asv;
     acc.edges += deg;
