@@ -288,14 +288,16 @@ static di_status choose_l2_window(di_ctx *ctx) {
   ctx->l2_bytes = 0;
   const int opt = ctx->opt.l2_persist;
   const long long n = ctx->n_local;
-  if (opt < 0 || ctx->blk_hist.empty() || n == 0) return DI_OK;
+  if (opt < 0 || n == 0 || (opt == 0 && ctx->blk_hist.empty())) return DI_OK;
   const long long f_bytes = n * (long long)sizeof(double);
   if (opt == 0 && f_bytes <= (64LL << 20)) return DI_OK;
   int l2 = 0;
   CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device));
   const long long auto_mb = f_bytes <= 2LL * l2 ? 28 : 20;
   const long long want_rows = ((opt > 0 ? (long long)opt : auto_mb) << 20) / (long long)sizeof(double);
-  const std::vector<unsigned> &h = ctx->blk_hist;
+  // no in-degree sample (hot window off): a forced window starts at the owned range
+  const std::vector<unsigned> h = ctx->blk_hist.empty() ? std::vector<unsigned>((size_t)((ctx->lo + n + 1023) >> 10), 0u)
+                                                        : ctx->blk_hist;
   const long long b_lo = ctx->lo >> 10, b_hi = std::min<long long>((long long)h.size(), (ctx->lo + n + 1023) >> 10);
   const long long wb = std::max(1LL, std::min(want_rows >> 10, b_hi - b_lo));
   long long tot = 0, win = 0, best = -1, best_b = b_lo;

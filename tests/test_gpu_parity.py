@@ -440,13 +440,15 @@ def test_far_push_large_segment_prefix():
     assert abs(s1["passes"] - s0["passes"]) <= 1
 
 
-@pytest.mark.parametrize("mb", [4, 64])
-def test_l2_persist_window_forced(mb):
+@pytest.mark.parametrize("opts", [{"l2_persist": 4}, {"l2_persist": 64}, {"l2_persist": 8, "hot_window": -1}])
+def test_l2_persist_window_forced(opts):
     """options.l2_persist > 0 forces a persisting L2 window over F's most-pushed rows (a
-    cache hint only): the solve is unchanged -- exact identity, same passes as without."""
+    cache hint only; without the in-degree sample -- hot window off -- it starts at row
+    0): the solve is unchanged -- exact identity, same passes as without."""
     p = gen.config("C2", 2)
-    H0, F0, _, r0, s0 = _gpu(p.n, p.col_ptr, p.row_idx, p.stop, l2_persist=-1)
-    H1, F1, _, r1, s1 = _gpu(p.n, p.col_ptr, p.row_idx, p.stop, l2_persist=mb)
+    H0, F0, _, r0, s0 = _gpu(p.n, p.col_ptr, p.row_idx, p.stop, l2_persist=-1,
+                             hot_window=opts.get("hot_window", 0))
+    H1, F1, _, r1, s1 = _gpu(p.n, p.col_ptr, p.row_idx, p.stop, **opts)
     _check_state(p.n, p.col_ptr, p.row_idx, None, None, 0.85, H1, F1, r1, p.stop)
     assert np.abs(H1 - H0).sum() <= 2 * p.stop / 0.15
     assert abs(s1["passes"] - s0["passes"]) <= 1
