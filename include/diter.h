@@ -179,6 +179,8 @@ typedef struct {
                               DI_REMOTE_INCREMENT; the receiver's in-edge adds with
                               DI_REMOTE_RECEIVER) */
   int64_t rebalances;      /* distributed: ownership changes (di_rebalance / adapt_rounds) */
+  int64_t l2_window_bytes; /* L2 persisting window over F chosen at create (options.l2_persist), 0 = none */
+  int64_t l2_window_row;   /* its first row (global id) */
 } di_stats;
 
 /* Fill *opt with the defaults above. */

@@ -920,6 +920,8 @@ extern "C" di_status di_get_stats(const di_ctx *ctx, di_stats *s) {
   s->scatter_bytes = (ctx->vals ? 28LL : 20LL) * ctx->edges + 16LL * ctx->nodes;
   s->remote_pushes = ctx->remote_pushes;
   s->rebalances = ctx->rebalances;
+  s->l2_window_bytes = ctx->l2_bytes;
+  s->l2_window_row = ctx->l2_bytes > 0 ? ctx->lo + ctx->l2_lo : 0;
   return DI_OK;
 }
 
