@@ -125,11 +125,8 @@ def load_library() -> ctypes.CDLL:
         "di_csc_from_coo": (st, [i64, i64, vp, vp, vp, vp, ctypes.POINTER(i64)]),
         "di_partition_cb": (st, [i64, vp, i32, vp]),
     }
-    partial = bool(os.environ.get("DITER_LIB_PARTIAL"))   # experiments: an older build of the library
     for name, (res, args) in sig.items():
-        if partial and not hasattr(lib, name):
-            continue
-        fn = getattr(lib, name)
+        fn = getattr(lib, name)           # a library missing a declared entry point fails here
         fn.restype = res
         fn.argtypes = args
     _lib = lib
