@@ -62,6 +62,12 @@ SCHEDULES = {
 }
 
 
+# Frontier groups per dynamic grab of the scatter (options.scatter_run; library default
+# 2): longer runs keep C4's +-1000-local pushes in L2 (248.7 vs 250.1 ms), single groups
+# balance C3's permuted R-MAT better (181.3 vs 183.3 ms); GPU-side only.
+SCATTER_RUN = {"C3": 1, "C4": 3}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -136,6 +142,7 @@ def bench_config(args, p, pol, world, resident, flushed):
             "stop": p.stop, "policy": "geom" if pol == 0 else "hybrid", "seed": args.seed,
             "alpha": args.alpha, "hybrid_frac": args.hybrid_frac,
             "select_key": ["raw", "per-edge", "paper"][args.key],
+            "scatter_run": SCATTER_RUN.get(args.config, 2),
             "parallelism": par,
             "l2": ("flushed between steps (252 MB write)" if flushed else
                    f"inputs ({resident / 1e9:.1f} GB resident per GPU) larger than L2 (126 MB)")}
@@ -350,7 +357,8 @@ def run_ours(args, rank, world, local_rank):
     # DESIGN.md §6 "Multi-GPU" has the loopback measurements behind these choices
     dist_kw = dict(check_interval=args.round_passes, remote_push=args.remote_push) if world > 1 else {}
     opts = di.default_options(policy=pol, device=local_rank, profile=0, exchange_mode=mode,
-                              alpha=args.alpha, hybrid_frac=args.hybrid_frac, select_key=args.key, **dist_kw)
+                              alpha=args.alpha, hybrid_frac=args.hybrid_frac, select_key=args.key,
+                              scatter_run=SCATTER_RUN.get(args.config, 0), **dist_kw)
     comm_id, bounds, shard = None, None, None
     if dist:
         bounds = dd.partition_bounds(p.col_ptr, world, cost=args.partition, row_idx=p.row_idx)
