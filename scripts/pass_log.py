@@ -17,7 +17,8 @@ pol, alpha, frac, key = bench.SCHEDULES[a.config]
 
 def solve(profile):
     o = di.default_options(profile=profile, pass_kernel=a.pass_kernel, hot_window=a.hot, policy=pol,
-                           alpha=alpha, hybrid_frac=frac, select_key=key)
+                           alpha=alpha, hybrid_frac=frac, select_key=key,
+                           scatter_run=bench.SCATTER_RUN.get(a.config, 0))
     ctx = di.di_create(p.n, p.col_ptr, p.row_idx, p.values, p.b, p.d, o)
     for _ in range(3):
         di.di_reset(ctx); di.di_run(ctx, p.stop)
