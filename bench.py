@@ -95,8 +95,10 @@ def parse():
     ap.add_argument("--round-passes", type=int, default=4, help="N > 1, ASYNC: local passes per exchange round")
     ap.add_argument("--remote-push", type=int, default=1, choices=[0, 1],
                     help="N > 1: 0 per diffusion, 1 H increments at rounds (NEXT f2)")
-    ap.add_argument("--partition", default="inout", choices=["out", "inout"],
-                    help="edge-balanced contiguous ranges by out-edges or in+out edges")
+    ap.add_argument("--partition", default="out", choices=["out", "inout"],
+                    help="edge-balanced contiguous ranges by out-edges (default: with remote edges "
+                         "pushed by the senders as H increments, receiving is a cheap merge; "
+                         "scripts/exp_scaling_model.py) or by in+out edges")
     return ap.parse_args()
 
 

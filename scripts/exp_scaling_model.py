@@ -1,0 +1,84 @@
+"""Multi-GPU model from K loopback ranks on ONE GPU (experiment; no multi-GPU box here).
+
+Runs the bench's N > 1 configuration (ASYNC, rounds every 4 passes, remote edges as H
+increments, in+out-balanced ranges, the config's schedule) as K in-process ranks on one
+GPU and records what each rank would do on its own GPU: passes, scanned nodes, edges,
+remote pushes, exchange rounds and bytes.  The ranks share the GPU here, so their times
+mean nothing; the work split and the traffic do.  Model of the K-GPU time:
+
+    T_K = T_1 * max_k [ s * (passes_k n_k) / (passes_1 N) + (1 - s) * (E_k + R_k) / E_1 ]
+          + rounds * (max_k bytes_k per round / B_link + t_round)
+
+with T_1, s (select share) and E_1 from the 1-GPU bench line, B_link = 450 GB/s (half the
+900 GB/s per direction of NVLink 5 through NVSwitch, for an all-to-all-v) and t_round =
+40 us (a grouped ncclSend/Recv, two all-reduces and the host sync of a round).
+
+    python scripts/exp_scaling_model.py C4 248.7 0.224 2.6595e10 [out|inout]
+"""
+import json, os, sys, threading, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import diter_inputs as gen
+import paper_1202_6168_b200 as di
+from paper_1202_6168_b200 import dist
+import bench
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "C4"
+T1 = float(sys.argv[2]) if len(sys.argv) > 2 else 248.7
+s_sel = float(sys.argv[3]) if len(sys.argv) > 3 else 0.224
+E1 = float(sys.argv[4]) if len(sys.argv) > 4 else 2.6595e10
+COST = sys.argv[5] if len(sys.argv) > 5 else "inout"     # partition cost: "out" or "inout"
+B_LINK, T_ROUND = 450e9, 40e-6
+
+p = gen.config(cfg, 1)
+if cfg == "C3":
+    src, dst = gen.rmat_coo(24, 1)
+    p.col_ptr, p.row_idx = di.di_csc_from_coo(p.n, src, dst)
+    del src, dst
+pol, alpha, frac, key = bench.SCHEDULES[cfg]
+# passes of the 1-GPU solve (scan term of the model)
+o1 = di.default_options(policy=pol, alpha=alpha, hybrid_frac=frac, select_key=key)
+c1 = di.di_create(p.n, p.col_ptr, p.row_idx, p.values, p.b, p.d, o1)
+di.di_run(c1, p.stop)
+P1 = di.di_get_stats(c1)["passes"]
+di.di_destroy(c1)
+out = {"config": cfg, "partition": COST, "T1_ms": T1, "select_share": s_sel, "E1": E1, "passes_1": P1, "K": {}}
+for K in (2, 4, 8):
+    bounds = dist.partition_bounds(p.col_ptr, K, cost=COST, row_idx=p.row_idx)
+    st = [None] * K
+    err = [None] * K
+    cid = dist.loopback_comm_id(f"model{cfg}{K}")
+
+    def w(r):
+        try:
+            lcp, lri, lv, lb = dist.shard_csc(p.col_ptr, p.row_idx, p.values, p.b, bounds, r)
+            o = di.default_options(policy=pol, alpha=alpha, hybrid_frac=frac, select_key=key,
+                                   exchange_mode=di.DI_EXCHANGE_ASYNC, check_interval=4, remote_push=1)
+            ctx = di.di_create_dist(r, K, cid, bounds, p.n, lcp, lri, lv, lb, p.d, o)
+            di.di_run(ctx, p.stop)
+            st[r] = di.di_get_stats(ctx)
+            di.di_destroy(ctx)
+        except Exception as e:
+            err[r] = e
+    t = time.perf_counter()
+    th = [threading.Thread(target=w, args=(r,)) for r in range(K)]
+    [x.start() for x in th]
+    [x.join() for x in th]
+    for e in err:
+        if e is not None:
+            raise e
+    wall = time.perf_counter() - t
+    rounds = max(s["exchanges"] for s in st)
+    comp = max(s_sel * (s["passes"] * s["n_local"]) / (P1 * p.n) + (1 - s_sel) * (s["edges"] + s["remote_pushes"]) / E1
+               for s in st)
+    per_round = max(s["exchanged_bytes"] for s in st) / max(1, rounds)
+    TK = T1 * 1e-3 * comp + rounds * (per_round / B_LINK + T_ROUND)
+    eff = T1 * 1e-3 / (K * TK)
+    out["K"][K] = {"passes": [s["passes"] for s in st], "n_local": [s["n_local"] for s in st],
+                   "edges": [s["edges"] for s in st], "remote_pushes": [s["remote_pushes"] for s in st],
+                   "rounds": rounds, "bytes_per_round_max": per_round,
+                   "exchanged_bytes_total": sum(s["exchanged_bytes"] for s in st),
+                   "compute_fraction_of_T1": comp, "T_K_model_ms": TK * 1e3, "efficiency_model": eff,
+                   "loopback_wall_s": wall}
+    print(f"K={K}: rounds={rounds} max bytes/round={per_round / 1e6:.1f} MB  edges sum={sum(s['edges'] for s in st):.4e} "
+          f"(1 GPU {E1:.4e})  compute max/T1={comp:.3f}  T_K model={TK * 1e3:.1f} ms  efficiency={eff:.2f}", flush=True)
+print(json.dumps(out))
