@@ -28,6 +28,9 @@ s_sel = float(sys.argv[3]) if len(sys.argv) > 3 else 0.224
 E1 = float(sys.argv[4]) if len(sys.argv) > 4 else 2.6595e10
 COST = sys.argv[5] if len(sys.argv) > 5 else "inout"     # partition cost: "out" or "inout"
 B_LINK, T_ROUND = 450e9, 40e-6
+KS = [int(k) for k in os.environ.get("MODEL_K", "2,4,8").split(",")]
+ROUND = int(os.environ.get("MODEL_ROUND_PASSES", "4"))      # bench --round-passes
+REMOTE = int(os.environ.get("MODEL_REMOTE_PUSH", "1"))      # bench --remote-push
 
 p = gen.config(cfg, 1)
 if cfg == "C3":
@@ -41,8 +44,8 @@ c1 = di.di_create(p.n, p.col_ptr, p.row_idx, p.values, p.b, p.d, o1)
 di.di_run(c1, p.stop)
 P1 = di.di_get_stats(c1)["passes"]
 di.di_destroy(c1)
-out = {"config": cfg, "partition": COST, "T1_ms": T1, "select_share": s_sel, "E1": E1, "passes_1": P1, "K": {}}
-for K in (2, 4, 8):
+out = {"config": cfg, "partition": COST, "round_passes": ROUND, "remote_push": REMOTE, "T1_ms": T1, "select_share": s_sel, "E1": E1, "passes_1": P1, "K": {}}
+for K in KS:
     bounds = dist.partition_bounds(p.col_ptr, K, cost=COST, row_idx=p.row_idx)
     st = [None] * K
     err = [None] * K
@@ -52,7 +55,7 @@ for K in (2, 4, 8):
         try:
             lcp, lri, lv, lb = dist.shard_csc(p.col_ptr, p.row_idx, p.values, p.b, bounds, r)
             o = di.default_options(policy=pol, alpha=alpha, hybrid_frac=frac, select_key=key,
-                                   exchange_mode=di.DI_EXCHANGE_ASYNC, check_interval=4, remote_push=1)
+                                   exchange_mode=di.DI_EXCHANGE_ASYNC, check_interval=ROUND, remote_push=REMOTE)
             ctx = di.di_create_dist(r, K, cid, bounds, p.n, lcp, lri, lv, lb, p.d, o)
             di.di_run(ctx, p.stop)
             st[r] = di.di_get_stats(ctx)
