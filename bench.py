@@ -433,7 +433,9 @@ def run_ours(args, rank, world, local_rank):
         e_ = torch.tensor([float(tot["edges"]), float(tot["exchanged_bytes"])], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(e_)
         tot["run_ms"] = float(t_.item())
-        edges_all = int(e_[0].item())
+        # di_stats.edges is the rank's own count under ASYNC but the global count under
+        # SYNC (pass totals are all-reduced every pass): sum only the former
+        edges_all = int(e_[0].item()) if mode == di.DI_EXCHANGE_ASYNC else int(tot["edges"])
         xbytes_all = int(e_[1].item())
     run_s = tot["run_ms"] / 1e3
     value = edges_all / run_s

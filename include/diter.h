@@ -155,7 +155,9 @@ typedef struct {
 
 typedef struct {
   int64_t passes;          /* passes executed since create */
-  int64_t edges;           /* elementary diffusions since create (sum of E_p) */
+  int64_t edges;           /* elementary diffusions since create (sum of E_p); distributed: this
+                              rank's under ASYNC, all ranks' under SYNC (whose pass totals are
+                              all-reduced every pass) -- likewise nodes */
   int64_t nodes;           /* node diffusions since create (sum of |S_p|) */
   double residual;         /* last measured/predicted |F|_1 (exact after di_get_residual) */
   double threshold;        /* current T */

@@ -31,6 +31,7 @@ B_LINK, T_ROUND = 450e9, 40e-6
 KS = [int(k) for k in os.environ.get("MODEL_K", "2,4,8").split(",")]
 ROUND = int(os.environ.get("MODEL_ROUND_PASSES", "4"))      # bench --round-passes
 REMOTE = int(os.environ.get("MODEL_REMOTE_PUSH", "1"))      # bench --remote-push
+MODE = di.DI_EXCHANGE_ASYNC      # SYNC's di_stats.edges are global totals: not modeled per rank
 
 p = gen.config(cfg, 1)
 if cfg == "C3":
@@ -55,7 +56,7 @@ for K in KS:
         try:
             lcp, lri, lv, lb = dist.shard_csc(p.col_ptr, p.row_idx, p.values, p.b, bounds, r)
             o = di.default_options(policy=pol, alpha=alpha, hybrid_frac=frac, select_key=key,
-                                   exchange_mode=di.DI_EXCHANGE_ASYNC, check_interval=ROUND, remote_push=REMOTE)
+                                   exchange_mode=MODE, check_interval=ROUND, remote_push=REMOTE)
             ctx = di.di_create_dist(r, K, cid, bounds, p.n, lcp, lri, lv, lb, p.d, o)
             di.di_run(ctx, p.stop)
             st[r] = di.di_get_stats(ctx)
