@@ -547,7 +547,8 @@ def run_e2e(args, p, opts, di, torch, rank=0, world=1, comm_id=None, bounds=None
         t_ = torch.tensor([dt, float(edges)], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t_[:1], op=torch.distributed.ReduceOp.MAX)
         e_ = t_[1:].clone()
-        torch.distributed.all_reduce(e_)
+        if opts.exchange_mode == di.DI_EXCHANGE_ASYNC:     # SYNC edge counts are global already
+            torch.distributed.all_reduce(e_)
         dt, edges = float(t_[0].item()), float(e_[0].item())
     return {"value": edges / dt, "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": steps, "ms_per_step": dt * 1e3 / steps}
