@@ -39,6 +39,8 @@ if cfg == "C3":
     p.col_ptr, p.row_idx = di.di_csc_from_coo(p.n, src, dst)
     del src, dst
 pol, alpha, frac, key = bench.SCHEDULES[cfg]
+alpha_k = float(os.environ.get("MODEL_ALPHA", alpha))        # schedule of the K ranks (default: 1 GPU's)
+frac_k = float(os.environ.get("MODEL_FRAC", frac))
 # passes of the 1-GPU solve (scan term of the model)
 o1 = di.default_options(policy=pol, alpha=alpha, hybrid_frac=frac, select_key=key)
 c1 = di.di_create(p.n, p.col_ptr, p.row_idx, p.values, p.b, p.d, o1)
@@ -55,7 +57,7 @@ for K in KS:
     def w(r):
         try:
             lcp, lri, lv, lb = dist.shard_csc(p.col_ptr, p.row_idx, p.values, p.b, bounds, r)
-            o = di.default_options(policy=pol, alpha=alpha, hybrid_frac=frac, select_key=key,
+            o = di.default_options(policy=pol, alpha=alpha_k, hybrid_frac=frac_k, select_key=key,
                                    exchange_mode=MODE, check_interval=ROUND, remote_push=REMOTE)
             ctx = di.di_create_dist(r, K, cid, bounds, p.n, lcp, lri, lv, lb, p.d, o)
             di.di_run(ctx, p.stop)
