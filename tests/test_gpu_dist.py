@@ -197,11 +197,13 @@ def _run_ranks_fn(K, key, fn):
     return out
 
 
-@pytest.mark.parametrize("remote", [0, 1, 2])
-def test_rebalance_moves_state_and_keeps_parity(remote):
+@pytest.mark.parametrize("remote,l2", [(0, 0), (1, 0), (2, 0), (1, 1)])
+def test_rebalance_moves_state_and_keeps_parity(remote, l2):
     """NEXT f4: di_rebalance ships columns, F, H (and B) of moved
     nodes mid-solve; the run resumes on the new ranges and reaches the same X with a
-    closed ledger.  Random positive B exercises the B transfer (di_reset after it)."""
+    closed ledger.  Random positive B exercises the B transfer (di_reset after it).
+    l2 = 1: every rank forces a 1 MB L2 persisting window, which the rebuilt context
+    re-applies on the stream it inherits."""
     K = 3
     p = gen.config("C2", 2, n=200_000)
     rng = np.random.default_rng(2)
@@ -215,11 +217,16 @@ def test_rebalance_moves_state_and_keeps_parity(remote):
 
     def fn(r, cid):
         lcp, lri, lv, lb = dist.shard_csc(p.col_ptr, p.row_idx, None, b, bounds, r)
-        o = di.default_options(exchange_mode=di.DI_EXCHANGE_ASYNC, check_interval=4, remote_push=remote)
+        o = di.default_options(exchange_mode=di.DI_EXCHANGE_ASYNC, check_interval=4, remote_push=remote,
+                               l2_persist=1 if l2 else 0)
         ctx = di.di_create_dist(r, K, cid, bounds, p.n, lcp, lri, lv, lb, p.d, o)
+        if l2:
+            assert di.di_get_stats(ctx)["l2_window_bytes"] > 0
         di.di_run(ctx, 1e-4)
         h0 = di.di_get_history(ctx).sum()
         di.di_rebalance(ctx, nb)
+        if l2:
+            assert di.di_get_stats(ctx)["l2_window_bytes"] > 0
         got = di.di_get_bounds(ctx)
         res = (list(got), ctx.n_local, h0)
         di.di_run(ctx, p.parity_stop)
@@ -228,7 +235,7 @@ def test_rebalance_moves_state_and_keeps_parity(remote):
         Fr = di.di_get_fluid(ctx)
         di.di_destroy(ctx)
         return res, H, F, st, Fr
-    outs = _run_ranks_fn(K, f"rebal{remote}", fn)
+    outs = _run_ranks_fn(K, f"rebal{remote}{l2}", fn)
     for r, o in enumerate(outs):
         assert o[0][0] == list(nb) and o[0][1] == nb[r + 1] - nb[r]
         assert o[3]["rebalances"] == 1
