@@ -67,6 +67,10 @@ SCHEDULES = {
 # balance C3's permuted R-MAT better (181.3 vs 183.3 ms); GPU-side only.
 SCATTER_RUN = {"C3": 1, "C4": 3}
 
+# The raw key |F_i| > T_p (north_star's literal selection) on C4, reported beside the
+# headline as `raw_key`: HYBRID alpha = 2, f = 0.15 (its best schedule).
+RAW_KEY_SCHEDULE = (1, 2.0, 0.15, 0)
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -87,6 +91,8 @@ def parse():
                     help="bound on the oracle sample for cpu_baseline / reference steps")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-raw-key", action="store_true",
+                    help="skip the extra raw-key (|F_i| > T, north_star's literal key) C4 solve")
     ap.add_argument("--scale", type=int, default=None, help="C3 scale override (tests)")
     ap.add_argument("--n", type=int, default=None, help="node-count override (tests)")
     ap.add_argument("--pass-csv", default=None, help="write the last solve's per-pass log here")
@@ -127,10 +133,11 @@ def load_problem(args):
     return p
 
 
-def graph_residency(p):
-    """(bytes resident per GPU at N = 1, whether bench flushes L2 between steps)."""
+def graph_residency(p, world=1):
+    """(bytes resident per GPU -- graph + F + H, split over `world` ranks -- and whether
+    bench flushes L2 between steps: when that is under 4x the L2)."""
     graph_bytes = 8 * (p.n + 1) + 4 * p.nnz + (8 * p.nnz if p.values is not None else 0)
-    resident = graph_bytes + 16 * p.n
+    resident = (graph_bytes + 16 * p.n) / world
     return resident, resident < 4 * L2_BYTES
 
 
@@ -235,6 +242,7 @@ class ClockSampler:
 # ------------------------------------------------------------ cpu baseline --
 
 _ORACLE_PROBLEM = {}
+ORACLE_CORE = 0     # the oracle's one pinned host core
 
 
 def oracle_sample(p, policy_geom: bool, seconds: float, state=None, alpha=1.5, hybrid_frac=0.05, key=0):
@@ -248,17 +256,23 @@ def oracle_sample(p, policy_geom: bool, seconds: float, state=None, alpha=1.5, h
     pol = oracle.GEOM if policy_geom else oracle.HYBRID
     e0, p0 = st.edges, st.passes
     edges = passes = 0
-    t0 = time.perf_counter()
-    while time.perf_counter() - t0 < seconds:
-        rc = P.snapshot(st, p.stop, pol, alpha, hybrid_frac, max_passes=1)
-        if rc == oracle.OK:
-            # the solve is done (small configs finish within one sample): start the
-            # same solve again from F = B so that the sample keeps doing real passes
-            edges += st.edges - e0
-            passes += st.passes - p0
-            st = P.init(alpha)
-            e0, p0 = 0, 0
-    dt = time.perf_counter() - t0
+    # one core, like `taskset -c <core>`: pid 0 = this thread
+    old_aff = os.sched_getaffinity(0)
+    os.sched_setaffinity(0, {ORACLE_CORE if ORACLE_CORE in old_aff else min(old_aff)})
+    try:
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < seconds:
+            rc = P.snapshot(st, p.stop, pol, alpha, hybrid_frac, max_passes=1)
+            if rc == oracle.OK:
+                # the solve is done (small configs finish within one sample): start the
+                # same solve again from F = B so that the sample keeps doing real passes
+                edges += st.edges - e0
+                passes += st.passes - p0
+                st = P.init(alpha)
+                e0, p0 = 0, 0
+        dt = time.perf_counter() - t0
+    finally:
+        os.sched_setaffinity(0, old_aff)
     return edges + st.edges - e0, dt, passes + st.passes - p0, st
 
 
@@ -285,18 +299,20 @@ def host_cpu():
     return f"{model}, nproc {os.cpu_count()}"
 
 
-def ncu_traffic(config, alg_bytes_per_launch):
-    """DRAM bytes (read + write) per k_scatter launch, from the committed ncu --set full
-    capture of one launch (profiles/ncu_traffic.json), scaled to the average launch by
-    that launch's traffic / algorithmic-bytes ratio.  None if not captured."""
+def ncu_traffic(config):
+    """(DRAM bytes read + written per k_scatter launch, source): the mean over every
+    launch of one solve of this config, measured by ncu (scripts/ncu_traffic.py ->
+    profiles/ncu_traffic.json; cold-cache serialised replays).  (None, why) if the
+    config has no capture."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            d = json.load(f)
-        ratio = d[config]["traffic_over_algorithmic"]
-        return ratio * alg_bytes_per_launch
+            d = json.load(f)[config]
+        return float(d["mean_dram_bytes_per_launch"]), (
+            f"ncu dram__bytes_read.sum + dram__bytes_write.sum, mean over the {d['launches']} k_scatter "
+            f"launches of one {config} solve (profiles/ncu_traffic.json; cold-cache replays)")
     except Exception:
-        return None
+        return None, "no ncu capture of this config"
 
 
 # -------------------------------------------------------------- reference arm --
@@ -325,9 +341,9 @@ def run_reference(args, rank, world):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3 / args.steps,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic",
-           "config": bench_config(args, p, policy_of(args), 1, *graph_residency(p)),
+           "config": bench_config(args, p, policy_of(args), world, *graph_residency(p, world)),
            "cpu_baseline": {"value": v, "unit": "edges/s", "cores": 1, "kind": "oracle", "host": host_cpu(),
-                            "sample": sample},
+                            "pinned_core": ORACLE_CORE, "sample": sample},
            "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -369,12 +385,9 @@ def run_ours(args, rank, world, local_rank):
     t = time.perf_counter()
     ctx = make_ctx(args, p, opts, di, rank, world, comm_id, bounds, shard)
     log(f"[bench] rank {rank} create {time.perf_counter() - t:.2f}s")
-    n_loc = ctx.n_local
-    nnz_loc = int(shard[0][-1]) if dist else p.nnz
-    graph_bytes = 8 * (n_loc + 1) + 4 * nnz_loc + (8 * nnz_loc if p.values is not None else 0)
-    resident = graph_bytes + 16 * n_loc
+    resident, flushed = graph_residency(p, world)
     flush = None
-    if resident < 4 * L2_BYTES:
+    if flushed:
         flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device="cuda")
 
     def step():
@@ -392,9 +405,11 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     if dist:
         torch.distributed.barrier()
+    # di_stats counters run since create (di_reset restarts the solve counters); the
+    # launch count is per di_run (run_kernel_launches), summed over the timed steps
     tot = {"run_ms": 0.0, "edges": 0, "passes": 0, "kt_scatter_ms": 0.0, "kt_select_ms": 0.0,
-           "kt_finalize_ms": 0.0, "scatter_bytes": 0, "alg_bytes": 0, "kernel_launches": 0,
-           "nodes": 0, "exchanged_bytes": 0, "exchanges": 0}
+           "kt_finalize_ms": 0.0, "scatter_bytes": 0, "alg_bytes": 0, "run_kernel_launches": 0,
+           "nodes": 0, "dangling": 0, "exchanged_bytes": 0, "exchanges": 0}
     wall0 = time.perf_counter()
     with ClockSampler(local_rank) as clk:
         for _ in range(args.steps):
@@ -442,10 +457,11 @@ def run_ours(args, rank, world, local_rank):
     peak, peak_kind = measured_peaks()
     scat_gbs = prof["scatter_bytes"] / (prof["kt_scatter_ms"] / 1e3) / 1e9
     n_launch = prof["passes"]                      # executed k_scatter launches
-    traffic = ncu_traffic(args.config, prof["scatter_bytes"] / max(1, n_launch))
+    traffic, traffic_src = ncu_traffic(args.config)
     kt_sum = prof["kt_scatter_ms"] + prof["kt_select_ms"] + prof["kt_finalize_ms"]
     roofline = {"bound": "hbm", "achieved": scat_gbs, "peak": peak, "unit": "GB/s",
                 "frac": scat_gbs / peak, "frac_of_nominal_8TBps": scat_gbs / 8000.0, "traffic": traffic,
+                "traffic_source": traffic_src,
                 "kernel": "k_scatter", "peak_kind": peak_kind,
                 "bytes_per_launch": prof["scatter_bytes"] / max(1, n_launch),
                 "avg_launch_ms": prof["kt_scatter_ms"] / max(1, n_launch),
@@ -457,6 +473,10 @@ def run_ours(args, rank, world, local_rank):
                           f"more steps right after the timed region (rank {rank}); their ms_per_step "
                           f"{prof['run_ms'] / args.steps:.3f} includes the events' own cost",
                 "path_alg_GBps": tot["alg_bytes"] / (run_ms_rank / 1e3) / 1e9}
+    # ---- the raw key on the same graph (extra key; the headline keeps the per-edge key)
+    raw = None
+    if world == 1 and args.config == "C4" and args.key != 0 and not args.no_raw_key:
+        raw = run_raw_key(args, p, opts, di, torch)
     # ---- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -466,9 +486,13 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         e, dt, npass, st = oracle_sample(p, pol == di.DI_POLICY_GEOM, args.cpu_seconds, None,
                                          args.alpha, args.hybrid_frac, args.key)
-        cpu = {"value": e / dt if dt > 0 else None, "unit": "edges/s", "cores": 1, "kind": "oracle", "host": host_cpu(),
+        rate = e / dt if dt > 0 else None
+        cpu = {"value": rate, "unit": "edges/s", "cores": 1, "kind": "oracle", "host": host_cpu(),
+               "pinned_core": ORACLE_CORE,
                "sample": f"first {npass} snapshot passes ({e} edges) of the same {args.config} solve "
-                         f"on the full graph, {dt:.1f}s on 1 host core"}
+                         f"on the full graph, {dt:.1f}s on 1 pinned host core",
+               # the whole solve at the sampled rate (the first passes are the densest)
+               "time_to_target_s_est": (edges_all / args.steps) / rate if rate else None}
     clocks = clk.summary()
     st_last = di.di_get_stats(ctx)
     l2_window = (f"{st_last['l2_window_bytes'] / 2**20:.0f} MB persisting over F rows from "
@@ -489,12 +513,14 @@ def run_ours(args, rank, world, local_rank):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot["run_ms"] / args.steps,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic",
-           "config": dict(bench_config(args, p, pol, world, resident, flush is not None), l2_window=l2_window),
+           "config": bench_config(args, p, pol, world, resident, flush is not None),
+           "l2_window": l2_window,
            "time_to_target_ms": tot["run_ms"] / args.steps,
            "passes_per_solve": tot["passes"] / args.steps,
            "normalized_iterations": edges_all / args.steps / p.nnz,
-           "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-           "gpu_launches": int(tot["kernel_launches"]),
+           "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "raw_key": raw,
+           # our kernels in the timed steps: di_run's (graph nodes counted) + di_reset's k_init_state
+           "gpu_launches": int(tot["run_kernel_launches"]) + args.steps,
            "clocks": clocks,
            "nvlink_bytes_per_round": (xbytes_all / max(1, tot["exchanges"])) if dist else 0,
            "nvlink_bytes_per_solve": (xbytes_all / args.steps) if dist else 0,
@@ -504,6 +530,33 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
+
+
+def run_raw_key(args, p, opts, di, torch):
+    """C4 with the raw key |F_i| > T_p: its own context (key weights are create-time),
+    1 warm-up + min(steps, 3) timed solves, same timing as the headline."""
+    import copy
+    pol, alpha, frac, key = RAW_KEY_SCHEDULE
+    o = copy.copy(opts)
+    o.policy, o.alpha, o.hybrid_frac, o.select_key, o.profile = pol, alpha, frac, key, 0
+    ctx = di.di_create(p.n, p.col_ptr, p.row_idx, p.values, p.b, p.d, o)
+    try:
+        di.di_reset(ctx)
+        di.di_run(ctx, p.stop)
+        steps = max(1, min(args.steps, 3))
+        ms = edges = passes = 0
+        for _ in range(steps):
+            di.di_reset(ctx)
+            di.di_run(ctx, p.stop)
+            st = di.di_get_stats(ctx)
+            ms += st["run_ms"]
+            edges += st["edges"]
+            passes += st["passes"]
+    finally:
+        di.di_destroy(ctx)
+    return {"select_key": "raw", "policy": "hybrid", "alpha": alpha, "hybrid_frac": frac, "steps": steps,
+            "time_to_target_ms": ms / steps, "edges_per_s": edges / (ms / 1e3),
+            "passes_per_solve": passes / steps, "normalized_iterations": edges / steps / p.nnz}
 
 
 def run_e2e(args, p, opts, di, torch, rank=0, world=1, comm_id=None, bounds=None, shard=None):
@@ -554,14 +607,43 @@ def run_e2e(args, p, opts, di, torch, rank=0, world=1, comm_id=None, bounds=None
             "d2h_bytes_per_step": int(d2h), "steps": steps, "ms_per_step": dt * 1e3 / steps}
 
 
+def launch_ranks(args):
+    """--gpus N > 1 without a torchrun environment: re-exec this command under
+    torch.distributed.run with N ranks on this node (one per GPU), or fail loudly
+    when the node has fewer than N GPUs -- never a 1-rank run labelled N."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        log(f"[bench] --gpus {args.gpus} needs {args.gpus} GPUs on this node, found {have}")
+        sys.exit(2)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    log("[bench] " + " ".join(cmd))
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            log(f"[bench] WORLD_SIZE={world} but --gpus {args.gpus}")
+            sys.exit(2)
+    else:
+        world = 1
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        # the oracle arm runs on rank 0's host cores only; without torchrun it still
+        # reports the job's N
+        run_reference(args, rank, max(world, args.gpus))
         return
+    if args.gpus > 1 and world == 1:
+        launch_ranks(args)
     run_ours(args, rank, world, local_rank)
 
 

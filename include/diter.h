@@ -175,7 +175,7 @@ typedef struct {
   double kt_finalize_ms;   /* profile=1: summed device time of k_finalize over executed passes */
   int64_t kt_passes;       /* profile=1: executed passes those sums cover */
   int64_t scatter_bytes;   /* algorithmic bytes of the scatter kernel since create: 20 E (28 E signed)
-                              + 16 per diffused node (its col_ptr pair) */
+                              + 16 per non-dangling diffused node (its col_ptr pair) */
   int64_t remote_pushes;   /* distributed: pushes into the remote outbox since create (one RED per
                               remote edge per diffusion, or per column increment with
                               DI_REMOTE_INCREMENT; the receiver's in-edge adds with
@@ -183,6 +183,10 @@ typedef struct {
   int64_t rebalances;      /* distributed: ownership changes (di_rebalance / adapt_rounds) */
   int64_t l2_window_bytes; /* L2 persisting window over F chosen at create (options.l2_persist), 0 = none */
   int64_t l2_window_row;   /* its first row (global id) */
+  int64_t dangling;        /* dangling node diffusions since create (in nodes; taken by the select,
+                              their fluid leaves; the scatter never reads their col_ptr) */
+  int64_t run_kernel_launches; /* kernels launched by the last di_run (graph nodes counted, including
+                              passes of a graph launch that return at once after convergence) */
 } di_stats;
 
 /* Fill *opt with the defaults above. */
@@ -250,8 +254,10 @@ DI_API di_status di_get_fluid_device(const di_ctx *ctx, double *d_out);
  * with dangling fluid leaving, the completed solution is X' = X / |X|_1, so this
  * writes H_i / |H|_1 (|H|_1 by a deterministic reduction, global if distributed;
  * collective then) into the caller's host buffer (n, or hi-lo when distributed).
- * Meaningful for PageRank contexts (values == NULL); H approximates X within
- * |F|_1/(1-d).  The device variant writes a device pointer. */
+ * Defined for PageRank contexts with the default B = (1-d)/N (values == NULL and
+ * b == NULL at create): A.4 needs B proportional to the completion vector V = 1/N;
+ * any other context returns DI_ERR_STATE.  H approximates X within |F|_1/(1-d)
+ * (P:104-107).  The device variant writes a device pointer. */
 DI_API di_status di_get_pagerank(di_ctx *ctx, double *x_out);
 DI_API di_status di_get_pagerank_device(di_ctx *ctx, double *d_out);
 /* Exact |F|_1 by a deterministic two-level reduction (global if distributed;

@@ -80,7 +80,8 @@ class di_stats(ctypes.Structure):
                 ("kt_scatter_ms", ctypes.c_double), ("kt_finalize_ms", ctypes.c_double),
                 ("kt_passes", ctypes.c_int64), ("scatter_bytes", ctypes.c_int64),
                 ("remote_pushes", ctypes.c_int64), ("rebalances", ctypes.c_int64),
-                ("l2_window_bytes", ctypes.c_int64), ("l2_window_row", ctypes.c_int64)]
+                ("l2_window_bytes", ctypes.c_int64), ("l2_window_row", ctypes.c_int64),
+                ("dangling", ctypes.c_int64), ("run_kernel_launches", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

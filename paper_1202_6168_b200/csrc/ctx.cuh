@@ -67,8 +67,9 @@ struct di_ctx {
   std::vector<cudaEvent_t> prof_ev;  // profile=1: 4 events per captured pass
 
   // stats
-  long long passes_done = 0, edges = 0, nodes = 0;
+  long long passes_done = 0, edges = 0, nodes = 0, dang = 0;
   long long graph_launches = 0, kernel_launches = 0;
+  long long run_kernel_launches = 0;   // kernels launched by the last di_run
   long long exchanged_bytes = 0, exchanges = 0, alg_bytes_exchange = 0;
   double residual = 0.0, threshold = 0.0, run_ms = 0.0, run_ms_total = 0.0;
   double kt_ms[3] = {0.0, 0.0, 0.0};
@@ -80,8 +81,12 @@ struct di_ctx {
 };
 
 void diter_set_err(di_ctx *ctx, const char *fmt, ...);
+// local part of a create: upload, validation, buffers (no collective; may fail on
+// one rank only)
 di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_idx,
                       const double *values, const double *b, const di_options *opt);
+// collective tail: paper-key in-degrees, T_0, control block, captured graph
+di_status diter_setup_finish(di_ctx *ctx);
 di_status diter_l1_launch(di_ctx *ctx);
 di_status diter_l1_launch_of(di_ctx *ctx, const double *v);
 diter::Graph diter_graph(const di_ctx *ctx);
@@ -93,8 +98,9 @@ di_status diter_set_l2_window(di_ctx *ctx);
 // context device memory (per-device stream-ordered pool, ordered on ctx->stream)
 di_status diter_alloc(di_ctx *ctx, void **p, size_t bytes);
 void diter_free(di_ctx *ctx, void *p);
-double diter_dist_max(di_ctx *ctx, double v);
-double diter_dist_sum(di_ctx *ctx, double v);
+// max / sum of one host double over the ranks (identity when not distributed); collective
+di_status diter_dist_max(di_ctx *ctx, double v, double *out);
+di_status diter_dist_sum(di_ctx *ctx, double v, double *out);
 di_status diter_dist_indegree(di_ctx *ctx, unsigned *indeg_local);   // DI_KEY_PAPER, collective
 di_status diter_dist_run(di_ctx *ctx, double target);
 di_status diter_dist_reset(di_ctx *ctx);

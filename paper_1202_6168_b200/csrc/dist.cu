@@ -77,7 +77,8 @@ struct Fabric {
   // records: send[soff[q] .. soff[q]+scnt[q]) to peer q, into recv[roff[q] ..]
   virtual di_status alltoallv(di_ctx *ctx, const Rec *send, const long long *soff, const long long *scnt,
                               Rec *recv, const long long *roff, const long long *rcnt) = 0;
-  virtual double host_max(di_ctx *ctx, double v) = 0;
+  // max over ranks of one host double (setup: T_0, validation agreement)
+  virtual di_status host_max(di_ctx *ctx, double v, double *out) = 0;
 };
 
 // In-process loopback: K contexts (one host thread each) on one device.
@@ -158,13 +159,14 @@ struct LoopFabric : Fabric {
     grp->barrier();                            // peers may now reuse their send buffers
     return DI_OK;
   }
-  double host_max(di_ctx *, double v) override {
+  di_status host_max(di_ctx *, double v, double *out) override {
     grp->hmax[rank] = v;
     grp->barrier();
-    double m = 0.0;
-    for (int k = 0; k < grp->world; ++k) m = std::max(m, grp->hmax[k]);
+    double m = grp->hmax[0];
+    for (int k = 1; k < grp->world; ++k) m = std::max(m, grp->hmax[k]);
     grp->barrier();
-    return m;
+    *out = m;
+    return DI_OK;
   }
 };
 
@@ -215,13 +217,14 @@ struct NcclFabric : Fabric {
     CKN(ncclGroupEnd());
     return DI_OK;
   }
-  double host_max(di_ctx *ctx, double v) override {
-    if (!d_tmp && cudaMalloc(&d_tmp, sizeof(double)) != cudaSuccess) return v;
-    cudaMemcpyAsync(d_tmp, &v, sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
-    ncclAllReduce(d_tmp, d_tmp, 1, ncclDouble, ncclMax, comm, ctx->stream);
-    cudaMemcpyAsync(&v, d_tmp, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
-    cudaStreamSynchronize(ctx->stream);
-    return v;
+  di_status host_max(di_ctx *ctx, double v, double *out) override {
+    if (!d_tmp) CKD(cudaMalloc(&d_tmp, sizeof(double)));
+    CKD(cudaMemcpyAsync(d_tmp, &v, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CKN(ncclAllReduce(d_tmp, d_tmp, 1, ncclDouble, ncclMax, comm, ctx->stream));
+    CKD(cudaMemcpyAsync(&v, d_tmp, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CKD(cudaStreamSynchronize(ctx->stream));
+    *out = v;
+    return DI_OK;
   }
 };
 #endif
@@ -234,7 +237,7 @@ struct DistState {
   Rec *send = nullptr, *recv = nullptr;
   long long send_cap = 0, recv_cap = 0;
   long long *d_scnt = nullptr;         // [world] records compacted per peer
-  double *d_sums = nullptr;            // [kSums + 2]
+  double *d_sums = nullptr;            // [kSums + 3] + [world] long long (send offsets)
   std::vector<long long> soff, scnt, roff, rcnt;
   double s_k = 0.0;                    // outbox mass (ASYNC)
   // DI_REMOTE_RECEIVER (NEXT f3).  Sender: per peer q the local
@@ -307,27 +310,45 @@ __global__ void k_outbox_mass(const double *__restrict__ G, const unsigned char 
   if (lane_id() == 0 && m != 0.0) atomicAdd(out, m);
 }
 
+// Largest selection key |v| w_row of what a merge added (key_max: a non-negative
+// double as its bit pattern, which orders like the value), for the rescale of an
+// idle rank's threshold (k_rescale_T).
+__device__ __forceinline__ void max_key(double key, double *key_max) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) key = fmax(key, __shfl_xor_sync(0xffffffffu, key, o));
+  if (lane_id() == 0 && key > 0.0)
+    atomicMax(reinterpret_cast<unsigned long long *>(key_max), (unsigned long long)__double_as_longlong(key));
+}
+
 // Merge received records: F[row] += val ("add them to existing
 // fluids, node per node").
-__global__ void k_merge(double *__restrict__ F, const Rec *__restrict__ recv, long long n, double *recv_mass) {
+__global__ void k_merge(double *__restrict__ F, const Rec *__restrict__ recv, long long n, double *recv_mass,
+                        const float *__restrict__ kw) {
   const long long stride = (long long)gridDim.x * blockDim.x;
-  double m = 0.0;
+  double m = 0.0, km = 0.0;
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
     const Rec r = recv[k];
     red_add(F + r.row, r.val);
     m += fabs(r.val);
+    km = fmax(km, fabs(r.val) * (kw ? (double)kw[r.row] : 1.0));
   }
   m = warp_sum(m);
   if (lane_id() == 0 && m != 0.0) atomicAdd(recv_mass, m);
+  max_key(km, recv_mass + 1);
 }
 
 // Receive-side threshold rescale ("update the threshold T_k,
 // rescaling up by a factor ... proportional to min((r_k + received)/r_k,
 // received)"; reading R13): T_k <- T_k (r_k + R) / r_k with R the fluid mass just
-// merged and r_k the local residual before the merge (r_k = 0: unchanged).
+// merged and r_k the local residual before the merge.  An idle rank (r_k = 0, the
+// ratio unbounded: the min picks the received side) restarts from the received
+// fluid as a create starts from B (reading R5): T_k = max key merged / alpha, so
+// T never stays at the value it sank to while the rank had nothing to diffuse.
 __global__ void k_rescale_T(Ctl *ctl, const double *recv_mass, double r_k) {
-  const double R = *recv_mass;
-  if (r_k > 0.0 && R > 0.0) ctl->T = ctl->T * ((r_k + R) / r_k);
+  const double R = recv_mass[0], kmax = recv_mass[1];
+  if (!(R > 0.0)) return;
+  if (r_k > 0.0) ctl->T = ctl->T * ((r_k + R) / r_k);
+  else if (kmax > 0.0) ctl->T = kmax / ctl->alpha;
 }
 
 // Setup: stable partition of every owned column into local rows (owned by this
@@ -532,9 +553,9 @@ __global__ void k_send_increments(const int *__restrict__ cols, const long long 
 __global__ void k_apply_remote_in(double *__restrict__ F, const Rec *__restrict__ recv, long long n_rec,
                                   const long long *__restrict__ src, const long long *__restrict__ off, long long ric_n,
                                   const int *__restrict__ row, const double *__restrict__ p, double *recv_mass,
-                                  unsigned long long *pushes) {
+                                  unsigned long long *pushes, const float *__restrict__ kw) {
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-  double m = 0.0;
+  double m = 0.0, km = 0.0;
   long long cnt = 0;
   for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_rec; r += warps) {
     const Rec rc = recv[r];
@@ -549,6 +570,7 @@ __global__ void k_apply_remote_in(double *__restrict__ F, const Rec *__restrict_
       const double v = rc.val * p[k];
       red_add(F + row[k], v);
       m += fabs(v);
+      km = fmax(km, fabs(v) * (kw ? (double)kw[row[k]] : 1.0));
     }
     cnt += e - b;
   }
@@ -557,6 +579,7 @@ __global__ void k_apply_remote_in(double *__restrict__ F, const Rec *__restrict_
     if (m != 0.0) atomicAdd(recv_mass, m);
     if (cnt) atomicAdd(pushes, (unsigned long long)cnt);
   }
+  max_key(km, recv_mass + 1);
 }
 
 __global__ void k_set_target(Ctl *ctl, double target, long long max_pass, int done) {
@@ -650,19 +673,21 @@ di_status diter_dist_indegree(di_ctx *ctx, unsigned *indeg_local) {
   return st;
 }
 
-double diter_dist_max(di_ctx *ctx, double v) {
-  if (!ctx->dist) return v;
-  return ctx->dist->fabric->host_max(ctx, v);
+di_status diter_dist_max(di_ctx *ctx, double v, double *out) {
+  *out = v;
+  if (!ctx->dist) return DI_OK;
+  return ctx->dist->fabric->host_max(ctx, v, out);
 }
 
-double diter_dist_sum(di_ctx *ctx, double v) {
-  if (!ctx->dist) return v;
+di_status diter_dist_sum(di_ctx *ctx, double v, double *out) {
+  *out = v;
+  if (!ctx->dist) return DI_OK;
   DistState *ds = ctx->dist;
-  cudaMemcpyAsync(ds->d_sums, &v, sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
-  if (ds->fabric->allreduce_sum(ctx, ds->d_sums, 1) != DI_OK) return v;
-  cudaMemcpyAsync(&v, ds->d_sums, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
-  cudaStreamSynchronize(ctx->stream);
-  return v;
+  CKD(cudaMemcpyAsync(ds->d_sums, &v, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  TRYD(ds->fabric->allreduce_sum(ctx, ds->d_sums, 1));
+  CKD(cudaMemcpyAsync(out, ds->d_sums, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CKD(cudaStreamSynchronize(ctx->stream));
+  return DI_OK;
 }
 
 di_status diter_dist_reset(di_ctx *ctx) {
@@ -704,9 +729,9 @@ static di_status exchange(di_ctx *ctx, bool send_now) {
   DistState *ds = ctx->dist;
   const int W = ctx->world;
   CKD(cudaMemsetAsync(ds->d_scnt, 0, sizeof(long long) * W, ctx->stream));
-  CKD(cudaMemsetAsync(ds->d_sums + kSums + 1, 0, sizeof(double), ctx->stream));   // received mass
+  CKD(cudaMemsetAsync(ds->d_sums + kSums + 1, 0, 2 * sizeof(double), ctx->stream));   // received mass, max key
   if (send_now) {
-    long long *d_soff = reinterpret_cast<long long *>(ds->d_sums + kSums + 2);
+    long long *d_soff = reinterpret_cast<long long *>(ds->d_sums + kSums + 3);
     CKD(cudaMemcpyAsync(d_soff, ds->soff.data(), sizeof(long long) * W, cudaMemcpyHostToDevice, ctx->stream));
     k_compact<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->G, ctx->dflags, ds->d_bounds, W, ctx->rank,
                                                          ds->send, d_soff, ds->d_scnt, 1);
@@ -730,7 +755,7 @@ static di_status exchange(di_ctx *ctx, bool send_now) {
   TRYD(ds->fabric->alltoallv(ctx, ds->send, ds->soff.data(), ds->scnt.data(), ds->recv, ds->roff.data(),
                              ds->rcnt.data()));
   if (tot > 0) {
-    k_merge<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->F, ds->recv, tot, ds->d_sums + kSums + 1);
+    k_merge<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->F, ds->recv, tot, ds->d_sums + kSums + 1, ctx->kw);
     ctx->kernel_launches += 1;
   }
   if (sent > 0) {
@@ -862,9 +887,9 @@ static di_status exchange_receiver(di_ctx *ctx, bool send_now) {
   DistState *ds = ctx->dist;
   const int W = ctx->world;
   CKD(cudaMemsetAsync(ds->d_scnt, 0, sizeof(long long) * W, ctx->stream));
-  CKD(cudaMemsetAsync(ds->d_sums + kSums + 1, 0, sizeof(double), ctx->stream));   // received mass
+  CKD(cudaMemsetAsync(ds->d_sums + kSums + 1, 0, 2 * sizeof(double), ctx->stream));   // received mass, max key
   if (send_now) {
-    long long *d_soff = reinterpret_cast<long long *>(ds->d_sums + kSums + 2);
+    long long *d_soff = reinterpret_cast<long long *>(ds->d_sums + kSums + 3);
     CKD(cudaMemcpyAsync(d_soff, ds->soff.data(), sizeof(long long) * W, cudaMemcpyHostToDevice, ctx->stream));
     k_send_increments<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ds->cols, ds->d_pair_off, W, ctx->rank, ctx->H,
                                                                  ctx->H_old, ctx->lo, ds->send, d_soff, ds->d_scnt);
@@ -889,7 +914,7 @@ static di_status exchange_receiver(di_ctx *ctx, bool send_now) {
   if (tot > 0) {
     k_apply_remote_in<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->F, ds->recv, tot, ds->ric_src, ds->ric_off,
                                                                  ds->ric_n, ds->ric_row, ds->ric_p,
-                                                                 ds->d_sums + kSums + 1, &ctx->ctl->remote_pushes);
+                                                                 ds->d_sums + kSums + 1, &ctx->ctl->remote_pushes, ctx->kw);
     ctx->kernel_launches += 1;
   }
   if (sent > 0) {
@@ -990,6 +1015,7 @@ di_status diter_dist_run(di_ctx *ctx, double target) {
   DistState *ds = ctx->dist;
   CKD(cudaSetDevice(ctx->device));
   CKD(cudaEventRecord(ctx->ev0, ctx->stream));
+  const long long launches0 = ctx->kernel_launches;
   const long long max_pass_abs = ctx->passes_done + ctx->opt.max_passes;
   const bool sync_mode = ctx->opt.exchange_mode == DI_EXCHANGE_SYNC;
   const bool incr = ctx->H_old != nullptr;   // DI_REMOTE_INCREMENT
@@ -1098,8 +1124,10 @@ out:
   ctx->passes_done = h->pass;
   ctx->edges = h->edges;
   ctx->nodes = h->nodes;
+  ctx->dang = h->dang;
   ctx->threshold = h->T;
   ctx->remote_pushes = (long long)h->remote_pushes;
+  ctx->run_kernel_launches = ctx->kernel_launches - launches0;
   if (st == DI_ERR_NOT_CONVERGED) diter_set_err(ctx, "max_passes reached before |F|_1 < %g", target);
   return st;
 }
@@ -1281,6 +1309,7 @@ extern "C" di_status di_rebalance(di_ctx *ctx, const int64_t *nb) {
   nc->passes_done = ctx->passes_done;
   nc->edges = ctx->edges;
   nc->nodes = ctx->nodes;
+  nc->dang = ctx->dang;
   nc->graph_launches = ctx->graph_launches;
   nc->kernel_launches += ctx->kernel_launches;
   nc->exchanged_bytes = ctx->exchanged_bytes + stot * (long long)sizeof(Rec);
@@ -1337,8 +1366,8 @@ static const char kLoopTag[8] = {'D', 'I', 'L', 'O', 'O', 'P', '0', '1'};
 // ctx->lo / n_local / nnz_local describing this rank's columns): device setup,
 // column partition, outbox and exchange buffers, receiver structures.  Shared by
 // di_create_dist and di_rebalance.  Collective.
-static di_status dist_build(di_ctx *ctx, const int64_t *col_ptr_local, const int32_t *row_idx_local,
-                            const double *values_local, const double *b_local, const di_options *opt) {
+static di_status dist_build_local(di_ctx *ctx, const int64_t *col_ptr_local, const int32_t *row_idx_local,
+                                  const double *values_local, const double *b_local, const di_options *opt) {
   DistState *ds = ctx->dist;
   const int world = ctx->world, rank = ctx->rank;
   const long long n_global = ctx->n_rows, nl = ctx->n_local;
@@ -1408,25 +1437,40 @@ static di_status dist_build(di_ctx *ctx, const int64_t *col_ptr_local, const int
         cudaMalloc(&ds->recv, sizeof(Rec) * ds->recv_cap) != cudaSuccess ||
         cudaMalloc(&ds->d_bounds, sizeof(long long) * (world + 1)) != cudaSuccess ||
         cudaMalloc(&ds->d_scnt, sizeof(long long) * world) != cudaSuccess ||
-        cudaMalloc(&ds->d_sums, sizeof(double) * (kSums + 2) + sizeof(long long) * world) != cudaSuccess) {
+        cudaMalloc(&ds->d_sums, sizeof(double) * (kSums + 3) + sizeof(long long) * world) != cudaSuccess) {
       diter_set_err(ctx, "cudaMalloc (exchange buffers) failed");
       return (DI_ERR_OOM);
     }
     cudaMemcpyAsync(ds->d_bounds, ds->bounds.data(), sizeof(long long) * (world + 1), cudaMemcpyHostToDevice, ctx->stream);
     s = diter_dist_reset(ctx);
     if (s != DI_OK) return (s);
-    if (ctx->opt.remote_push == DI_REMOTE_RECEIVER) {
-      s = setup_receiver(ctx);
-      if (s != DI_OK) return (s);
-    }
   }
-  // The threshold schedule is global: T_0 = max over ranks |B_i| / alpha (done in
-  // setup through diter_dist_max); SYNC applies the HYBRID rule to the global |S_p|
-  // and N; ASYNC applies it per rank to |S_p^k| and |Omega_k|.
+  return DI_OK;
+}
+
+// Local setup on every rank, then one agreement (a max over ranks of a failure
+// flag) so that a rank whose input fails validation makes every rank fail together
+// instead of leaving its peers waiting in a later collective; then the collective
+// tail (T_0 = max over ranks |B_i| w_i / alpha, the paper key's in-degrees, the
+// receiver structures).  The threshold schedule is global: SYNC applies the HYBRID
+// rule to the global |S_p| and N; ASYNC per rank to |S_p^k| and |Omega_k|.
+static di_status dist_build(di_ctx *ctx, const int64_t *col_ptr_local, const int32_t *row_idx_local,
+                            const double *values_local, const double *b_local, const di_options *opt) {
+  di_status s = dist_build_local(ctx, col_ptr_local, row_idx_local, values_local, b_local, opt);
+  double any_fail = 0.0;
+  const di_status sa = ctx->dist->fabric->host_max(ctx, s != DI_OK ? 1.0 : 0.0, &any_fail);
+  if (s != DI_OK) return s;
+  if (sa != DI_OK) return sa;
+  if (any_fail > 0.0) {
+    diter_set_err(ctx, "di_create_dist: a peer rank failed its local setup");
+    return DI_ERR_STATE;
+  }
+  TRYD(diter_setup_finish(ctx));
+  if (ctx->opt.remote_push == DI_REMOTE_RECEIVER) TRYD(setup_receiver(ctx));
   if (ctx->opt.exchange_mode == DI_EXCHANGE_ASYNC) {
-    ctx->ctl_init.n_total = (double)nl;
-    cudaMemcpyAsync(ctx->ctl, &ctx->ctl_init, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream);
-    cudaStreamSynchronize(ctx->stream);
+    ctx->ctl_init.n_total = (double)ctx->n_local;
+    CKD(cudaMemcpyAsync(ctx->ctl, &ctx->ctl_init, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream));
+    CKD(cudaStreamSynchronize(ctx->stream));
   }
   return DI_OK;
 }

@@ -506,7 +506,7 @@ static di_status initial_threshold(di_ctx *ctx, double *T0) {
     CK(cudaStreamSynchronize(ctx->stream));
     for (double v : hp) mx = std::max(mx, v);
   }
-  mx = diter_dist_max(ctx, mx);   // global max over ranks (identity when not distributed)
+  TRY(diter_dist_max(ctx, mx, &mx));   // global max over ranks (identity when not distributed)
   *T0 = mx / ctx->opt.alpha;
   return DI_OK;
 }
@@ -600,11 +600,10 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
   // state: F = B, H = 0
   ctx->b_uniform = (1.0 - ctx->d) / (double)ctx->n_rows;
   k_init_state<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->F, ctx->H, ctx->d_b, ctx->b_uniform, n);
-  // selection-key weights: the paper key needs in-degrees (row_idx), after the census
+  // selection-key weights: the paper key needs in-degrees (row_idx), after the census;
+  // T_0 (a max over ranks when distributed) comes last, in diter_setup_finish
   const bool key_early = o.select_key != DI_KEY_PAPER;
   if (key_early) TRY(setup_key(ctx));
-  double T0 = o.t0;
-  if (key_early) TRY(initial_threshold(ctx, &T0));
   tr.mark(ctx->stream, "col_ptr-only setup");
   // validation + bin census on the device, once the rows are in
   CK(cudaStreamWaitEvent(ctx->stream, rows_in, 0));
@@ -635,9 +634,7 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
   TRY(choose_l2_window(ctx));
   tr.mark(ctx->stream, "hot window + L2 window");
   TRY(setup_far(ctx));
-  if (!key_early) TRY(setup_key(ctx));
-  if (!key_early) TRY(initial_threshold(ctx, &T0));
-  tr.mark(ctx->stream, "far bins + paper key");
+  tr.mark(ctx->stream, "far bins");
   ctx->cap_low = hc.n_low;
   ctx->cap_mid = hc.n_mid;
   ctx->cap_hub = hc.n_hub;
@@ -645,6 +642,20 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
   TRY(dalloc(ctx, &ctx->fr.hub_b0, hc.n_hub));
   TRY(dalloc(ctx, &ctx->fr.hub_deg, hc.n_hub));
   TRY(dalloc(ctx, &ctx->fr.hub_chunk, hc.n_hub));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return DI_OK;
+}
+
+// The collective tail of a create (distributed: every rank calls it, after all
+// ranks agreed that their local setup succeeded): the paper key's in-degrees,
+// T_0 = max over ranks, the control block, the captured pass graph.
+di_status diter_setup_finish(di_ctx *ctx) {
+  SetupTrace tr;
+  const di_options &o = ctx->opt;
+  if (o.select_key == DI_KEY_PAPER) TRY(setup_key(ctx));
+  double T0 = o.t0;
+  TRY(initial_threshold(ctx, &T0));
+  tr.mark(ctx->stream, "paper key + T_0");
   Ctl hc0;
   std::memset(&hc0, 0, sizeof(hc0));
   hc0.T = T0;
@@ -687,6 +698,7 @@ extern "C" di_status di_create(di_ctx **out, int64_t n, const int64_t *col_ptr, 
   ctx->lo = 0;
   ctx->d = d;
   di_status s = diter_setup(ctx, col_ptr, row_idx, values, b, opt);
+  if (s == DI_OK) s = diter_setup_finish(ctx);
   if (s != DI_OK) {
     g_thread_err = ctx->err;
     free_ctx(ctx);
@@ -720,6 +732,7 @@ extern "C" di_status di_run(di_ctx *ctx, double target) {
   if (ctx->world > 1) return diter_dist_run(ctx, target);
   CK(cudaSetDevice(ctx->device));
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  const long long launches0 = ctx->kernel_launches;
   di_status st = DI_OK;
   const long long max_pass_abs = ctx->passes_done + ctx->opt.max_passes;
   for (;;) {
@@ -797,7 +810,9 @@ extern "C" di_status di_run(di_ctx *ctx, double target) {
   ctx->passes_done = h->pass;
   ctx->edges = h->edges;
   ctx->nodes = h->nodes;
+  ctx->dang = h->dang;
   ctx->threshold = h->T;
+  ctx->run_kernel_launches = ctx->kernel_launches - launches0;
   if (st == DI_ERR_NOT_CONVERGED) diter_set_err(ctx, "max_passes reached before |F|_1 < %g", target);
   return st;
 }
@@ -828,7 +843,8 @@ extern "C" di_status di_reset(di_ctx *ctx) {
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaGetLastError());
   ctx->kernel_launches += 1;
-  ctx->passes_done = ctx->edges = ctx->nodes = 0;
+  ctx->passes_done = ctx->edges = ctx->nodes = ctx->dang = 0;
+  ctx->run_kernel_launches = 0;
   ctx->kt_ms[0] = ctx->kt_ms[1] = ctx->kt_ms[2] = 0.0;
   ctx->kt_passes = 0;
   ctx->pass_us.clear();
@@ -865,12 +881,18 @@ extern "C" di_status di_get_fluid_device(const di_ctx *ctx, double *f) {
 // staged in the frontier value buffer, which di_run rewrites every pass).
 static di_status pagerank_out(di_ctx *ctx, double *d_dst, double *h_dst) {
   if (!ctx || (!d_dst && !h_dst)) { diter_set_err(ctx, "NULL argument"); return DI_ERR_INVALID_ARG; }
+  if (ctx->vals || ctx->d_b) {
+    // X / |X|_1 is the completed PageRank only for P = dQ and B = (1-d) V with the
+    // completion vector V = 1/N (App. A.4); a signed P or a personalised B has none
+    diter_set_err(ctx, "di_get_pagerank: needs a PageRank context with the default B = (1-d)/N");
+    return DI_ERR_STATE;
+  }
   CK(cudaSetDevice(ctx->device));
   TRY(diter_l1_launch_of(ctx, ctx->H));
   double sh = 0.0;
   CK(cudaMemcpyAsync(&sh, ctx->l1_out, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  sh = diter_dist_sum(ctx, sh);
+  TRY(diter_dist_sum(ctx, sh, &sh));
   if (!(sh > 0.0)) { diter_set_err(ctx, "|H|_1 = 0: run the solver first"); return DI_ERR_STATE; }
   double *dst = d_dst ? d_dst : ctx->fr.S;
   k_div<<<ctx->grid_l1, 256, 0, ctx->stream>>>(dst, ctx->H, sh, ctx->n_local);
@@ -889,7 +911,7 @@ extern "C" di_status di_get_residual(di_ctx *ctx, double *r_out) {
   double r = 0.0;
   CK(cudaMemcpyAsync(&r, ctx->l1_out, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  r = diter_dist_sum(ctx, r);
+  TRY(diter_dist_sum(ctx, r, &r));
   ctx->residual = r;
   *r_out = r;
   return DI_OK;
@@ -917,7 +939,11 @@ extern "C" di_status di_get_stats(const di_ctx *ctx, di_stats *s) {
   s->kt_scatter_ms = ctx->kt_ms[1];
   s->kt_finalize_ms = ctx->kt_ms[2];
   s->kt_passes = ctx->kt_passes;
-  s->scatter_bytes = (ctx->vals ? 28LL : 20LL) * ctx->edges + 16LL * ctx->nodes;
+  // the scatter reads the col_ptr pair of every node it diffuses: the selected
+  // nodes minus the dangling ones, which the select takes itself
+  s->scatter_bytes = (ctx->vals ? 28LL : 20LL) * ctx->edges + 16LL * (ctx->nodes - ctx->dang);
+  s->dangling = ctx->dang;
+  s->run_kernel_launches = ctx->run_kernel_launches;
   s->remote_pushes = ctx->remote_pushes;
   s->rebalances = ctx->rebalances;
   s->l2_window_bytes = ctx->l2_bytes;

@@ -695,6 +695,7 @@ __device__ __forceinline__ void apply_pass(Ctl *ctl, const double *sums, di_pass
   }
   ctl->edges += edges;
   ctl->nodes += cnt;
+  ctl->dang += (long long)sums[4];
   ctl->r = r;
   const double pred = r - loss;
   ctl->r_pred = pred;

@@ -50,6 +50,7 @@ struct Ctl {
   long long max_pass;  // run stops with done = 2 when pass reaches this
   long long edges;     // cumulative E_p
   long long nodes;     // cumulative |S_p|
+  long long dang;      // cumulative dangling nodes of S_p (taken by the select, never scattered)
   int done;            // 0 running, 1 converged, 2 max passes reached
   int policy;          // DI_POLICY_*
   unsigned long long hub_packed;  // (hub slots << 32) | hub chunks; reset by k_finalize

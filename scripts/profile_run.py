@@ -11,6 +11,7 @@ ap.add_argument("--config", default="C4")
 ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--max-passes", type=int, default=40)
 ap.add_argument("--opt", action="append", default=[])
+ap.add_argument("--pass-csv", default=None, help="write the solve's pass log (frontier, edges, dangling)")
 a = ap.parse_args()
 p = gen.config(a.config, 1, n=a.n)
 if a.config == "C3":
@@ -25,4 +26,10 @@ ctx = di.di_create(p.n, p.col_ptr, p.row_idx, p.values, p.b, p.d, di.default_opt
 t = time.perf_counter()
 st = di.di_run(ctx, p.stop, raise_on_not_converged=False)
 print("status", st, "passes", di.di_get_stats(ctx)["passes"], "s", time.perf_counter() - t)
+if a.pass_csv:
+    lg = di.di_get_pass_log(ctx)
+    with open(a.pass_csv, "w") as f:
+        f.write(",".join(lg.dtype.names) + "\n")
+        for row in lg:
+            f.write(",".join(str(x) for x in row) + "\n")
 di.di_destroy(ctx)

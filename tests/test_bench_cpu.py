@@ -32,7 +32,29 @@ def test_helpers():
     peak, kind = bench.measured_peaks()
     assert peak > 1000 and kind in ("measured", "fallback")
     assert "nproc" in bench.host_cpu()
-    # the committed ncu capture scales to any launch size; unknown configs give None
-    t = bench.ncu_traffic("C4", 1e9)
-    assert t is None or 0.5e9 < t < 3e9
-    assert bench.ncu_traffic("no-such-config", 1e9) is None
+    # measured per-launch DRAM bytes of a committed ncu capture, or None with a reason
+    t, src = bench.ncu_traffic("C4")
+    assert (t is None and src) or (1e8 < t < 3e10 and "ncu" in src)
+    t, src = bench.ncu_traffic("no-such-config")
+    assert t is None and src
+
+
+def test_gpus_flag_fails_loudly_without_gpus():
+    """--gpus N > 1 outside torchrun re-executes under torch.distributed.run with N ranks,
+    or exits non-zero when the node has fewer GPUs: never a 1-rank line labelled N."""
+    import torch
+    if torch.cuda.device_count() >= 2:
+        return
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", "C1",
+                          "--steps", "1", "--warmup", "3"], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode != 0
+    assert "needs 2 GPUs" in out.stderr
+    assert out.stdout.strip() == ""
+
+
+def test_world_size_must_match_gpus():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", "C1",
+                          "--steps", "1", "--warmup", "3"], capture_output=True, text=True, timeout=300,
+                         cwd=ROOT, env=env)
+    assert out.returncode != 0 and "WORLD_SIZE=1 but --gpus 2" in out.stderr

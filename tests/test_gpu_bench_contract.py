@@ -25,7 +25,7 @@ def test_bench_line_contract():
     assert d["higher_is_better"] is True and d["dtype"] == "f64" and d["vs_baseline"] is None
     assert "workload" in d["config"]
     r = d["roofline"]
-    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic", "traffic_source"):
         assert k in r, k
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
@@ -33,5 +33,9 @@ def test_bench_line_contract():
     assert c["kind"] == "oracle" and c["cores"] == 1 and c["value"] > 0 and c["sample"]
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] == 8 * d["config"]["n"]
-    assert d["gpu_launches"] > 0
+    # launches of the timed steps only: per solve at least select + scatter + finalize per
+    # pass, at most one captured graph (16 passes) of overrun plus the per-run kernels
+    per = d["gpu_launches"] / d["steps"]
+    assert 3 * d["passes_per_solve"] <= per <= 3 * (d["passes_per_solve"] + 16) + 16, (per, d["passes_per_solve"])
+    assert c["pinned_core"] >= 0 and "l2_window" in d
     assert set(("sm_mhz", "sm_max_mhz", "reasons")) <= set(d["clocks"])

@@ -31,7 +31,7 @@ def run_ranks(K, n, cp, ri, vals, b, d, target, bounds, mode, key, **opts):
             di.di_run(ctx, target)
             out[r] = (di.di_get_history(ctx), di.di_get_fluid(ctx), di.di_get_pass_log(ctx),
                       di.di_get_stats(ctx), di.di_get_residual(ctx),
-                      di.di_get_pagerank(ctx) if vals is None else None)
+                      di.di_get_pagerank(ctx) if vals is None and b is None else None)
             di.di_destroy(ctx)
         except Exception as e:          # surfaced below
             err[r] = e
