@@ -96,6 +96,8 @@ def parse():
     ap.add_argument("--scale", type=int, default=None, help="C3 scale override (tests)")
     ap.add_argument("--n", type=int, default=None, help="node-count override (tests)")
     ap.add_argument("--pass-csv", default=None, help="write the last solve's per-pass log here")
+    ap.add_argument("--l2-persist", type=int, default=0,
+                    help="options.l2_persist: 0 auto, -1 off, > 0 window MB (experiments)")
     ap.add_argument("--exchange", default="async", choices=["sync", "async"],
                     help="multi-GPU exchange mode (DESIGN.md: SYNC = per-pass rounds, ASYNC = paper's send rule)")
     ap.add_argument("--round-passes", type=int, default=4, help="N > 1, ASYNC: local passes per exchange round")
@@ -376,7 +378,7 @@ def run_ours(args, rank, world, local_rank):
     dist_kw = dict(check_interval=args.round_passes, remote_push=args.remote_push) if world > 1 else {}
     opts = di.default_options(policy=pol, device=local_rank, profile=0, exchange_mode=mode,
                               alpha=args.alpha, hybrid_frac=args.hybrid_frac, select_key=args.key,
-                              scatter_run=SCATTER_RUN.get(args.config, 0), **dist_kw)
+                              scatter_run=SCATTER_RUN.get(args.config, 0), l2_persist=args.l2_persist, **dist_kw)
     comm_id, bounds, shard = None, None, None
     if dist:
         bounds = dd.partition_bounds(p.col_ptr, world, cost=args.partition, row_idx=p.row_idx)

@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <cstring>
 #include <map>
@@ -79,6 +80,9 @@ struct Fabric {
                               Rec *recv, const long long *roff, const long long *rcnt) = 0;
   // max over ranks of one host double (setup: T_0, validation agreement)
   virtual di_status host_max(di_ctx *ctx, double v, double *out) = 0;
+  // a rank failed mid-collective-sequence: release the peers (loopback) instead of
+  // leaving them waiting
+  virtual void abort() {}
 };
 
 // In-process loopback: K contexts (one host thread each) on one device.
@@ -96,18 +100,42 @@ struct LoopGroup {
 
   explicit LoopGroup(int w) : world(w), red(w * 8), counts(w * w), sendp(w), soff(w), scnt(w), hmax(w) {}
 
-  void barrier() {
+  // false when the group was aborted (a rank failed) or a peer did not arrive in
+  // time: the caller reports an error instead of waiting forever
+  bool aborted = false;
+  bool barrier() {
     std::unique_lock<std::mutex> lk(mu);
+    if (aborted) return false;
     const long long gen = generation;
     if (++arrived == world) {
       arrived = 0;
       ++generation;
       cv.notify_all();
-    } else {
-      cv.wait(lk, [&] { return generation != gen; });
+      return true;
     }
+    if (!cv.wait_for(lk, std::chrono::seconds(kLoopTimeoutS), [&] { return generation != gen || aborted; }) ||
+        aborted) {
+      aborted = true;
+      cv.notify_all();
+      return false;
+    }
+    return true;
   }
+  void abort() {
+    std::lock_guard<std::mutex> lk(mu);
+    aborted = true;
+    cv.notify_all();
+  }
+  static constexpr int kLoopTimeoutS = 600;
 };
+
+#define LOOP_BARRIER(ctx)                                                               \
+  do {                                                                                 \
+    if (!grp->barrier()) {                                                             \
+      diter_set_err(ctx, "loopback group aborted (a peer rank failed or timed out)");  \
+      return DI_ERR_STATE;                                                             \
+    }                                                                                  \
+  } while (0)
 
 static std::mutex g_loop_mu;
 static std::map<std::string, std::weak_ptr<LoopGroup>> g_loop_groups;
@@ -116,6 +144,7 @@ struct LoopFabric : Fabric {
   std::shared_ptr<LoopGroup> grp;
   int rank;
   LoopFabric(std::shared_ptr<LoopGroup> g, int r) : grp(std::move(g)), rank(r) {}
+  void abort() override { grp->abort(); }
 
   di_status allreduce_sum(di_ctx *ctx, double *dev, int count) override {
     if (count > 8) return DI_ERR_INVALID_ARG;
@@ -123,23 +152,23 @@ struct LoopFabric : Fabric {
     CKD(cudaMemcpyAsync(h, dev, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
     CKD(cudaStreamSynchronize(ctx->stream));
     std::memcpy(&grp->red[rank * 8], h, sizeof(double) * count);
-    grp->barrier();
+    LOOP_BARRIER(ctx);
     for (int q = 0; q < count; ++q) {
       double s = 0.0;
       for (int k = 0; k < grp->world; ++k) s += grp->red[k * 8 + q];   // fixed rank order
       h[q] = s;
     }
-    grp->barrier();
+    LOOP_BARRIER(ctx);
     CKD(cudaMemcpyAsync(dev, h, sizeof(double) * count, cudaMemcpyHostToDevice, ctx->stream));
     CKD(cudaStreamSynchronize(ctx->stream));
     return DI_OK;
   }
-  di_status alltoall_counts(di_ctx *, const long long *send, long long *recv) override {
+  di_status alltoall_counts(di_ctx *ctx, const long long *send, long long *recv) override {
     const int W = grp->world;
     for (int q = 0; q < W; ++q) grp->counts[rank * W + q] = send[q];
-    grp->barrier();
+    LOOP_BARRIER(ctx);
     for (int q = 0; q < W; ++q) recv[q] = grp->counts[q * W + rank];
-    grp->barrier();
+    LOOP_BARRIER(ctx);
     return DI_OK;
   }
   di_status alltoallv(di_ctx *ctx, const Rec *send, const long long *soff, const long long *scnt, Rec *recv,
@@ -149,22 +178,22 @@ struct LoopFabric : Fabric {
     grp->sendp[rank] = send;
     grp->soff[rank].assign(soff, soff + W);
     grp->scnt[rank].assign(scnt, scnt + W);
-    grp->barrier();
+    LOOP_BARRIER(ctx);
     for (int q = 0; q < W; ++q) {
       if (rcnt[q] == 0) continue;
       const Rec *src = grp->sendp[q] + grp->soff[q][rank];
       CKD(cudaMemcpyAsync(recv + roff[q], src, sizeof(Rec) * rcnt[q], cudaMemcpyDeviceToDevice, ctx->stream));
     }
     CKD(cudaStreamSynchronize(ctx->stream));
-    grp->barrier();                            // peers may now reuse their send buffers
+    LOOP_BARRIER(ctx);                         // peers may now reuse their send buffers
     return DI_OK;
   }
-  di_status host_max(di_ctx *, double v, double *out) override {
+  di_status host_max(di_ctx *ctx, double v, double *out) override {
     grp->hmax[rank] = v;
-    grp->barrier();
+    LOOP_BARRIER(ctx);
     double m = grp->hmax[0];
     for (int k = 1; k < grp->world; ++k) m = std::max(m, grp->hmax[k]);
-    grp->barrier();
+    LOOP_BARRIER(ctx);
     *out = m;
     return DI_OK;
   }
@@ -1011,7 +1040,7 @@ static di_status adapt_bounds(di_ctx *ctx, double r_k, long long work, std::vect
   return DI_OK;
 }
 
-di_status diter_dist_run(di_ctx *ctx, double target) {
+static di_status dist_run_impl(di_ctx *ctx, double target) {
   DistState *ds = ctx->dist;
   CKD(cudaSetDevice(ctx->device));
   CKD(cudaEventRecord(ctx->ev0, ctx->stream));
@@ -1129,6 +1158,16 @@ out:
   ctx->remote_pushes = (long long)h->remote_pushes;
   ctx->run_kernel_launches = ctx->kernel_launches - launches0;
   if (st == DI_ERR_NOT_CONVERGED) diter_set_err(ctx, "max_passes reached before |F|_1 < %g", target);
+  return st;
+}
+
+// A rank that fails inside the collective sequence releases its loopback peers
+// (they return DI_ERR_STATE instead of waiting forever).  max_passes is reached by
+// every rank in the same round (local pass counts advance together), so it is not
+// a failure of one rank.
+di_status diter_dist_run(di_ctx *ctx, double target) {
+  const di_status st = dist_run_impl(ctx, target);
+  if (st != DI_OK && st != DI_ERR_NOT_CONVERGED && ctx->dist && ctx->dist->fabric) ctx->dist->fabric->abort();
   return st;
 }
 
@@ -1563,7 +1602,10 @@ extern "C" di_status di_create_dist(di_ctx **out, int32_t rank, int32_t world, c
 #endif
   }
   di_status s = dist_build(ctx, col_ptr_local, row_idx_local, values_local, b_local, opt);
-  if (s != DI_OK) return fail(s);
+  if (s != DI_OK) {
+    ds->fabric->abort();
+    return fail(s);
+  }
   *out = ctx;
   return DI_OK;
 }

@@ -370,8 +370,11 @@ static di_status setup_far(di_ctx *ctx) {
   ctx->far.n_bins = n_bins;
   {
     // the far scatter stages records in 24 KB more shared memory per CTA: static +
-    // dynamic then exceed the default 48 KB, which needs the opt-in
-    const int dyn = (int)ctx->scatter_smem;
+    // dynamic then exceed the default 48 KB, which needs the opt-in.  The attribute is
+    // per function, process-wide: every context sets the same value (the largest
+    // prefix), so contexts of different sizes on concurrent threads never shrink the
+    // limit under one another's launches.
+    const int dyn = (int)(sizeof(int) * (size_t)(kMaxSegments + 1));
     CK(cudaFuncSetAttribute(k_scatter<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
     CK(cudaFuncSetAttribute(k_scatter<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
     int occ = 0;

@@ -36,9 +36,12 @@ def run_ranks(K, n, cp, ri, vals, b, d, target, bounds, mode, key, **opts):
         except Exception as e:          # surfaced below
             err[r] = e
 
-    th = [threading.Thread(target=worker, args=(r,)) for r in range(K)]
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(K)]
     for t in th:
         t.start()
+    for t in th:
+        t.join(timeout=900)             # a failed rank aborts the loopback group: peers return
+        assert not t.is_alive(), f"rank thread hung; errors: {err}"
     for t in th:
         t.join(timeout=600)
     for e in err:
@@ -186,9 +189,12 @@ def _run_ranks_fn(K, key, fn):
             out[r] = fn(r, cid)
         except Exception as e:
             err[r] = e
-    th = [threading.Thread(target=worker, args=(r,)) for r in range(K)]
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(K)]
     for t in th:
         t.start()
+    for t in th:
+        t.join(timeout=900)             # a failed rank aborts the loopback group: peers return
+        assert not t.is_alive(), f"rank thread hung; errors: {err}"
     for t in th:
         t.join(timeout=600)
     for e in err:

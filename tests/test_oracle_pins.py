@@ -522,3 +522,25 @@ def test_completed_pagerank_is_normalised_fluid_leaves_solution(seed):
     for _ in range(400):
         x = D * G @ x + (1 - D) / n
     np.testing.assert_allclose(Xc, x, rtol=1e-12, atol=1e-16)
+
+
+def test_identity_check_helper_catches_a_misrouted_push():
+    """tests/identity_check.py (the every-row check the full-scale GPU tests use) is ~0
+    on the oracle's state after real passes, and flags one push sent to the wrong row
+    (mass-conserving, so global checks miss it) at both rows it touched."""
+    import identity_check as ic
+    n = 3000
+    cp, ri = gen.web_graph(n, 4)
+    P = oracle.Problem(n, cp, ri)
+    st = P.init(1.5)
+    P.snapshot(st, 1e-30, oracle.HYBRID, 1.5, 0.05, max_passes=12)
+    b = np.full(n, 0.15 / n)
+    e, _ = ic.identity_residual(n, cp, ri, st.H, st.F, b, 0.85)
+    assert e <= 1e-13, e
+    F = st.F.copy()
+    j = int(np.argmax(st.F))
+    v = 0.5 * F[j]
+    F[j] -= v
+    F[(j + 17) % n] += v
+    e, row = ic.identity_residual(n, cp, ri, st.H, F, b, 0.85)
+    assert e > 1e-3 and row in (j, (j + 17) % n)
