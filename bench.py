@@ -98,8 +98,10 @@ def parse():
     ap.add_argument("--pass-csv", default=None, help="write the last solve's per-pass log here")
     ap.add_argument("--l2-persist", type=int, default=0,
                     help="options.l2_persist: 0 auto, -1 off, > 0 window MB (experiments)")
-    ap.add_argument("--exchange", default="async", choices=["sync", "async"],
-                    help="multi-GPU exchange mode (DESIGN.md: SYNC = per-pass rounds, ASYNC = paper's send rule)")
+    ap.add_argument("--exchange", default="p2p", choices=["sync", "async", "p2p"],
+                    help="multi-GPU exchange mode (DESIGN.md §6): sync = per-pass rounds, async = the paper's "
+                         "send rule in bulk rounds every rank joins, p2p = the paper's send rule with records "
+                         "written into the receivers' inbox rings (no collective per round; default)")
     ap.add_argument("--round-passes", type=int, default=4, help="N > 1, ASYNC: local passes per exchange round")
     ap.add_argument("--remote-push", type=int, default=1, choices=[0, 1],
                     help="N > 1: 0 per diffusion, 1 H increments at rounds (NEXT f2)")
@@ -371,7 +373,7 @@ def run_ours(args, rank, world, local_rank):
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     p = load_problem(args)
     pol = policy_of(args)
-    mode = di.DI_EXCHANGE_SYNC if args.exchange == "sync" else di.DI_EXCHANGE_ASYNC
+    mode = {"sync": di.DI_EXCHANGE_SYNC, "async": di.DI_EXCHANGE_ASYNC, "p2p": di.DI_EXCHANGE_P2P}[args.exchange]
     # N > 1 (ASYNC): exchange rounds every 4 passes, remote edges pushed as H
     # increments at the rounds (NEXT f2), receive-side T rescale --
     # DESIGN.md §6 "Multi-GPU" has the loopback measurements behind these choices
@@ -412,6 +414,7 @@ def run_ours(args, rank, world, local_rank):
     tot = {"run_ms": 0.0, "edges": 0, "passes": 0, "kt_scatter_ms": 0.0, "kt_select_ms": 0.0,
            "kt_finalize_ms": 0.0, "scatter_bytes": 0, "alg_bytes": 0, "run_kernel_launches": 0,
            "nodes": 0, "dangling": 0, "exchanged_bytes": 0, "exchanges": 0}
+    coll0 = di.di_get_stats(ctx)
     wall0 = time.perf_counter()
     with ClockSampler(local_rank) as clk:
         for _ in range(args.steps):
@@ -420,6 +423,7 @@ def run_ours(args, rank, world, local_rank):
                 tot[k] += s[k]
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
+    coll1 = di.di_get_stats(ctx)
     # Kernel durations for the roofline: the same K steps again with CUDA events
     # between the pass kernels (di_set_profile).  The events split the captured pass
     # graph and cost ~25 us of device time per pass, so `value` is timed without them.
@@ -452,7 +456,7 @@ def run_ours(args, rank, world, local_rank):
         tot["run_ms"] = float(t_.item())
         # di_stats.edges is the rank's own count under ASYNC but the global count under
         # SYNC (pass totals are all-reduced every pass): sum only the former
-        edges_all = int(e_[0].item()) if mode == di.DI_EXCHANGE_ASYNC else int(tot["edges"])
+        edges_all = int(e_[0].item()) if mode != di.DI_EXCHANGE_SYNC else int(tot["edges"])
         xbytes_all = int(e_[1].item())
     run_s = tot["run_ms"] / 1e3
     value = edges_all / run_s
@@ -526,6 +530,10 @@ def run_ours(args, rank, world, local_rank):
            "clocks": clocks,
            "nvlink_bytes_per_round": (xbytes_all / max(1, tot["exchanges"])) if dist else 0,
            "nvlink_bytes_per_solve": (xbytes_all / args.steps) if dist else 0,
+           # fabric collectives (all-reduce, all-to-all) and P2P confirmations per timed solve, rank 0
+           "collectives_per_solve": (coll1["collectives"] - coll0["collectives"]) / args.steps if dist else 0,
+           "confirms_per_solve": (coll1["confirms"] - coll0["confirms"]) / args.steps if dist else 0,
+           "exchange_bytes_resident": coll1["exchange_bytes_resident"] if dist else 0,
            "wall_s_timed": wall}
     if rank == 0:
         print(json.dumps(out), flush=True)
@@ -602,7 +610,7 @@ def run_e2e(args, p, opts, di, torch, rank=0, world=1, comm_id=None, bounds=None
         t_ = torch.tensor([dt, float(edges)], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t_[:1], op=torch.distributed.ReduceOp.MAX)
         e_ = t_[1:].clone()
-        if opts.exchange_mode == di.DI_EXCHANGE_ASYNC:     # SYNC edge counts are global already
+        if opts.exchange_mode != di.DI_EXCHANGE_SYNC:      # SYNC edge counts are global already
             torch.distributed.all_reduce(e_)
         dt, edges = float(t_[0].item()), float(e_[0].item())
     return {"value": edges / dt, "unit": "edges/s", "h2d_bytes_per_step": int(h2d),

@@ -94,7 +94,20 @@ enum {
 /* Exchange modes of distributed contexts. */
 enum {
   DI_EXCHANGE_SYNC = 0,    /* exchange + merge after every pass (reproduces the 1-GPU passes) */
-  DI_EXCHANGE_ASYNC = 1    /* send when s_k > r_k / K (eq. send) */
+  DI_EXCHANGE_ASYNC = 1,   /* send when s_k > r_k / K (eq. send), shipped in a
+                              bulk round every rank joins (counts, all-to-all-v, all-reduce) */
+  DI_EXCHANGE_P2P = 2      /* the paper's asynchronous scheme without a barrier (PAPER.md:50-53,
+                              223-256, 274-280, 516-521): each rank decides s_k > r_k / K on its
+                              own and writes the records straight into its inbox ring in the
+                              receiver's memory (CUDA IPC / NVLink, a system-scope release of the
+                              ring head); receivers merge whatever has arrived at the start of
+                              their next round.  Termination: a board of r_k + s_k + in-flight in
+                              every rank's memory triggers a quiesce-then-reduce confirmation,
+                              the only collectives of a run.  Needs remote_push =
+                              DI_REMOTE_INCREMENT, adapt_rounds = 0, <= 64 ranks; di_rebalance is
+                              not available.  Memory per rank: a compact outbox over the distinct
+                              remote rows of its columns, and inbox rings of twice the distinct
+                              rows each peer can send it */
 };
 
 typedef struct {
@@ -187,6 +200,12 @@ typedef struct {
                               their fluid leaves; the scatter never reads their col_ptr) */
   int64_t run_kernel_launches; /* kernels launched by the last di_run (graph nodes counted, including
                               passes of a graph launch that return at once after convergence) */
+  int64_t collectives;     /* distributed: fabric collectives (all-reduce, all-to-all, ...) since create,
+                              setup included -- one or more per round under SYNC / ASYNC, only at
+                              termination confirmations under P2P */
+  int64_t confirms;        /* DI_EXCHANGE_P2P: quiesce-then-reduce confirmations run since create */
+  int64_t exchange_bytes_resident; /* distributed: device bytes of the exchange state (outbox, flags,
+                              record buffers or inbox rings) */
 } di_stats;
 
 /* Fill *opt with the defaults above. */

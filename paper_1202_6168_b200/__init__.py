@@ -25,7 +25,7 @@ LIB_PATH = os.environ.get("DITER_LIB") or os.path.join(_HERE, "libditer.so")
 DI_OK, DI_ERR_INVALID_ARG, DI_ERR_CONTRACTION, DI_ERR_OOM, DI_ERR_CUDA, DI_ERR_NCCL, \
     DI_ERR_NOT_CONVERGED, DI_ERR_STATE, DI_ERR_UNSUPPORTED = range(9)
 DI_POLICY_GEOM, DI_POLICY_HYBRID = 0, 1
-DI_EXCHANGE_SYNC, DI_EXCHANGE_ASYNC = 0, 1
+DI_EXCHANGE_SYNC, DI_EXCHANGE_ASYNC, DI_EXCHANGE_P2P = 0, 1, 2
 DI_KEY_RAW, DI_KEY_EDGE, DI_KEY_PAPER = 0, 1, 2
 DI_REMOTE_PER_DIFFUSION, DI_REMOTE_INCREMENT, DI_REMOTE_RECEIVER = 0, 1, 2
 
@@ -81,7 +81,9 @@ class di_stats(ctypes.Structure):
                 ("kt_passes", ctypes.c_int64), ("scatter_bytes", ctypes.c_int64),
                 ("remote_pushes", ctypes.c_int64), ("rebalances", ctypes.c_int64),
                 ("l2_window_bytes", ctypes.c_int64), ("l2_window_row", ctypes.c_int64),
-                ("dangling", ctypes.c_int64), ("run_kernel_launches", ctypes.c_int64)]
+                ("dangling", ctypes.c_int64), ("run_kernel_launches", ctypes.c_int64),
+                ("collectives", ctypes.c_int64), ("confirms", ctypes.c_int64),
+                ("exchange_bytes_resident", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

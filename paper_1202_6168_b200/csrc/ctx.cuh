@@ -103,4 +103,5 @@ di_status diter_dist_max(di_ctx *ctx, double v, double *out);
 di_status diter_dist_sum(di_ctx *ctx, double v, double *out);
 di_status diter_dist_indegree(di_ctx *ctx, unsigned *indeg_local);   // DI_KEY_PAPER, collective
 di_status diter_dist_run(di_ctx *ctx, double target);
+void diter_dist_stats(const di_ctx *ctx, di_stats *s);   // collectives, confirmations, exchange memory
 di_status diter_dist_reset(di_ctx *ctx);

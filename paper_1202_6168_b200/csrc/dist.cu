@@ -38,6 +38,7 @@
 
 #include "../../include/diter.h"
 #include "ctx.cuh"
+#include "dist.cuh"
 #include "kernels.cuh"
 
 #if DITER_WITH_NCCL
@@ -62,29 +63,6 @@ using namespace diter;
     if (s_ != DI_OK) return s_;     \
   } while (0)
 
-// One exchanged record: destination row (local to the receiver) and fluid.
-struct Rec {
-  long long row;
-  double val;
-};
-
-// ------------------------------------------------------------------ fabric --
-struct Fabric {
-  virtual ~Fabric() {}
-  // in-place sum over ranks of `count` doubles on the device
-  virtual di_status allreduce_sum(di_ctx *ctx, double *dev, int count) = 0;
-  // host-side exchange of per-peer record counts
-  virtual di_status alltoall_counts(di_ctx *ctx, const long long *send, long long *recv) = 0;
-  // records: send[soff[q] .. soff[q]+scnt[q]) to peer q, into recv[roff[q] ..]
-  virtual di_status alltoallv(di_ctx *ctx, const Rec *send, const long long *soff, const long long *scnt,
-                              Rec *recv, const long long *roff, const long long *rcnt) = 0;
-  // max over ranks of one host double (setup: T_0, validation agreement)
-  virtual di_status host_max(di_ctx *ctx, double v, double *out) = 0;
-  // a rank failed mid-collective-sequence: release the peers (loopback) instead of
-  // leaving them waiting
-  virtual void abort() {}
-};
-
 // In-process loopback: K contexts (one host thread each) on one device.
 struct LoopGroup {
   int world = 0;
@@ -97,6 +75,7 @@ struct LoopGroup {
   std::vector<const Rec *> sendp;
   std::vector<std::vector<long long>> soff, scnt;
   std::vector<double> hmax;
+  std::vector<unsigned char> gath;         // allgather staging
 
   explicit LoopGroup(int w) : world(w), red(w * 8), counts(w * w), sendp(w), soff(w), scnt(w), hmax(w) {}
 
@@ -146,7 +125,21 @@ struct LoopFabric : Fabric {
   LoopFabric(std::shared_ptr<LoopGroup> g, int r) : grp(std::move(g)), rank(r) {}
   void abort() override { grp->abort(); }
 
+  di_status allgather(di_ctx *ctx, const void *mine, size_t bytes, void *all) override {
+    ++calls;
+    {
+      std::lock_guard<std::mutex> lk(grp->mu);
+      if (grp->gath.size() < bytes * grp->world) grp->gath.resize(bytes * grp->world);
+    }
+    LOOP_BARRIER(ctx);
+    std::memcpy(grp->gath.data() + bytes * rank, mine, bytes);
+    LOOP_BARRIER(ctx);
+    std::memcpy(all, grp->gath.data(), bytes * grp->world);
+    LOOP_BARRIER(ctx);
+    return DI_OK;
+  }
   di_status allreduce_sum(di_ctx *ctx, double *dev, int count) override {
+    ++calls;
     if (count > 8) return DI_ERR_INVALID_ARG;
     double h[8];
     CKD(cudaMemcpyAsync(h, dev, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
@@ -164,6 +157,7 @@ struct LoopFabric : Fabric {
     return DI_OK;
   }
   di_status alltoall_counts(di_ctx *ctx, const long long *send, long long *recv) override {
+    ++calls;
     const int W = grp->world;
     for (int q = 0; q < W; ++q) grp->counts[rank * W + q] = send[q];
     LOOP_BARRIER(ctx);
@@ -173,6 +167,7 @@ struct LoopFabric : Fabric {
   }
   di_status alltoallv(di_ctx *ctx, const Rec *send, const long long *soff, const long long *scnt, Rec *recv,
                       const long long *roff, const long long *rcnt) override {
+    ++calls;
     const int W = grp->world;
     CKD(cudaStreamSynchronize(ctx->stream));   // send buffer complete
     grp->sendp[rank] = send;
@@ -189,6 +184,7 @@ struct LoopFabric : Fabric {
     return DI_OK;
   }
   di_status host_max(di_ctx *ctx, double v, double *out) override {
+    ++calls;
     grp->hmax[rank] = v;
     LOOP_BARRIER(ctx);
     double m = grp->hmax[0];
@@ -220,10 +216,27 @@ struct NcclFabric : Fabric {
     if (comm) ncclCommDestroy(comm);
   }
   di_status allreduce_sum(di_ctx *ctx, double *dev, int count) override {
+    ++calls;
     CKN(ncclAllReduce(dev, dev, count, ncclDouble, ncclSum, comm, ctx->stream));
     return DI_OK;
   }
+  di_status allgather(di_ctx *ctx, const void *mine, size_t bytes, void *all) override {
+    ++calls;
+    unsigned char *d = nullptr;
+    CKD(cudaMalloc(&d, bytes * (world + 1)));
+    di_status st = DI_OK;
+    if (cudaMemcpyAsync(d + bytes * world, mine, bytes, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
+        ncclAllGather(d + bytes * world, d, bytes, ncclChar, comm, ctx->stream) != ncclSuccess ||
+        cudaMemcpyAsync(all, d, bytes * world, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+      diter_set_err(ctx, "NCCL allgather failed");
+      st = DI_ERR_NCCL;
+    }
+    cudaFree(d);
+    return st;
+  }
   di_status alltoall_counts(di_ctx *ctx, const long long *send, long long *recv) override {
+    ++calls;
     CKD(cudaMemcpyAsync(d_cnt, send, sizeof(long long) * world, cudaMemcpyHostToDevice, ctx->stream));
     CKN(ncclGroupStart());
     for (int q = 0; q < world; ++q) {
@@ -237,6 +250,7 @@ struct NcclFabric : Fabric {
   }
   di_status alltoallv(di_ctx *ctx, const Rec *send, const long long *soff, const long long *scnt, Rec *recv,
                       const long long *roff, const long long *rcnt) override {
+    ++calls;
     CKN(ncclGroupStart());
     for (int q = 0; q < world; ++q) {
       if (q == rank) continue;
@@ -247,6 +261,7 @@ struct NcclFabric : Fabric {
     return DI_OK;
   }
   di_status host_max(di_ctx *ctx, double v, double *out) override {
+    ++calls;
     if (!d_tmp) CKD(cudaMalloc(&d_tmp, sizeof(double)));
     CKD(cudaMemcpyAsync(d_tmp, &v, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     CKN(ncclAllReduce(d_tmp, d_tmp, 1, ncclDouble, ncclMax, comm, ctx->stream));
@@ -257,31 +272,6 @@ struct NcclFabric : Fabric {
   }
 };
 #endif
-
-// ------------------------------------------------------------ dist state --
-struct DistState {
-  std::unique_ptr<Fabric> fabric;
-  std::vector<long long> bounds;       // [world + 1]
-  long long *d_bounds = nullptr;
-  Rec *send = nullptr, *recv = nullptr;
-  long long send_cap = 0, recv_cap = 0;
-  long long *d_scnt = nullptr;         // [world] records compacted per peer
-  double *d_sums = nullptr;            // [kSums + 3] + [world] long long (send offsets)
-  std::vector<long long> soff, scnt, roff, rcnt;
-  double s_k = 0.0;                    // outbox mass (ASYNC)
-  // DI_REMOTE_RECEIVER (NEXT f3).  Sender: per peer q the local
-  // columns with at least one row in Omega_q, cols[pair_off[q] ..).  Receiver: the
-  // remote in-edges of the owned rows grouped by source column: ric_src sorted
-  // global source ids, edges [ric_off[k], ric_off[k+1]) of (ric_row local row,
-  // ric_p weight p_ij).
-  int *cols = nullptr;
-  long long *d_pair_off = nullptr;     // [world + 1]
-  std::vector<long long> pair_off;
-  long long *ric_src = nullptr, *ric_off = nullptr;
-  int *ric_row = nullptr;
-  double *ric_p = nullptr;
-  long long ric_n = 0, ric_e = 0;
-};
 
 // ----------------------------------------------------------------- kernels --
 // Records of the outbox rows owned by peer q, compacted block by block: a warp
@@ -622,6 +612,7 @@ __global__ void k_set_target(Ctl *ctl, double target, long long max_pass, int do
 // ------------------------------------------------------------ host helpers --
 void diter_dist_free(di_ctx *ctx) {
   if (!ctx || !ctx->dist) return;
+  p2p_free(ctx);
   DistState *ds = ctx->dist;
   void *ptrs[] = {ds->d_bounds, ds->send, ds->recv, ds->d_scnt, ds->d_sums, ds->cols, ds->d_pair_off,
                   ds->ric_src, ds->ric_off, ds->ric_row, ds->ric_p};
@@ -708,6 +699,20 @@ di_status diter_dist_max(di_ctx *ctx, double v, double *out) {
   return ctx->dist->fabric->host_max(ctx, v, out);
 }
 
+void diter_dist_stats(const di_ctx *ctx, di_stats *s) {
+  const DistState *ds = ctx->dist;
+  if (!ds) return;
+  s->collectives = ds->fabric ? ds->fabric->calls : 0;
+  s->confirms = ds->p2p.confirms;
+  if (ds->p2p.on) {
+    s->exchange_bytes_resident = (long long)(ds->p2p.m * (sizeof(double) + sizeof(int)) + ((ds->p2p.m + 31) >> 5) +
+                                             ds->p2p.win_bytes);
+  } else {
+    s->exchange_bytes_resident = (long long)(ctx->n_rows * sizeof(double) + ((ctx->n_rows + 31) >> 5) +
+                                             (ds->send_cap + ds->recv_cap) * sizeof(Rec));
+  }
+}
+
 di_status diter_dist_sum(di_ctx *ctx, double v, double *out) {
   *out = v;
   if (!ctx->dist) return DI_OK;
@@ -721,6 +726,7 @@ di_status diter_dist_sum(di_ctx *ctx, double v, double *out) {
 
 di_status diter_dist_reset(di_ctx *ctx) {
   if (!ctx->dist) return DI_OK;
+  if (ctx->dist->p2p.on) return p2p_reset(ctx);
   CKD(cudaMemsetAsync(ctx->G, 0, sizeof(double) * ctx->n_rows, ctx->stream));
   CKD(cudaMemsetAsync(ctx->dflags, 0, (size_t)((ctx->n_rows + 31) >> 5), ctx->stream));
   if (ctx->H_old) CKD(cudaMemsetAsync(ctx->H_old, 0, sizeof(double) * ctx->n_local, ctx->stream));
@@ -730,10 +736,21 @@ di_status diter_dist_reset(di_ctx *ctx) {
 }
 
 // DI_REMOTE_INCREMENT: push H - H_old along the remote edges into the outbox.
-static void push_increment(di_ctx *ctx) {
+void dist_push_increment(di_ctx *ctx) {
   k_push_increment<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->col_ptr, ctx->nloc, ctx->row_idx, ctx->vals,
                                                               ctx->d, ctx->H, ctx->H_old, ctx->n_local, ctx->G,
                                                               ctx->dflags, &ctx->ctl->remote_pushes);
+  ctx->kernel_launches += 1;
+}
+
+void dist_pending_mass(di_ctx *ctx, double *out) {
+  k_pending_mass<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->col_ptr, ctx->nloc, ctx->vals, ctx->d, ctx->H,
+                                                            ctx->H_old, ctx->n_local, out);
+  ctx->kernel_launches += 1;
+}
+
+void dist_set_target(di_ctx *ctx, double target, long long max_pass) {
+  k_set_target<<<1, 1, 0, ctx->stream>>>(ctx->ctl, target, max_pass, 0);
   ctx->kernel_launches += 1;
 }
 
@@ -958,7 +975,7 @@ static di_status exchange_receiver(di_ctx *ctx, bool send_now) {
 // One exchange round in the context's remote-push mode (collective).
 static di_status round_exchange(di_ctx *ctx, bool send_now) {
   if (ctx->opt.remote_push == DI_REMOTE_RECEIVER) return exchange_receiver(ctx, send_now);
-  if (ctx->opt.remote_push == DI_REMOTE_INCREMENT && send_now) push_increment(ctx);
+  if (ctx->opt.remote_push == DI_REMOTE_INCREMENT && send_now) dist_push_increment(ctx);
   return exchange(ctx, send_now);
 }
 
@@ -982,7 +999,7 @@ static di_status prof_collect(di_ctx *ctx, int npasses) {
   return DI_OK;
 }
 
-static void launch_pass_kernels(di_ctx *ctx, int slot) {
+void dist_launch_pass_kernels(di_ctx *ctx, int slot) {
   Graph g = diter_graph(ctx);
   prof_mark(ctx, slot, 0);
   k_select<<<ctx->grid_select, kSelectThreads, 0, ctx->stream>>>(ctx->F, ctx->H, ctx->fr, ctx->n_local, ctx->ctl,
@@ -1041,6 +1058,7 @@ static di_status adapt_bounds(di_ctx *ctx, double r_k, long long work, std::vect
 }
 
 static di_status dist_run_impl(di_ctx *ctx, double target) {
+  if (ctx->dist->p2p.on) return p2p_run(ctx, target);
   DistState *ds = ctx->dist;
   CKD(cudaSetDevice(ctx->device));
   CKD(cudaEventRecord(ctx->ev0, ctx->stream));
@@ -1059,7 +1077,7 @@ static di_status dist_run_impl(di_ctx *ctx, double target) {
     // -------- SYNC: one exchange per pass, pass totals all-reduced ----------
     k_set_target<<<1, 1, 0, ctx->stream>>>(ctx->ctl, target, max_pass_abs, 0);
     for (;;) {
-      launch_pass_kernels(ctx, 0);
+      dist_launch_pass_kernels(ctx, 0);
       k_reduce_partials<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->ctl, ctx->sel_part, ctx->grid_select,
                                                                   ctx->sc_part, ctx->grid_scatter, ds->d_sums);
       TRYD(ds->fabric->allreduce_sum(ctx, ds->d_sums, kSums));
@@ -1083,11 +1101,18 @@ static di_status dist_run_impl(di_ctx *ctx, double target) {
     for (;;) {
       // local passes: no target (never "done" locally), local threshold policy
       k_set_target<<<1, 1, 0, ctx->stream>>>(ctx->ctl, 0.0, max_pass_abs, 0);
-      for (int k = 0; k < ctx->check_interval; ++k) {
-        launch_pass_kernels(ctx, k);
-        k_finalize<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->ctl, ctx->sel_part, ctx->grid_select, ctx->sc_part,
-                                                            ctx->grid_scatter, ctx->log);
-        ctx->kernel_launches += 1;
+      if (ctx->graph_exec && !ctx->opt.profile) {
+        // the round's local passes as one captured graph (select, scatter, hubs, finalize)
+        CKD(cudaGraphLaunch(ctx->graph_exec, ctx->stream));
+        ctx->graph_launches += 1;
+        ctx->kernel_launches += (3LL + (ctx->cap_hub > 0)) * ctx->check_interval;
+      } else {
+        for (int k = 0; k < ctx->check_interval; ++k) {
+          dist_launch_pass_kernels(ctx, k);
+          k_finalize<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->ctl, ctx->sel_part, ctx->grid_select, ctx->sc_part,
+                                                              ctx->grid_scatter, ctx->log);
+          ctx->kernel_launches += 1;
+        }
       }
       // round: s_k (outbox mass, or the pending increment mass) and r_k decide the
       // send (eq. send)
@@ -1202,6 +1227,10 @@ const unsigned char *get(const unsigned char *c, T *p, size_t n) {
 extern "C" di_status di_rebalance(di_ctx *ctx, const int64_t *nb) {
   if (!ctx || !nb) { diter_set_err(ctx, "NULL argument"); return DI_ERR_INVALID_ARG; }
   if (!ctx->dist || ctx->world < 2) { diter_set_err(ctx, "di_rebalance: distributed contexts only"); return DI_ERR_INVALID_ARG; }
+  if (ctx->dist->p2p.on) {
+    diter_set_err(ctx, "di_rebalance: not available with DI_EXCHANGE_P2P (its outbox slots are fixed at create)");
+    return DI_ERR_UNSUPPORTED;
+  }
   const int W = ctx->world, rank = ctx->rank;
   if (nb[0] != 0 || nb[W] != ctx->n_rows) { diter_set_err(ctx, "bounds must start at 0 and end at N"); return DI_ERR_INVALID_ARG; }
   for (int k = 0; k < W; ++k)
@@ -1412,6 +1441,17 @@ static di_status dist_build_local(di_ctx *ctx, const int64_t *col_ptr_local, con
   const long long n_global = ctx->n_rows, nl = ctx->n_local;
   di_status s = diter_setup(ctx, col_ptr_local, row_idx_local, values_local, b_local, opt);
   if (s != DI_OK) return s;
+  if (ctx->opt.exchange_mode != DI_EXCHANGE_SYNC && ctx->opt.exchange_mode != DI_EXCHANGE_ASYNC &&
+      ctx->opt.exchange_mode != DI_EXCHANGE_P2P) {
+    diter_set_err(ctx, "exchange_mode must be DI_EXCHANGE_SYNC, _ASYNC or _P2P");
+    return DI_ERR_INVALID_ARG;
+  }
+  if (ctx->opt.exchange_mode == DI_EXCHANGE_P2P &&
+      (ctx->opt.remote_push != DI_REMOTE_INCREMENT || ctx->opt.adapt_rounds != 0 || world > kP2PMaxWorld)) {
+    diter_set_err(ctx, "DI_EXCHANGE_P2P needs remote_push = DI_REMOTE_INCREMENT, adapt_rounds = 0 and <= %d ranks",
+                  kP2PMaxWorld);
+    return DI_ERR_INVALID_ARG;
+  }
   // local rows first in every column (nloc), in place via a scratch copy
   {
     const long long n = ctx->n_local, nnz = ctx->nnz_local;
@@ -1452,8 +1492,22 @@ static di_status dist_build_local(di_ctx *ctx, const int64_t *col_ptr_local, con
       return (DI_ERR_INVALID_ARG);
     }
   }
-  // outbox, flags, exchange buffers
-  {
+  // outbox, flags, exchange buffers (P2P: the compact outbox is built by p2p_setup,
+  // and no bulk send/receive buffers exist)
+  const bool p2p = ctx->opt.exchange_mode == DI_EXCHANGE_P2P;
+  if (p2p) {
+    ds->p2p.on = true;
+    if (cudaMalloc(&ds->d_bounds, sizeof(long long) * (world + 1)) != cudaSuccess ||
+        cudaMalloc(&ds->d_sums, sizeof(double) * (kSums + 3) + sizeof(long long) * world) != cudaSuccess) {
+      diter_set_err(ctx, "cudaMalloc (exchange buffers) failed");
+      return (DI_ERR_OOM);
+    }
+    cudaMemcpyAsync(ds->d_bounds, ds->bounds.data(), sizeof(long long) * (world + 1), cudaMemcpyHostToDevice, ctx->stream);
+    ds->soff.assign(world, 0);
+    ds->scnt.assign(world, 0);
+    ds->roff.assign(world, 0);
+    ds->rcnt.assign(world, 0);
+  } else {
     const long long nb = (n_global + 31) >> 5;
     if (diter_alloc(ctx, (void **)&ctx->G, sizeof(double) * n_global) != DI_OK ||
         diter_alloc(ctx, (void **)&ctx->dflags, (size_t)nb) != DI_OK) {
@@ -1506,7 +1560,8 @@ static di_status dist_build(di_ctx *ctx, const int64_t *col_ptr_local, const int
   }
   TRYD(diter_setup_finish(ctx));
   if (ctx->opt.remote_push == DI_REMOTE_RECEIVER) TRYD(setup_receiver(ctx));
-  if (ctx->opt.exchange_mode == DI_EXCHANGE_ASYNC) {
+  if (ctx->dist->p2p.on) TRYD(p2p_setup(ctx));
+  if (ctx->opt.exchange_mode != DI_EXCHANGE_SYNC) {
     ctx->ctl_init.n_total = (double)ctx->n_local;
     CKD(cudaMemcpyAsync(ctx->ctl, &ctx->ctl_init, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream));
     CKD(cudaStreamSynchronize(ctx->stream));

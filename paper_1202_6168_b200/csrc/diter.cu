@@ -463,11 +463,14 @@ static di_status capture_graph(di_ctx *ctx) {
     k_select<<<ctx->grid_select, kSelectThreads, 0, ctx->stream>>>(ctx->F, ctx->H, ctx->fr, ctx->n_local,
                                                                   ctx->ctl, ctx->sel_part, ctx->kw);
     if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 1], ctx->stream, cudaEventRecordExternal));
+    // a distributed rank's scatter routes rows outside its range (DIST): its ASYNC / P2P
+    // rounds launch this graph for their local passes
+    const bool dist = ctx->world > 1;
     if (ctx->vals)
-      (ctx->far.on ? k_scatter<true, false, true> : k_scatter<true, false, false>)
+      (dist ? k_scatter<true, true, false> : ctx->far.on ? k_scatter<true, false, true> : k_scatter<true, false, false>)
           <<<ctx->grid_scatter, kScatterThreads, ctx->scatter_smem, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part);
     else
-      (ctx->far.on ? k_scatter<false, false, true> : k_scatter<false, false, false>)
+      (dist ? k_scatter<false, true, false> : ctx->far.on ? k_scatter<false, false, true> : k_scatter<false, false, false>)
           <<<ctx->grid_scatter, kScatterThreads, ctx->scatter_smem, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part);
     if (ctx->cap_hub > 0) {
       if (ctx->vals)
@@ -833,7 +836,7 @@ extern "C" di_status di_set_profile(di_ctx *ctx, int32_t on) {
     CK(cudaGraphExecDestroy(ctx->graph_exec));
     ctx->graph_exec = nullptr;
   }
-  if (ctx->world == 1 && !ctx->fused) TRY(capture_graph(ctx));
+  if (!ctx->fused) TRY(capture_graph(ctx));
   return DI_OK;
 }
 
@@ -951,6 +954,7 @@ extern "C" di_status di_get_stats(const di_ctx *ctx, di_stats *s) {
   s->rebalances = ctx->rebalances;
   s->l2_window_bytes = ctx->l2_bytes;
   s->l2_window_row = ctx->l2_bytes > 0 ? ctx->lo + ctx->l2_lo : 0;
+  diter_dist_stats(ctx, s);
   return DI_OK;
 }
 

@@ -113,3 +113,172 @@ class RankModel:
                 self.exchanged += sent
                 return R
         raise RuntimeError("no convergence")
+
+
+# ------------------------------------------------------------------ P2P model --
+# DI_EXCHANGE_P2P (csrc/p2p.cu) as a protocol model: every rank owns a window in
+# POSIX shared memory (header: head/tail/acked/board per peer and the quiesce
+# epoch; one inbox ring per peer), ranks run rounds at their own pace (merge what
+# has arrived, local passes, board, send rule with records written straight into
+# the receiver's ring and the head published after them), and gloo collectives
+# appear only in the quiesce-then-reduce confirmation and at the start of a run.
+
+class P2PWindow:
+    """Header + per-peer rings over one shared-memory block (the device window)."""
+
+    def __init__(self, shm, world, cap):
+        W = world
+        self.shm, self.cap = shm, cap
+        buf, off = shm.buf, 0
+
+        def view(dtype, count):
+            nonlocal off
+            a = np.ndarray((count,), dtype=dtype, buffer=buf, offset=off)
+            off += a.nbytes
+            return a
+        self.head = view(np.uint64, W)
+        self.tail = view(np.uint64, W)
+        self.acked = view(np.float64, W)
+        self.board = view(np.float64, W)
+        self.quiesce = view(np.uint64, 1)
+        self.rows = [view(np.int64, cap) for _ in range(W)]
+        self.vals = [view(np.float64, cap) for _ in range(W)]
+
+    @staticmethod
+    def nbytes(world, cap):
+        return 8 * (4 * world + 1) + 16 * cap * world
+
+
+class P2PRank(RankModel):
+    def __init__(self, rank, world, bounds, cp, ri, b_local, n, key, **kw):
+        from multiprocessing import shared_memory
+        super().__init__(rank, world, bounds, cp, ri, b_local, n, **kw)
+        self.cap = 2 * n + 64
+        self.collectives = 0
+        size = P2PWindow.nbytes(world, self.cap)
+        self._mine = shared_memory.SharedMemory(name=f"{key}_{rank}", create=True, size=size)
+        self.win = P2PWindow(self._mine, world, self.cap)
+        self.win.head[:] = 0
+        self.win.tail[:] = 0
+        self.win.acked[:] = 0.0
+        self.win.board[:] = np.inf
+        self.win.quiesce[:] = 0
+        dist.barrier()
+        self._peers = [shared_memory.SharedMemory(name=f"{key}_{q}") if q != rank else None for q in range(world)]
+        self.peer = [P2PWindow(s, world, self.cap) if s is not None else self.win for s in self._peers]
+        self.head_out = np.zeros(world, dtype=np.uint64)
+        self.tail_in = np.zeros(world, dtype=np.uint64)
+        self.sent = np.zeros(world)
+        self.merged = np.zeros(world)
+        self.epoch = 0
+        self.confirms = 0
+
+    def close(self):
+        dist.barrier()
+        for s in self._peers:
+            if s is not None:
+                s.close()
+        self._mine.close()
+        dist.barrier()
+        self._mine.unlink()
+
+    def _coll(self, x):
+        self.collectives += 1
+        return _allreduce(x)
+
+    def _merge(self):
+        for q in range(self.world):
+            if q == self.rank:
+                continue
+            h = int(self.win.head[q])                 # snapshot (acquire)
+            t = int(self.tail_in[q])
+            if h == t:
+                continue
+            pos = np.arange(t, h) % self.cap
+            rows, vals = self.win.rows[q][pos].copy(), self.win.vals[q][pos].copy()
+            np.add.at(self.F, rows, vals)
+            self.tail_in[q] = h
+            self.merged[q] += float(np.abs(vals).sum())
+            self.peer[q].acked[self.rank] = self.merged[q]     # into the sender's header
+            self.peer[q].tail[self.rank] = h
+
+    def _send(self, mask):
+        for q in range(self.world):
+            if q == self.rank or not (mask >> q) & 1:
+                continue
+            a, b = int(self.bounds[q]), int(self.bounds[q + 1])
+            idx = np.nonzero(self.G[a:b])[0]
+            if len(idx) == 0:
+                continue
+            ring = self.peer[q]
+            pos = (int(self.head_out[q]) + np.arange(len(idx))) % self.cap
+            ring.rows[self.rank][pos] = idx
+            ring.vals[self.rank][pos] = self.G[a:b][idx]
+            self.sent[q] += float(np.abs(self.G[a:b][idx]).sum())
+            self.exchanged += len(idx)
+            self.G[a:b][idx] = 0.0
+            self.head_out[q] += len(idx)
+            ring.head[self.rank] = self.head_out[q]           # published after the records
+
+    def _board(self):
+        inflight = sum(self.sent[q] - self.win.acked[q] for q in range(self.world) if q != self.rank)
+        v = float(np.abs(self.F).sum()) + float(np.abs(self.G).sum()) + max(inflight, 0.0)
+        for q in range(self.world):
+            self.peer[q].board[self.rank] = v
+
+    def _confirm(self, my_oop):
+        self.confirms += 1
+        everyone = sum(1 << q for q in range(self.world) if q != self.rank)
+        self._merge()
+        self._coll(0.0)                # every publish of the round loops done
+        self._merge()
+        self._coll(0.0)                # every ring consumed
+        self._send(everyone)
+        self._coll(0.0)                # flushes published
+        self._merge()
+        self.collectives += 1
+        t = torch.tensor([float(np.abs(self.F).sum()), 1.0 if my_oop else 0.0], dtype=torch.float64)
+        dist.all_reduce(t)
+        self.epoch += 1
+        return float(t[0]), float(t[1]) > 0
+
+    def run_p2p(self, target, m=4, max_rounds=20000, delay=None):
+        import time
+        nl = self.hi - self.lo
+        R = self._coll(float(np.abs(self.F).sum()))
+        if R < target:
+            return R
+        for rnd in range(max_rounds):
+            self._merge()
+            for _ in range(m):
+                cnt = self._pass()
+                self.log.append((self.T, cnt))
+                if cnt <= self.f * nl:
+                    self.T /= self.alpha
+            if delay:
+                time.sleep(delay(rnd))
+            self._board()
+            s_k = float(np.abs(self.G).sum())
+            r_k = float(np.abs(self.F).sum())
+            oop = rnd + 1 >= max_rounds
+            if int(self.win.quiesce[0]) > self.epoch or float(self.win.board.sum()) < target or oop:
+                if int(self.win.quiesce[0]) <= self.epoch:
+                    for q in range(self.world):
+                        self.peer[q].quiesce[0] = self.epoch + 1
+                R, any_oop = self._confirm(oop)
+                if R < target:
+                    return R
+                if any_oop:
+                    raise RuntimeError("no convergence")
+                self._board()
+                continue
+            if s_k > r_k / self.world or (r_k == 0.0 and s_k > 0.0):
+                mask = 0
+                for q in range(self.world):
+                    if q == self.rank:
+                        continue
+                    used = int(self.head_out[q]) - int(self.win.tail[q])
+                    if self.cap - used >= self.bounds[q + 1] - self.bounds[q]:
+                        mask |= 1 << q
+                self._send(mask)
+        raise RuntimeError("no convergence")

@@ -98,6 +98,57 @@ def _protocol(rank, world, port, mode):
         dist.destroy_process_group()
 
 
+def _p2p_protocol(rank, world, port, key):
+    _init(rank, world, port)
+    try:
+        import diter_inputs as gen
+        import oracle
+        from dist_model import P2PRank
+        from paper_1202_6168_b200 import dist as dd
+        n = 4000
+        cp, ri = gen.web_graph(n, 6, window=100, max_deg=300)
+        rng = np.random.default_rng(1)
+        b = rng.random(n) + 0.5
+        b *= 0.15 / b.sum()
+        bounds = dd.partition_bounds(cp, world)
+        lcp, lri, _, lb = dd.shard_csc(cp, ri, None, b, bounds, rank)
+        m = P2PRank(rank, world, bounds, lcp, lri, lb, n, key)
+        target = 1e-10 * 0.15
+        # rank 1 runs its rounds slower: the ranks drift apart, messages arrive late
+        delay = (lambda r: 0.002 * ((r * 7919) % 3)) if rank == 1 else None
+        try:
+            R = m.run_p2p(target, delay=delay)
+        finally:
+            m.close()
+        out = [None] * world
+        dist.all_gather_object(out, (m.H.tolist(), m.F.tolist(), m.exchanged, m.collectives, m.confirms,
+                                     len(m.log)))
+        H = np.concatenate([np.asarray(h[0]) for h in out])
+        F = np.concatenate([np.asarray(h[1]) for h in out])
+        X = oracle.Problem(n, cp, ri, None, b).solve(1e-14 * 0.15).H
+        assert np.abs(H - X).sum() <= 1e-8 * 0.15
+        deg = np.diff(cp)
+        ledger = np.abs(F).sum() + 0.15 * H.sum() + 0.85 * H[deg == 0].sum()
+        assert abs(ledger - 0.15) <= 1e-13                    # nothing lost or duplicated in flight
+        assert R < target and np.abs(F).sum() < target
+        assert sum(h[2] for h in out) > 0
+        for h in out:
+            # one all-reduce to start the run + four per confirmation, none per round
+            assert h[3] == 1 + 4 * h[4] and h[4] >= 1
+            assert h[5] // 4 > 3 * h[4]                       # rounds >> confirmations
+    finally:
+        dist.destroy_process_group()
+
+
+def test_p2p_protocol_two_ranks():
+    """The barrier-free exchange (DI_EXCHANGE_P2P) as a protocol: shared-memory windows
+    with inbox rings and published heads, ranks drifting apart, board-triggered
+    quiesce-then-reduce termination -- parity, closed ledger, collectives only in the
+    confirmations."""
+    key = f"dip2p{os.getpid()}"
+    mp.spawn(_p2p_protocol, args=(2, _free_port(), key), nprocs=2, join=True)
+
+
 def test_host_logic_two_ranks():
     mp.spawn(_host_logic, args=(2, _free_port()), nprocs=2, join=True)
 

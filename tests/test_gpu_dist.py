@@ -339,3 +339,118 @@ def test_dist_profile_kernel_times(mode):
         s = o[3]
         assert s["kt_scatter_ms"] > 0 and s["kt_select_ms"] > 0
         assert s["kt_passes"] == s["passes"]
+
+
+# ---------------------------------------------------------------- P2P exchange --
+# DI_EXCHANGE_P2P (csrc/p2p.cu): the paper's send rule with records written straight
+# into the receiver's inbox ring (here: contexts of one process map each other's
+# windows by pointer), merges at the start of each round, and a board-triggered
+# quiesce-then-reduce confirmation as the only collectives of a run.
+
+def _p2p_opts(**kw):
+    return dict(check_interval=4, remote_push=di.DI_REMOTE_INCREMENT, **kw)
+
+
+@pytest.mark.parametrize("K,cost", [(2, "out"), (3, "inout"), (4, "out"), (8, "out")])
+def test_p2p_parity_ledger_and_no_collective_per_round(K, cost):
+    """Parity with the oracle's fixed point, a closed mass ledger (nothing lost or
+    duplicated in flight), the global residual on every rank -- and the collective
+    count of the run: one all-reduce at its start plus four per confirmation, however
+    many rounds ran (the bulk ASYNC rounds need >= 3 per round)."""
+    p = gen.config("C2", 2, n=300_000)
+    bn = 0.15
+    bounds = dist.partition_bounds(p.col_ptr, K, cost=cost, row_idx=p.row_idx)
+
+    def fn(r, cid):
+        lcp, lri, lv, lb = dist.shard_csc(p.col_ptr, p.row_idx, None, None, bounds, r)
+        o = di.default_options(exchange_mode=di.DI_EXCHANGE_P2P, **_p2p_opts())
+        ctx = di.di_create_dist(r, K, cid, bounds, p.n, lcp, lri, lv, lb, p.d, o)
+        c0 = di.di_get_stats(ctx)["collectives"]
+        di.di_run(ctx, p.parity_stop)
+        st = di.di_get_stats(ctx)
+        out = (di.di_get_history(ctx), di.di_get_fluid(ctx), st, st["collectives"] - c0,
+               di.di_get_residual(ctx), di.di_get_pagerank(ctx))
+        di.di_destroy(ctx)
+        return out
+    outs = _run_ranks_fn(K, f"p2p{K}{cost}", fn)
+    H = np.concatenate([o[0] for o in outs])
+    F = np.concatenate([o[1] for o in outs])
+    X = oracle.Problem(p.n, p.col_ptr, p.row_idx).solve(1e-12 * bn * 0.15).H
+    assert np.abs(H - X).sum() <= 1e-8 * bn
+    deg = np.diff(p.col_ptr)
+    ledger = np.abs(F).sum() + 0.15 * H.sum() + 0.85 * H[deg == 0].sum()
+    assert abs(ledger - bn) <= 1e-12 * bn
+    for o in outs:
+        st, run_coll = o[2], o[3]
+        assert o[4] < p.parity_stop
+        rounds = st["passes"] // 4
+        assert st["confirms"] >= 1 and rounds > 3 * st["confirms"], (rounds, st["confirms"])
+        assert run_coll == 1 + 4 * st["confirms"], (run_coll, st["confirms"])
+        assert st["exchanges"] > 0 and st["exchanged_bytes"] > 0
+    Xp = np.concatenate([o[5] for o in outs])
+    assert abs(Xp.sum() - 1.0) <= 1e-12
+
+
+def test_p2p_memory_scales_with_ranks():
+    """Per-rank exchange memory: the compact outbox and inbox rings of P2P shrink as K
+    grows and stay below the bulk mode's dense outbox of N doubles."""
+    p = gen.config("C2", 1, n=400_000)
+    per = {}
+    for mode in (di.DI_EXCHANGE_ASYNC, di.DI_EXCHANGE_P2P):
+        for K in (2, 4, 8):
+            bounds = dist.partition_bounds(p.col_ptr, K)
+
+            def fn(r, cid):
+                lcp, lri, lv, lb = dist.shard_csc(p.col_ptr, p.row_idx, None, None, bounds, r)
+                o = di.default_options(exchange_mode=mode, **_p2p_opts())
+                ctx = di.di_create_dist(r, K, cid, bounds, p.n, lcp, lri, lv, lb, p.d, o)
+                b = di.di_get_stats(ctx)["exchange_bytes_resident"]
+                di.di_destroy(ctx)
+                return b
+            per[(mode, K)] = max(_run_ranks_fn(K, f"mem{mode}{K}", fn))
+    for K in (2, 4, 8):
+        assert per[(di.DI_EXCHANGE_P2P, K)] < per[(di.DI_EXCHANGE_ASYNC, K)]
+    assert per[(di.DI_EXCHANGE_P2P, 8)] < per[(di.DI_EXCHANGE_P2P, 4)] < per[(di.DI_EXCHANGE_P2P, 2)]
+
+
+def test_p2p_signed_reset_rerun_and_limits():
+    """Signed P (C5-like) over 3 ranks against the oracle's Jacobi fixed point; a
+    di_reset + second run reproduces the parity; rebalance is refused (slots fixed at
+    create); P2P without remote increments is refused at create on every rank."""
+    n, K = 60_000, 3
+    cp, ri, v, b = gen.signed_system(n, 2)
+    bn = float(np.abs(b).sum())
+    bounds = dist.partition_bounds(cp, K)
+    X, _ = oracle.Problem(n, cp, ri, v, b, 0.9).jacobi(1e-13 * bn)
+
+    def fn(r, cid):
+        lcp, lri, lv, lb = dist.shard_csc(cp, ri, v, b, bounds, r)
+        o = di.default_options(exchange_mode=di.DI_EXCHANGE_P2P, **_p2p_opts())
+        ctx = di.di_create_dist(r, K, cid, bounds, n, lcp, lri, lv, lb, 0.9, o)
+        di.di_run(ctx, 5e-10 * bn)
+        H1 = di.di_get_history(ctx)
+        di.di_reset(ctx)
+        di.di_run(ctx, 5e-10 * bn)
+        H2 = di.di_get_history(ctx)
+        try:
+            di.di_rebalance(ctx, bounds)
+            rb = None
+        except di.DiError as e:
+            rb = e.status
+        di.di_destroy(ctx)
+        return H1, H2, rb
+    outs = _run_ranks_fn(K, "p2psigned", fn)
+    for j in (0, 1):
+        H = np.concatenate([o[j] for o in outs])
+        assert np.abs(H - X).sum() <= 1e-8 * bn
+    assert all(o[2] == di.DI_ERR_UNSUPPORTED for o in outs)
+
+    def bad(r, cid):
+        lcp, lri, lv, lb = dist.shard_csc(cp, ri, v, b, bounds, r)
+        o = di.default_options(exchange_mode=di.DI_EXCHANGE_P2P, remote_push=di.DI_REMOTE_PER_DIFFUSION)
+        try:
+            di.di_create_dist(r, K, cid, bounds, n, lcp, lri, lv, lb, 0.9, o)
+        except di.DiError as e:
+            return e.status
+        return None
+    assert _run_ranks_fn(K, "p2pbad", bad) == [di.DI_ERR_INVALID_ARG] * K
