@@ -42,7 +42,7 @@ for r in csv.DictReader(lines):
         order.append(k)
     v = float(r["Metric Value"].replace(",", ""))
     unit = r["Metric Unit"]
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6,
              "msecond": 1e-3, "second": 1.0}.get(unit, 1.0)
     launches[k][r["Metric Name"]] = v * scale
 
