@@ -106,8 +106,8 @@ enum {
                               the only collectives of a run.  Needs remote_push =
                               DI_REMOTE_INCREMENT, adapt_rounds = 0, <= 64 ranks; di_rebalance is
                               not available.  Memory per rank: a compact outbox over the distinct
-                              remote rows of its columns, and inbox rings of twice the distinct
-                              rows each peer can send it */
+                              remote rows of its columns, and one inbox ring per peer holding one
+                              message (the distinct rows that peer can send it) */
 };
 
 typedef struct {
@@ -232,8 +232,16 @@ DI_API di_status di_create(di_ctx **out, int64_t n, const int64_t *col_ptr, cons
  * [F]_k and [H]_k), and the columns of that range:
  * col_ptr_local[hi-lo+1] (starting at 0), row_idx_local with GLOBAL row ids.
  * bounds[world+1] must be identical on all ranks (di_partition_cb).
- * comm_id: the 128-byte ncclUniqueId created by rank 0 and broadcast by the
- * caller.  Returns DI_ERR_UNSUPPORTED if the library was built without NCCL. */
+ * comm_id (128 bytes) selects the fabric of the collectives:
+ *   - an ncclUniqueId created by rank 0 (di_get_unique_id) and broadcast by the
+ *     caller: NCCL, one GPU per rank (DI_ERR_UNSUPPORTED if built without NCCL);
+ *   - "DILOOP01" + key: K contexts of ONE process (host threads), host-side
+ *     collectives, any devices (tests: K ranks on one GPU);
+ *   - "DISHM001" + name: K processes of one host through POSIX shared memory,
+ *     host-side collectives, no bulk all-to-all-v (use DI_EXCHANGE_P2P; its
+ *     windows are mapped with CUDA IPC).
+ * A failure of one rank inside a collective sequence releases its peers with
+ * DI_ERR_STATE (loopback / shared memory) instead of leaving them waiting. */
 DI_API di_status di_create_dist(di_ctx **out, int32_t rank, int32_t world, const void *comm_id,
                          const int64_t *bounds, int64_t n_global,
                          const int64_t *col_ptr_local, const int32_t *row_idx_local,

@@ -22,6 +22,9 @@
 // (threads) share one GPU for testing -- no kernel ever waits on another rank;
 // all waiting is host-side.
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -193,6 +196,112 @@ struct LoopFabric : Fabric {
     *out = m;
     return DI_OK;
   }
+};
+
+// Cross-process loopback over POSIX shared memory: K processes (one GPU or
+// several) with host-side collectives only -- what the tests use to run
+// DI_EXCHANGE_P2P across processes on one GPU, so that its windows are mapped with
+// cudaIpcOpenMemHandle exactly as between the processes of an 8-GPU box (NCCL
+// refuses two ranks on one device).  No bulk all-to-all-v (the P2P mode does not use
+// one; the paper key's in-degrees, the receiver-computes mode and di_rebalance need
+// NCCL or the in-process loopback).
+struct ShmGroup {
+  std::atomic<int> arrived;
+  std::atomic<int> generation;
+  std::atomic<int> aborted;
+  int world;
+  double red[kP2PMaxWorld * 8];
+  long long counts[kP2PMaxWorld * kP2PMaxWorld];
+  double hmax[kP2PMaxWorld];
+  unsigned char gath[kP2PMaxWorld * 256];
+};
+static_assert(std::atomic<int>::is_always_lock_free, "process-shared atomics need lock-free int");
+
+struct ShmFabric : Fabric {
+  ShmGroup *g = nullptr;
+  std::string name;
+  int rank = 0, world = 1;
+  ~ShmFabric() override {
+    if (g) munmap(g, sizeof(ShmGroup));
+    if (rank == 0 && !name.empty()) shm_unlink(name.c_str());
+  }
+  bool barrier() {
+    const int gen = g->generation.load();
+    if (g->arrived.fetch_add(1) + 1 == world) {
+      g->arrived.store(0);
+      g->generation.fetch_add(1);
+      return true;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    while (g->generation.load() == gen) {
+      if (g->aborted.load()) return false;
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(LoopGroup::kLoopTimeoutS)) {
+        g->aborted.store(1);
+        return false;
+      }
+      usleep(20);
+    }
+    return !g->aborted.load();
+  }
+  void abort() override { if (g) g->aborted.store(1); }
+#define SHM_BARRIER(ctx)                                                                \
+  do {                                                                                 \
+    if (!barrier()) {                                                                  \
+      diter_set_err(ctx, "shared-memory group aborted (a peer failed or timed out)");  \
+      return DI_ERR_STATE;                                                             \
+    }                                                                                  \
+  } while (0)
+  di_status allreduce_sum(di_ctx *ctx, double *dev, int count) override {
+    ++calls;
+    if (count > 8) return DI_ERR_INVALID_ARG;
+    double h[8];
+    CKD(cudaMemcpyAsync(h, dev, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
+    CKD(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(&g->red[rank * 8], h, sizeof(double) * count);
+    SHM_BARRIER(ctx);
+    for (int q = 0; q < count; ++q) {
+      double v = 0.0;
+      for (int k = 0; k < world; ++k) v += g->red[k * 8 + q];   // fixed rank order
+      h[q] = v;
+    }
+    SHM_BARRIER(ctx);
+    CKD(cudaMemcpyAsync(dev, h, sizeof(double) * count, cudaMemcpyHostToDevice, ctx->stream));
+    CKD(cudaStreamSynchronize(ctx->stream));
+    return DI_OK;
+  }
+  di_status alltoall_counts(di_ctx *ctx, const long long *send, long long *recv) override {
+    ++calls;
+    for (int q = 0; q < world; ++q) g->counts[rank * world + q] = send[q];
+    SHM_BARRIER(ctx);
+    for (int q = 0; q < world; ++q) recv[q] = g->counts[q * world + rank];
+    SHM_BARRIER(ctx);
+    return DI_OK;
+  }
+  di_status alltoallv(di_ctx *ctx, const Rec *, const long long *, const long long *, Rec *, const long long *,
+                      const long long *) override {
+    diter_set_err(ctx, "the shared-memory fabric has no bulk all-to-all-v (use DI_EXCHANGE_P2P, NCCL or loopback)");
+    return DI_ERR_UNSUPPORTED;
+  }
+  di_status host_max(di_ctx *ctx, double v, double *out) override {
+    ++calls;
+    g->hmax[rank] = v;
+    SHM_BARRIER(ctx);
+    double m = g->hmax[0];
+    for (int k = 1; k < world; ++k) m = std::max(m, g->hmax[k]);
+    SHM_BARRIER(ctx);
+    *out = m;
+    return DI_OK;
+  }
+  di_status allgather(di_ctx *ctx, const void *mine, size_t bytes, void *all) override {
+    ++calls;
+    if (bytes > 256) return DI_ERR_INVALID_ARG;
+    std::memcpy(g->gath + 256 * rank, mine, bytes);
+    SHM_BARRIER(ctx);
+    for (int k = 0; k < world; ++k) std::memcpy(static_cast<unsigned char *>(all) + bytes * k, g->gath + 256 * k, bytes);
+    SHM_BARRIER(ctx);
+    return DI_OK;
+  }
+#undef SHM_BARRIER
 };
 
 #if DITER_WITH_NCCL
@@ -1429,6 +1538,7 @@ extern "C" di_status di_get_unique_id(void *comm_id_out) {
 }
 
 static const char kLoopTag[8] = {'D', 'I', 'L', 'O', 'O', 'P', '0', '1'};
+static const char kShmTag[8] = {'D', 'I', 'S', 'H', 'M', '0', '0', '1'};
 
 // Everything of a distributed context after its fabric exists (ds->bounds set,
 // ctx->lo / n_local / nnz_local describing this rank's columns): device setup,
@@ -1620,7 +1730,27 @@ extern "C" di_status di_create_dist(di_ctx **out, int32_t rank, int32_t world, c
     if (cudaSetDevice(dev) != cudaSuccess) { diter_set_err(ctx, "cudaSetDevice failed"); return fail(DI_ERR_CUDA); }
   }
   // fabric
-  if (std::memcmp(comm_id, kLoopTag, 8) == 0) {
+  if (std::memcmp(comm_id, kShmTag, 8) == 0) {
+    if (world > kP2PMaxWorld) { diter_set_err(ctx, "shared-memory fabric: at most %d ranks", kP2PMaxWorld); return fail(DI_ERR_INVALID_ARG); }
+    const char *raw = static_cast<const char *>(comm_id) + 8;
+    std::string nm = "/diter_" + std::string(raw, strnlen(raw, 120));
+    const int fd = shm_open(nm.c_str(), O_CREAT | O_RDWR, 0600);
+    if (fd < 0 || ftruncate(fd, sizeof(ShmGroup)) != 0) {
+      if (fd >= 0) close(fd);
+      diter_set_err(ctx, "shm_open/ftruncate %s failed", nm.c_str());
+      return fail(DI_ERR_STATE);
+    }
+    void *p = mmap(nullptr, sizeof(ShmGroup), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) { diter_set_err(ctx, "mmap %s failed", nm.c_str()); return fail(DI_ERR_STATE); }
+    ShmFabric *sf = new ShmFabric();
+    sf->g = static_cast<ShmGroup *>(p);     // a fresh segment is zero-filled: counters at 0
+    sf->name = nm;
+    sf->rank = rank;
+    sf->world = world;
+    sf->g->world = world;
+    ds->fabric.reset(sf);
+  } else if (std::memcmp(comm_id, kLoopTag, 8) == 0) {
     std::string key(static_cast<const char *>(comm_id), 128);
     std::shared_ptr<LoopGroup> grp;
     {

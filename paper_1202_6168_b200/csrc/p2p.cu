@@ -364,11 +364,15 @@ di_status p2p_setup(di_ctx *ctx) {
   cudaFree(cnt);
   cudaFree(woff);
   cudaFree(tmp);
-  // 2. ring capacities: a message to q holds at most one record per slot of q's rows
+  // 2. ring capacities: a message to q holds at most one record per slot of q's rows;
+  //    a ring holds one such message (a sender ships when the ring has room for it,
+  //    receivers drain their rings every round).  Sized per sender: the Zipf-over-id
+  //    head's owner receives from every peer, so its inbox grows with K while the
+  //    mean per rank falls
   std::vector<long long> m_out(W, 0), m_in(W, 0), cap_in(W, 0), off_in(W, 0), off_out(W, 0);
   for (int q = 0; q < W; ++q) m_out[q] = q == rank ? 0 : P.slot_off[q + 1] - P.slot_off[q];
   TRYP(ds->fabric->alltoall_counts(ctx, m_out.data(), m_in.data()));
-  auto ring_cap = [](long long msg) { return msg > 0 ? 2 * msg + 64 : 0; };
+  auto ring_cap = [](long long msg) { return msg > 0 ? msg + 64 : 0; };
   size_t off = align_up(sizeof(P2PHeader), 256);
   for (int q = 0; q < W; ++q) {
     cap_in[q] = q == rank ? 0 : ring_cap(m_in[q]);

@@ -8,6 +8,7 @@ libditer.so (csrc/dist.cu).
     bounds = partition_bounds(col_ptr, K, cost="out")      # Cost-Balanced ranges
     cp, ri, v, b = shard_csc(col_ptr, row_idx, values, b, bounds, rank)
     cid = loopback_comm_id("test")    # K contexts of one process on one GPU (tests)
+    cid = shm_comm_id("job42")        # K processes of one host, host-side collectives (tests)
     cid = nccl_comm_id(process_group) # one GPU per rank (rank 0 creates, broadcast)
 """
 from __future__ import annotations
@@ -17,6 +18,7 @@ import numpy as np
 from . import di_get_unique_id, di_partition_cb
 
 LOOP_TAG = b"DILOOP01"
+SHM_TAG = b"DISHM001"
 
 
 def in_degree(row_idx, n: int) -> np.ndarray:
@@ -60,6 +62,15 @@ def shard_csc(col_ptr, row_idx, values, b, bounds, rank: int):
 def loopback_comm_id(key: str) -> bytes:
     """Communicator id of the in-process loopback fabric (K ranks = K threads, one GPU)."""
     raw = LOOP_TAG + key.encode()[:120]
+    return raw + b"\0" * (128 - len(raw))
+
+
+def shm_comm_id(name: str) -> bytes:
+    """Communicator id of the cross-process shared-memory fabric: K processes on one
+    host (one GPU or several) with host-side collectives; their DI_EXCHANGE_P2P windows
+    are mapped with CUDA IPC (tests: IPC between processes on one GPU, where NCCL
+    refuses two ranks per device).  `name` must be unique per group."""
+    raw = SHM_TAG + name.encode()[:100]
     return raw + b"\0" * (128 - len(raw))
 
 

@@ -392,8 +392,10 @@ def test_p2p_parity_ledger_and_no_collective_per_round(K, cost):
 
 
 def test_p2p_memory_scales_with_ranks():
-    """Per-rank exchange memory: the compact outbox and inbox rings of P2P shrink as K
-    grows and stay below the bulk mode's dense outbox of N doubles."""
+    """Per-rank exchange memory: the compact outbox and inbox rings of P2P stay below the
+    bulk mode's dense outbox of N doubles on every rank, and their mean per rank falls
+    as K grows.  (The owner of the Zipf-over-id head receives from
+    every peer, so the largest rank's inbox does not shrink with K.)"""
     p = gen.config("C2", 1, n=400_000)
     per = {}
     for mode in (di.DI_EXCHANGE_ASYNC, di.DI_EXCHANGE_P2P):
@@ -407,10 +409,11 @@ def test_p2p_memory_scales_with_ranks():
                 b = di.di_get_stats(ctx)["exchange_bytes_resident"]
                 di.di_destroy(ctx)
                 return b
-            per[(mode, K)] = max(_run_ranks_fn(K, f"mem{mode}{K}", fn))
+            per[(mode, K)] = _run_ranks_fn(K, f"mem{mode}{K}", fn)
+    mean = {K: np.mean(per[(di.DI_EXCHANGE_P2P, K)]) for K in (2, 4, 8)}
     for K in (2, 4, 8):
-        assert per[(di.DI_EXCHANGE_P2P, K)] < per[(di.DI_EXCHANGE_ASYNC, K)]
-    assert per[(di.DI_EXCHANGE_P2P, 8)] < per[(di.DI_EXCHANGE_P2P, 4)] < per[(di.DI_EXCHANGE_P2P, 2)]
+        assert max(per[(di.DI_EXCHANGE_P2P, K)]) < min(per[(di.DI_EXCHANGE_ASYNC, K)]) / 2
+    assert mean[8] < mean[4] < mean[2], mean
 
 
 def test_p2p_signed_reset_rerun_and_limits():
