@@ -102,14 +102,18 @@ def parse():
                     help="multi-GPU exchange mode (DESIGN.md §6): sync = per-pass rounds, async = the paper's "
                          "send rule in bulk rounds every rank joins, p2p = the paper's send rule with records "
                          "written into the receivers' inbox rings (no collective per round; default)")
-    ap.add_argument("--round-passes", type=int, default=4, help="N > 1, ASYNC: local passes per exchange round")
+    ap.add_argument("--round-passes", type=int, default=None,
+                    help="N > 1: local passes per round (default: 2 for p2p, 4 for async; DESIGN.md §6 model)")
     ap.add_argument("--remote-push", type=int, default=1, choices=[0, 1],
                     help="N > 1: 0 per diffusion, 1 H increments at rounds (NEXT f2)")
     ap.add_argument("--partition", default="out", choices=["out", "inout"],
                     help="edge-balanced contiguous ranges by out-edges (default: with remote edges "
                          "pushed by the senders as H increments, receiving is a cheap merge; "
                          "scripts/exp_scaling_model.py) or by in+out edges")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.round_passes is None:
+        a.round_passes = 2 if a.exchange == "p2p" else 4
+    return a
 
 
 def log(*a):

@@ -104,4 +104,6 @@ di_status diter_dist_sum(di_ctx *ctx, double v, double *out);
 di_status diter_dist_indegree(di_ctx *ctx, unsigned *indeg_local);   // DI_KEY_PAPER, collective
 di_status diter_dist_run(di_ctx *ctx, double target);
 void diter_dist_stats(const di_ctx *ctx, di_stats *s);   // collectives, confirmations, exchange memory
+void diter_dist_pass_prologue(di_ctx *ctx);               // kernels before each pass (P2P: inbox merge)
+di_status diter_capture_graph(di_ctx *ctx);               // (re)capture check_interval passes as a graph
 di_status diter_dist_reset(di_ctx *ctx);

@@ -808,6 +808,10 @@ di_status diter_dist_max(di_ctx *ctx, double v, double *out) {
   return ctx->dist->fabric->host_max(ctx, v, out);
 }
 
+void diter_dist_pass_prologue(di_ctx *ctx) {
+  if (ctx->dist && ctx->dist->p2p.on && ctx->dist->p2p.d_peers) p2p_pass_merge(ctx);
+}
+
 void diter_dist_stats(const di_ctx *ctx, di_stats *s) {
   const DistState *ds = ctx->dist;
   if (!ds) return;
@@ -1110,6 +1114,7 @@ static di_status prof_collect(di_ctx *ctx, int npasses) {
 
 void dist_launch_pass_kernels(di_ctx *ctx, int slot) {
   Graph g = diter_graph(ctx);
+  diter_dist_pass_prologue(ctx);
   prof_mark(ctx, slot, 0);
   k_select<<<ctx->grid_select, kSelectThreads, 0, ctx->stream>>>(ctx->F, ctx->H, ctx->fr, ctx->n_local, ctx->ctl,
                                                                 ctx->sel_part, ctx->kw);

@@ -129,6 +129,7 @@ struct DistState {
 di_status p2p_setup(di_ctx *ctx);     // collective (create): outbox slots, windows, IPC
 di_status p2p_run(di_ctx *ctx, double target);
 di_status p2p_reset(di_ctx *ctx);     // every rank, before the next di_run
+void p2p_pass_merge(di_ctx *ctx);     // merge + ack + rescale, enqueued before each pass (graph)
 void p2p_free(di_ctx *ctx);
 // dist.cu helpers used by p2p.cu
 void dist_push_increment(di_ctx *ctx);

@@ -449,7 +449,11 @@ Graph diter_graph(const di_ctx *ctx) {
 }
 
 // Capture check_interval passes of (select, scatter, finalize) once.
-static di_status capture_graph(di_ctx *ctx) {
+di_status diter_capture_graph(di_ctx *ctx) {
+  if (ctx->graph_exec) {
+    CK(cudaGraphExecDestroy(ctx->graph_exec));
+    ctx->graph_exec = nullptr;
+  }
   cudaGraph_t graph;
   CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
   Graph g = diter_graph(ctx);
@@ -459,6 +463,7 @@ static di_status capture_graph(di_ctx *ctx) {
     for (auto &e : ctx->prof_ev) CK(cudaEventCreate(&e));
   }
   for (int k = 0; k < ctx->check_interval; ++k) {
+    diter_dist_pass_prologue(ctx);   // DI_EXCHANGE_P2P: merge what has arrived before every pass
     if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 0], ctx->stream, cudaEventRecordExternal));
     k_select<<<ctx->grid_select, kSelectThreads, 0, ctx->stream>>>(ctx->F, ctx->H, ctx->fr, ctx->n_local,
                                                                   ctx->ctl, ctx->sel_part, ctx->kw);
@@ -678,7 +683,7 @@ di_status diter_setup_finish(di_ctx *ctx) {
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->threshold = T0;
   tr.mark(ctx->stream, "init ctl");
-  TRY(capture_graph(ctx));
+  TRY(diter_capture_graph(ctx));
   tr.mark(ctx->stream, "graph capture");
   return DI_OK;
 }
@@ -836,7 +841,7 @@ extern "C" di_status di_set_profile(di_ctx *ctx, int32_t on) {
     CK(cudaGraphExecDestroy(ctx->graph_exec));
     ctx->graph_exec = nullptr;
   }
-  if (!ctx->fused) TRY(capture_graph(ctx));
+  if (!ctx->fused) TRY(diter_capture_graph(ctx));
   return DI_OK;
 }
 

@@ -8,10 +8,10 @@
 //
 // Rank k owns a device window (P2PHeader + one inbox ring per peer).  A round of
 // rank k, with no collective and no wait on any peer:
-//   1. merge: snapshot the heads peers published into k's header (acquire), add
+//   1-2. check_interval local passes (one captured CUDA graph), each preceded by a
+//      merge: snapshot the heads peers published into k's header (acquire), add
 //      every record in [tail, head) of each ring to F (RED), write the new tail and
-//      the merged mass back into the sender's header; rescale T (reading R13);
-//   2. check_interval local passes (one captured CUDA graph);
+//      the merged mass back into the sender's header, rescale T (reading R13);
 //   3. s_k and r_k; the board value r_k + s_k + in-flight_k into every header;
 //      one device->host copy of k's header and counters;
 //   4. send rule: if s_k > r_k / K, push the remote increments into the compact
@@ -275,6 +275,16 @@ __global__ void k_p2p_rescale(Ctl *ctl, const double *round) {
   else if (kmax > 0.0) ctl->T = kmax / ctl->alpha;
 }
 
+// The same before each pass inside the captured graph: r_k is the residual the last
+// pass predicted (ctl->r_pred, r_p minus the pass's guaranteed drop, App. A.2);
+// none yet (start of a run) -> no rescale
+__global__ void k_p2p_rescale_ctl(Ctl *ctl, const double *round) {
+  const double R = round[kRoundRecv], kmax = round[kRoundKeyMax], r_k = ctl->r_pred;
+  if (!(R > 0.0) || !isfinite(r_k)) return;
+  if (r_k > 0.0) ctl->T = ctl->T * ((r_k + R) / r_k);
+  else if (kmax > 0.0) ctl->T = kmax / ctl->alpha;
+}
+
 // Board: r_k + s_k + in-flight_k (sent minus what the receivers acknowledged) into
 // every rank's header; in-flight can be counted twice or not at all across ranks'
 // samples, hence only a trigger for the confirmation
@@ -439,6 +449,8 @@ di_status p2p_setup(di_ctx *ctx) {
   CKP(cudaMalloc(&P.d_mass, sizeof(double) * 2 * W));   // [W] per-send mass, [W] per-merge mass
   CKP(cudaMalloc(&P.d_round, sizeof(double) * kRoundN));
   TRYP(p2p_reset(ctx));
+  // the pass graph again, now with the inbox merge before every pass
+  if (ctx->graph_exec) TRYP(diter_capture_graph(ctx));
   // 5. the peers' windows are zeroed: nobody writes into another window before
   //    every rank is past this point
   TRYP(ds->fabric->allreduce_sum(ctx, ds->d_sums, 1));
@@ -508,6 +520,20 @@ static di_status merge_inbox(di_ctx *ctx, bool rescale) {
   }
   CKP(cudaGetLastError());
   return DI_OK;
+}
+
+// Enqueued before every pass (captured in the context's pass graph): what peers have
+// published is in F before the select looks at it ("can be delayed", by at
+// most one pass), with the receive rescale of T.
+void p2p_pass_merge(di_ctx *ctx) {
+  P2PState &P = ctx->dist->p2p;
+  const int W = ctx->world, rank = ctx->rank;
+  cudaMemsetAsync(P.d_round + kRoundRecv, 0, 2 * sizeof(double), ctx->stream);
+  k_p2p_snap<<<1, kP2PMaxWorld, 0, ctx->stream>>>(reinterpret_cast<const P2PHeader *>(P.win), W, rank, P.d_snap);
+  k_p2p_merge<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->F, ctx->kw, P.d_peers, W, rank, P.d_snap, P.d_tail_in,
+                                                        P.d_mass + W, P.d_round + kRoundRecv);
+  k_p2p_ack<<<1, kP2PMaxWorld, 0, ctx->stream>>>(P.d_peers, W, rank, P.d_snap, P.d_tail_in, P.d_mass + W, P.d_merged);
+  if (ctx->opt.receive_rescale) k_p2p_rescale_ctl<<<1, 1, 0, ctx->stream>>>(ctx->ctl, P.d_round);
 }
 
 // Compact the outbox into the rings of the peers in `mask` and publish.
@@ -617,21 +643,19 @@ di_status p2p_run(di_ctx *ctx, double target) {
   if (R >= target) {
     dist_set_target(ctx, 0.0, max_pass_abs);   // local passes never stop on their own
     const bool graph = ctx->graph_exec != nullptr && !ctx->opt.profile;
-    const int kpp = 3 + (ctx->cap_hub > 0 ? 1 : 0);
+    const int kpp = 3 + (ctx->cap_hub > 0 ? 1 : 0) + 3 + (ctx->opt.receive_rescale ? 1 : 0);
     for (;;) {
-      // 1. merge what has arrived; rescale T to it
-      TRYP(merge_inbox(ctx, ctx->opt.receive_rescale != 0));
-      // 2. local passes
+      // 1-2. local passes, each after a merge of what has arrived (p2p_pass_merge)
       if (graph) {
         CKP(cudaGraphLaunch(ctx->graph_exec, ctx->stream));
         ctx->graph_launches += 1;
         ctx->kernel_launches += (long long)kpp * ctx->check_interval;
       } else {
         for (int k = 0; k < ctx->check_interval; ++k) {
-          dist_launch_pass_kernels(ctx, k);
+          dist_launch_pass_kernels(ctx, k);   // the P2P merge first (diter_dist_pass_prologue)
           k_finalize<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->ctl, ctx->sel_part, ctx->grid_select,
                                                               ctx->sc_part, ctx->grid_scatter, ctx->log);
-          ctx->kernel_launches += 1;
+          ctx->kernel_launches += 4 + (ctx->opt.receive_rescale ? 1 : 0);
         }
       }
       // 3. s_k, r_k, board; one host copy

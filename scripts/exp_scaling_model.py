@@ -14,6 +14,15 @@ with T_1, s (select share) and E_1 from the 1-GPU bench line, B_link = 450 GB/s 
 40 us (a grouped ncclSend/Recv, two all-reduces and the host sync of a round).
 
     python scripts/exp_scaling_model.py C4 248.7 0.224 2.6595e10 [out|inout]
+
+MODEL_MODE=p2p models DI_EXCHANGE_P2P instead: no round barrier, so each rank runs
+at its own pace and the job ends at the last confirmation:
+
+    T_K = max_k [ T_1 * compute_k + rounds_k * t_round + bytes_k / B_p2p ] + confirms * t_confirm
+
+with B_p2p = 900 GB/s (NVLink 5 per direction; the records are stores into the
+receiver's memory), t_round = 40 us (the round's host sync and small kernels) and
+t_confirm = 150 us (four collectives and three merges).
 """
 import json, os, sys, threading, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -31,7 +40,10 @@ B_LINK, T_ROUND = 450e9, 40e-6
 KS = [int(k) for k in os.environ.get("MODEL_K", "2,4,8").split(",")]
 ROUND = int(os.environ.get("MODEL_ROUND_PASSES", "4"))      # bench --round-passes
 REMOTE = int(os.environ.get("MODEL_REMOTE_PUSH", "1"))      # bench --remote-push
-MODE = di.DI_EXCHANGE_ASYNC      # SYNC's di_stats.edges are global totals: not modeled per rank
+RESCALE = int(os.environ.get("MODEL_RESCALE", "1"))          # options.receive_rescale
+P2P = os.environ.get("MODEL_MODE", "async") == "p2p"
+MODE = di.DI_EXCHANGE_P2P if P2P else di.DI_EXCHANGE_ASYNC   # SYNC's di_stats.edges are global totals
+B_P2P, T_CONFIRM = 900e9, 150e-6
 
 p = gen.config(cfg, 1)
 if cfg == "C3":
@@ -47,7 +59,7 @@ c1 = di.di_create(p.n, p.col_ptr, p.row_idx, p.values, p.b, p.d, o1)
 di.di_run(c1, p.stop)
 P1 = di.di_get_stats(c1)["passes"]
 di.di_destroy(c1)
-out = {"config": cfg, "partition": COST, "round_passes": ROUND, "remote_push": REMOTE, "T1_ms": T1, "select_share": s_sel, "E1": E1, "passes_1": P1, "K": {}}
+out = {"mode": "p2p" if P2P else "async", "config": cfg, "partition": COST, "round_passes": ROUND, "remote_push": REMOTE, "T1_ms": T1, "select_share": s_sel, "E1": E1, "passes_1": P1, "K": {}}
 for K in KS:
     bounds = dist.partition_bounds(p.col_ptr, K, cost=COST, row_idx=p.row_idx)
     st = [None] * K
@@ -58,7 +70,8 @@ for K in KS:
         try:
             lcp, lri, lv, lb = dist.shard_csc(p.col_ptr, p.row_idx, p.values, p.b, bounds, r)
             o = di.default_options(policy=pol, alpha=alpha_k, hybrid_frac=frac_k, select_key=key,
-                                   exchange_mode=MODE, check_interval=ROUND, remote_push=REMOTE)
+                                   exchange_mode=MODE, check_interval=ROUND, remote_push=REMOTE,
+                                   receive_rescale=RESCALE)
             ctx = di.di_create_dist(r, K, cid, bounds, p.n, lcp, lri, lv, lb, p.d, o)
             di.di_run(ctx, p.stop)
             st[r] = di.di_get_stats(ctx)
@@ -74,16 +87,25 @@ for K in KS:
             raise e
     wall = time.perf_counter() - t
     rounds = max(s["exchanges"] for s in st)
-    comp = max(s_sel * (s["passes"] * s["n_local"]) / (P1 * p.n) + (1 - s_sel) * (s["edges"] + s["remote_pushes"]) / E1
-               for s in st)
+    comps = [s_sel * (s["passes"] * s["n_local"]) / (P1 * p.n) + (1 - s_sel) * (s["edges"] + s["remote_pushes"]) / E1
+             for s in st]
+    comp = max(comps)
     per_round = max(s["exchanged_bytes"] for s in st) / max(1, rounds)
-    TK = T1 * 1e-3 * comp + rounds * (per_round / B_LINK + T_ROUND)
+    if P2P:
+        # ranks do not wait for each other between confirmations
+        TK = max(T1 * 1e-3 * c + (s["passes"] / ROUND) * T_ROUND + s["exchanged_bytes"] / B_P2P
+                 for c, s in zip(comps, st)) + max(s["confirms"] for s in st) * T_CONFIRM
+    else:
+        TK = T1 * 1e-3 * comp + rounds * (per_round / B_LINK + T_ROUND)
     eff = T1 * 1e-3 / (K * TK)
     out["K"][K] = {"passes": [s["passes"] for s in st], "n_local": [s["n_local"] for s in st],
                    "edges": [s["edges"] for s in st], "remote_pushes": [s["remote_pushes"] for s in st],
                    "rounds": rounds, "bytes_per_round_max": per_round,
                    "exchanged_bytes_total": sum(s["exchanged_bytes"] for s in st),
-                   "compute_fraction_of_T1": comp, "T_K_model_ms": TK * 1e3, "efficiency_model": eff,
+                   "compute_fraction_of_T1": comp, "compute_per_rank": comps, "T_K_model_ms": TK * 1e3,
+                   "efficiency_model": eff, "confirms": [s["confirms"] for s in st],
+                   "collectives": [s["collectives"] for s in st],
+                   "exchange_bytes_resident": [s["exchange_bytes_resident"] for s in st],
                    "loopback_wall_s": wall}
     print(f"K={K}: rounds={rounds} max bytes/round={per_round / 1e6:.1f} MB  edges sum={sum(s['edges'] for s in st):.4e} "
           f"(1 GPU {E1:.4e})  compute max/T1={comp:.3f}  T_K model={TK * 1e3:.1f} ms  efficiency={eff:.2f}", flush=True)
