@@ -457,3 +457,29 @@ def test_p2p_signed_reset_rerun_and_limits():
             return e.status
         return None
     assert _run_ranks_fn(K, "p2pbad", bad) == [di.DI_ERR_INVALID_ARG] * K
+
+
+def test_create_failure_on_one_rank_fails_every_rank():
+    """One rank's input fails validation (a row index out of range): every rank's
+    di_create_dist fails -- that rank with DI_ERR_INVALID_ARG, its peers with
+    DI_ERR_STATE after the agreement -- and none waits forever in a later collective."""
+    K = 3
+    p = gen.config("C2", 1, n=30_000)
+    bounds = dist.partition_bounds(p.col_ptr, K)
+
+    def fn(r, cid):
+        lcp, lri, lv, lb = dist.shard_csc(p.col_ptr, p.row_idx, None, None, bounds, r)
+        if r == 1:
+            lri = lri.copy()
+            lri[len(lri) // 2] = p.n + 5
+        for mode in (di.DI_EXCHANGE_ASYNC,):
+            try:
+                ctx = di.di_create_dist(r, K, cid, bounds, p.n, lcp, lri, lv, lb, p.d,
+                                        di.default_options(exchange_mode=mode, select_key=di.DI_KEY_PAPER))
+                di.di_destroy(ctx)
+            except di.DiError as e:
+                return e.status
+        return None
+    st = _run_ranks_fn(K, "createfail", fn)
+    assert st[1] == di.DI_ERR_INVALID_ARG
+    assert st[0] == st[2] == di.DI_ERR_STATE

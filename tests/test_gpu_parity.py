@@ -372,6 +372,22 @@ def test_completed_pagerank_output(seed):
     np.testing.assert_array_equal(d.cpu().numpy(), x)
 
 
+def test_completed_pagerank_needs_default_pagerank_context():
+    """H/|H|_1 is the completed PageRank only for P = dQ with B = (1-d)/N (App. A.4): a
+    personalised B or a signed P makes di_get_pagerank return DI_ERR_STATE."""
+    n = 2000
+    cp, ri = gen.web_graph(n, 3, window=100, max_deg=200)
+    b = np.random.default_rng(0).random(n)
+    b *= 0.15 / b.sum()
+    for kw in ({"b": b}, {"values": np.full(len(ri), 0.5 / np.maximum(1, np.diff(cp)).repeat(np.diff(cp)))}):
+        ctx = di.di_create(n, cp, ri, kw.get("values"), kw.get("b"), 0.85)
+        di.di_run(ctx, 1e-10)
+        with pytest.raises(di.DiError) as e:
+            di.di_get_pagerank(ctx)
+        assert e.value.status == di.DI_ERR_STATE
+        di.di_destroy(ctx)
+
+
 @pytest.mark.parametrize("opts", [{"far_push": 1, "far_warm_log2": 12}, {"pass_kernel": 2},
                                   {"select_key": di.DI_KEY_EDGE}])
 def test_signed_variants(opts):
