@@ -106,7 +106,7 @@ def parse():
                     help="N > 1: local passes per round (default: 2 for p2p, 4 for async; DESIGN.md §6 model)")
     ap.add_argument("--remote-push", type=int, default=1, choices=[0, 1],
                     help="N > 1: 0 per diffusion, 1 H increments at rounds (NEXT f2)")
-    ap.add_argument("--partition", default="out", choices=["out", "inout"],
+    ap.add_argument("--partition", default="out", choices=["out", "inout", "inhalf"],
                     help="edge-balanced contiguous ranges by out-edges (default: with remote edges "
                          "pushed by the senders as H increments, receiving is a cheap merge; "
                          "scripts/exp_scaling_model.py) or by in+out edges")

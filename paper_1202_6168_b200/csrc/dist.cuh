@@ -53,6 +53,7 @@ struct alignas(128) P2PHeader {
   unsigned long long tail[kP2PMaxWorld];   // [q]: records of MY ring at q that q has merged (written by q)
   double acked[kP2PMaxWorld];              // [q]: fluid mass of those records (written by q)
   double board[kP2PMaxWorld];              // [q]: q's latest r_q + s_q + in-flight_q (written by q)
+  double tval[kP2PMaxWorld];               // [q]: q's current threshold T_q (written by q)
   unsigned long long quiesce;              // confirmation epoch requested by any rank
   unsigned long long pad[15];
 };

@@ -701,7 +701,7 @@ __device__ __forceinline__ void apply_pass(Ctl *ctl, const double *sums, di_pass
   ctl->r_pred = pred;
   // T_{p+1}: GEOM divides every pass; HYBRID only when |S_p| <= f N (readings R4/R6).
   if (ctl->policy == DI_POLICY_GEOM || (double)cnt <= ctl->hybrid_frac * ctl->n_total)
-    ctl->T = T / ctl->alpha;
+    ctl->T = fmax(T / ctl->alpha, ctl->T_floor);
   ctl->pass = p + 1;
   if (r < ctl->target || pred < ctl->target) ctl->done = 1;
   else if (p + 1 >= ctl->max_pass) ctl->done = 2;

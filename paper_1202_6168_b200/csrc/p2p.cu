@@ -289,7 +289,7 @@ __global__ void k_p2p_rescale_ctl(Ctl *ctl, const double *round) {
 // every rank's header; in-flight can be counted twice or not at all across ranks'
 // samples, hence only a trigger for the confirmation
 __global__ void k_p2p_board(const P2PPeer *__restrict__ peers, int W, int rank, const P2PHeader *my,
-                            const double *round, const double *sent) {
+                            const double *round, const double *sent, const Ctl *ctl) {
   __shared__ double s_v;
   if (threadIdx.x == 0) {
     double inflight = 0.0;
@@ -301,8 +301,18 @@ __global__ void k_p2p_board(const P2PPeer *__restrict__ peers, int W, int rank, 
   const int q = threadIdx.x;
   if (q < W) {
     st_volatile(&peers[q].hdr->board[rank], s_v);
+    st_volatile(&peers[q].hdr->tval[rank], ctl->T);
     __threadfence_system();
   }
+}
+
+// Threshold coupling (reading R25): the local schedule may not lower T_k below
+// max_q T_q / alpha^2, the other ranks' thresholds as last published on the board
+__global__ void k_p2p_floor(Ctl *ctl, const P2PHeader *my, int W, int rank) {
+  double m = 0.0;
+  for (int q = 0; q < W; ++q)
+    if (q != rank) m = fmax(m, *(volatile const double *)&my->tval[q]);
+  ctl->T_floor = m / (ctl->alpha * ctl->alpha);
 }
 
 // Quiesce request: epoch into every rank's header
@@ -316,7 +326,10 @@ __global__ void k_p2p_quiesce(const P2PPeer *__restrict__ peers, int W, unsigned
 __global__ void k_copy_double(double *dst, const double *src) { *dst = *src; }
 
 // No board entry counts as low until its rank has written one.
-__global__ void k_p2p_board_init(P2PHeader *hdr) { hdr->board[threadIdx.x] = INFINITY; }
+__global__ void k_p2p_board_init(P2PHeader *hdr) {
+  hdr->board[threadIdx.x] = INFINITY;
+  hdr->tval[threadIdx.x] = 0.0;
+}
 
 }  // namespace
 }  // namespace diter
@@ -574,8 +587,15 @@ static di_status round_measure(di_ctx *ctx, RoundHost *hb) {
   TRYP(diter_l1_launch(ctx));
   k_copy_double<<<1, 1, 0, ctx->stream>>>(P.d_round + kRoundR, ctx->l1_out);
   k_p2p_board<<<1, kP2PMaxWorld, 0, ctx->stream>>>(P.d_peers, W, ctx->rank, reinterpret_cast<const P2PHeader *>(P.win),
-                                                  P.d_round, P.d_sent);
+                                                  P.d_round, P.d_sent, ctx->ctl);
   ctx->kernel_launches += 3;
+#ifndef DITER_P2P_FLOOR
+#define DITER_P2P_FLOOR 1
+#endif
+  if (DITER_P2P_FLOOR) {
+    k_p2p_floor<<<1, 1, 0, ctx->stream>>>(ctx->ctl, reinterpret_cast<const P2PHeader *>(P.win), W, ctx->rank);
+    ctx->kernel_launches += 1;
+  }
   CKP(cudaMemcpyAsync(&hb->hdr, P.win, sizeof(P2PHeader), cudaMemcpyDeviceToHost, ctx->stream));
   CKP(cudaMemcpyAsync(hb->round, P.d_round, sizeof(double) * kRoundN, cudaMemcpyDeviceToHost, ctx->stream));
   CKP(cudaMemcpyAsync(hb->head_out, P.d_head_out, sizeof(unsigned long long) * W, cudaMemcpyDeviceToHost, ctx->stream));

@@ -59,6 +59,7 @@ struct Ctl {
   unsigned long long remote_pushes;   // distributed: pushes into the outbox (one atomic per CTA per pass)
   double t_sel_us;     // fused kernel: accumulated select / scatter phase time (%globaltimer)
   double t_sc_us;
+  double T_floor;      // P2P: the local schedule does not lower T below this (0 = no floor)
   // scatter tickets: one counter per stripe of the frontier groups, each on its
   // own 128-byte line (reset per pass)
   alignas(128) unsigned tickets[kStripes * 32];

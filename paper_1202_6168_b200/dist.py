@@ -31,16 +31,18 @@ def partition_bounds(col_ptr, K: int, cost: str = "out", row_idx=None) -> np.nda
     cost="out": balance sum of #out_n (the paper's Cost-Balanced partition);
     cost="inout": balance #out_n + #in_n (still contiguous and balanced by edge
     count; SURVEY.md §8e shows it lifts the work-balance bound on Zipf-over-id
-    graphs from 0.50 to 0.71 at K = 8).
+    graphs from 0.50 to 0.71 at K = 8); cost="inhalf" / "in/<m>": #out_n + floor(#in_n / m).
     """
     col_ptr = np.asarray(col_ptr, dtype=np.int64)
     n = len(col_ptr) - 1
     if cost == "out":
         prefix = col_ptr
-    elif cost == "inout":
+    elif cost in ("inout", "inhalf") or cost.startswith("in/"):
         if row_idx is None:
-            raise ValueError("cost='inout' needs row_idx")
+            raise ValueError(f"cost='{cost}' needs row_idx")
         indeg = in_degree(row_idx, n)
+        div = 2 if cost == "inhalf" else int(cost[3:]) if cost.startswith("in/") else 1
+        indeg = indeg // div
         prefix = col_ptr + np.concatenate([[0], np.cumsum(indeg)])
     else:
         raise ValueError(cost)

@@ -106,7 +106,7 @@ for K in KS:
                    "efficiency_model": eff, "confirms": [s["confirms"] for s in st],
                    "collectives": [s["collectives"] for s in st],
                    "exchange_bytes_resident": [s["exchange_bytes_resident"] for s in st],
-                   "loopback_wall_s": wall}
+                   "loopback_wall_s": wall, "passes_per_rank": [s["passes"] for s in st]}
     print(f"K={K}: rounds={rounds} max bytes/round={per_round / 1e6:.1f} MB  edges sum={sum(s['edges'] for s in st):.4e} "
           f"(1 GPU {E1:.4e})  compute max/T1={comp:.3f}  T_K model={TK * 1e3:.1f} ms  efficiency={eff:.2f}", flush=True)
 print(json.dumps(out))
