@@ -1,6 +1,7 @@
 // ctx.cuh -- the opaque di_ctx behind include/diter.h (host-side layout).
 #pragma once
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <string>
 #include <utility>
@@ -10,6 +11,15 @@
 #include "types.cuh"
 
 struct DistState;  // dist.cu
+
+// NVTX range over a host-side phase (create, run, exchange round, confirmation):
+// visible in nsys / ncu timelines; free when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 struct di_ctx {
   // problem

@@ -885,6 +885,7 @@ static di_status global_residual(di_ctx *ctx, double add, double *out) {
 // One exchange round: optional compaction of the whole outbox, record counts,
 // all-to-all-v, merge.  Collective.
 static di_status exchange(di_ctx *ctx, bool send_now) {
+  NvtxRange nv("bulk exchange");
   DistState *ds = ctx->dist;
   const int W = ctx->world;
   CKD(cudaMemsetAsync(ds->d_scnt, 0, sizeof(long long) * W, ctx->stream));
@@ -1339,6 +1340,7 @@ const unsigned char *get(const unsigned char *c, T *p, size_t n) {
 }  // namespace
 
 extern "C" di_status di_rebalance(di_ctx *ctx, const int64_t *nb) {
+  NvtxRange nv("di_rebalance");
   if (!ctx || !nb) { diter_set_err(ctx, "NULL argument"); return DI_ERR_INVALID_ARG; }
   if (!ctx->dist || ctx->world < 2) { diter_set_err(ctx, "di_rebalance: distributed contexts only"); return DI_ERR_INVALID_ARG; }
   if (ctx->dist->p2p.on) {

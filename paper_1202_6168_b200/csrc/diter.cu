@@ -539,6 +539,7 @@ struct SetupTrace {
 // Shared by di_create and di_create_dist: upload, validate, allocate, init.
 di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_idx,
                       const double *values, const double *b, const di_options *opt) {
+  NvtxRange nv("diter setup");
   di_options o;
   if (opt) o = *opt; else di_default_options(&o);
   if (!(o.alpha > 1.0) || o.check_interval < 1 || o.check_interval > 4096 || o.max_passes < 1 ||
@@ -661,6 +662,7 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
 // ranks agreed that their local setup succeeded): the paper key's in-degrees,
 // T_0 = max over ranks, the control block, the captured pass graph.
 di_status diter_setup_finish(di_ctx *ctx) {
+  NvtxRange nv("diter setup (collective tail)");
   SetupTrace tr;
   const di_options &o = ctx->opt;
   if (o.select_key == DI_KEY_PAPER) TRY(setup_key(ctx));
@@ -738,6 +740,7 @@ static di_status read_ctl(di_ctx *ctx) {
 }
 
 extern "C" di_status di_run(di_ctx *ctx, double target) {
+  NvtxRange nv("di_run");
   if (!ctx) { diter_set_err(nullptr, "ctx is NULL"); return DI_ERR_INVALID_ARG; }
   if (!(target >= 0.0)) { diter_set_err(ctx, "target must be >= 0"); return DI_ERR_INVALID_ARG; }
   if (ctx->world > 1) return diter_dist_run(ctx, target);

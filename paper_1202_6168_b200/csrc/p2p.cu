@@ -347,6 +347,7 @@ struct WinDesc {
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 di_status p2p_setup(di_ctx *ctx) {
+  NvtxRange nv("p2p setup");
   DistState *ds = ctx->dist;
   P2PState &P = ds->p2p;
   const int W = ctx->world, rank = ctx->rank;
@@ -551,6 +552,7 @@ void p2p_pass_merge(di_ctx *ctx) {
 
 // Compact the outbox into the rings of the peers in `mask` and publish.
 static di_status send_outbox(di_ctx *ctx, unsigned long long mask) {
+  NvtxRange nv("p2p send");
   DistState *ds = ctx->dist;
   P2PState &P = ds->p2p;
   const int W = ctx->world;
@@ -608,6 +610,7 @@ static di_status round_measure(di_ctx *ctx, RoundHost *hb) {
 // once it has seen the epoch.  Returns the exact global residual in *R and whether
 // any rank ran out of passes in *oop.
 static di_status confirm(di_ctx *ctx, bool my_oop, double *R, bool *oop) {
+  NvtxRange nv("p2p confirm");
   DistState *ds = ctx->dist;
   P2PState &P = ds->p2p;
   Fabric &fab = *ds->fabric;
