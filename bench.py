@@ -96,6 +96,8 @@ def parse():
     ap.add_argument("--scale", type=int, default=None, help="C3 scale override (tests)")
     ap.add_argument("--n", type=int, default=None, help="node-count override (tests)")
     ap.add_argument("--pass-csv", default=None, help="write the last solve's per-pass log here")
+    ap.add_argument("--dist-path", action="store_true",
+                    help="tests: run the N > 1 code path (di_create_dist over NCCL) even with one rank")
     ap.add_argument("--l2-persist", type=int, default=0,
                     help="options.l2_persist: 0 auto, -1 off, > 0 window MB (experiments)")
     ap.add_argument("--exchange", default="p2p", choices=["sync", "async", "p2p"],
@@ -361,7 +363,7 @@ def run_reference(args, rank, world):
 def make_ctx(args, p, opts, di, rank, world, comm_id, bounds, host=None):
     """One GPU: di_create; N ranks: di_create_dist on this rank's shard (NCCL)."""
     cp, ri, vv, bb = host if host is not None else (p.col_ptr, p.row_idx, p.values, p.b)
-    if world == 1:
+    if world == 1 and not args.dist_path:
         return di.di_create(p.n, cp, ri, vv, bb, p.d, opts)
     return di.di_create_dist(rank, world, comm_id, bounds, p.n, cp, ri, vv, bb, p.d, opts)
 
@@ -372,16 +374,23 @@ def run_ours(args, rank, world, local_rank):
     from paper_1202_6168_b200 import dist as dd
 
     torch.cuda.set_device(local_rank)
-    dist = world > 1
+    dist = world > 1 or args.dist_path
     if dist:
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if "MASTER_PORT" not in os.environ:
+            import socket
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank),
+                                             rank=rank, world_size=world)
     p = load_problem(args)
     pol = policy_of(args)
     mode = {"sync": di.DI_EXCHANGE_SYNC, "async": di.DI_EXCHANGE_ASYNC, "p2p": di.DI_EXCHANGE_P2P}[args.exchange]
     # N > 1 (ASYNC): exchange rounds every 4 passes, remote edges pushed as H
     # increments at the rounds (NEXT f2), receive-side T rescale --
     # DESIGN.md §6 "Multi-GPU" has the loopback measurements behind these choices
-    dist_kw = dict(check_interval=args.round_passes, remote_push=args.remote_push) if world > 1 else {}
+    dist_kw = dict(check_interval=args.round_passes, remote_push=args.remote_push) if dist else {}
     opts = di.default_options(policy=pol, device=local_rank, profile=0, exchange_mode=mode,
                               alpha=args.alpha, hybrid_frac=args.hybrid_frac, select_key=args.key,
                               scatter_run=SCATTER_RUN.get(args.config, 0), l2_persist=args.l2_persist, **dist_kw)
@@ -485,12 +494,12 @@ def run_ours(args, rank, world, local_rank):
                 "path_alg_GBps": tot["alg_bytes"] / (run_ms_rank / 1e3) / 1e9}
     # ---- the raw key on the same graph (extra key; the headline keeps the per-edge key)
     raw = None
-    if world == 1 and args.config == "C4" and args.key != 0 and not args.no_raw_key:
+    if not dist and args.config == "C4" and args.key != 0 and not args.no_raw_key:
         raw = run_raw_key(args, p, opts, di, torch)
     # ---- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, p, opts, di, torch, rank, world, comm_id, bounds, shard)
+        e2e = run_e2e(args, p, opts, di, torch, rank, world, comm_id, bounds, shard, dist)
     # ---- cpu baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -573,7 +582,7 @@ def run_raw_key(args, p, opts, di, torch):
             "passes_per_solve": passes / steps, "normalized_iterations": edges / steps / p.nnz}
 
 
-def run_e2e(args, p, opts, di, torch, rank=0, world=1, comm_id=None, bounds=None, shard=None):
+def run_e2e(args, p, opts, di, torch, rank=0, world=1, comm_id=None, bounds=None, shard=None, dist=False):
     """Same metric through di_create/di_run/di_get_history with pinned host buffers."""
     src = shard if shard is not None else (p.col_ptr, p.row_idx, p.values, p.b)
     pin = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() if a is not None else None for a in src]
@@ -589,7 +598,7 @@ def run_e2e(args, p, opts, di, torch, rank=0, world=1, comm_id=None, bounds=None
         # an ncclUniqueId initialises one communicator only: every distributed
         # context gets a fresh one (collective over the torch process group)
         cid = comm_id
-        if world > 1:
+        if dist:
             from paper_1202_6168_b200 import dist as dd
             cid = dd.nccl_comm_id()
         ctx = make_ctx(args, p, o2, di, rank, world, cid, bounds, pin)
@@ -601,7 +610,7 @@ def run_e2e(args, p, opts, di, torch, rank=0, world=1, comm_id=None, bounds=None
 
     one()                                          # warm (allocator, module load)
     torch.cuda.synchronize()
-    if world > 1:
+    if dist:
         torch.distributed.barrier()
     edges = 0
     t0 = time.perf_counter()
@@ -610,7 +619,7 @@ def run_e2e(args, p, opts, di, torch, rank=0, world=1, comm_id=None, bounds=None
         edges += one()
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    if world > 1:
+    if dist:
         t_ = torch.tensor([dt, float(edges)], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t_[:1], op=torch.distributed.ReduceOp.MAX)
         e_ = t_[1:].clone()

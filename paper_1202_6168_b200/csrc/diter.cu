@@ -176,7 +176,7 @@ static di_status setup_geometry(di_ctx *ctx) {
   // fused cooperative pass kernel (small graphs, one GPU): every CTA co-resident, and the
   // select phase runs on the fused grid, so the segmentation follows that grid
   const int pk = ctx->opt.pass_kernel;
-  ctx->fused = ctx->world == 1 && pk == 2;
+  ctx->fused = ctx->dist == nullptr && pk == 2;
   if (ctx->fused) {
     const size_t dyn = sizeof(int) * (size_t)(std::min(ctx->num_sms * 4 * kWarps, kMaxSegments) + 1);
     int occ_f = 0;
@@ -348,7 +348,7 @@ static di_status setup_far(di_ctx *ctx) {
   const int mode = ctx->opt.far_push;
   const long long n = ctx->n_rows;
   const bool want = mode > 0;   // auto = off: on C4 the emission costs more than the tail REDs it saves
-  if (!want || mode < 0 || ctx->world > 1 || ctx->fused || ctx->nnz_local == 0 || ctx->blk_hist.empty()) return DI_OK;
+  if (!want || mode < 0 || ctx->dist || ctx->fused || ctx->nnz_local == 0 || ctx->blk_hist.empty()) return DI_OK;
   int shift = 20;
   while (((n - 1) >> shift) + 1 > kMaxBins) ++shift;
   const int n_bins = (int)(((n - 1) >> shift) + 1);
@@ -470,7 +470,7 @@ di_status diter_capture_graph(di_ctx *ctx) {
     if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 1], ctx->stream, cudaEventRecordExternal));
     // a distributed rank's scatter routes rows outside its range (DIST): its ASYNC / P2P
     // rounds launch this graph for their local passes
-    const bool dist = ctx->world > 1;
+    const bool dist = ctx->dist != nullptr;
     if (ctx->vals)
       (dist ? k_scatter<true, true, false> : ctx->far.on ? k_scatter<true, false, true> : k_scatter<true, false, false>)
           <<<ctx->grid_scatter, kScatterThreads, ctx->scatter_smem, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part);
@@ -743,7 +743,7 @@ extern "C" di_status di_run(di_ctx *ctx, double target) {
   NvtxRange nv("di_run");
   if (!ctx) { diter_set_err(nullptr, "ctx is NULL"); return DI_ERR_INVALID_ARG; }
   if (!(target >= 0.0)) { diter_set_err(ctx, "target must be >= 0"); return DI_ERR_INVALID_ARG; }
-  if (ctx->world > 1) return diter_dist_run(ctx, target);
+  if (ctx->dist) return diter_dist_run(ctx, target);   // any distributed context, one rank included
   CK(cudaSetDevice(ctx->device));
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
   const long long launches0 = ctx->kernel_launches;

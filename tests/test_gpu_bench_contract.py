@@ -39,3 +39,21 @@ def test_bench_line_contract():
     assert 3 * d["passes_per_solve"] <= per <= 3 * (d["passes_per_solve"] + 16) + 16, (per, d["passes_per_solve"])
     assert c["pinned_core"] >= 0 and "l2_window" in d
     assert set(("sm_mhz", "sm_max_mhz", "reasons")) <= set(d["clocks"])
+
+
+@pytest.mark.parametrize("exchange", ["p2p", "async"])
+def test_bench_distributed_path_one_rank(exchange):
+    """bench.py's N > 1 code path on one GPU (--dist-path: di_create_dist over a real
+    one-rank NCCL communicator made through torch.distributed): the NCCL fabric's
+    collectives run, the exchange mode's stats reach the line."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "C2", "--steps", "2",
+                          "--warmup", "3", "--cpu-seconds", "1", "--dist-path", "--exchange", exchange,
+                          "--no-cpu-baseline"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    assert d["n_gpus"] == 1 and d["value"] > 0
+    assert d["collectives_per_solve"] > 0 and d["exchange_bytes_resident"] > 0
+    if exchange == "p2p":
+        assert d["confirms_per_solve"] >= 1
+        assert d["collectives_per_solve"] == 1 + 4 * d["confirms_per_solve"]
+    assert d["e2e"]["value"] > 0
