@@ -256,6 +256,16 @@ DI_API di_status di_get_unique_id(void *comm_id_out);
  * the next di_run solves from scratch.  Collective for distributed contexts. */
 DI_API di_status di_reset(di_ctx *ctx);
 
+/* Checkpoint / resume: load a state (F, H) -- host arrays of n (or hi-lo when
+ * distributed) doubles, e.g. from di_get_fluid / di_get_history of an earlier run
+ * on the same (P, B) -- and restart the schedule from it: the counters, pass log
+ * and stats are cleared as by di_reset, T = max_i |F_i| w_i / alpha (reading R5
+ * applied to the loaded F; a max over ranks when distributed), nothing in flight
+ * (remote increments start from H).  The caller vouches that F = B - (I - P) H (the
+ * identity every D-iteration state satisfies): the solve then
+ * converges to the same X.  Collective for distributed contexts. */
+DI_API di_status di_set_state(di_ctx *ctx, const double *f_in, const double *h_in);
+
 /* Switch per-kernel timing on (1) or off (0) for the following di_run calls:
  * with it on, CUDA events recorded between the pass kernels give the select /
  * scatter / finalize durations in di_stats (kt_*_ms) and the pass log, at a cost

@@ -34,7 +34,8 @@ STATUS_NAMES = {0: "DI_OK", 1: "DI_ERR_INVALID_ARG", 2: "DI_ERR_CONTRACTION", 3:
                 8: "DI_ERR_UNSUPPORTED"}
 
 # every symbol include/diter.h declares (checked by tests/test_abi.py)
-EXPORTS = ["di_default_options", "di_struct_size", "di_create", "di_create_dist", "di_get_unique_id", "di_reset", "di_set_profile", "di_run",
+EXPORTS = ["di_default_options", "di_struct_size", "di_create", "di_create_dist", "di_get_unique_id", "di_reset",
+           "di_set_state", "di_set_profile", "di_run",
            "di_get_history", "di_get_fluid", "di_get_history_device", "di_get_fluid_device",
            "di_get_pagerank", "di_get_pagerank_device", "di_rebalance", "di_get_bounds",
            "di_get_residual", "di_get_stats", "di_get_pass_log", "di_last_error", "di_destroy",
@@ -110,6 +111,7 @@ def load_library() -> ctypes.CDLL:
                                 ctypes.POINTER(di_options)]),
         "di_get_unique_id": (st, [vp]),
         "di_reset": (st, [vp]),
+        "di_set_state": (st, [vp, vp, vp]),
         "di_set_profile": (st, [vp, i32]),
         "di_run": (st, [vp, f64]),
         "di_get_history": (st, [vp, vp]),
@@ -239,6 +241,15 @@ def di_run(ctx: Context, residual_target: float, raise_on_not_converged: bool = 
 
 def di_reset(ctx: Context):
     _check(load_library().di_reset(ctx.handle), ctx.handle)
+
+
+def di_set_state(ctx: Context, F, H):
+    """Load (F, H) (n_local float64 each) and restart the schedule from them (include/diter.h)."""
+    kf, pf = _hostptr(F, np.float64)
+    kh, ph = _hostptr(H, np.float64)
+    if len(kf) != ctx.n_local or len(kh) != ctx.n_local:
+        raise ValueError(f"F and H must hold n_local = {ctx.n_local} values")
+    _check(load_library().di_set_state(ctx.handle, pf, ph), ctx.handle)
 
 
 def di_set_profile(ctx: Context, on: bool):

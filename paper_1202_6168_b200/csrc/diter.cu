@@ -869,6 +869,24 @@ extern "C" di_status di_reset(di_ctx *ctx) {
   return diter_dist_reset(ctx);
 }
 
+extern "C" di_status di_set_state(di_ctx *ctx, const double *f_in, const double *h_in) {
+  if (!ctx || !f_in || !h_in) { diter_set_err(ctx, "NULL argument"); return DI_ERR_INVALID_ARG; }
+  TRY(di_reset(ctx));
+  CK(cudaSetDevice(ctx->device));
+  const size_t bytes = sizeof(double) * (size_t)ctx->n_local;
+  CK(cudaMemcpyAsync(ctx->F, f_in, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->H, h_in, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  if (ctx->H_old) CK(cudaMemcpyAsync(ctx->H_old, ctx->H, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  double T0 = 0.0;
+  TRY(initial_threshold(ctx, &T0));      // synchronises the stream; collective when distributed
+  Ctl c = ctx->ctl_init;
+  c.T = T0;
+  CK(cudaMemcpyAsync(ctx->ctl, &c, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->threshold = T0;
+  return DI_OK;
+}
+
 static di_status copy_out(const di_ctx *cctx, const double *src, double *dst, cudaMemcpyKind kind) {
   di_ctx *ctx = const_cast<di_ctx *>(cctx);
   if (!ctx || !dst) { diter_set_err(ctx, "NULL argument"); return DI_ERR_INVALID_ARG; }

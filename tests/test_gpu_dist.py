@@ -483,3 +483,41 @@ def test_create_failure_on_one_rank_fails_every_rank():
     st = _run_ranks_fn(K, "createfail", fn)
     assert st[1] == di.DI_ERR_INVALID_ARG
     assert st[0] == st[2] == di.DI_ERR_STATE
+
+
+def test_p2p_checkpoint_resume():
+    """di_set_state on distributed P2P contexts: a run stopped by max_passes on K = 2
+    loopback ranks, each rank's (F, H) loaded into a new pair of contexts, continues to
+    the oracle's fixed point with a closed ledger."""
+    K = 2
+    p = gen.config("C2", 2, n=200_000)
+    bounds = dist.partition_bounds(p.col_ptr, K)
+
+    def first(r, cid):
+        lcp, lri, lv, lb = dist.shard_csc(p.col_ptr, p.row_idx, None, None, bounds, r)
+        o = di.default_options(exchange_mode=di.DI_EXCHANGE_P2P, max_passes=12, **_p2p_opts())
+        ctx = di.di_create_dist(r, K, cid, bounds, p.n, lcp, lri, lv, lb, p.d, o)
+        st = di.di_run(ctx, p.parity_stop, raise_on_not_converged=False)
+        out = (st, di.di_get_fluid(ctx), di.di_get_history(ctx))
+        di.di_destroy(ctx)
+        return out
+    a = _run_ranks_fn(K, "ckpt1", first)
+    assert all(o[0] == di.DI_ERR_NOT_CONVERGED for o in a)
+
+    def second(r, cid):
+        lcp, lri, lv, lb = dist.shard_csc(p.col_ptr, p.row_idx, None, None, bounds, r)
+        o = di.default_options(exchange_mode=di.DI_EXCHANGE_P2P, **_p2p_opts())
+        ctx = di.di_create_dist(r, K, cid, bounds, p.n, lcp, lri, lv, lb, p.d, o)
+        di.di_set_state(ctx, a[r][1], a[r][2])
+        di.di_run(ctx, p.parity_stop)
+        out = (di.di_get_history(ctx), di.di_get_fluid(ctx))
+        di.di_destroy(ctx)
+        return out
+    b = _run_ranks_fn(K, "ckpt2", second)
+    H = np.concatenate([o[0] for o in b])
+    F = np.concatenate([o[1] for o in b])
+    X = oracle.Problem(p.n, p.col_ptr, p.row_idx).solve(1e-12 * 0.15 * 0.15).H
+    assert np.abs(H - X).sum() <= 1e-8 * 0.15
+    deg = np.diff(p.col_ptr)
+    ledger = np.abs(F).sum() + 0.15 * H.sum() + 0.85 * H[deg == 0].sum()
+    assert abs(ledger - 0.15) <= 1e-12 * 0.15

@@ -468,3 +468,29 @@ def test_l2_persist_window_forced(opts):
     _check_state(p.n, p.col_ptr, p.row_idx, None, None, 0.85, H1, F1, r1, p.stop)
     assert np.abs(H1 - H0).sum() <= 2 * p.stop / 0.15
     assert abs(s1["passes"] - s0["passes"]) <= 1
+
+
+def test_checkpoint_resume_set_state():
+    """di_set_state (checkpoint / resume): a solve stopped by max_passes, its (F, H)
+    loaded into a fresh context, continues to the same fixed point; the
+    restarted schedule begins at T = max |F_i| w_i / alpha, and F = B - (I-P)H holds."""
+    p = gen.config("C2", 3, n=200_000)
+    o = di.default_options(select_key=di.DI_KEY_EDGE, alpha=2.0, hybrid_frac=0.3, max_passes=25)
+    ctx = di.di_create(p.n, p.col_ptr, p.row_idx, None, None, p.d, o)
+    assert di.di_run(ctx, p.parity_stop, raise_on_not_converged=False) == di.DI_ERR_NOT_CONVERGED
+    F, H = di.di_get_fluid(ctx), di.di_get_history(ctx)
+    di.di_destroy(ctx)
+    o2 = di.default_options(select_key=di.DI_KEY_EDGE, alpha=2.0, hybrid_frac=0.3)
+    ctx = di.di_create(p.n, p.col_ptr, p.row_idx, None, None, p.d, o2)
+    di.di_set_state(ctx, F, H)
+    w = oracle.key_weights(p.n, p.col_ptr, p.row_idx, oracle.KEY_EDGE).astype(np.float64)
+    assert di.di_get_stats(ctx)["threshold"] == pytest.approx(float(np.max(np.abs(F) * w)) / 2.0, rel=1e-15)
+    di.di_run(ctx, p.parity_stop)
+    H2, F2 = di.di_get_history(ctx), di.di_get_fluid(ctx)
+    di.di_destroy(ctx)
+    X = oracle.Problem(p.n, p.col_ptr, p.row_idx).solve(1e-12 * 0.15 * 0.15).H
+    assert np.abs(H2 - X).sum() <= 1e-8 * 0.15
+    assert np.all(H2 >= H)                          # the resumed history only grows
+    deg = np.diff(p.col_ptr)
+    ledger = np.abs(F2).sum() + 0.15 * H2.sum() + 0.85 * H2[deg == 0].sum()
+    assert abs(ledger - 0.15) <= 1e-12 * 0.15
