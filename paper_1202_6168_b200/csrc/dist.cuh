@@ -95,6 +95,7 @@ struct P2PState {
   long long *d_cnt = nullptr;                 // [world] records compacted this send
   double *d_mass = nullptr;                   // [world] their mass
   double *d_round = nullptr;                  // [8] round scalars (s_k, r_k, r before merge, ...)
+  void *h_round = nullptr;                    // pinned host copy of a round's header + scalars
   unsigned long long epoch = 0;               // confirmations completed
   long long confirms = 0;                     // confirmations run (stats)
   long long publishes = 0;

@@ -336,6 +336,13 @@ __global__ void k_p2p_board_init(P2PHeader *hdr) {
 
 using namespace diter;
 
+// Host copy of what a round decides on (one device->host transfer per round).
+struct RoundHost {
+  P2PHeader hdr;
+  double round[kRoundN];
+  unsigned long long head_out[kP2PMaxWorld];
+};
+
 // ------------------------------------------------------------------- setup --
 struct WinDesc {
   unsigned long long ptr;
@@ -357,7 +364,12 @@ di_status p2p_setup(di_ctx *ctx) {
   unsigned *bits = nullptr;
   int *cnt = nullptr, *woff = nullptr;
   void *tmp = nullptr;
+  long long *d_so = nullptr;
   size_t tmp_bytes = 0;
+  struct Temps {   // setup scratch, freed on every return path
+    void **p[5];
+    ~Temps() { for (void **q : p) if (*q) { cudaFree(*q); *q = nullptr; } }
+  } temps{{(void **)&bits, (void **)&cnt, (void **)&woff, &tmp, (void **)&d_so}};
   CKP(cudaMalloc(&bits, sizeof(unsigned) * nw));
   CKP(cudaMalloc(&cnt, sizeof(int) * (nw + 1)));
   CKP(cudaMalloc(&woff, sizeof(int) * (nw + 1)));
@@ -377,17 +389,11 @@ di_status p2p_setup(di_ctx *ctx) {
   TRYP(diter_alloc(ctx, (void **)&ctx->dflags, (size_t)((P.m + 31) >> 5) + 1));
   k_p2p_targets<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(bits, woff, nw, P.tgt);
   k_p2p_remap<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ctx->col_ptr, ctx->nloc, ctx->row_idx, n, bits, woff);
-  long long *d_so = nullptr;
   CKP(cudaMalloc(&d_so, sizeof(long long) * (W + 1)));
   k_p2p_slot_bounds<<<1, 128, 0, ctx->stream>>>(ds->d_bounds, W, n_rows, P.m, bits, woff, d_so);
   P.slot_off.assign(W + 1, 0);
   CKP(cudaMemcpyAsync(P.slot_off.data(), d_so, sizeof(long long) * (W + 1), cudaMemcpyDeviceToHost, ctx->stream));
   CKP(cudaStreamSynchronize(ctx->stream));
-  cudaFree(d_so);
-  cudaFree(bits);
-  cudaFree(cnt);
-  cudaFree(woff);
-  cudaFree(tmp);
   // 2. ring capacities: a message to q holds at most one record per slot of q's rows;
   //    a ring holds one such message (a sender ships when the ring has room for it,
   //    receivers drain their rings every round).  Sized per sender: the Zipf-over-id
@@ -462,6 +468,7 @@ di_status p2p_setup(di_ctx *ctx) {
   CKP(cudaMalloc(&P.d_cnt, sizeof(long long) * W));
   CKP(cudaMalloc(&P.d_mass, sizeof(double) * 2 * W));   // [W] per-send mass, [W] per-merge mass
   CKP(cudaMalloc(&P.d_round, sizeof(double) * kRoundN));
+  CKP(cudaMallocHost(&P.h_round, sizeof(RoundHost)));
   TRYP(p2p_reset(ctx));
   // the pass graph again, now with the inbox merge before every pass
   if (ctx->graph_exec) TRYP(diter_capture_graph(ctx));
@@ -502,18 +509,12 @@ void p2p_free(di_ctx *ctx) {
                   P.d_round};
   for (void *p : ptrs)
     if (p) cudaFree(p);
+  if (P.h_round) cudaFreeHost(P.h_round);
   diter_free(ctx, P.tgt);
   P = P2PState{};
 }
 
 // -------------------------------------------------------------------- run --
-// Host copy of what a round decides on (one device->host transfer per round).
-struct RoundHost {
-  P2PHeader hdr;
-  double round[kRoundN];
-  unsigned long long head_out[kP2PMaxWorld];
-};
-
 static di_status merge_inbox(di_ctx *ctx, bool rescale) {
   DistState *ds = ctx->dist;
   P2PState &P = ds->p2p;
@@ -649,9 +650,7 @@ di_status p2p_run(di_ctx *ctx, double target) {
   const long long max_pass_abs = ctx->passes_done + ctx->opt.max_passes;
   Ctl *h = reinterpret_cast<Ctl *>(ctx->h_ctl);
   di_status st = DI_OK;
-  RoundHost *hb = nullptr;
-  CKP(cudaMallocHost(&hb, sizeof(RoundHost)));
-  struct Free { RoundHost *p; ~Free() { cudaFreeHost(p); } } free_hb{hb};
+  RoundHost *hb = reinterpret_cast<RoundHost *>(P.h_round);   // pinned, allocated at setup
   // a run starts (and every run ended) with nothing in flight: the exact global
   // residual decides whether there is anything to do
   double R = 0.0;
