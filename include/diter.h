@@ -148,7 +148,11 @@ typedef struct {
                               refcounted over contexts): 0 = auto (off while F fits in 64 MB, else
                               28 MB when F <= 2x L2 and 20 MB above: C3 219 -> 184 ms, C4 265 ->
                               250 ms), -1 = off, > 0 = a window of that many MB */
-  int32_t reserved[3];
+  int32_t p2p_sleep;       /* DI_EXCHANGE_P2P: a rank whose local residual r_k is below target / K
+                              sleeps: its rounds only merge, send and measure,
+                              no local passes, until received fluid lifts r_k again; 0 = on
+                              (default), -1 = off */
+  int32_t reserved[2];
 } di_options;
 
 /* One record per executed pass (device-logged, read with di_get_pass_log). */
@@ -206,6 +210,7 @@ typedef struct {
   int64_t confirms;        /* DI_EXCHANGE_P2P: quiesce-then-reduce confirmations run since create */
   int64_t exchange_bytes_resident; /* distributed: device bytes of the exchange state (outbox, flags,
                               record buffers or inbox rings) */
+  int64_t sleep_rounds;    /* DI_EXCHANGE_P2P: rounds this rank spent asleep since create */
 } di_stats;
 
 /* Fill *opt with the defaults above. */

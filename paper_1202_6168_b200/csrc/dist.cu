@@ -817,6 +817,7 @@ void diter_dist_stats(const di_ctx *ctx, di_stats *s) {
   if (!ds) return;
   s->collectives = ds->fabric ? ds->fabric->calls : 0;
   s->confirms = ds->p2p.confirms;
+  s->sleep_rounds = ds->p2p.sleep_rounds;
   if (ds->p2p.on) {
     s->exchange_bytes_resident = (long long)(ds->p2p.m * (sizeof(double) + sizeof(int)) + ((ds->p2p.m + 31) >> 5) +
                                              ds->p2p.win_bytes);

@@ -99,6 +99,7 @@ struct P2PState {
   unsigned long long epoch = 0;               // confirmations completed
   long long confirms = 0;                     // confirmations run (stats)
   long long publishes = 0;
+  long long sleep_rounds = 0;                 // rounds spent asleep (merge only, no local passes)
 };
 
 // ------------------------------------------------------------ dist state --

@@ -665,10 +665,19 @@ di_status p2p_run(di_ctx *ctx, double target) {
   if (R >= target) {
     dist_set_target(ctx, 0.0, max_pass_abs);   // local passes never stop on their own
     const bool graph = ctx->graph_exec != nullptr && !ctx->opt.profile;
+    bool asleep = false;
     const int kpp = 3 + (ctx->cap_hub > 0 ? 1 : 0) + 3 + (ctx->opt.receive_rescale ? 1 : 0);
     for (;;) {
-      // 1-2. local passes, each after a merge of what has arrived (p2p_pass_merge)
-      if (graph) {
+      // 1-2. local passes, each after a merge of what has arrived (p2p_pass_merge) --
+      //      or, asleep (r_k below this rank's share of the target), only the
+      //      merge: the rank keeps receiving and answering, and wakes up when what it
+      //      receives lifts r_k again
+      if (asleep) {
+        usleep(50);                           // nothing to diffuse: do not spin on the device
+        p2p_pass_merge(ctx);
+        ctx->kernel_launches += 3 + (ctx->opt.receive_rescale ? 1 : 0);
+        P.sleep_rounds += 1;
+      } else if (graph) {
         CKP(cudaGraphLaunch(ctx->graph_exec, ctx->stream));
         ctx->graph_launches += 1;
         ctx->kernel_launches += (long long)kpp * ctx->check_interval;
@@ -681,8 +690,9 @@ di_status p2p_run(di_ctx *ctx, double target) {
         }
       }
       // 3. s_k, r_k, board; one host copy
+      const bool slept = asleep;
       TRYP(round_measure(ctx, hb));
-      if (ctx->opt.profile) {
+      if (ctx->opt.profile && !slept) {
         for (int k = 0; k < ctx->check_interval; ++k) {
           float a = 0.f, b = 0.f;
           CKP(cudaEventElapsedTime(&a, ctx->prof_ev[4 * k + 0], ctx->prof_ev[4 * k + 1]));
@@ -696,6 +706,7 @@ di_status p2p_run(di_ctx *ctx, double target) {
       ctx->passes_done = h->pass;
       const double s_k = hb->round[kRoundS] + hb->round[kRoundPend];
       const double r_k = hb->round[kRoundR];
+      asleep = ctx->opt.p2p_sleep >= 0 && r_k < target / W;
       ds->s_k = s_k;
       double board = 0.0;
       for (int q = 0; q < W; ++q) board += hb->hdr.board[q];

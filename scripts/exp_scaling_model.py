@@ -41,6 +41,7 @@ KS = [int(k) for k in os.environ.get("MODEL_K", "2,4,8").split(",")]
 ROUND = int(os.environ.get("MODEL_ROUND_PASSES", "4"))      # bench --round-passes
 REMOTE = int(os.environ.get("MODEL_REMOTE_PUSH", "1"))      # bench --remote-push
 RESCALE = int(os.environ.get("MODEL_RESCALE", "1"))          # options.receive_rescale
+SLEEP = int(os.environ.get("MODEL_SLEEP", "0"))              # options.p2p_sleep (0 on, -1 off)
 P2P = os.environ.get("MODEL_MODE", "async") == "p2p"
 MODE = di.DI_EXCHANGE_P2P if P2P else di.DI_EXCHANGE_ASYNC   # SYNC's di_stats.edges are global totals
 B_P2P, T_CONFIRM = 900e9, 150e-6
@@ -71,7 +72,7 @@ for K in KS:
             lcp, lri, lv, lb = dist.shard_csc(p.col_ptr, p.row_idx, p.values, p.b, bounds, r)
             o = di.default_options(policy=pol, alpha=alpha_k, hybrid_frac=frac_k, select_key=key,
                                    exchange_mode=MODE, check_interval=ROUND, remote_push=REMOTE,
-                                   receive_rescale=RESCALE)
+                                   receive_rescale=RESCALE, p2p_sleep=SLEEP)
             ctx = di.di_create_dist(r, K, cid, bounds, p.n, lcp, lri, lv, lb, p.d, o)
             di.di_run(ctx, p.stop)
             st[r] = di.di_get_stats(ctx)
@@ -106,7 +107,8 @@ for K in KS:
                    "efficiency_model": eff, "confirms": [s["confirms"] for s in st],
                    "collectives": [s["collectives"] for s in st],
                    "exchange_bytes_resident": [s["exchange_bytes_resident"] for s in st],
-                   "loopback_wall_s": wall, "passes_per_rank": [s["passes"] for s in st]}
+                   "loopback_wall_s": wall, "passes_per_rank": [s["passes"] for s in st],
+                   "sleep_rounds": [s["sleep_rounds"] for s in st]}
     print(f"K={K}: rounds={rounds} max bytes/round={per_round / 1e6:.1f} MB  edges sum={sum(s['edges'] for s in st):.4e} "
           f"(1 GPU {E1:.4e})  compute max/T1={comp:.3f}  T_K model={TK * 1e3:.1f} ms  efficiency={eff:.2f}", flush=True)
 print(json.dumps(out))
