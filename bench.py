@@ -98,10 +98,8 @@ def parse():
     ap.add_argument("--pass-csv", default=None, help="write the last solve's per-pass log here")
     ap.add_argument("--dist-path", action="store_true",
                     help="tests: run the N > 1 code path (di_create_dist over NCCL) even with one rank")
-    ap.add_argument("--near-pull", type=int, default=0, choices=[-1, 0, 1],
-                    help="options.near_pull: 0 auto (on for the web-like configs), 1 on, -1 off (push only)")
-    ap.add_argument("--pull-permille", type=int, default=0,
-                    help="options.pull_permille: pull a pass when its E_p estimate >= this/1000 of the edges")
+    ap.add_argument("--far-defer", type=int, default=0,
+                    help="options.far_defer (one GPU): 0 auto, -1 off, > 0 passes between far-edge flushes")
     ap.add_argument("--l2-persist", type=int, default=0,
                     help="options.l2_persist: 0 auto, -1 off, > 0 window MB (experiments)")
     ap.add_argument("--exchange", default="p2p", choices=["sync", "async", "p2p"],
@@ -398,7 +396,7 @@ def run_ours(args, rank, world, local_rank):
     opts = di.default_options(policy=pol, device=local_rank, profile=0, exchange_mode=mode,
                               alpha=args.alpha, hybrid_frac=args.hybrid_frac, select_key=args.key,
                               scatter_run=SCATTER_RUN.get(args.config, 0), l2_persist=args.l2_persist,
-                              near_pull=args.near_pull, pull_permille=args.pull_permille, **dist_kw)
+                              far_defer=args.far_defer, **dist_kw)
     comm_id, bounds, shard = None, None, None
     if dist:
         bounds = dd.partition_bounds(p.col_ptr, world, cost=args.partition, row_idx=p.row_idx)

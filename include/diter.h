@@ -152,14 +152,15 @@ typedef struct {
                               sleeps: its rounds only merge, send and measure,
                               no local passes, until received fluid lifts r_k again; 0 = on
                               (default), -1 = off */
-  int32_t near_pull;       /* one GPU, PageRank: near-edge pull -- the edges joining
-                              nodes <= 1024 ids apart are stored last in their columns and, in a
-                              dense pass, added row by row from a sliced in-edge table (no atomic)
-                              instead of one fp64 RED each; same block pass, only the
-                              summation order differs.  0 = auto (on when such edges are >= 25 %
-                              of the edges and n >= 16384), 1 = on, -1 = off */
-  int32_t pull_permille;   /* a pass pulls when the select's estimate of E_p is >= this / 1000 of
-                              the edges (0 = default 120) */
+  int32_t far_defer;       /* one GPU, PageRank: far-edge deferral -- a column's
+                              edges to rows more than 2048 ids away and outside the L2 persisting
+                              window (else the shared-memory hot window) are pushed not at every
+                              diffusion but every far_defer passes, as (H_i - H_old_i) p_ji (the
+                              paper's increment push); a run stops on
+                              |F|_1 + pending and only with nothing pending.  Same fixed point X
+                              (P:93-94), another pass schedule.  0 = off (default: slower on C4 at
+                              every cadence measured), > 0 = passes between flushes */
+  int32_t reserved1;
 } di_options;
 
 /* One record per executed pass (device-logged, read with di_get_pass_log). */
@@ -218,8 +219,8 @@ typedef struct {
   int64_t exchange_bytes_resident; /* distributed: device bytes of the exchange state (outbox, flags,
                               record buffers or inbox rings) */
   int64_t sleep_rounds;    /* DI_EXCHANGE_P2P: rounds this rank spent asleep since create */
-  int64_t pull_passes;     /* near-edge pull: passes that added their near edges row-wise */
-  int64_t pull_near_edges; /* near-edge pull: edges in the near in-edge table (0 = pull off) */
+  int64_t far_flushes;     /* far-edge deferral: flushes of the far-edge increments since create */
+  int64_t far_edges;       /* far-edge deferral: edges deferred to the flushes (0 = deferral off) */
 } di_stats;
 
 /* Fill *opt with the defaults above. */

@@ -60,7 +60,7 @@ class di_options(ctypes.Structure):
                 ("select_key", ctypes.c_int32), ("remote_push", ctypes.c_int32),
                 ("receive_rescale", ctypes.c_int32), ("adapt_rounds", ctypes.c_int32),
                 ("l2_persist", ctypes.c_int32), ("p2p_sleep", ctypes.c_int32),
-                ("near_pull", ctypes.c_int32), ("pull_permille", ctypes.c_int32)]
+                ("far_defer", ctypes.c_int32), ("reserved1", ctypes.c_int32)]
 
 
 class di_pass_log(ctypes.Structure):
@@ -86,7 +86,7 @@ class di_stats(ctypes.Structure):
                 ("dangling", ctypes.c_int64), ("run_kernel_launches", ctypes.c_int64),
                 ("collectives", ctypes.c_int64), ("confirms", ctypes.c_int64),
                 ("exchange_bytes_resident", ctypes.c_int64), ("sleep_rounds", ctypes.c_int64),
-                ("pull_passes", ctypes.c_int64), ("pull_near_edges", ctypes.c_int64)]
+                ("far_flushes", ctypes.c_int64), ("far_edges", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

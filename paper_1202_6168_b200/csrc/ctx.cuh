@@ -77,7 +77,7 @@ struct di_ctx {
   std::vector<cudaEvent_t> prof_ev;  // profile=1: 4 events per captured pass
 
   // stats
-  long long passes_done = 0, edges = 0, nodes = 0, dang = 0, pull_passes = 0;
+  long long passes_done = 0, edges = 0, nodes = 0, dang = 0;
   long long graph_launches = 0, kernel_launches = 0;
   long long run_kernel_launches = 0;   // kernels launched by the last di_run
   long long exchanged_bytes = 0, exchanges = 0, alg_bytes_exchange = 0;
@@ -86,16 +86,10 @@ struct di_ctx {
   long long kt_passes = 0;
   std::vector<std::pair<double, double>> pass_us;  // profile=1: (select, scatter) us per pass
 
-  // near-edge pull (pull.cu; one GPU, PageRank)
-  int pull_on = 0;
-  unsigned short *pull_nn = nullptr;    // [n] near edges per column (stored last)
-  unsigned short *pull_perm = nullptr;  // [tiles * kPullR] row of each sorted tile slot
-  unsigned *pull_sptr = nullptr;        // [slices + 1] first pair word of each slice
-  unsigned *pull_off = nullptr;         // [pairs * 32] int16 source offsets, two per word
-  double *pull_sw = nullptr;            // [n] s_i d / #out_i of this pass's taken nodes
-  unsigned *pull_bits = nullptr;        // [n / 32] taken non-dangling nodes of this pass
-  long long pull_tiles = 0, pull_near = 0, pull_pairs = 0;
-  int grid_pull = 0;
+  // far-edge deferral (defer.cu; one GPU, PageRank): nloc = near edges per column
+  int defer_m = 0;                // passes between flushes (0 = off)
+  long long far_edges = 0;        // edges deferred to the flushes
+  long long far_flushes = 0;
 
   DistState *dist = nullptr;
   std::string err;
@@ -128,7 +122,8 @@ void diter_dist_stats(const di_ctx *ctx, di_stats *s);   // collectives, confirm
 void diter_dist_pass_prologue(di_ctx *ctx);               // kernels before each pass (P2P: inbox merge)
 di_status diter_capture_graph(di_ctx *ctx);               // (re)capture check_interval passes as a graph
 di_status diter_dist_reset(di_ctx *ctx);
-// near-edge pull (pull.cu): setup after the upload, the pass kernel, release
-di_status diter_setup_pull(di_ctx *ctx);
-void diter_pull_launch(di_ctx *ctx);
-void diter_pull_free(di_ctx *ctx);
+// far-edge deferral (defer.cu): setup after the upload, the flush pair of a pass, a
+// host-driven flush
+di_status diter_setup_defer(di_ctx *ctx);
+void diter_defer_launch(di_ctx *ctx);
+di_status diter_defer_flush_now(di_ctx *ctx, int done);

@@ -145,7 +145,6 @@ static void free_ctx(di_ctx *c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   mark("sync");
   for (void *p : ptrs) diter_free(c, p);
-  diter_pull_free(c);
   mark("frees");
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
   mark("free host");
@@ -447,12 +446,7 @@ Graph diter_graph(const di_ctx *ctx) {
   Graph g{ctx->col_ptr, ctx->row_idx, ctx->vals, ctx->n_local, ctx->d, ctx->hot_lo,
           ctx->lo, ctx->G, ctx->dflags, ctx->far, ctx->nloc,
           ctx->opt.remote_push != DI_REMOTE_PER_DIFFUSION ? 1 : 0};
-  g.nn = ctx->pull_on ? ctx->pull_nn : nullptr;
-  g.sw = ctx->pull_sw;
-  g.sel_part = ctx->sel_part;
-  g.n_sel_part = ctx->grid_select;
-  const int pm = ctx->opt.pull_permille > 0 ? ctx->opt.pull_permille : 120;
-  g.pull_min_edges = 1e-3 * pm * (double)ctx->nnz_local;
+  g.defer = ctx->defer_m > 0 ? 1 : 0;
   return g;
 }
 
@@ -493,10 +487,10 @@ di_status diter_capture_graph(di_ctx *ctx) {
     }
     if (ctx->far.on)
       k_apply_far<<<ctx->num_sms * 4, kApplyThreads, 0, ctx->stream>>>(ctx->F, ctx->far, ctx->lo, ctx->ctl);
-    diter_pull_launch(ctx);     // near edges of a pull pass (returns at once otherwise)
     if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 2], ctx->stream, cudaEventRecordExternal));
     k_finalize<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->ctl, ctx->sel_part, ctx->grid_select, ctx->sc_part,
                                                         ctx->grid_scatter, ctx->log);
+    diter_defer_launch(ctx);    // far-edge increments when k_finalize asked (returns at once otherwise)
     if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 3], ctx->stream, cudaEventRecordExternal));
   }
   cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
@@ -663,10 +657,8 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
   TRY(dalloc(ctx, &ctx->fr.hub_b0, hc.n_hub));
   TRY(dalloc(ctx, &ctx->fr.hub_deg, hc.n_hub));
   TRY(dalloc(ctx, &ctx->fr.hub_chunk, hc.n_hub));
-  // mean #out over non-dangling nodes: the select's E_p estimate under the raw key
-  ctx->fr.mean_deg = (double)nnz / (double)std::max(1ULL, (unsigned long long)n - hc.n_dang);
-  TRY(diter_setup_pull(ctx));
-  tr.mark(ctx->stream, "near-edge pull");
+  TRY(diter_setup_defer(ctx));
+  tr.mark(ctx->stream, "far-edge deferral");
   CK(cudaStreamSynchronize(ctx->stream));
   return DI_OK;
 }
@@ -689,6 +681,7 @@ di_status diter_setup_finish(di_ctx *ctx) {
   hc0.hybrid_frac = o.hybrid_frac;
   hc0.n_total = (double)ctx->n_rows;
   hc0.policy = o.policy;
+  hc0.defer_m = ctx->defer_m;
   hc0.done = 1;
   hc0.max_pass = o.max_passes;
   hc0.log_cap = ctx->log_cap;
@@ -800,7 +793,7 @@ extern "C" di_status di_run(di_ctx *ctx, double target) {
       const long long pass_before = h->pass;
       CK(cudaGraphLaunch(ctx->graph_exec, ctx->stream));
       ctx->graph_launches += 1;
-      ctx->kernel_launches += (3LL + (ctx->cap_hub > 0) + (ctx->far.on ? 1 : 0) + ctx->pull_on) * ctx->check_interval;
+      ctx->kernel_launches += (3LL + (ctx->cap_hub > 0) + (ctx->far.on ? 1 : 0) + (ctx->defer_m ? 2 : 0)) * ctx->check_interval;
       TRY(read_ctl(ctx));
       if (ctx->opt.profile) {
         const long long active = std::min<long long>(h->pass - pass_before, ctx->check_interval);
@@ -815,6 +808,10 @@ extern "C" di_status di_run(di_ctx *ctx, double target) {
         ctx->kt_passes += active;
       }
       if (h->done) break;
+    }
+    if (h->pending > 0.0) {            // guard: a run never ends with far-edge mass undelivered
+      TRY(diter_defer_flush_now(ctx, h->done));
+      TRY(read_ctl(ctx));
     }
     ctx->passes_done = h->pass;
     if (h->done == 2) {
@@ -838,7 +835,7 @@ extern "C" di_status di_run(di_ctx *ctx, double target) {
   ctx->edges = h->edges;
   ctx->nodes = h->nodes;
   ctx->dang = h->dang;
-  ctx->pull_passes = h->pull_passes;
+  ctx->far_flushes = h->flushes;
   ctx->threshold = h->T;
   ctx->run_kernel_launches = ctx->kernel_launches - launches0;
   if (st == DI_ERR_NOT_CONVERGED) diter_set_err(ctx, "max_passes reached before |F|_1 < %g", target);
@@ -871,7 +868,8 @@ extern "C" di_status di_reset(di_ctx *ctx) {
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaGetLastError());
   ctx->kernel_launches += 1;
-  ctx->passes_done = ctx->edges = ctx->nodes = ctx->dang = ctx->pull_passes = 0;
+  ctx->passes_done = ctx->edges = ctx->nodes = ctx->dang = ctx->far_flushes = 0;
+  if (ctx->defer_m) CK(cudaMemsetAsync(ctx->H_old, 0, sizeof(double) * (size_t)ctx->n_local, ctx->stream));
   ctx->run_kernel_launches = 0;
   ctx->kt_ms[0] = ctx->kt_ms[1] = ctx->kt_ms[2] = 0.0;
   ctx->kt_passes = 0;
@@ -994,8 +992,8 @@ extern "C" di_status di_get_stats(const di_ctx *ctx, di_stats *s) {
   s->rebalances = ctx->rebalances;
   s->l2_window_bytes = ctx->l2_bytes;
   s->l2_window_row = ctx->l2_bytes > 0 ? ctx->lo + ctx->l2_lo : 0;
-  s->pull_passes = ctx->pull_passes;
-  s->pull_near_edges = ctx->pull_on ? ctx->pull_near : 0;
+  s->far_flushes = ctx->far_flushes;
+  s->far_edges = ctx->far_edges;
   diter_dist_stats(ctx, s);
   return DI_OK;
 }

@@ -53,7 +53,7 @@ __device__ __forceinline__ void reset_tickets(Ctl *ctl) {
 template <bool KEY>
 __device__ __forceinline__ void select_loop(double *__restrict__ F, double *__restrict__ H, const Frontier &fr,
                                             long long beg, long long end, const double T, const float *__restrict__ kw,
-                                            double &r, int &cnt, int &sel_all, double &dloss, double &est) {
+                                            double &r, int &cnt, int &sel_all, double &dloss) {
   const unsigned lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
   int *__restrict__ ids = fr.ids + beg;
@@ -70,7 +70,6 @@ __device__ __forceinline__ void select_loop(double *__restrict__ F, double *__re
     // lane k < 16 holds the dangling word of item k (32 nodes, base is 512-aligned)
     const long long wi = (base >> 5) + lane;
     const unsigned dword = ((int)lane < kSelectItems && (wi << 5) < end) ? __ldg(fr.dang_bits + wi) : 0u;
-    unsigned mword = 0u;    // lane k: the taken non-dangling nodes of item k (sel_bits)
 #pragma unroll
     for (int k = 0; k < kSelectItems; ++k) {
       const long long i = base + 32 * k + lane;
@@ -80,9 +79,6 @@ __device__ __forceinline__ void select_loop(double *__restrict__ F, double *__re
       const bool sel = (KEY ? af * (double)w[k] : af) > T;
       const bool dang = (__shfl_sync(0xffffffffu, dword, k) >> lane) & 1u;
       const unsigned m = __ballot_sync(0xffffffffu, sel && !dang);
-      if ((int)lane == k) mword = m;
-      // E_p estimate for the pull decision: #out_i = 1/w_i - 1 under the per-edge key
-      if (KEY && sel && !dang) est += 1.0 / (double)w[k] - 1.0;
       if (sel) {
         F[i] = 0.0;            // F_i := 0
         red_add(H + i, f[k]);  // H_i += sent
@@ -97,7 +93,6 @@ __device__ __forceinline__ void select_loop(double *__restrict__ F, double *__re
       cnt += __popc(m);
       sel_all += __popc(__ballot_sync(0xffffffffu, sel));
     }
-    if (fr.sel_bits && (int)lane < kSelectItems && (wi << 5) < end) fr.sel_bits[wi] = mword;
   }
 }
 
@@ -108,25 +103,24 @@ __device__ __forceinline__ void select_body(double *__restrict__ F, double *__re
   const int gw = blockIdx.x * (kSelectThreads / 32) + (threadIdx.x >> 5);
   const long long beg = (long long)gw * fr.seg_len;
   const long long end = min(n, beg + fr.seg_len);
-  double r = 0.0, dloss = 0.0, est = 0.0;
+  double r = 0.0, dloss = 0.0;
   int cnt = 0, sel_all = 0;                      // warp-uniform running counts
-  if (kw) select_loop<true>(F, H, fr, beg, end, T, kw, r, cnt, sel_all, dloss, est);
-  else select_loop<false>(F, H, fr, beg, end, T, kw, r, cnt, sel_all, dloss, est);
+  if (kw) select_loop<true>(F, H, fr, beg, end, T, kw, r, cnt, sel_all, dloss);
+  else select_loop<false>(F, H, fr, beg, end, T, kw, r, cnt, sel_all, dloss);
   if (gw < fr.n_seg && lane == 0) fr.seg_cnt[gw] = cnt;
   r = warp_sum(r);
   dloss = warp_sum(dloss);
-  est = kw ? warp_sum(est) : (double)cnt * fr.mean_deg;
-  __shared__ double s_r[kSelectThreads / 32], s_l[kSelectThreads / 32], s_e[kSelectThreads / 32];
+  __shared__ double s_r[kSelectThreads / 32], s_l[kSelectThreads / 32];
   __shared__ int s_c[kSelectThreads / 32], s_d[kSelectThreads / 32];
   if (lane == 0) {
-    s_r[threadIdx.x >> 5] = r; s_l[threadIdx.x >> 5] = dloss; s_e[threadIdx.x >> 5] = est;
+    s_r[threadIdx.x >> 5] = r; s_l[threadIdx.x >> 5] = dloss;
     s_c[threadIdx.x >> 5] = sel_all; s_d[threadIdx.x >> 5] = sel_all - cnt;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    SelPartial p{0.0, 0, 0.0, 0, 0.0};
+    SelPartial p{0.0, 0, 0.0, 0};
     for (int k = 0; k < kSelectThreads / 32; ++k) {
-      p.r += s_r[k]; p.cnt += s_c[k]; p.loss += s_l[k]; p.dang += s_d[k]; p.est_edges += s_e[k];
+      p.r += s_r[k]; p.cnt += s_c[k]; p.loss += s_l[k]; p.dang += s_d[k];
     }
     part[blockIdx.x] = p;
   }
@@ -359,6 +353,7 @@ __device__ __forceinline__ void push_group(const Graph &g, const Sink &s, Ctl *c
 
 struct ScAcc {
   double loss = 0.0;
+  double pend = 0.0;      // far-edge deferral: mass left for the flush
   long long edges = 0;
   long long remote = 0;   // distributed, per-diffusion mode: pushes into the outbox
   int dang = 0, lo = 0, mi = 0, hu = 0;
@@ -429,8 +424,7 @@ __device__ __forceinline__ int find_segment(const int *s_goff, int n_seg, int q)
 
 template <bool SIGNED, bool DIST, bool FAR>
 __device__ __forceinline__ void scatter_group(const Graph &g, const Sink &s, const Frontier &fr, Ctl *ctl,
-                                              const int *s_goff, int *st, int q, int &seg, ScAcc &acc, Stage &sg,
-                                              bool pull) {
+                                              const int *s_goff, int *st, int q, int &seg, ScAcc &acc, Stage &sg) {
   // a warp's groups mostly ascend within one segment: walk forward from the
   // last segment, search only after a jump
   if (q < s_goff[seg] || q >= s_goff[seg + 4 < fr.n_seg ? seg + 4 : fr.n_seg]) seg = find_segment(s_goff, fr.n_seg, q);
@@ -464,11 +458,12 @@ __device__ __forceinline__ void scatter_group(const Graph &g, const Sink &s, con
         const long long nl = __ldg(g.nloc + i);
         if (g.local_only) dpush = nl;
         else acc.remote += deg - nl;
-      } else if (pull) {
-        // pull pass: the near edges (stored last in the column) are added row-wise
-        // by k_pull from sw; push the others
-        dpush = deg - (long long)__ldg(g.nn + i);
-        g.sw[i] = w;
+      } else if (g.defer) {
+        // far-edge deferral: push the near edges now; the far ones (stored last) get
+        // this fluid at the next flush, as part of H_i - H_old_i
+        const long long nl = __ldg(g.nloc + i);
+        dpush = nl;
+        acc.pend += asv * (g.d * (double)(deg - nl) / (double)deg);
       }
       if (deg <= kLowMax) acc.lo += 1;
       else if (deg <= kMidMax) acc.mi += 1;
@@ -508,21 +503,6 @@ __device__ __forceinline__ void scatter_body(const Graph &g, double *__restrict_
   for (int b = (int)lane_id(); b < kMaxBins; b += 32) { st[b] = -1; st[kMaxBins + b] = 0; }
   __shared__ unsigned s_dead;      // stripes this CTA has seen exhausted
   if (threadIdx.x == 0) s_dead = 0u;
-  // near-edge pull decision (one GPU, PageRank): every CTA sums the select's E_p
-  // estimates in the same order, so all agree; CTA 0 publishes it for k_pull
-  bool pull = false;
-  if (!DIST && g.nn != nullptr) {
-    __shared__ double s_est[kScatterThreads / 32];
-    double e = 0.0;
-    for (int k = threadIdx.x; k < g.n_sel_part; k += blockDim.x) e += g.sel_part[k].est_edges;
-    e = warp_sum(e);
-    if (lane_id() == 0) s_est[threadIdx.x >> 5] = e;
-    __syncthreads();
-    double t = 0.0;
-    for (int k = 0; k < kScatterThreads / 32; ++k) t += s_est[k];
-    pull = t >= g.pull_min_edges;
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->pull_pass = pull ? 1 : 0;
-  }
   const int total = build_group_prefix(fr, s_goff);    // ends with __syncthreads
   const Sink s{F, s_hot, g.hot_lo, g.lo, g.n, g.G, g.dflags};
   const unsigned lane = lane_id();
@@ -556,7 +536,7 @@ __device__ __forceinline__ void scatter_body(const Graph &g, double *__restrict_
         break;
       }
       const int q1 = min(s1, s0 + (int)q0 + run);
-      for (int q = s0 + (int)q0; q < q1; ++q) scatter_group<SIGNED, DIST, FAR>(g, s, fr, ctl, s_goff, st, q, seg, acc, sg, pull);
+      for (int q = s0 + (int)q0; q < q1; ++q) scatter_group<SIGNED, DIST, FAR>(g, s, fr, ctl, s_goff, st, q, seg, acc, sg);
     }
   }
   if constexpr (FAR) {
@@ -577,14 +557,15 @@ __device__ __forceinline__ void scatter_body(const Graph &g, double *__restrict_
   acc.mi = warp_sum(acc.mi);
   acc.hu = warp_sum(acc.hu);
   if (DIST) acc.remote = warp_sum(acc.remote);
+  if (!DIST) acc.pend = warp_sum(acc.pend);
   __shared__ ScAcc s_acc[kScatterThreads / 32];
   if (lane == 0) s_acc[threadIdx.x >> 5] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
-    ScPartial p{0.0, 0, 0, 0, 0, 0};
+    ScPartial p{0.0, 0, 0, 0, 0, 0, 0.0};
     long long remote = 0;
     for (int k = 0; k < kScatterThreads / 32; ++k) {
-      p.loss += s_acc[k].loss; p.edges += s_acc[k].edges; p.dang += s_acc[k].dang;
+      p.loss += s_acc[k].loss; p.edges += s_acc[k].edges; p.dang += s_acc[k].dang; p.pend += s_acc[k].pend;
       p.n_low += s_acc[k].lo; p.n_mid += s_acc[k].mi; p.n_hub += s_acc[k].hu;
       remote += s_acc[k].remote;
     }
@@ -677,17 +658,18 @@ k_apply_far(double *__restrict__ F, Far far, long long lo, const Ctl *ctl) {
 // -------------------------------------------------------------- K5 finalize --
 // Pass totals as doubles (integers < 2^53 are exact), so a distributed context
 // can all-reduce them in one call: r, loss, |S_p|, E_p, dangling, low, mid, hub.
-constexpr int kSums = 8;
+constexpr int kSums = 9;     // ... and the far-edge mass deferred by this pass
 
 __device__ __forceinline__ void reduce_partials(const SelPartial *__restrict__ sp, int n_sp,
                                                 const ScPartial *__restrict__ cp, int n_cp, double *out) {
-  double v[kSums] = {0, 0, 0, 0, 0, 0, 0, 0};
+  double v[kSums] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int k = threadIdx.x; k < n_sp; k += blockDim.x) {
     v[0] += sp[k].r; v[2] += (double)sp[k].cnt; v[1] += sp[k].loss; v[4] += (double)sp[k].dang;
   }
   for (int k = threadIdx.x; k < n_cp; k += blockDim.x) {
     const ScPartial p = cp[k];
     v[1] += p.loss; v[3] += (double)p.edges; v[4] += p.dang; v[5] += p.n_low; v[6] += p.n_mid; v[7] += p.n_hub;
+    v[8] += p.pend;
   }
   constexpr int W = kFinalizeThreads / 32;
   __shared__ double s_v[kSums][W];
@@ -724,17 +706,28 @@ __device__ __forceinline__ void apply_pass(Ctl *ctl, const double *sums, di_pass
   ctl->nodes += cnt;
   ctl->dang += (long long)sums[4];
   ctl->r = r;
-  const double pred = r - loss;
+  // Far-edge deferral: the state is (F, D) with D the far-edge fluid not yet delivered,
+  // |D|_1 <= pending, and F + D = B - (I - P)H; |F + D|_1 drops by >= loss per pass
+  // (App. A.2), so r + pending - loss bounds the true residual after this pass.
+  const double pend0 = ctl->pending;
+  const double pend1 = pend0 + sums[8];
+  ctl->pending = pend1;
+  const double pred = r + pend0 - loss;
   ctl->r_pred = pred;
   // T_{p+1}: GEOM divides every pass; HYBRID only when |S_p| <= f N (readings R4/R6).
   if (ctl->policy == DI_POLICY_GEOM || (double)cnt <= ctl->hybrid_frac * ctl->n_total)
     ctl->T = fmax(T / ctl->alpha, ctl->T_floor);
   ctl->pass = p + 1;
-  if (r < ctl->target || pred < ctl->target) ctl->done = 1;
-  else if (p + 1 >= ctl->max_pass) ctl->done = 2;
+  if (r + pend0 < ctl->target || pred < ctl->target) {
+    if (pend1 == 0.0) ctl->done = 1;
+    else { ctl->flush_now = 1; ctl->stop_after_flush = 1; }     // deliver D, then stop
+  } else if (p + 1 >= ctl->max_pass) {
+    if (pend1 == 0.0) ctl->done = 2;
+    else { ctl->flush_now = 1; ctl->stop_after_flush = 2; }
+  } else if (ctl->defer_m > 0 && (p + 1) % ctl->defer_m == 0 && pend1 > 0.0) {
+    ctl->flush_now = 1;
+  }
   ctl->hub_packed = 0ull;
-  ctl->pull_passes += ctl->pull_pass;
-  ctl->pull_pass = 0;
   reset_tickets(ctl);
 }
 

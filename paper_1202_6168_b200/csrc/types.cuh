@@ -36,13 +36,6 @@ constexpr int kStripes = 32;                         // max scatter ticket count
 constexpr int kMaxBins = 64;                         // far-push destination bins (propagation blocking)
 constexpr int kNear = 2048;                          // pushes within +-kNear rows of the group are "near"
 constexpr int kFarChunk = 128;                       // far-record slots per warp-owned chunk
-// Near-edge pull (one GPU, PageRank): an edge i -> j is "near" when |j - i| <= kPullW
-// (and #out_i <= 65535); pull passes add those edges row-wise from a sliced in-edge
-// table instead of one RED per edge (pull.cu).
-constexpr int kPullW = 1024;                         // near window half-width (rows)
-constexpr int kPullR = 2048;                         // rows per pull tile
-constexpr int kPullThreads = 256;
-constexpr int kPullZero = kPullR + 2 * kPullW;       // index of the always-zero window slot
 
 // Device-resident control block of one context.
 struct Ctl {
@@ -62,12 +55,18 @@ struct Ctl {
   int policy;          // DI_POLICY_*
   unsigned long long hub_packed;  // (hub slots << 32) | hub chunks; reset by k_finalize
   long long log_cap;
-  int pull_pass;       // this pass adds near edges by the pull kernel (set by the scatter)
+  int flush_now;       // far-edge deferral: k_far_flush delivers the increments after this pass
   unsigned long long remote_pushes;   // distributed: pushes into the outbox (one atomic per CTA per pass)
   double t_sel_us;     // fused kernel: accumulated select / scatter phase time (%globaltimer)
   double t_sc_us;
   double T_floor;      // P2P: the local schedule does not lower T below this (0 = no floor)
-  long long pull_passes;  // passes that added their near edges by k_pull
+  // far-edge deferral (one GPU; defer.cu): the far edges of diffused nodes wait for a
+  // flush that pushes (H_i - H_old_i) p_ji along them (PAPER.md:227-250 applied to the
+  // rows far from their source); `pending` bounds the undelivered mass |D|_1
+  double pending;
+  int defer_m;         // passes between flushes (0 = deferral off)
+  int stop_after_flush;   // the bound met the target with mass pending: stop once it is delivered
+  long long flushes;   // flushes executed since create
   // scatter tickets: one counter per stripe of the frontier groups, each on its
   // own 128-byte line (reset per pass)
   alignas(128) unsigned tickets[kStripes * 32];
@@ -81,7 +80,6 @@ struct SelPartial {
   long long cnt;      // |S_p|, dangling nodes included
   double loss;        // sum |s_i| over the dangling nodes taken (their fluid leaves, App. A.2)
   long long dang;     // dangling nodes taken (they never reach the scatter)
-  double est_edges;   // estimate of E_p over the non-dangling nodes taken (pull decision)
 };
 
 // k_scatter partials (one per CTA): guaranteed |F|_1 drop and frontier census.
@@ -89,6 +87,7 @@ struct ScPartial {
   double loss;      // sum over taken nodes of (1 - c_i)|s_i|, c_i = d (0 if dangling)
   long long edges;  // E_p
   int dang, n_low, n_mid, n_hub;
+  double pend;      // far-edge deferral: sum |s_i| d #far_i / #out_i (mass left for the flush)
 };
 
 // Far pushes (propagation blocking).  A push whose row lies outside the shared-
@@ -125,14 +124,10 @@ struct Graph {
   double *G;                 // remote outbox over global ids, or nullptr on one GPU
   unsigned char *dflags;     // dirty flag per 32-row block of G
   Far far;
-  const int *nloc;           // distributed: local edges of each column (stored first), else nullptr
+  const int *nloc;           // distributed: local edges of each column (stored first); one GPU with
+                             // far-edge deferral: near edges of each column (stored first); else nullptr
   int local_only;            // DI_REMOTE_INCREMENT: the scatter pushes [b0, b0 + nloc) only
-  // near-edge pull (1 GPU, PageRank; nn == nullptr when off)
-  const unsigned short *nn;  // [n] near edges of each column, stored LAST in the column
-  double *sw;                // [n] s_i d / #out_i of the nodes taken in a pull pass
-  const SelPartial *sel_part;  // this pass's select partials (the pull decision)
-  int n_sel_part;
-  double pull_min_edges;     // pull when the select's E_p estimate reaches this
+  int defer;                 // one GPU: far-edge deferral on (the scatter pushes [b0, b0 + nloc))
 };
 
 // Frontier of one pass, compacted per select warp: warp w scans the owned nodes
@@ -152,9 +147,6 @@ struct Frontier {
   long long *hub_b0;
   long long *hub_deg;
   unsigned *hub_chunk;   // first 2048-edge chunk id of the hub (prefix in slot order)
-  unsigned *sel_bits;    // [ceil(n/32)] bit i%32 of word i/32: non-dangling i taken this pass
-                         // (written when the near-edge pull is on, else nullptr)
-  double mean_deg;       // #out averaged over non-dangling nodes (E_p estimate of the raw key)
 };
 
 // Validation + degree census in one pass over the columns.

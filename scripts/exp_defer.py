@@ -1,6 +1,6 @@
-"""A/B of the near-edge pull on one generated graph (GPU):
+"""A/B of the far-edge deferral on one generated graph (GPU):
     python scripts/exp_pull.py C4 "-1:0 1:0 1:60 1:200" [steps]
-Each variant near_pull:pull_permille gets a fresh context (create time printed),
+Each variant far_defer:unused gets a fresh context (create time printed),
 2 warm-up solves, then `steps` timed solves (di_run device time, stats.run_ms)."""
 import os
 import sys
@@ -23,7 +23,7 @@ print(f"generated {cfg} n={p.n} nnz={p.nnz} in {time.perf_counter() - t:.1f}s", 
 for v in variants:
     npull, pm = (int(x) for x in v.split(":"))
     opts = di.default_options(policy=pol, alpha=alpha, hybrid_frac=frac, select_key=key,
-                              scatter_run=bench.SCATTER_RUN.get(cfg, 0), near_pull=npull, pull_permille=pm)
+                              scatter_run=bench.SCATTER_RUN.get(cfg, 0), far_defer=npull, reserved1=pm)
     t = time.perf_counter()
     ctx = di.di_create(p.n, p.col_ptr, p.row_idx, None, None, 0.85, opts)
     t_create = time.perf_counter() - t
@@ -35,7 +35,7 @@ for v in variants:
         if k >= warm:
             ms.append(di.di_get_stats(ctx)["run_ms"])
     st = di.di_get_stats(ctx)
-    print(f"{cfg} near_pull={npull:2d} permille={pm:3d}: {np.median(ms):8.2f} ms/solve (min {min(ms):.2f}) "
-          f"passes {st['passes']} pull_passes {st['pull_passes']} edges {st['edges']:.4e} "
-          f"near_edges {st['pull_near_edges']} create {t_create:.2f}s", flush=True)
+    print(f"{cfg} far_defer={npull:2d}: {np.median(ms):8.2f} ms/solve (min {min(ms):.2f}) "
+          f"passes {st['passes']} flushes {st['far_flushes']} edges {st['edges']:.4e} "
+          f"far_edges {st['far_edges']} create {t_create:.2f}s", flush=True)
     di.di_destroy(ctx)

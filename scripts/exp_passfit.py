@@ -23,7 +23,7 @@ if cfg == "C3":
 else:
     p = gen.config(cfg, 1)
 opts = di.default_options(policy=pol, alpha=alpha, hybrid_frac=frac, select_key=key,
-                          scatter_run=bench.SCATTER_RUN.get(cfg, 0), near_pull=npull,
+                          scatter_run=bench.SCATTER_RUN.get(cfg, 0), far_defer=npull,
                           **{k: int(v) for k, v in extra.items()})
 ctx = di.di_create(p.n, p.col_ptr, p.row_idx, None, None, 0.85, opts)
 for _ in range(2):
