@@ -160,7 +160,13 @@ typedef struct {
                               |F|_1 + pending and only with nothing pending.  Same fixed point X
                               (P:93-94), another pass schedule.  0 = off (default: slower on C4 at
                               every cadence measured), > 0 = passes between flushes */
-  int32_t reserved1;
+  int32_t sweep;           /* one GPU: 1 = one-kernel asynchronous sweeps (reading R26) --
+                              the paper's cyclic scan with immediate diffusion (PAPER.md:116-134,
+                              213-216) run by the whole grid: each node above T_p is taken
+                              (atomic exchange of F_i) and diffused at once, its pushes visible to
+                              nodes scanned later in the same sweep; no frontier list.  Same fixed
+                              point X; the pass log is per sweep and not the snapshot
+                              oracle's.  0 = snapshot passes (select, then scatter; default) */
 } di_options;
 
 /* One record per executed pass (device-logged, read with di_get_pass_log). */

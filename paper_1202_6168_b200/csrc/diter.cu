@@ -467,6 +467,26 @@ di_status diter_capture_graph(di_ctx *ctx) {
   for (int k = 0; k < ctx->check_interval; ++k) {
     diter_dist_pass_prologue(ctx);   // DI_EXCHANGE_P2P: merge what has arrived before every pass
     if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 0], ctx->stream, cudaEventRecordExternal));
+    if (ctx->sweep_on) {
+      // one-kernel async sweep (select + diffusion; options.sweep): the profile's
+      // "select" span is empty, its "scatter" span is the sweep + hub chunks
+      if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 1], ctx->stream, cudaEventRecordExternal));
+      auto sw = ctx->vals ? (ctx->kw ? k_sweep<true, true> : k_sweep<true, false>)
+                          : (ctx->kw ? k_sweep<false, true> : k_sweep<false, false>);
+      sw<<<ctx->grid_sweep, kScatterThreads, kSweepDynSmem, ctx->stream>>>(g, ctx->F, ctx->H, ctx->fr, ctx->ctl,
+                                                                           ctx->sel_part, ctx->sc_part, ctx->kw);
+      if (ctx->cap_hub > 0) {
+        if (ctx->vals)
+          k_scatter_hubs<true><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
+        else
+          k_scatter_hubs<false><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
+      }
+      if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 2], ctx->stream, cudaEventRecordExternal));
+      k_finalize<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->ctl, ctx->sel_part, ctx->grid_sweep, ctx->sc_part,
+                                                          ctx->grid_sweep, ctx->log);
+      if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 3], ctx->stream, cudaEventRecordExternal));
+      continue;
+    }
     k_select<<<ctx->grid_select, kSelectThreads, 0, ctx->stream>>>(ctx->F, ctx->H, ctx->fr, ctx->n_local,
                                                                   ctx->ctl, ctx->sel_part, ctx->kw);
     if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 1], ctx->stream, cudaEventRecordExternal));
@@ -604,8 +624,8 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
     k_dangling_bits<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->col_ptr, n, db);
     ctx->fr.dang_bits = db;
   }
-  TRY(dalloc(ctx, &ctx->sel_part, (size_t)std::max(ctx->grid_select, ctx->grid_fused)));
-  TRY(dalloc(ctx, &ctx->sc_part, (size_t)ctx->grid_scatter));
+  TRY(dalloc(ctx, &ctx->sel_part, (size_t)std::max(std::max(ctx->grid_select, ctx->grid_fused), ctx->num_sms * 4)));
+  TRY(dalloc(ctx, &ctx->sc_part, (size_t)std::max(ctx->grid_scatter, ctx->num_sms * 4)));
   TRY(dalloc(ctx, &ctx->l1_part, (size_t)ctx->grid_l1));
   TRY(dalloc(ctx, &ctx->l1_out, 1));
   TRY(dalloc(ctx, &ctx->ctl, 1));
@@ -657,7 +677,21 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
   TRY(dalloc(ctx, &ctx->fr.hub_b0, hc.n_hub));
   TRY(dalloc(ctx, &ctx->fr.hub_deg, hc.n_hub));
   TRY(dalloc(ctx, &ctx->fr.hub_chunk, hc.n_hub));
-  TRY(diter_setup_defer(ctx));
+  // one-kernel async sweeps (options.sweep): one GPU, per-phase launches, no far bins
+  ctx->sweep_on = (o.sweep == 1 && !ctx->dist && !ctx->fused && !ctx->far.on) ? 1 : 0;
+  if (ctx->sweep_on) {
+    // per-warp staging in dynamic shared memory (beyond the default 48 KB with the hot window)
+    auto attr = [&](const void *fn) { return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepDynSmem); };
+    CK(attr((const void *)k_sweep<false, false>));
+    CK(attr((const void *)k_sweep<false, true>));
+    CK(attr((const void *)k_sweep<true, false>));
+    CK(attr((const void *)k_sweep<true, true>));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep<false, true>, kScatterThreads, kSweepDynSmem));
+    ctx->grid_sweep = (int)std::max(1LL, std::min<long long>((long long)ctx->num_sms * std::max(1, occ),
+                                                             (n + kSweepSpan - 1) / kSweepSpan));
+  }
+  if (!ctx->sweep_on) TRY(diter_setup_defer(ctx));
   tr.mark(ctx->stream, "far-edge deferral");
   CK(cudaStreamSynchronize(ctx->stream));
   return DI_OK;
@@ -682,6 +716,7 @@ di_status diter_setup_finish(di_ctx *ctx) {
   hc0.n_total = (double)ctx->n_rows;
   hc0.policy = o.policy;
   hc0.defer_m = ctx->defer_m;
+  hc0.sweep = ctx->sweep_on;
   hc0.done = 1;
   hc0.max_pass = o.max_passes;
   hc0.log_cap = ctx->log_cap;
@@ -793,7 +828,9 @@ extern "C" di_status di_run(di_ctx *ctx, double target) {
       const long long pass_before = h->pass;
       CK(cudaGraphLaunch(ctx->graph_exec, ctx->stream));
       ctx->graph_launches += 1;
-      ctx->kernel_launches += (3LL + (ctx->cap_hub > 0) + (ctx->far.on ? 1 : 0) + (ctx->defer_m ? 2 : 0)) * ctx->check_interval;
+      ctx->kernel_launches += (ctx->sweep_on ? 2LL + (ctx->cap_hub > 0)
+                                             : 3LL + (ctx->cap_hub > 0) + (ctx->far.on ? 1 : 0) + (ctx->defer_m ? 2 : 0)) *
+                              ctx->check_interval;
       TRY(read_ctl(ctx));
       if (ctx->opt.profile) {
         const long long active = std::min<long long>(h->pass - pass_before, ctx->check_interval);

@@ -613,6 +613,231 @@ k_scatter_hubs(Graph g, double *__restrict__ F, Frontier fr, const Ctl *ctl) {
   hubs_body<SIGNED>(g, F, fr, ctl);
 }
 
+// ------------------------------------------------------ K1+K2 async sweep --
+// options.sweep = 1 (one GPU): the paper's cyclic scan with immediate diffusion
+// (SURVEY §8c step 4 "sequential mode"), run by the whole
+// grid at once.  One kernel per pass ("sweep"): warps claim spans of kSweepSpan
+// consecutive nodes in ascending order (striped tickets, as the scatter's groups),
+// load F over the span (8 coalesced 256-byte loads per warp), and for every node with
+// key |F_i| w_i > T_p take it and diffuse it at once:
+//   s_i = atomicExch(F_i, 0)     (a push landing between the read and the take stays
+//                                 in s_i, a later one stays in F_i: nothing is lost)
+//   H_i += s_i;  F_j += p_ji s_i along its out-edges (push_group, the scatter's
+//   edge-balanced lanes, shared-memory hot window, hub columns to k_scatter_hubs).
+// Pushes are visible to spans scanned later in the same sweep, as in the paper's
+// sequential scan; the limit is the same X.  There is no frontier list:
+// no select/scatter kernel boundary, no list traffic, and the streaming scan hides
+// under the latency-bound pushes.  |F|_1 is not re-measured per sweep: it drops by
+// exactly sum (1 - c_i)|s_i| (App. A.2; an upper bound for signed P), so k_finalize
+// advances the bound r_pred and di_run confirms convergence with an exact |F|_1.
+constexpr int kSweepItems = 8;
+constexpr int kSweepSpan = 32 * kSweepItems;
+constexpr int kSweepStage = 32 + kSweepSpan;     // per-warp staging: a partial group + one span
+
+// Per-warp staging of diffused nodes (shared memory): the selected non-dangling nodes
+// of a span are compacted here (ballot ranks) and pushed 32 at a time by push_group,
+// so a group is as dense as the snapshot scatter's frontier groups.
+struct SweepStage {
+  long long *b0;
+  int *deg;
+  double *w;
+  int cnt;     // warp-uniform fill
+};
+
+template <bool SIGNED>
+__device__ __forceinline__ void sweep_flush(const Graph &g, const Sink &s, Ctl *ctl, SweepStage &st, Stage &sg,
+                                            bool all) {
+  const unsigned lane = lane_id();
+  int done = 0;
+  while (st.cnt - done >= 32 || (all && st.cnt - done > 0)) {
+    __syncwarp();
+    const int e = done + (int)lane;
+    const bool ok = e < st.cnt;
+    push_group<SIGNED, false>(g, s, ctl, nullptr, ok ? st.b0[e] : 0, ok ? st.deg[e] : 0, ok ? st.w[e] : 0.0, 0, 0,
+                              sg);
+    done += 32;
+  }
+  if (done > 0) {
+    const int rest = max(0, st.cnt - done);
+    __syncwarp();
+    long long b = 0; int d = 0; double w = 0.0;
+    if ((int)lane < rest) { b = st.b0[done + lane]; d = st.deg[done + lane]; w = st.w[done + lane]; }
+    __syncwarp();
+    if ((int)lane < rest) { st.b0[lane] = b; st.deg[lane] = d; st.w[lane] = w; }
+    __syncwarp();
+    st.cnt = rest;
+  }
+}
+
+template <bool SIGNED, bool KEY>
+__device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double *__restrict__ F,
+                                           double *__restrict__ H, const Frontier &fr, Ctl *ctl,
+                                           const float *__restrict__ kw, double T, long long base,
+                                           ScAcc &acc, int &sel_all, double &dloss, int &dang_cnt,
+                                           SweepStage &st) {
+  const unsigned lane = lane_id();
+  const unsigned lt = (1u << lane) - 1u;
+  const long long n = g.n;
+  double f[kSweepItems];
+  float w[KEY ? kSweepItems : 1];
+  long long cp[kSweepItems];
+#pragma unroll
+  for (int k = 0; k < kSweepItems; ++k) {
+    const long long i = base + 32 * k + lane;
+    f[k] = (i < n) ? F[i] : 0.0;
+    if (KEY) w[k] = (i < n) ? __ldcs(kw + i) : 0.0f;
+    cp[k] = __ldcs(g.col_ptr + (i < n ? i : n));
+  }
+  const long long iend = base + kSweepSpan;
+  const long long cp_end = __ldcs(g.col_ptr + (iend < n ? iend : n));
+  const long long wi = (base >> 5) + lane;
+  const unsigned dword = ((int)lane < kSweepItems && (wi << 5) < n) ? __ldg(fr.dang_bits + wi) : 0u;
+  // take every selected node of the span (independent atomics, issued together)
+  unsigned msel[kSweepItems];
+#pragma unroll
+  for (int k = 0; k < kSweepItems; ++k) {
+    const long long i = base + 32 * k + lane;
+    const double af = fabs(f[k]);
+    const bool sel = (KEY ? af * (double)w[k] : af) > T;     // strict ">" (R7)
+    msel[k] = __ballot_sync(0xffffffffu, sel);
+    if (sel)                                                 // s_i
+      f[k] = __longlong_as_double((long long)atomicExch(reinterpret_cast<unsigned long long *>(F + i), 0ull));
+  }
+#pragma unroll
+  for (int k = 0; k < kSweepItems; ++k) {
+    const unsigned m = msel[k];
+    if (m == 0u) continue;
+    const long long i = base + 32 * k + lane;
+    const bool sel = (m >> lane) & 1u;
+    const bool dang = (__shfl_sync(0xffffffffu, dword, k) >> lane) & 1u;
+    // #out_i from the span's col_ptr values: lane 31's successor is the next item's lane 0
+    long long nxt = __shfl_down_sync(0xffffffffu, cp[k], 1);
+    const long long nxt0 = (k + 1 < kSweepItems) ? __shfl_sync(0xffffffffu, cp[k + 1 < kSweepItems ? k + 1 : k], 0)
+                                                 : cp_end;
+    if (lane == 31) nxt = nxt0;
+    const double sv = f[k];
+    const long long b0 = cp[k];
+    const long long deg = nxt - b0;
+    bool stage = false;
+    double wv = 0.0;
+    sel_all += __popc(m);
+    if (sel) {
+      red_add(H + i, sv);                                    // H_i += s_i
+      const double asv = fabs(sv);
+      if (dang || deg <= 0) {
+        dloss += asv;                                        // fluid leaves (App. A.2)
+        dang_cnt += 1;
+      } else {
+        acc.loss += (1.0 - g.d) * asv;
+        acc.edges += deg;
+        wv = SIGNED ? sv : sv * (g.d / (double)deg);
+        if (deg <= kLowMax) acc.lo += 1;
+        else if (deg <= kMidMax) acc.mi += 1;
+        else acc.hu += 1;
+        if (deg <= kMidMax) {
+          stage = true;
+        } else {
+          const unsigned long long nch = (unsigned long long)((deg + kHubChunk - 1) / kHubChunk);
+          const unsigned long long old = atomicAdd(&ctl->hub_packed, (1ull << 32) | nch);
+          const unsigned sl = (unsigned)(old >> 32);
+          fr.hub_w[sl] = wv; fr.hub_b0[sl] = b0; fr.hub_deg[sl] = deg;
+          fr.hub_chunk[sl] = (unsigned)(old & 0xffffffffull);
+        }
+      }
+    }
+    const unsigned ms = __ballot_sync(0xffffffffu, stage);
+    if (stage) {
+      const int pos = st.cnt + __popc(ms & lt);
+      st.b0[pos] = b0; st.deg[pos] = (int)deg; st.w[pos] = wv;
+    }
+    st.cnt += __popc(ms);
+  }
+}
+
+template <bool SIGNED, bool KEY>
+__global__ void __launch_bounds__(kScatterThreads, kScatterMinBlocks)
+k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ctl *ctl,
+        SelPartial *__restrict__ sp, ScPartial *__restrict__ part, const float *__restrict__ kw) {
+  if (ctl->done) return;
+  __shared__ double s_hot[kHot];
+  extern __shared__ double s_dyn[];       // per-warp staging: w[kSweepStage], b0[kSweepStage], deg[kSweepStage]
+  for (int t = threadIdx.x; t < kHot; t += blockDim.x) s_hot[t] = 0.0;
+  __shared__ unsigned s_dead;
+  if (threadIdx.x == 0) s_dead = 0u;
+  __syncthreads();
+  constexpr int kW = kScatterThreads / 32;
+  const int warp = threadIdx.x >> 5;
+  SweepStage st;
+  st.w = s_dyn + warp * kSweepStage;
+  st.b0 = reinterpret_cast<long long *>(s_dyn + kW * kSweepStage) + warp * kSweepStage;
+  st.deg = reinterpret_cast<int *>(s_dyn + 2 * kW * kSweepStage) + warp * kSweepStage;
+  st.cnt = 0;
+  const Sink s{F, s_hot, g.hot_lo, g.lo, g.n, nullptr, nullptr};
+  Stage sg{nullptr, nullptr, 0};
+  const double T = ctl->T;
+  const unsigned lane = lane_id();
+  ScAcc acc;
+  int sel_all = 0, dang_cnt = 0;
+  double dloss = 0.0;
+  const long long spans = (g.n + kSweepSpan - 1) / kSweepSpan;
+  const int gw = blockIdx.x * kW + warp;
+  const int ns = fr.stripes;
+  const int run = fr.run;
+  for (int k = 0; k < ns; ++k) {
+    const int sq = (gw + k) % ns;
+    const long long s0 = spans * sq / ns, s1 = spans * (sq + 1) / ns;
+    for (;;) {
+      unsigned q0 = (unsigned)(s1 - s0);
+      if (lane == 0 && !((*(volatile unsigned *)&s_dead >> sq) & 1u)) q0 = atomicAdd(&ctl->tickets[32 * sq], (unsigned)run);
+      q0 = __shfl_sync(0xffffffffu, q0, 0);
+      if ((long long)q0 >= s1 - s0) {
+        if (lane == 0) atomicOr(&s_dead, 1u << sq);
+        break;
+      }
+      const long long q1 = min(s1, s0 + (long long)q0 + run);
+      for (long long q = s0 + q0; q < q1; ++q) {
+        if (KEY) sweep_span<SIGNED, true>(g, s, F, H, fr, ctl, kw, T, q * kSweepSpan, acc, sel_all, dloss, dang_cnt, st);
+        else sweep_span<SIGNED, false>(g, s, F, H, fr, ctl, kw, T, q * kSweepSpan, acc, sel_all, dloss, dang_cnt, st);
+        sweep_flush<SIGNED>(g, s, ctl, st, sg, false);
+      }
+    }
+  }
+  sweep_flush<SIGNED>(g, s, ctl, st, sg, true);
+  __syncthreads();
+  for (int t = threadIdx.x; t < kHot; t += blockDim.x) {
+    const double v = s_hot[t];
+    if (v != 0.0) red_add(F + (g.hot_lo - g.lo) + t, v);
+  }
+  // partials in the select / scatter layouts, so k_finalize runs unchanged
+  acc.loss = warp_sum(acc.loss);
+  acc.edges = warp_sum(acc.edges);
+  acc.lo = warp_sum(acc.lo);
+  acc.mi = warp_sum(acc.mi);
+  acc.hu = warp_sum(acc.hu);
+  dloss = warp_sum(dloss);
+  dang_cnt = warp_sum(dang_cnt);
+  __shared__ ScAcc s_acc[kW];
+  __shared__ double s_dl[kW];
+  __shared__ int s_sel[kW], s_dc[kW];
+  if (lane == 0) {
+    s_acc[warp] = acc; s_dl[warp] = dloss;
+    s_sel[warp] = sel_all; s_dc[warp] = dang_cnt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ScPartial p{0.0, 0, 0, 0, 0, 0, 0.0};
+    SelPartial q{0.0, 0, 0.0, 0};
+    for (int k = 0; k < kW; ++k) {
+      p.loss += s_acc[k].loss; p.edges += s_acc[k].edges;
+      p.n_low += s_acc[k].lo; p.n_mid += s_acc[k].mi; p.n_hub += s_acc[k].hu;
+      q.cnt += s_sel[k]; q.loss += s_dl[k]; q.dang += s_dc[k];
+    }
+    part[blockIdx.x] = p;
+    sp[blockIdx.x] = q;
+  }
+}
+constexpr size_t kSweepDynSmem = (size_t)(kScatterThreads / 32) * kSweepStage * (sizeof(double) + sizeof(long long) + sizeof(int));
+
 // ------------------------------------------------------- K4b far-push apply --
 // Opened chunks of every bin, bins in ascending order (prefix of the chunk
 // counters); CTAs take two chunks at a time round-robin, so the grid works on one
@@ -691,10 +916,13 @@ __device__ __forceinline__ void reduce_partials(const SelPartial *__restrict__ s
 //   r_{p+1} <= r_p - sum (1 - c_i)|s_i|   (App. A.2; equality up to rounding for
 //   PageRank), so the run can stop after a pass without re-reading F.
 __device__ __forceinline__ void apply_pass(Ctl *ctl, const double *sums, di_pass_log *log) {
-  const double r = sums[0], loss = sums[1];
+  double r = sums[0];
+  const double loss = sums[1];
   const long long cnt = (long long)sums[2], edges = (long long)sums[3];
   const long long p = ctl->pass;
   const double T = ctl->T;
+  // async sweep: |F|_1 is not re-measured; the carried bound is the pass's r_p
+  if (ctl->sweep) r = ctl->r_pred;
   if (p < ctl->log_cap) {
     di_pass_log L;
     L.pass = p; L.T = T; L.r = r; L.frontier = cnt; L.edges = edges; L.dangling = (long long)sums[4];

@@ -67,6 +67,7 @@ struct Ctl {
   int defer_m;         // passes between flushes (0 = deferral off)
   int stop_after_flush;   // the bound met the target with mass pending: stop once it is delivered
   long long flushes;   // flushes executed since create
+  int sweep;           // one-kernel async sweeps (options.sweep): r_p is the carried bound r_pred
   // scatter tickets: one counter per stripe of the frontier groups, each on its
   // own 128-byte line (reset per pass)
   alignas(128) unsigned tickets[kStripes * 32];

@@ -1,0 +1,81 @@
+"""One-kernel asynchronous sweeps (options.sweep = 1) against the CPU oracle.
+
+A sweep takes and diffuses every node above T_p at once (the paper's cyclic scan
+with immediate diffusion), so the pass log is not the
+snapshot oracle's; the limit is the same X.  Bars: H within 1e-8 |B|_1
+of the oracle's X, the identity F = B - (I-P)H on every row (App. A.1), |F|_1
+below the target; on every config kind (web-like with and without the key, R-MAT
+with hub columns, signed P, uniform).
+"""
+import numpy as np
+import pytest
+
+import diter_inputs as gen
+import paper_1202_6168_b200 as di
+
+from test_gpu_parity import TOL, _check_state, _gpu, _xref
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("key", [0, 1, 2])
+@pytest.mark.parametrize("policy", [di.DI_POLICY_GEOM, di.DI_POLICY_HYBRID])
+def test_sweep_web(key, policy):
+    n = 150_001
+    cp, ri = gen.web_graph(n, 2, gen.XMIN_C4)
+    X, P, bn = _xref(n, cp, ri)
+    target = 1e-9 * bn
+    H, F, log, r, st = _gpu(n, cp, ri, target, sweep=1, select_key=key, policy=policy, alpha=2.0,
+                            hybrid_frac=0.5)
+    assert np.abs(H - X).sum() <= TOL * bn
+    _check_state(n, cp, ri, None, None, 0.85, H, F, r, target)
+    assert st["edges"] == log["edges"].sum() and st["passes"] == len(log)
+
+
+def test_sweep_rmat_hubs():
+    """R-MAT scale 16 (columns > 8192 edges go through the hub kernel after the sweep)."""
+    src, dst = gen.rmat_coo(16, 1)
+    n = 1 << 16
+    cp, ri = di.di_csc_from_coo(n, src, dst)
+    X, P, bn = _xref(n, cp, ri)
+    target = 1e-9 * bn
+    H, F, log, r, st = _gpu(n, cp, ri, target, sweep=1, select_key=1)
+    assert np.abs(H - X).sum() <= TOL * bn
+    _check_state(n, cp, ri, None, None, 0.85, H, F, r, target)
+
+
+def test_sweep_signed_and_small():
+    n = 30_000
+    cp, ri, v, b = gen.signed_system(n, 2)
+    X, P, bn = _xref(n, cp, ri, v, b, 0.9)
+    target = 5e-10 * bn
+    H, F, log, r, st = _gpu(n, cp, ri, target, vals=v, b=b, d=0.9, sweep=1)
+    assert np.abs(H - X).sum() <= TOL * bn
+    _check_state(n, cp, ri, v, b, 0.9, H, F, r, target)
+    for n in (1, 33, 257, 1000):
+        cp, ri = gen.uniform_graph(max(n, 2), 3)
+        n = max(n, 2)
+        X, P, bn = _xref(n, cp, ri)
+        H, F, log, r, st = _gpu(n, cp, ri, 1e-12, sweep=1)
+        assert np.abs(H - X).sum() <= TOL * bn
+        _check_state(n, cp, ri, None, None, 0.85, H, F, r, 1e-12)
+
+
+def test_sweep_resume_reset_state():
+    n = 60_000
+    cp, ri = gen.web_graph(n, 4, gen.XMIN_C4)
+    X, P, bn = _xref(n, cp, ri)
+    target = 1e-9 * bn
+    ctx = di.di_create(n, cp, ri, None, None, 0.85, di.default_options(sweep=1, select_key=1))
+    di.di_run(ctx, 1e-6)
+    _check_state(n, cp, ri, None, None, 0.85, di.di_get_history(ctx), di.di_get_fluid(ctx),
+                 di.di_get_residual(ctx), 1e-6)
+    di.di_run(ctx, target)
+    H1 = di.di_get_history(ctx)
+    di.di_reset(ctx)
+    di.di_run(ctx, target)
+    H2, F2, r2 = di.di_get_history(ctx), di.di_get_fluid(ctx), di.di_get_residual(ctx)
+    di.di_destroy(ctx)
+    for H in (H1, H2):
+        assert np.abs(H - X).sum() <= TOL * bn
+    _check_state(n, cp, ri, None, None, 0.85, H2, F2, r2, target)
