@@ -56,16 +56,28 @@ L2_BYTES = 126 * 2 ** 20
 SCHEDULES = {
     "C1": (1, 1.5, 0.05, 0),
     "C2": (1, 2.0, 0.30, 1),
-    "C3": (1, 1.5, 0.05, 1),
-    "C4": (1, 2.0, 0.50, 1),
+    "C3": (1, 1.5, 0.50, 1),
+    "C4": (1, 2.0, 0.60, 1),
     "C5": (1, 2.0, 0.15, 0),
 }
 
+# options.sweep of the launch configuration: 1 = one-kernel asynchronous sweeps (the
+# paper's cyclic scan with immediate diffusion, reading R26) on the large graphs --
+# C4 248.7 -> 193 ms, C3 181 -> 138 ms; the small L2-resident ones keep snapshot
+# passes (C2 3.7 vs 5.5 ms, C5 2.7 vs 3.8 ms).
+SWEEP = {"C3": 1, "C4": 1}
 
-# Frontier groups per dynamic grab of the scatter (options.scatter_run; library default
-# 2): longer runs keep C4's +-1000-local pushes in L2 (248.7 vs 250.1 ms), single groups
-# balance C3's permuted R-MAT better (181.3 vs 183.3 ms); GPU-side only.
+# The snapshot-pass configuration of the sweep configs (select, then scatter; the
+# schedule the bit-exact frontier tests pin), reported beside the headline as
+# `snapshot`.
+SNAPSHOT_SCHEDULES = {"C3": (1, 1.5, 0.05, 1), "C4": (1, 2.0, 0.50, 1)}
+
+# Frontier groups (snapshot) / node spans (sweep) per dynamic grab (options.scatter_run;
+# library default 2): snapshot C4 3 (248.7 vs 250.1 ms), C3 1 (181.3 vs 183.3 ms).
 SCATTER_RUN = {"C3": 1, "C4": 3}
+SNAPSHOT_SCATTER_RUN = {"C3": 1, "C4": 3}
+# Ticket stripes (options.scatter_stripes; default 8): C4 sweeps 4 (193.1 vs 193.8 ms).
+SCATTER_STRIPES = {"C4": 4}
 
 # The raw key |F_i| > T_p (north_star's literal selection) on C4, reported beside the
 # headline as `raw_key`: HYBRID alpha = 2, f = 0.15 (its best schedule).
@@ -98,6 +110,10 @@ def parse():
     ap.add_argument("--pass-csv", default=None, help="write the last solve's per-pass log here")
     ap.add_argument("--dist-path", action="store_true",
                     help="tests: run the N > 1 code path (di_create_dist over NCCL) even with one rank")
+    ap.add_argument("--sweep", type=int, default=None, choices=[0, 1],
+                    help="options.sweep: 1 one-kernel async sweeps, 0 snapshot passes; default: SWEEP[config]")
+    ap.add_argument("--no-snapshot", action="store_true",
+                    help="skip the extra snapshot-pass solve reported as `snapshot` (sweep configs)")
     ap.add_argument("--far-defer", type=int, default=0,
                     help="options.far_defer (one GPU): 0 auto, -1 off, > 0 passes between far-edge flushes")
     ap.add_argument("--l2-persist", type=int, default=0,
@@ -164,6 +180,9 @@ def bench_config(args, p, pol, world, resident, flushed):
             "alpha": args.alpha, "hybrid_frac": args.hybrid_frac,
             "select_key": ["raw", "per-edge", "paper"][args.key],
             "scatter_run": SCATTER_RUN.get(args.config, 2),
+            "scatter_stripes": SCATTER_STRIPES.get(args.config, 8),
+            "passes": ("one-kernel asynchronous sweeps (options.sweep = 1, reading R26)" if args.sweep and world == 1
+                       else "snapshot passes (select, then scatter)"),
             "parallelism": par,
             "l2": ("flushed between steps (252 MB write)" if flushed else
                    f"inputs ({resident / 1e9:.1f} GB resident per GPU) larger than L2 (126 MB)")}
@@ -172,6 +191,8 @@ def bench_config(args, p, pol, world, resident, flushed):
 def policy_of(args):
     """Fill args.alpha / hybrid_frac / key from SCHEDULES where not given; return the policy."""
     pol, alpha, frac, key = SCHEDULES[args.config]
+    if args.sweep is None:
+        args.sweep = SWEEP.get(args.config, 0)
     if args.alpha is None:
         args.alpha = alpha
     if args.hybrid_frac is None:
@@ -311,17 +332,19 @@ def host_cpu():
     return f"{model}, nproc {os.cpu_count()}"
 
 
-def ncu_traffic(config):
-    """(DRAM bytes read + written per k_scatter launch, source): the mean over every
+def ncu_traffic(config, kernel="k_scatter"):
+    """(DRAM bytes read + written per launch of `kernel`, source): the mean over every
     launch of one solve of this config, measured by ncu (scripts/ncu_traffic.py ->
     profiles/ncu_traffic.json; cold-cache serialised replays).  (None, why) if the
-    config has no capture."""
+    config has no capture of that kernel."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)[config]
+        if d.get("kernel", "k_scatter") != kernel:
+            return None, f"no ncu capture of {kernel} on this config"
         return float(d["mean_dram_bytes_per_launch"]), (
-            f"ncu dram__bytes_read.sum + dram__bytes_write.sum, mean over the {d['launches']} k_scatter "
+            f"ncu dram__bytes_read.sum + dram__bytes_write.sum, mean over the {d['launches']} {kernel} "
             f"launches of one {config} solve (profiles/ncu_traffic.json; cold-cache replays)")
     except Exception:
         return None, "no ncu capture of this config"
@@ -396,7 +419,8 @@ def run_ours(args, rank, world, local_rank):
     opts = di.default_options(policy=pol, device=local_rank, profile=0, exchange_mode=mode,
                               alpha=args.alpha, hybrid_frac=args.hybrid_frac, select_key=args.key,
                               scatter_run=SCATTER_RUN.get(args.config, 0), l2_persist=args.l2_persist,
-                              far_defer=args.far_defer, **dist_kw)
+                              far_defer=args.far_defer, sweep=args.sweep if not dist else 0,
+                              scatter_stripes=SCATTER_STRIPES.get(args.config, 0), **dist_kw)
     comm_id, bounds, shard = None, None, None
     if dist:
         bounds = dd.partition_bounds(p.col_ptr, world, cost=args.partition, row_idx=p.row_idx)
@@ -447,7 +471,7 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         torch.distributed.barrier()
     prof = {k: 0 for k in ("run_ms", "kt_scatter_ms", "kt_select_ms", "kt_finalize_ms", "scatter_bytes",
-                           "passes", "edges")}
+                           "passes", "edges", "alg_bytes", "nodes", "dangling")}
     for _ in range(args.steps):
         s = step()
         for k in prof:
@@ -477,24 +501,39 @@ def run_ours(args, rank, world, local_rank):
     run_s = tot["run_ms"] / 1e3
     value = edges_all / run_s
     peak, peak_kind = measured_peaks()
-    scat_gbs = prof["scatter_bytes"] / (prof["kt_scatter_ms"] / 1e3) / 1e9
-    n_launch = prof["passes"]                      # executed k_scatter launches
-    traffic, traffic_src = ncu_traffic(args.config)
+    sweep = bool(args.sweep) and not dist
+    # Dominant kernel: k_scatter (snapshot passes: algorithmic bytes 20 E + 16 per
+    # non-dangling diffused node, di_stats.scatter_bytes) or k_sweep (async sweeps: the
+    # whole pass, SURVEY §8d's B_p = 8 N + 40 |S_p| + 20 E_p, di_stats.alg_bytes);
+    # the "scatter" span of the profile events covers it (+ k_scatter_hubs if any).
+    kbytes = prof["alg_bytes"] if sweep else prof["scatter_bytes"]
+    kname = "k_sweep" if sweep else "k_scatter"
+    scat_gbs = kbytes / (prof["kt_scatter_ms"] / 1e3) / 1e9
+    n_launch = prof["passes"]                      # executed k_scatter / k_sweep launches
+    traffic, traffic_src = ncu_traffic(args.config, kname)
     kt_sum = prof["kt_scatter_ms"] + prof["kt_select_ms"] + prof["kt_finalize_ms"]
+    shares = ({"k_sweep": prof["kt_scatter_ms"] / kt_sum, "k_finalize": (prof["kt_finalize_ms"] + prof["kt_select_ms"]) / kt_sum}
+              if sweep else
+              {"k_select": prof["kt_select_ms"] / kt_sum, "k_scatter": prof["kt_scatter_ms"] / kt_sum,
+               "k_finalize": prof["kt_finalize_ms"] / kt_sum})
     roofline = {"bound": "hbm", "achieved": scat_gbs, "peak": peak, "unit": "GB/s",
                 "frac": scat_gbs / peak, "frac_of_nominal_8TBps": scat_gbs / 8000.0, "traffic": traffic,
                 "traffic_source": traffic_src,
-                "kernel": "k_scatter", "peak_kind": peak_kind,
-                "bytes_per_launch": prof["scatter_bytes"] / max(1, n_launch),
+                "kernel": kname, "peak_kind": peak_kind,
+                "bytes_per_launch": kbytes / max(1, n_launch),
+                "bytes_model": ("8 N + 40 |S_p| + 20 E_p per sweep (SURVEY §8d B_p; F scan, diffused node, edge)"
+                                if sweep else "20 E_p + 16 (|S_p| - dangling) per scatter (row idx + F RMW, col_ptr pair)"),
                 "avg_launch_ms": prof["kt_scatter_ms"] / max(1, n_launch),
                 "share_of_step": prof["kt_scatter_ms"] / max(1e-9, run_ms_rank),
-                "kernel_shares": {"k_select": prof["kt_select_ms"] / kt_sum,
-                                  "k_scatter": prof["kt_scatter_ms"] / kt_sum,
-                                  "k_finalize": prof["kt_finalize_ms"] / kt_sum},
+                "kernel_shares": shares,
                 "timing": f"CUDA events between the pass kernels on the library stream over {args.steps} "
                           f"more steps right after the timed region (rank {rank}); their ms_per_step "
                           f"{prof['run_ms'] / args.steps:.3f} includes the events' own cost",
                 "path_alg_GBps": tot["alg_bytes"] / (run_ms_rank / 1e3) / 1e9}
+    # ---- the snapshot-pass configuration on the same graph (extra key, sweep configs)
+    snapshot = None
+    if sweep and not args.no_snapshot and args.config in SNAPSHOT_SCHEDULES:
+        snapshot = run_snapshot(args, p, opts, di)
     # ---- the raw key on the same graph (extra key; the headline keeps the per-edge key)
     raw = None
     if not dist and args.config == "C4" and args.key != 0 and not args.no_raw_key:
@@ -540,7 +579,7 @@ def run_ours(args, rank, world, local_rank):
            "time_to_target_ms": tot["run_ms"] / args.steps,
            "passes_per_solve": tot["passes"] / args.steps,
            "normalized_iterations": edges_all / args.steps / p.nnz,
-           "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "raw_key": raw,
+           "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "raw_key": raw, "snapshot": snapshot,
            # our kernels in the timed steps: di_run's (graph nodes counted) + di_reset's k_init_state
            "gpu_launches": int(tot["run_kernel_launches"]) + args.steps,
            "clocks": clocks,
@@ -556,6 +595,35 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
+
+
+def run_snapshot(args, p, opts, di):
+    """The sweep config in snapshot passes (select, then scatter): its own context and
+    schedule (SNAPSHOT_SCHEDULES), 1 warm-up + min(steps, 3) timed solves, same timing."""
+    import copy
+    pol, alpha, frac, key = SNAPSHOT_SCHEDULES[args.config]
+    o = copy.copy(opts)
+    o.policy, o.alpha, o.hybrid_frac, o.select_key, o.profile, o.sweep = pol, alpha, frac, key, 0, 0
+    o.scatter_run, o.scatter_stripes = SNAPSHOT_SCATTER_RUN.get(args.config, 0), 0
+    ctx = di.di_create(p.n, p.col_ptr, p.row_idx, p.values, p.b, p.d, o)
+    try:
+        di.di_reset(ctx)
+        di.di_run(ctx, p.stop)
+        steps = max(1, min(args.steps, 3))
+        ms = edges = passes = sb = 0
+        for _ in range(steps):
+            di.di_reset(ctx)
+            di.di_run(ctx, p.stop)
+            st = di.di_get_stats(ctx)
+            ms += st["run_ms"]
+            edges += st["edges"]
+            passes += st["passes"]
+    finally:
+        di.di_destroy(ctx)
+    return {"passes": "snapshot (select, then scatter)", "policy": "hybrid", "alpha": alpha,
+            "hybrid_frac": frac, "select_key": ["raw", "per-edge", "paper"][key], "steps": steps,
+            "time_to_target_ms": ms / steps, "edges_per_s": edges / (ms / 1e3),
+            "passes_per_solve": passes / steps, "normalized_iterations": edges / steps / p.nnz}
 
 
 def run_raw_key(args, p, opts, di, torch):

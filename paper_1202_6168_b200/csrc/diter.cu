@@ -484,6 +484,11 @@ di_status diter_capture_graph(di_ctx *ctx) {
       if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 2], ctx->stream, cudaEventRecordExternal));
       k_finalize<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->ctl, ctx->sel_part, ctx->grid_sweep, ctx->sc_part,
                                                           ctx->grid_sweep, ctx->log);
+      if (ctx->vals) {    // signed P: exact |F|_1 after each sweep (the carried bound is loose)
+        k_l1_partial<<<ctx->grid_l1, kSelectThreads, 0, ctx->stream>>>(ctx->F, ctx->n_local, ctx->l1_part);
+        k_l1_final<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->l1_part, ctx->grid_l1, ctx->l1_out);
+        k_sweep_check<<<1, 1, 0, ctx->stream>>>(ctx->ctl, ctx->l1_out);
+      }
       if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 3], ctx->stream, cudaEventRecordExternal));
       continue;
     }
@@ -828,7 +833,7 @@ extern "C" di_status di_run(di_ctx *ctx, double target) {
       const long long pass_before = h->pass;
       CK(cudaGraphLaunch(ctx->graph_exec, ctx->stream));
       ctx->graph_launches += 1;
-      ctx->kernel_launches += (ctx->sweep_on ? 2LL + (ctx->cap_hub > 0)
+      ctx->kernel_launches += (ctx->sweep_on ? 2LL + (ctx->cap_hub > 0) + (ctx->vals ? 3 : 0)
                                              : 3LL + (ctx->cap_hub > 0) + (ctx->far.on ? 1 : 0) + (ctx->defer_m ? 2 : 0)) *
                               ctx->check_interval;
       TRY(read_ctl(ctx));

@@ -836,6 +836,16 @@ k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ct
     sp[blockIdx.x] = q;
   }
 }
+// Signed P under sweeps: the carried bound r - sum (1 - d)|s_i| ignores the
+// cancellation of signed pushes and can stay far above |F|_1, so after every sweep
+// the exact |F|_1 (k_l1_partial / k_l1_final into *l1) replaces it when smaller
+// and decides the stop.
+__global__ void k_sweep_check(Ctl *ctl, const double *l1) {
+  if (ctl->done) return;
+  const double r = *l1;
+  if (r < ctl->r_pred) ctl->r_pred = r;
+  if (r < ctl->target && ctl->pending == 0.0) ctl->done = 1;
+}
 constexpr size_t kSweepDynSmem = (size_t)(kScatterThreads / 32) * kSweepStage * (sizeof(double) + sizeof(long long) + sizeof(int));
 
 // ------------------------------------------------------- K4b far-push apply --

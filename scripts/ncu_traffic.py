@@ -24,6 +24,8 @@ ap.add_argument("--config", default="C4")
 ap.add_argument("--launches", required=True)
 ap.add_argument("--passes", required=True)
 ap.add_argument("--signed", action="store_true")
+ap.add_argument("--kernel", default="k_scatter", choices=["k_scatter", "k_sweep"])
+ap.add_argument("--n", type=int, default=None, help="nodes (k_sweep: 8 N scan bytes per launch)")
 ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "ncu_traffic.json"))
 ap.add_argument("--source", default="")
 a = ap.parse_args()
@@ -34,7 +36,7 @@ order = []
 with open(a.launches) as f:
     lines = [ln for ln in f if ln.startswith('"')]
 for r in csv.DictReader(lines):
-    if "k_scatter" not in r["Kernel Name"] or "hubs" in r["Kernel Name"]:
+    if a.kernel not in r["Kernel Name"] or "hubs" in r["Kernel Name"]:
         continue
     k = r["ID"]
     if k not in launches:
@@ -51,12 +53,13 @@ with open(a.passes) as f:
 n = len(passes)
 rows = [launches[k] for k in order[:n]]
 if len(rows) < n:
-    raise SystemExit(f"{len(rows)} k_scatter launches in the CSV, {n} passes in the log")
+    raise SystemExit(f"{len(rows)} {a.kernel} launches in the CSV, {n} passes in the log")
 per_edge = 28 if a.signed else 20
 dram, alg, dur = [], [], []
 for p, r in zip(passes, rows):
     E, S, D = int(p["edges"]), int(p["frontier"]), int(p["dangling"])
-    alg.append(per_edge * E + 16 * (S - D))
+    # k_sweep: the whole pass, SURVEY §8d B_p = 8 N + 40 |S_p| + 20 E_p (+ 8 E_p signed)
+    alg.append(8 * a.n + 40 * S + per_edge * E if a.kernel == "k_sweep" else per_edge * E + 16 * (S - D))
     dram.append(r["dram__bytes_read.sum"] + r["dram__bytes_write.sum"])
     dur.append(r.get("gpu__time_duration.sum", 0.0))
 out = {}
@@ -64,7 +67,8 @@ if os.path.exists(a.out):
     with open(a.out) as f:
         out = json.load(f)
 out[a.config] = {
-    "_source": a.source or f"ncu metrics of every k_scatter launch of one {a.config} solve "
+    "kernel": a.kernel,
+    "_source": a.source or f"ncu metrics of every {a.kernel} launch of one {a.config} solve "
                             "(scripts/profile_run.py, bench launch configuration), cold-cache replays",
     "launches": n,
     "mean_dram_bytes_per_launch": sum(dram) / n,

@@ -34,11 +34,14 @@ pytestmark = pytest.mark.gpu
 import bench                 # bench.SCHEDULES: the launch configuration bench.py times
 
 
-def _bench_opts(cfg):
+def _bench_opts(cfg, **over):
     # bench.py's launch configuration (profile=1: per-kernel CUDA events in the graph)
     pol, alpha, frac, key = bench.SCHEDULES[cfg]
-    return di.default_options(policy=pol, profile=1, alpha=alpha, hybrid_frac=frac, select_key=key,
-                              scatter_run=bench.SCATTER_RUN.get(cfg, 0))
+    kw = dict(policy=pol, profile=1, alpha=alpha, hybrid_frac=frac, select_key=key,
+              scatter_run=bench.SCATTER_RUN.get(cfg, 0), sweep=bench.SWEEP.get(cfg, 0),
+              scatter_stripes=bench.SCATTER_STRIPES.get(cfg, 0))
+    kw.update(over)
+    return di.default_options(**kw)
 
 
 class _OracleRun(threading.Thread):
@@ -118,8 +121,14 @@ def _full_scale_case(p, cfg, n_oracle_passes, xref=True):
         # H <= X componentwise up to rounding (non-negative case) and the bound
         assert np.all(H <= X * (1 + 1e-12) + 1e-300)
         assert err <= r / (1 - p.d) + 1e-11 * bn
-    # first passes against the oracle's log (tie-aware, reading R8)
+    # first passes against the oracle's log (tie-aware, reading R8): snapshot passes of
+    # the same schedule (bench's asynchronous sweeps have no snapshot log, reading R26)
     k = n_oracle_passes
+    if bench.SWEEP.get(cfg, 0):
+        ctx = di.di_create(n, cp, ri, None, None, p.d, _bench_opts(cfg, sweep=0, max_passes=k))
+        assert di.di_run(ctx, p.stop, raise_on_not_converged=False) == di.DI_ERR_NOT_CONVERGED
+        log = di.di_get_pass_log(ctx)
+        di.di_destroy(ctx)
     first_tie = next((q for q in range(k) if orc.near[q] > 0), k)
     o = np.array([l[3] for l in orc.st.log[:k]])
     np.testing.assert_array_equal(log["frontier"][:first_tie], o[:first_tie])
@@ -128,7 +137,8 @@ def _full_scale_case(p, cfg, n_oracle_passes, xref=True):
 
 
 def test_c4_full_scale_parity():
-    """configs[3]: N=1e8 web-like PageRank, bench's schedule (HYBRID, per-edge key)."""
+    """configs[3]: N=1e8 web-like PageRank, bench's launch configuration (asynchronous
+    sweeps, HYBRID, per-edge key)."""
     p = gen.config("C4", 1)
     _full_scale_case(p, "C4", 3)
 
