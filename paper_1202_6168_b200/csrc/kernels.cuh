@@ -630,7 +630,13 @@ k_scatter_hubs(Graph g, double *__restrict__ F, Frontier fr, const Ctl *ctl) {
 // under the latency-bound pushes.  |F|_1 is not re-measured per sweep: it drops by
 // exactly sum (1 - c_i)|s_i| (App. A.2; an upper bound for signed P), so k_finalize
 // advances the bound r_pred and di_run confirms convergence with an exact |F|_1.
-constexpr int kSweepItems = 8;
+#ifndef DITER_SWEEP_ITEMS
+#define DITER_SWEEP_ITEMS 8
+#endif
+#ifndef DITER_SWEEP_TAKE_RED
+#define DITER_SWEEP_TAKE_RED 0
+#endif
+constexpr int kSweepItems = DITER_SWEEP_ITEMS;
 constexpr int kSweepSpan = 32 * kSweepItems;
 constexpr int kSweepStage = 32 + kSweepSpan;     // per-warp staging: a partial group + one span
 
@@ -700,8 +706,14 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
     const double af = fabs(f[k]);
     const bool sel = (KEY ? af * (double)w[k] : af) > T;     // strict ">" (R7)
     msel[k] = __ballot_sync(0xffffffffu, sel);
+#if DITER_SWEEP_TAKE_RED
+    // take by a fire-and-forget RED of -s_i: F_i = (s_i + pushes since the load) - s_i,
+    // so fluid pushed after the load stays (exact up to the RED's rounding)
+    if (sel) red_add(F + i, -f[k]);
+#else
     if (sel)                                                 // s_i
       f[k] = __longlong_as_double((long long)atomicExch(reinterpret_cast<unsigned long long *>(F + i), 0ull));
+#endif
   }
 #pragma unroll
   for (int k = 0; k < kSweepItems; ++k) {

@@ -118,8 +118,13 @@ def _full_scale_case(p, cfg, n_oracle_passes, xref=True):
         print(f"{cfg}: ||H - X_ref||_1 / |B|_1 = {err / bn:.3e} (r/(1-d)/|B| = {r / (1 - p.d) / bn:.3e}); "
               f"identity {ident:.2e}; oracle {orc.st.passes} passes, {orc.st.edges} edges, {orc.secs:.0f} s")
         assert err <= 1e-8 * bn, err / bn
-        # H <= X componentwise up to rounding (non-negative case) and the bound
-        assert np.all(H <= X * (1 + 1e-12) + 1e-300)
+        # H <= X componentwise (non-negative case): X_ref itself lies below X by
+        # (I-P)^-1 F_ref >= 0 with |X - X_ref|_1 <= r_ref / (1-d), so the part of H above
+        # X_ref must fit in that (an asynchronous sweep may reach a row further than the
+        # oracle's snapshot run did) -- plus rounding
+        excess = float(np.maximum(H - X, 0.0).sum())
+        print(f"{cfg}: sum max(H - X_ref, 0) = {excess / bn:.3e} |B|_1 (r_ref/(1-d) = {orc.r_ref / (1 - p.d) / bn:.3e})")
+        assert excess <= orc.r_ref / (1 - p.d) + 1e-13 * bn
         assert err <= r / (1 - p.d) + 1e-11 * bn
     # first passes against the oracle's log (tie-aware, reading R8): snapshot passes of
     # the same schedule (bench's asynchronous sweeps have no snapshot log, reading R26)
