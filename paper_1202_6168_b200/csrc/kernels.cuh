@@ -631,7 +631,10 @@ k_scatter_hubs(Graph g, double *__restrict__ F, Frontier fr, const Ctl *ctl) {
 // exactly sum (1 - c_i)|s_i| (App. A.2; an upper bound for signed P), so k_finalize
 // advances the bound r_pred and di_run confirms convergence with an exact |F|_1.
 #ifndef DITER_SWEEP_ITEMS
-#define DITER_SWEEP_ITEMS 8
+#define DITER_SWEEP_ITEMS 4        // 128-node spans: C4 193.1 -> 188.1 ms vs 8, C3 138.6 -> 135.4 (16: spills)
+#endif
+#ifndef DITER_SWEEP_MIN_BLOCKS
+#define DITER_SWEEP_MIN_BLOCKS kScatterMinBlocks
 #endif
 #ifndef DITER_SWEEP_TAKE_RED
 #define DITER_SWEEP_TAKE_RED 0
@@ -767,7 +770,7 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
 }
 
 template <bool SIGNED, bool KEY>
-__global__ void __launch_bounds__(kScatterThreads, kScatterMinBlocks)
+__global__ void __launch_bounds__(kScatterThreads, DITER_SWEEP_MIN_BLOCKS)
 k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ctl *ctl,
         SelPartial *__restrict__ sp, ScPartial *__restrict__ part, const float *__restrict__ kw) {
   if (ctl->done) return;
