@@ -73,8 +73,9 @@ SWEEP = {"C3": 1, "C4": 1}
 SNAPSHOT_SCHEDULES = {"C3": (1, 1.5, 0.05, 1), "C4": (1, 2.0, 0.50, 1)}
 
 # Frontier groups (snapshot) / node spans (sweep) per dynamic grab (options.scatter_run;
-# library default 2): snapshot C4 3 (248.7 vs 250.1 ms), C3 1 (181.3 vs 183.3 ms).
-SCATTER_RUN = {"C3": 1, "C4": 3}
+# library default 2): snapshot C4 3 (248.7 vs 250.1 ms), C3 1 (181.3 vs 183.3 ms); sweeps
+# C4 6 (spans after the first of a grab are prefetched: 182.2 vs 185.1 ms at 3), C3 1.
+SCATTER_RUN = {"C3": 1, "C4": 6}
 SNAPSHOT_SCATTER_RUN = {"C3": 1, "C4": 3}
 # Ticket stripes (options.scatter_stripes; default 8): C4 sweeps 4 (193.1 vs 193.8 ms).
 SCATTER_STRIPES = {"C4": 4}

@@ -678,29 +678,91 @@ __device__ __forceinline__ void sweep_flush(const Graph &g, const Sink &s, Ctl *
   }
 }
 
-template <bool SIGNED, bool KEY>
+// Per-warp prefetch of the next span's scan inputs (F, key weights, col_ptr, dangling
+// words) into shared memory with cp.async (LDGSTS, no registers held), issued before the
+// current span's pushes so their latency hides the next scan's loads.  Lanes beyond n
+// get zero fill (src-size 0).
+// per-warp prefetch buffer in doubles: f[span], cp[span + 1], w[span] (fp32) + dw[items]
+constexpr int kSweepPfWords = 2 * kSweepSpan + 1 + (kSweepSpan + kSweepItems + 1) / 2;
+struct SweepPf {
+  double *f;          // [kSweepSpan]
+  long long *cp;      // [kSweepSpan + 1]
+  float *w;           // [kSweepSpan]
+  unsigned *dw;       // [kSweepItems]
+};
+
+__device__ __forceinline__ void cp_async(void *smem, const void *gmem, int bytes, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" :: "r"(sa), "l"(gmem), "r"(valid ? 8 : 0) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" :: "r"(sa), "l"(gmem), "r"(valid ? 4 : 0) : "memory");
+}
+
+template <bool KEY>
+__device__ __forceinline__ void sweep_prefetch(const Graph &g, const double *F, const float *kw, const Frontier &fr,
+                                               long long base, const SweepPf &pf) {
+  const unsigned lane = lane_id();
+  const long long n = g.n;
+#pragma unroll
+  for (int k = 0; k < kSweepItems; ++k) {
+    const long long i = base + 32 * k + lane;
+    const long long ic = i < n ? i : n - 1;
+    cp_async(pf.f + 32 * k + lane, F + ic, 8, i < n);
+    if (KEY) cp_async(pf.w + 32 * k + lane, kw + ic, 4, i < n);
+    cp_async(pf.cp + 32 * k + lane, g.col_ptr + (i < n ? i : n), 8, true);
+  }
+  if (lane == 0) {
+    const long long iend = base + kSweepSpan;
+    cp_async(pf.cp + kSweepSpan, g.col_ptr + (iend < n ? iend : n), 8, true);
+  }
+  const long long wi = (base >> 5) + lane;
+  if ((int)lane < kSweepItems) cp_async(pf.dw + lane, fr.dang_bits + ((wi << 5) < n ? wi : 0), 4, (wi << 5) < n);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+template <bool SIGNED, bool KEY, bool PF>
 __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double *__restrict__ F,
                                            double *__restrict__ H, const Frontier &fr, Ctl *ctl,
                                            const float *__restrict__ kw, double T, long long base,
                                            ScAcc &acc, int &sel_all, double &dloss, int &dang_cnt,
-                                           SweepStage &st) {
+                                           SweepStage &st, const SweepPf &pf, bool prefetch_next) {
   const unsigned lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
-  const long long n = g.n;
   double f[kSweepItems];
   float w[KEY ? kSweepItems : 1];
   long long cp[kSweepItems];
+  long long cp_end;
+  unsigned dword;
+  if (PF) {
+    // this span's inputs, prefetched into the warp's buffer
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
 #pragma unroll
-  for (int k = 0; k < kSweepItems; ++k) {
-    const long long i = base + 32 * k + lane;
-    f[k] = (i < n) ? F[i] : 0.0;
-    if (KEY) w[k] = (i < n) ? __ldcs(kw + i) : 0.0f;
-    cp[k] = __ldcs(g.col_ptr + (i < n ? i : n));
+    for (int k = 0; k < kSweepItems; ++k) {
+      f[k] = pf.f[32 * k + lane];
+      if (KEY) w[k] = pf.w[32 * k + lane];
+      cp[k] = pf.cp[32 * k + lane];
+    }
+    cp_end = pf.cp[kSweepSpan];
+    dword = (int)lane < kSweepItems ? pf.dw[lane] : 0u;
+    __syncwarp();
+    if (prefetch_next) sweep_prefetch<KEY>(g, F, kw, fr, base + kSweepSpan, pf);
+  } else {
+    // single-span claims (options.scatter_run = 1): direct loads
+    const long long n = g.n;
+#pragma unroll
+    for (int k = 0; k < kSweepItems; ++k) {
+      const long long i = base + 32 * k + lane;
+      f[k] = (i < n) ? F[i] : 0.0;
+      if (KEY) w[k] = (i < n) ? __ldcs(kw + i) : 0.0f;
+      cp[k] = __ldcs(g.col_ptr + (i < n ? i : n));
+    }
+    const long long iend = base + kSweepSpan;
+    cp_end = __ldcs(g.col_ptr + (iend < n ? iend : n));
+    const long long wi = (base >> 5) + lane;
+    dword = ((int)lane < kSweepItems && (wi << 5) < n) ? __ldg(fr.dang_bits + wi) : 0u;
   }
-  const long long iend = base + kSweepSpan;
-  const long long cp_end = __ldcs(g.col_ptr + (iend < n ? iend : n));
-  const long long wi = (base >> 5) + lane;
-  const unsigned dword = ((int)lane < kSweepItems && (wi << 5) < n) ? __ldg(fr.dang_bits + wi) : 0u;
   // take every selected node of the span (independent atomics, issued together)
   unsigned msel[kSweepItems];
 #pragma unroll
@@ -775,7 +837,7 @@ k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ct
         SelPartial *__restrict__ sp, ScPartial *__restrict__ part, const float *__restrict__ kw) {
   if (ctl->done) return;
   __shared__ double s_hot[kHot];
-  extern __shared__ double s_dyn[];       // per-warp staging: w[kSweepStage], b0[kSweepStage], deg[kSweepStage]
+  extern __shared__ double s_dyn[];       // per-warp staging (w, b0, deg) then per-warp prefetch buffers
   for (int t = threadIdx.x; t < kHot; t += blockDim.x) s_hot[t] = 0.0;
   __shared__ unsigned s_dead;
   if (threadIdx.x == 0) s_dead = 0u;
@@ -787,6 +849,10 @@ k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ct
   st.b0 = reinterpret_cast<long long *>(s_dyn + kW * kSweepStage) + warp * kSweepStage;
   st.deg = reinterpret_cast<int *>(s_dyn + 2 * kW * kSweepStage) + warp * kSweepStage;
   st.cnt = 0;
+  // prefetch buffers after the staging arrays (f, cp: 8-byte aligned at a double boundary)
+  double *pfb = s_dyn + 2 * kW * kSweepStage + (kW * kSweepStage + 1) / 2 + warp * kSweepPfWords;
+  SweepPf pf{pfb, reinterpret_cast<long long *>(pfb + kSweepSpan), reinterpret_cast<float *>(pfb + 2 * kSweepSpan + 1),
+             reinterpret_cast<unsigned *>(pfb + 2 * kSweepSpan + 1) + kSweepSpan};
   const Sink s{F, s_hot, g.hot_lo, g.lo, g.n, nullptr, nullptr};
   Stage sg{nullptr, nullptr, 0};
   const double T = ctl->T;
@@ -810,9 +876,16 @@ k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ct
         break;
       }
       const long long q1 = min(s1, s0 + (long long)q0 + run);
-      for (long long q = s0 + q0; q < q1; ++q) {
-        if (KEY) sweep_span<SIGNED, true>(g, s, F, H, fr, ctl, kw, T, q * kSweepSpan, acc, sel_all, dloss, dang_cnt, st);
-        else sweep_span<SIGNED, false>(g, s, F, H, fr, ctl, kw, T, q * kSweepSpan, acc, sel_all, dloss, dang_cnt, st);
+      if (run > 1) {
+        sweep_prefetch<KEY>(g, F, kw, fr, (s0 + q0) * kSweepSpan, pf);
+        for (long long q = s0 + q0; q < q1; ++q) {
+          sweep_span<SIGNED, KEY, true>(g, s, F, H, fr, ctl, kw, T, q * kSweepSpan, acc, sel_all, dloss, dang_cnt, st,
+                                        pf, q + 1 < q1);
+          sweep_flush<SIGNED>(g, s, ctl, st, sg, false);
+        }
+      } else {
+        sweep_span<SIGNED, KEY, false>(g, s, F, H, fr, ctl, kw, T, (s0 + q0) * kSweepSpan, acc, sel_all, dloss,
+                                       dang_cnt, st, pf, false);
         sweep_flush<SIGNED>(g, s, ctl, st, sg, false);
       }
     }
@@ -861,7 +934,9 @@ __global__ void k_sweep_check(Ctl *ctl, const double *l1) {
   if (r < ctl->r_pred) ctl->r_pred = r;
   if (r < ctl->target && ctl->pending == 0.0) ctl->done = 1;
 }
-constexpr size_t kSweepDynSmem = (size_t)(kScatterThreads / 32) * kSweepStage * (sizeof(double) + sizeof(long long) + sizeof(int));
+constexpr size_t kSweepDynSmem = sizeof(double) * ((size_t)2 * (kScatterThreads / 32) * kSweepStage +
+                                                   ((kScatterThreads / 32) * kSweepStage + 1) / 2 +
+                                                   (size_t)(kScatterThreads / 32) * kSweepPfWords);
 
 // ------------------------------------------------------- K4b far-push apply --
 // Opened chunks of every bin, bins in ascending order (prefix of the chunk
