@@ -182,7 +182,8 @@ def bench_config(args, p, pol, world, resident, flushed):
             "select_key": ["raw", "per-edge", "paper"][args.key],
             "scatter_run": SCATTER_RUN.get(args.config, 2),
             "scatter_stripes": SCATTER_STRIPES.get(args.config, 8),
-            "passes": ("one-kernel asynchronous sweeps (options.sweep = 1, reading R26)" if args.sweep and world == 1
+            "passes": ("one-kernel asynchronous sweeps (options.sweep = 1, reading R26)"
+                       if args.sweep and (world == 1 or args.exchange != "sync")
                        else "snapshot passes (select, then scatter)"),
             "parallelism": par,
             "l2": ("flushed between steps (252 MB write)" if flushed else
@@ -420,7 +421,7 @@ def run_ours(args, rank, world, local_rank):
     opts = di.default_options(policy=pol, device=local_rank, profile=0, exchange_mode=mode,
                               alpha=args.alpha, hybrid_frac=args.hybrid_frac, select_key=args.key,
                               scatter_run=SCATTER_RUN.get(args.config, 0), l2_persist=args.l2_persist,
-                              far_defer=args.far_defer, sweep=args.sweep if not dist else 0,
+                              far_defer=args.far_defer, sweep=args.sweep,
                               scatter_stripes=SCATTER_STRIPES.get(args.config, 0), **dist_kw)
     comm_id, bounds, shard = None, None, None
     if dist:
@@ -502,7 +503,7 @@ def run_ours(args, rank, world, local_rank):
     run_s = tot["run_ms"] / 1e3
     value = edges_all / run_s
     peak, peak_kind = measured_peaks()
-    sweep = bool(args.sweep) and not dist
+    sweep = bool(args.sweep) and (not dist or mode != di.DI_EXCHANGE_SYNC)
     # Dominant kernel: k_scatter (snapshot passes: algorithmic bytes 20 E + 16 per
     # non-dangling diffused node, di_stats.scatter_bytes) or k_sweep (async sweeps: the
     # whole pass, SURVEY §8d's B_p = 8 N + 40 |S_p| + 20 E_p, di_stats.alg_bytes);

@@ -129,3 +129,8 @@ di_status diter_dist_reset(di_ctx *ctx);
 di_status diter_setup_defer(di_ctx *ctx);
 void diter_defer_launch(di_ctx *ctx);
 di_status diter_defer_flush_now(di_ctx *ctx, int done);
+// per-CTA partial counts a pass's k_finalize reduces (the sweep grid when sweeps run)
+inline int diter_n_sel_part(const di_ctx *ctx) { return ctx->sweep_on ? ctx->grid_sweep : ctx->grid_select; }
+inline int diter_n_sc_part(const di_ctx *ctx) { return ctx->sweep_on ? ctx->grid_sweep : ctx->grid_scatter; }
+// one sweep of a distributed rank (dist.cu's non-graph pass path)
+void diter_launch_sweep(di_ctx *ctx);

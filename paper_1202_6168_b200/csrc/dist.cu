@@ -1118,6 +1118,13 @@ void dist_launch_pass_kernels(di_ctx *ctx, int slot) {
   Graph g = diter_graph(ctx);
   diter_dist_pass_prologue(ctx);
   prof_mark(ctx, slot, 0);
+  if (ctx->sweep_on) {            // ASYNC / P2P local passes as asynchronous sweeps (R26)
+    prof_mark(ctx, slot, 1);
+    diter_launch_sweep(ctx);
+    prof_mark(ctx, slot, 2);
+    ctx->kernel_launches += ctx->cap_hub > 0 ? 2 : 1;
+    return;
+  }
   k_select<<<ctx->grid_select, kSelectThreads, 0, ctx->stream>>>(ctx->F, ctx->H, ctx->fr, ctx->n_local, ctx->ctl,
                                                                 ctx->sel_part, ctx->kw);
   prof_mark(ctx, slot, 1);
@@ -1188,6 +1195,7 @@ static di_status dist_run_impl(di_ctx *ctx, double target) {
   // outbox fluid counts toward the residual (in-flight mass)
   TRYD(global_residual(ctx, ds->s_k, &R));
   ctx->residual = R;
+  if (ctx->sweep_on) k_rpred_set<<<1, 1, 0, ctx->stream>>>(ctx->ctl, ctx->l1_out);   // sweeps carry |F|_1
   if (R < target) goto out;
   if (sync_mode) {
     // -------- SYNC: one exchange per pass, pass totals all-reduced ----------
@@ -1223,12 +1231,12 @@ static di_status dist_run_impl(di_ctx *ctx, double target) {
         // the round's local passes as one captured graph (select, scatter, hubs, finalize)
         CKD(cudaGraphLaunch(ctx->graph_exec, ctx->stream));
         ctx->graph_launches += 1;
-        ctx->kernel_launches += (3LL + (ctx->cap_hub > 0)) * ctx->check_interval;
+        ctx->kernel_launches += ((ctx->sweep_on ? 2LL : 3LL) + (ctx->cap_hub > 0)) * ctx->check_interval;
       } else {
         for (int k = 0; k < ctx->check_interval; ++k) {
           dist_launch_pass_kernels(ctx, k);
-          k_finalize<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->ctl, ctx->sel_part, ctx->grid_select, ctx->sc_part,
-                                                              ctx->grid_scatter, ctx->log);
+          k_finalize<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->ctl, ctx->sel_part, diter_n_sel_part(ctx),
+                                                              ctx->sc_part, diter_n_sc_part(ctx), ctx->log);
           ctx->kernel_launches += 1;
         }
       }
@@ -1259,6 +1267,7 @@ static di_status dist_run_impl(di_ctx *ctx, double target) {
       ctx->passes_done = h->pass;
       TRYD(global_residual(ctx, ds->s_k, &R));
       ctx->residual = R;
+      if (ctx->sweep_on) k_rpred_set<<<1, 1, 0, ctx->stream>>>(ctx->ctl, ctx->l1_out);
       const bool stop = R < target, out_of_passes = h->pass >= max_pass_abs;
       if (stop || out_of_passes) {
         // deliver what is left in the outboxes, so that on return F (with H) is

@@ -450,6 +450,24 @@ Graph diter_graph(const di_ctx *ctx) {
   return g;
 }
 
+// One sweep (k_sweep, + the hub chunks it listed) on the context's stream.
+void diter_launch_sweep(di_ctx *ctx) {
+  const Graph g = diter_graph(ctx);
+  const bool dist = ctx->dist != nullptr;
+  auto sw = dist ? (ctx->vals ? (ctx->kw ? k_sweep<true, true, true> : k_sweep<true, false, true>)
+                              : (ctx->kw ? k_sweep<false, true, true> : k_sweep<false, false, true>))
+                 : (ctx->vals ? (ctx->kw ? k_sweep<true, true> : k_sweep<true, false>)
+                              : (ctx->kw ? k_sweep<false, true> : k_sweep<false, false>));
+  sw<<<ctx->grid_sweep, kScatterThreads, kSweepDynSmem, ctx->stream>>>(g, ctx->F, ctx->H, ctx->fr, ctx->ctl,
+                                                                       ctx->sel_part, ctx->sc_part, ctx->kw);
+  if (ctx->cap_hub > 0) {
+    if (ctx->vals)
+      k_scatter_hubs<true><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
+    else
+      k_scatter_hubs<false><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
+  }
+}
+
 // Capture check_interval passes of (select, scatter, finalize) once.
 di_status diter_capture_graph(di_ctx *ctx) {
   if (ctx->graph_exec) {
@@ -467,20 +485,12 @@ di_status diter_capture_graph(di_ctx *ctx) {
   for (int k = 0; k < ctx->check_interval; ++k) {
     diter_dist_pass_prologue(ctx);   // DI_EXCHANGE_P2P: merge what has arrived before every pass
     if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 0], ctx->stream, cudaEventRecordExternal));
+    const bool dist = ctx->dist != nullptr;
     if (ctx->sweep_on) {
       // one-kernel async sweep (select + diffusion; options.sweep): the profile's
       // "select" span is empty, its "scatter" span is the sweep + hub chunks
       if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 1], ctx->stream, cudaEventRecordExternal));
-      auto sw = ctx->vals ? (ctx->kw ? k_sweep<true, true> : k_sweep<true, false>)
-                          : (ctx->kw ? k_sweep<false, true> : k_sweep<false, false>);
-      sw<<<ctx->grid_sweep, kScatterThreads, kSweepDynSmem, ctx->stream>>>(g, ctx->F, ctx->H, ctx->fr, ctx->ctl,
-                                                                           ctx->sel_part, ctx->sc_part, ctx->kw);
-      if (ctx->cap_hub > 0) {
-        if (ctx->vals)
-          k_scatter_hubs<true><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
-        else
-          k_scatter_hubs<false><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
-      }
+      diter_launch_sweep(ctx);
       if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 2], ctx->stream, cudaEventRecordExternal));
       k_finalize<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->ctl, ctx->sel_part, ctx->grid_sweep, ctx->sc_part,
                                                           ctx->grid_sweep, ctx->log);
@@ -497,7 +507,6 @@ di_status diter_capture_graph(di_ctx *ctx) {
     if (prof) CK(cudaEventRecordWithFlags(ctx->prof_ev[4 * k + 1], ctx->stream, cudaEventRecordExternal));
     // a distributed rank's scatter routes rows outside its range (DIST): its ASYNC / P2P
     // rounds launch this graph for their local passes
-    const bool dist = ctx->dist != nullptr;
     if (ctx->vals)
       (dist ? k_scatter<true, true, false> : ctx->far.on ? k_scatter<true, false, true> : k_scatter<true, false, false>)
           <<<ctx->grid_scatter, kScatterThreads, ctx->scatter_smem, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part);
@@ -683,7 +692,10 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
   TRY(dalloc(ctx, &ctx->fr.hub_deg, hc.n_hub));
   TRY(dalloc(ctx, &ctx->fr.hub_chunk, hc.n_hub));
   // one-kernel async sweeps (options.sweep): one GPU, per-phase launches, no far bins
-  ctx->sweep_on = (o.sweep == 1 && !ctx->dist && !ctx->fused && !ctx->far.on) ? 1 : 0;
+  // distributed ranks: sweeps for the local passes of ASYNC / P2P rounds (SYNC keeps the
+  // snapshot pass, which reproduces the one-GPU pass log)
+  const bool dist_sweepable = ctx->dist && (o.exchange_mode == DI_EXCHANGE_ASYNC || o.exchange_mode == DI_EXCHANGE_P2P);
+  ctx->sweep_on = (o.sweep == 1 && (!ctx->dist || dist_sweepable) && !ctx->fused && !ctx->far.on) ? 1 : 0;
   if (ctx->sweep_on) {
     // per-warp staging in dynamic shared memory (beyond the default 48 KB with the hot window)
     auto attr = [&](const void *fn) { return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepDynSmem); };
@@ -691,6 +703,10 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
     CK(attr((const void *)k_sweep<false, true>));
     CK(attr((const void *)k_sweep<true, false>));
     CK(attr((const void *)k_sweep<true, true>));
+    CK(attr((const void *)k_sweep<false, false, true>));
+    CK(attr((const void *)k_sweep<false, true, true>));
+    CK(attr((const void *)k_sweep<true, false, true>));
+    CK(attr((const void *)k_sweep<true, true, true>));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep<false, true>, kScatterThreads, kSweepDynSmem));
     ctx->grid_sweep = (int)std::max(1LL, std::min<long long>((long long)ctx->num_sms * std::max(1, occ),

@@ -721,7 +721,7 @@ __device__ __forceinline__ void sweep_prefetch(const Graph &g, const double *F, 
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-template <bool SIGNED, bool KEY, bool PF>
+template <bool SIGNED, bool KEY, bool PF, bool DIST>
 __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double *__restrict__ F,
                                            double *__restrict__ H, const Frontier &fr, Ctl *ctl,
                                            const float *__restrict__ kw, double T, long long base,
@@ -795,6 +795,7 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
     const double sv = f[k];
     const long long b0 = cp[k];
     const long long deg = nxt - b0;
+    long long dpush = 0;
     bool stage = false;
     double wv = 0.0;
     sel_all += __popc(m);
@@ -811,13 +812,22 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
         if (deg <= kLowMax) acc.lo += 1;
         else if (deg <= kMidMax) acc.mi += 1;
         else acc.hu += 1;
-        if (deg <= kMidMax) {
-          stage = true;
+        // distributed rank: its local edges are stored first (nloc_i); with remote
+        // increments / receivers the sweep pushes only those, else all (remote rows to
+        // the outbox through the Sink)
+        dpush = deg;
+        if (DIST) {
+          const long long nl = __ldg(g.nloc + i);
+          if (g.local_only) dpush = nl;
+          else acc.remote += deg - nl;
+        }
+        if (dpush <= kMidMax) {
+          stage = dpush > 0;
         } else {
-          const unsigned long long nch = (unsigned long long)((deg + kHubChunk - 1) / kHubChunk);
+          const unsigned long long nch = (unsigned long long)((dpush + kHubChunk - 1) / kHubChunk);
           const unsigned long long old = atomicAdd(&ctl->hub_packed, (1ull << 32) | nch);
           const unsigned sl = (unsigned)(old >> 32);
-          fr.hub_w[sl] = wv; fr.hub_b0[sl] = b0; fr.hub_deg[sl] = deg;
+          fr.hub_w[sl] = wv; fr.hub_b0[sl] = b0; fr.hub_deg[sl] = dpush;
           fr.hub_chunk[sl] = (unsigned)(old & 0xffffffffull);
         }
       }
@@ -825,13 +835,13 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
     const unsigned ms = __ballot_sync(0xffffffffu, stage);
     if (stage) {
       const int pos = st.cnt + __popc(ms & lt);
-      st.b0[pos] = b0; st.deg[pos] = (int)deg; st.w[pos] = wv;
+      st.b0[pos] = b0; st.deg[pos] = (int)dpush; st.w[pos] = wv;
     }
     st.cnt += __popc(ms);
   }
 }
 
-template <bool SIGNED, bool KEY>
+template <bool SIGNED, bool KEY, bool DIST = false>
 __global__ void __launch_bounds__(kScatterThreads, DITER_SWEEP_MIN_BLOCKS)
 k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ctl *ctl,
         SelPartial *__restrict__ sp, ScPartial *__restrict__ part, const float *__restrict__ kw) {
@@ -853,7 +863,7 @@ k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ct
   double *pfb = s_dyn + 2 * kW * kSweepStage + (kW * kSweepStage + 1) / 2 + warp * kSweepPfWords;
   SweepPf pf{pfb, reinterpret_cast<long long *>(pfb + kSweepSpan), reinterpret_cast<float *>(pfb + 2 * kSweepSpan + 1),
              reinterpret_cast<unsigned *>(pfb + 2 * kSweepSpan + 1) + kSweepSpan};
-  const Sink s{F, s_hot, g.hot_lo, g.lo, g.n, nullptr, nullptr};
+  const Sink s{F, s_hot, g.hot_lo, g.lo, g.n, DIST ? g.G : nullptr, DIST ? g.dflags : nullptr};
   Stage sg{nullptr, nullptr, 0};
   const double T = ctl->T;
   const unsigned lane = lane_id();
@@ -879,13 +889,13 @@ k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ct
       if (run > 1) {
         sweep_prefetch<KEY>(g, F, kw, fr, (s0 + q0) * kSweepSpan, pf);
         for (long long q = s0 + q0; q < q1; ++q) {
-          sweep_span<SIGNED, KEY, true>(g, s, F, H, fr, ctl, kw, T, q * kSweepSpan, acc, sel_all, dloss, dang_cnt, st,
-                                        pf, q + 1 < q1);
+          sweep_span<SIGNED, KEY, true, DIST>(g, s, F, H, fr, ctl, kw, T, q * kSweepSpan, acc, sel_all, dloss,
+                                              dang_cnt, st, pf, q + 1 < q1);
           sweep_flush<SIGNED>(g, s, ctl, st, sg, false);
         }
       } else {
-        sweep_span<SIGNED, KEY, false>(g, s, F, H, fr, ctl, kw, T, (s0 + q0) * kSweepSpan, acc, sel_all, dloss,
-                                       dang_cnt, st, pf, false);
+        sweep_span<SIGNED, KEY, false, DIST>(g, s, F, H, fr, ctl, kw, T, (s0 + q0) * kSweepSpan, acc, sel_all,
+                                             dloss, dang_cnt, st, pf, false);
         sweep_flush<SIGNED>(g, s, ctl, st, sg, false);
       }
     }
@@ -904,6 +914,7 @@ k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ct
   acc.hu = warp_sum(acc.hu);
   dloss = warp_sum(dloss);
   dang_cnt = warp_sum(dang_cnt);
+  if (DIST) acc.remote = warp_sum(acc.remote);
   __shared__ ScAcc s_acc[kW];
   __shared__ double s_dl[kW];
   __shared__ int s_sel[kW], s_dc[kW];
@@ -915,11 +926,14 @@ k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ct
   if (threadIdx.x == 0) {
     ScPartial p{0.0, 0, 0, 0, 0, 0, 0.0};
     SelPartial q{0.0, 0, 0.0, 0};
+    long long remote = 0;
     for (int k = 0; k < kW; ++k) {
       p.loss += s_acc[k].loss; p.edges += s_acc[k].edges;
       p.n_low += s_acc[k].lo; p.n_mid += s_acc[k].mi; p.n_hub += s_acc[k].hu;
       q.cnt += s_sel[k]; q.loss += s_dl[k]; q.dang += s_dc[k];
+      remote += s_acc[k].remote;
     }
+    if (DIST && remote) atomicAdd(&ctl->remote_pushes, (unsigned long long)remote);
     part[blockIdx.x] = p;
     sp[blockIdx.x] = q;
   }
@@ -934,6 +948,13 @@ __global__ void k_sweep_check(Ctl *ctl, const double *l1) {
   if (r < ctl->r_pred) ctl->r_pred = r;
   if (r < ctl->target && ctl->pending == 0.0) ctl->done = 1;
 }
+// Distributed sweeps: merged fluid R raises the carried bound (|F|_1 grows by <= R)
+__global__ void k_rpred_add(Ctl *ctl, const double *recv) {
+  const double R = *recv;
+  if (R > 0.0 && isfinite(ctl->r_pred)) ctl->r_pred += R;
+}
+__global__ void k_rpred_set(Ctl *ctl, const double *l1) { ctl->r_pred = *l1; }
+
 constexpr size_t kSweepDynSmem = sizeof(double) * ((size_t)2 * (kScatterThreads / 32) * kSweepStage +
                                                    ((kScatterThreads / 32) * kSweepStage + 1) / 2 +
                                                    (size_t)(kScatterThreads / 32) * kSweepPfWords);

@@ -549,6 +549,7 @@ void p2p_pass_merge(di_ctx *ctx) {
                                                         P.d_mass + W, P.d_round + kRoundRecv);
   k_p2p_ack<<<1, kP2PMaxWorld, 0, ctx->stream>>>(P.d_peers, W, rank, P.d_snap, P.d_tail_in, P.d_mass + W, P.d_merged);
   if (ctx->opt.receive_rescale) k_p2p_rescale_ctl<<<1, 1, 0, ctx->stream>>>(ctx->ctl, P.d_round);
+  if (ctx->sweep_on) k_rpred_add<<<1, 1, 0, ctx->stream>>>(ctx->ctl, P.d_round + kRoundRecv);   // merged mass
 }
 
 // Compact the outbox into the rings of the peers in `mask` and publish.
@@ -589,6 +590,7 @@ static di_status round_measure(di_ctx *ctx, RoundHost *hb) {
   k_p2p_outbox_mass<<<ctx->num_sms * 2, 256, 0, ctx->stream>>>(ctx->G, ctx->dflags, P.m, P.d_round + kRoundS);
   TRYP(diter_l1_launch(ctx));
   k_copy_double<<<1, 1, 0, ctx->stream>>>(P.d_round + kRoundR, ctx->l1_out);
+  if (ctx->sweep_on) k_rpred_set<<<1, 1, 0, ctx->stream>>>(ctx->ctl, ctx->l1_out);   // sweeps carry |F|_1
   k_p2p_board<<<1, kP2PMaxWorld, 0, ctx->stream>>>(P.d_peers, W, ctx->rank, reinterpret_cast<const P2PHeader *>(P.win),
                                                   P.d_round, P.d_sent, ctx->ctl);
   ctx->kernel_launches += 3;
@@ -666,7 +668,7 @@ di_status p2p_run(di_ctx *ctx, double target) {
     dist_set_target(ctx, 0.0, max_pass_abs);   // local passes never stop on their own
     const bool graph = ctx->graph_exec != nullptr && !ctx->opt.profile;
     bool asleep = false;
-    const int kpp = 3 + (ctx->cap_hub > 0 ? 1 : 0) + 3 + (ctx->opt.receive_rescale ? 1 : 0);
+    const int kpp = (ctx->sweep_on ? 2 + 1 : 3) + (ctx->cap_hub > 0 ? 1 : 0) + 3 + (ctx->opt.receive_rescale ? 1 : 0);
     for (;;) {
       // 1-2. local passes, each after a merge of what has arrived (p2p_pass_merge) --
       //      or, asleep (r_k below this rank's share of the target), only the
@@ -684,8 +686,8 @@ di_status p2p_run(di_ctx *ctx, double target) {
       } else {
         for (int k = 0; k < ctx->check_interval; ++k) {
           dist_launch_pass_kernels(ctx, k);   // the P2P merge first (diter_dist_pass_prologue)
-          k_finalize<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->ctl, ctx->sel_part, ctx->grid_select,
-                                                              ctx->sc_part, ctx->grid_scatter, ctx->log);
+          k_finalize<<<1, kFinalizeThreads, 0, ctx->stream>>>(ctx->ctl, ctx->sel_part, diter_n_sel_part(ctx),
+                                                              ctx->sc_part, diter_n_sc_part(ctx), ctx->log);
           ctx->kernel_launches += 4 + (ctx->opt.receive_rescale ? 1 : 0);
         }
       }

@@ -15,6 +15,9 @@ with T_1, s (select share) and E_1 from the 1-GPU bench line, B_link = 450 GB/s 
 
     python scripts/exp_scaling_model.py C4 248.7 0.224 2.6595e10 [out|inout]
 
+With sweeps (MODEL_SWEEP, default bench.SWEEP[cfg]) there is no select kernel: s is
+the scan's share of the sweep's algorithmic bytes (8 N of 8 N + 40 |S| + 20 E).
+
 MODEL_MODE=p2p models DI_EXCHANGE_P2P instead: no round barrier, so each rank runs
 at its own pace and the job ends at the last confirmation:
 
@@ -54,13 +57,16 @@ if cfg == "C3":
 pol, alpha, frac, key = bench.SCHEDULES[cfg]
 alpha_k = float(os.environ.get("MODEL_ALPHA", alpha))        # schedule of the K ranks (default: 1 GPU's)
 frac_k = float(os.environ.get("MODEL_FRAC", frac))
+SWEEP = int(os.environ.get("MODEL_SWEEP", bench.SWEEP.get(cfg, 0)))     # options.sweep (R26) on every rank
+RUN = bench.SCATTER_RUN.get(cfg, 0)
 # passes of the 1-GPU solve (scan term of the model)
-o1 = di.default_options(policy=pol, alpha=alpha, hybrid_frac=frac, select_key=key)
+o1 = di.default_options(policy=pol, alpha=alpha, hybrid_frac=frac, select_key=key, sweep=SWEEP, scatter_run=RUN,
+                        scatter_stripes=bench.SCATTER_STRIPES.get(cfg, 0))
 c1 = di.di_create(p.n, p.col_ptr, p.row_idx, p.values, p.b, p.d, o1)
 di.di_run(c1, p.stop)
 P1 = di.di_get_stats(c1)["passes"]
 di.di_destroy(c1)
-out = {"mode": "p2p" if P2P else "async", "config": cfg, "partition": COST, "round_passes": ROUND, "remote_push": REMOTE, "T1_ms": T1, "select_share": s_sel, "E1": E1, "passes_1": P1, "K": {}}
+out = {"mode": "p2p" if P2P else "async", "sweep": SWEEP, "config": cfg, "partition": COST, "round_passes": ROUND, "remote_push": REMOTE, "T1_ms": T1, "select_share": s_sel, "E1": E1, "passes_1": P1, "K": {}}
 for K in KS:
     bounds = dist.partition_bounds(p.col_ptr, K, cost=COST, row_idx=p.row_idx)
     st = [None] * K
@@ -72,7 +78,7 @@ for K in KS:
             lcp, lri, lv, lb = dist.shard_csc(p.col_ptr, p.row_idx, p.values, p.b, bounds, r)
             o = di.default_options(policy=pol, alpha=alpha_k, hybrid_frac=frac_k, select_key=key,
                                    exchange_mode=MODE, check_interval=ROUND, remote_push=REMOTE,
-                                   receive_rescale=RESCALE, p2p_sleep=SLEEP)
+                                   receive_rescale=RESCALE, p2p_sleep=SLEEP, sweep=SWEEP, scatter_run=RUN)
             ctx = di.di_create_dist(r, K, cid, bounds, p.n, lcp, lri, lv, lb, p.d, o)
             di.di_run(ctx, p.stop)
             st[r] = di.di_get_stats(ctx)

@@ -521,3 +521,27 @@ def test_p2p_checkpoint_resume():
     deg = np.diff(p.col_ptr)
     ledger = np.abs(F).sum() + 0.15 * H.sum() + 0.85 * H[deg == 0].sum()
     assert abs(ledger - 0.15) <= 1e-12 * 0.15
+
+
+@pytest.mark.parametrize("mode,K,remote", [(di.DI_EXCHANGE_ASYNC, 2, di.DI_REMOTE_PER_DIFFUSION),
+                                           (di.DI_EXCHANGE_ASYNC, 4, di.DI_REMOTE_INCREMENT),
+                                           (di.DI_EXCHANGE_ASYNC, 3, di.DI_REMOTE_RECEIVER),
+                                           (di.DI_EXCHANGE_P2P, 2, di.DI_REMOTE_INCREMENT),
+                                           (di.DI_EXCHANGE_P2P, 4, di.DI_REMOTE_INCREMENT),
+                                           (di.DI_EXCHANGE_P2P, 8, di.DI_REMOTE_INCREMENT)])
+def test_sweeps_on_ranks(mode, K, remote):
+    """Distributed ranks running their local passes as asynchronous sweeps (options.sweep,
+    reading R26): parity with the oracle, a closed mass ledger, the global residual on
+    every rank; with the per-edge key (f1)."""
+    p = gen.config("C2", 2, n=300_000)
+    bn = 0.15
+    bounds = dist.partition_bounds(p.col_ptr, K, cost="out", row_idx=p.row_idx)
+    H, F, outs = run_ranks(K, p.n, p.col_ptr, p.row_idx, None, None, 0.85, p.parity_stop, bounds, mode,
+                           f"sweep{mode}{K}{remote}", check_interval=4, remote_push=remote, sweep=1,
+                           select_key=di.DI_KEY_EDGE)
+    X = oracle.Problem(p.n, p.col_ptr, p.row_idx).solve(1e-12 * bn * 0.15).H
+    assert np.abs(H - X).sum() <= 1e-8 * bn
+    deg = np.diff(p.col_ptr)
+    ledger = np.abs(F).sum() + 0.15 * H.sum() + 0.85 * H[deg == 0].sum()
+    assert abs(ledger - bn) <= 1e-12 * bn
+    assert all(o[4] < p.parity_stop for o in outs)
