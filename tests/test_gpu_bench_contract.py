@@ -57,3 +57,22 @@ def test_bench_distributed_path_one_rank(exchange):
         assert d["confirms_per_solve"] >= 1
         assert d["collectives_per_solve"] == 1 + 4 * d["confirms_per_solve"]
     assert d["e2e"]["value"] > 0
+
+
+def test_bench_line_sweep_config():
+    """The sweep launch configuration (C4 shape, shrunk): k_sweep is the roofline kernel,
+    its bytes follow SURVEY §8d's B_p, launches are one sweep + one finalize per pass, and
+    the snapshot-pass solve is reported beside it."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "C4", "--n", "4000000",
+                          "--steps", "2", "--warmup", "3", "--cpu-seconds", "1", "--no-raw-key"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    r = d["roofline"]
+    assert r["kernel"] == "k_sweep" and "k_sweep" in r["kernel_shares"] and 0 < r["frac"] < 1
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert "sweeps" in d["config"]["passes"]
+    per = d["gpu_launches"] / d["steps"]
+    assert 2 * d["passes_per_solve"] <= per <= 2 * (d["passes_per_solve"] + 16) + 16, (per, d["passes_per_solve"])
+    s = d["snapshot"]
+    assert s["time_to_target_ms"] > 0 and s["passes_per_solve"] > 0
