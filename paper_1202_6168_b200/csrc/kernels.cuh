@@ -633,6 +633,9 @@ k_scatter_hubs(Graph g, double *__restrict__ F, Frontier fr, const Ctl *ctl) {
 #ifndef DITER_SWEEP_ITEMS
 #define DITER_SWEEP_ITEMS 4        // 128-node spans: C4 193.1 -> 188.1 ms vs 8, C3 138.6 -> 135.4 (16: spills)
 #endif
+#ifndef DITER_SWEEP_ALTERNATE
+#define DITER_SWEEP_ALTERNATE 0    // odd passes sweep each stripe in descending order
+#endif
 #ifndef DITER_SWEEP_MIN_BLOCKS
 #define DITER_SWEEP_MIN_BLOCKS kScatterMinBlocks
 #endif
@@ -726,7 +729,7 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
                                            double *__restrict__ H, const Frontier &fr, Ctl *ctl,
                                            const float *__restrict__ kw, double T, long long base,
                                            ScAcc &acc, int &sel_all, double &dloss, int &dang_cnt,
-                                           SweepStage &st, const SweepPf &pf, bool prefetch_next) {
+                                           SweepStage &st, const SweepPf &pf, long long next_base) {
   const unsigned lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
   double f[kSweepItems];
@@ -747,7 +750,7 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
     cp_end = pf.cp[kSweepSpan];
     dword = (int)lane < kSweepItems ? pf.dw[lane] : 0u;
     __syncwarp();
-    if (prefetch_next) sweep_prefetch<KEY>(g, F, kw, fr, base + kSweepSpan, pf);
+    if (next_base >= 0) sweep_prefetch<KEY>(g, F, kw, fr, next_base, pf);
   } else {
     // single-span claims (options.scatter_run = 1): direct loads
     const long long n = g.n;
@@ -871,6 +874,7 @@ k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ct
   int sel_all = 0, dang_cnt = 0;
   double dloss = 0.0;
   const long long spans = (g.n + kSweepSpan - 1) / kSweepSpan;
+  const bool down = DITER_SWEEP_ALTERNATE && (ctl->pass & 1);
   const int gw = blockIdx.x * kW + warp;
   const int ns = fr.stripes;
   const int run = fr.run;
@@ -886,16 +890,19 @@ k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ct
         break;
       }
       const long long q1 = min(s1, s0 + (long long)q0 + run);
+      // span of the k-th claimed index: ascending, or (odd passes with alternating
+      // directions) descending within the stripe
+      auto span_of = [&](long long q) { return down ? s1 - 1 - (q - s0) : q; };
       if (run > 1) {
-        sweep_prefetch<KEY>(g, F, kw, fr, (s0 + q0) * kSweepSpan, pf);
+        sweep_prefetch<KEY>(g, F, kw, fr, span_of(s0 + q0) * kSweepSpan, pf);
         for (long long q = s0 + q0; q < q1; ++q) {
-          sweep_span<SIGNED, KEY, true, DIST>(g, s, F, H, fr, ctl, kw, T, q * kSweepSpan, acc, sel_all, dloss,
-                                              dang_cnt, st, pf, q + 1 < q1);
+          sweep_span<SIGNED, KEY, true, DIST>(g, s, F, H, fr, ctl, kw, T, span_of(q) * kSweepSpan, acc, sel_all,
+                                              dloss, dang_cnt, st, pf, q + 1 < q1 ? span_of(q + 1) * kSweepSpan : -1);
           sweep_flush<SIGNED>(g, s, ctl, st, sg, false);
         }
       } else {
-        sweep_span<SIGNED, KEY, false, DIST>(g, s, F, H, fr, ctl, kw, T, (s0 + q0) * kSweepSpan, acc, sel_all,
-                                             dloss, dang_cnt, st, pf, false);
+        sweep_span<SIGNED, KEY, false, DIST>(g, s, F, H, fr, ctl, kw, T, span_of(s0 + q0) * kSweepSpan, acc, sel_all,
+                                             dloss, dang_cnt, st, pf, -1);
         sweep_flush<SIGNED>(g, s, ctl, st, sg, false);
       }
     }
