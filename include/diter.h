@@ -147,7 +147,8 @@ typedef struct {
                               (from the create-time in-degree sample; the set-aside is per device,
                               refcounted over contexts): 0 = auto (off while F fits in 64 MB, else
                               28 MB when F <= 2x L2 and 20 MB above: C3 219 -> 184 ms, C4 265 ->
-                              250 ms), -1 = off, > 0 = a window of that many MB */
+                              250 ms; with sweeps 36 / 28 MB), -1 = off, > 0 = a window of that
+                              many MB */
   int32_t p2p_sleep;       /* DI_EXCHANGE_P2P: a rank whose local residual r_k is below target / K
                               sleeps: its rounds only merge, send and measure,
                               no local passes, until received fluid lifts r_k again; 0 = on

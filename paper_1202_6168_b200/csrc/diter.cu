@@ -293,7 +293,12 @@ static di_status choose_l2_window(di_ctx *ctx) {
   if (opt == 0 && f_bytes <= (64LL << 20)) return DI_OK;
   int l2 = 0;
   CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device));
-  const long long auto_mb = f_bytes <= 2LL * l2 ? 28 : 20;
+  // asynchronous sweeps have no separate streaming select for the set-aside to slow
+  // down, so they take larger windows: C4 182.4 -> 178.8 ms at 28 MB, C3 135.6 -> 130.7
+  // ms at 36 MB (profiles/r02s_l2_window.txt)
+  const bool sweeps = ctx->opt.sweep == 1 && !ctx->fused &&
+                      (!ctx->dist || ctx->opt.exchange_mode != DI_EXCHANGE_SYNC);
+  const long long auto_mb = f_bytes <= 2LL * l2 ? (sweeps ? 36 : 28) : (sweeps ? 28 : 20);
   const long long want_rows = ((opt > 0 ? (long long)opt : auto_mb) << 20) / (long long)sizeof(double);
   // no in-degree sample (hot window off): a forced window starts at the owned range
   const std::vector<unsigned> h = ctx->blk_hist.empty() ? std::vector<unsigned>((size_t)((ctx->lo + n + 1023) >> 10), 0u)
