@@ -456,13 +456,29 @@ Graph diter_graph(const di_ctx *ctx) {
 }
 
 // One sweep (k_sweep, + the hub chunks it listed) on the context's stream.
+#ifndef DITER_SWEEP_KEY_DERIVED
+#define DITER_SWEEP_KEY_DERIVED 1    // per-edge key from col_ptr in sweeps (no weight stream)
+#endif
+typedef void (*SweepFn)(Graph, double *, double *, Frontier, Ctl *, SelPartial *, ScPartial *, const float *);
+
+// k_sweep instance: signed / PageRank x key mode (0 raw, 1 kw weights, 2 per-edge key
+// derived from col_ptr) x distributed
+template <bool SIGNED, bool DIST>
+static SweepFn sweep_fn(int key) {
+  return key == 0 ? k_sweep<SIGNED, 0, DIST> : key == 1 ? k_sweep<SIGNED, 1, DIST> : k_sweep<SIGNED, 2, DIST>;
+}
+
+static int sweep_key_mode(const di_ctx *ctx) {
+  if (!ctx->kw) return 0;
+  return (DITER_SWEEP_KEY_DERIVED && ctx->opt.select_key == DI_KEY_EDGE) ? 2 : 1;
+}
+
 void diter_launch_sweep(di_ctx *ctx) {
   const Graph g = diter_graph(ctx);
   const bool dist = ctx->dist != nullptr;
-  auto sw = dist ? (ctx->vals ? (ctx->kw ? k_sweep<true, true, true> : k_sweep<true, false, true>)
-                              : (ctx->kw ? k_sweep<false, true, true> : k_sweep<false, false, true>))
-                 : (ctx->vals ? (ctx->kw ? k_sweep<true, true> : k_sweep<true, false>)
-                              : (ctx->kw ? k_sweep<false, true> : k_sweep<false, false>));
+  const int key = sweep_key_mode(ctx);
+  SweepFn sw = dist ? (ctx->vals ? sweep_fn<true, true>(key) : sweep_fn<false, true>(key))
+                    : (ctx->vals ? sweep_fn<true, false>(key) : sweep_fn<false, false>(key));
   sw<<<ctx->grid_sweep, kScatterThreads, kSweepDynSmem, ctx->stream>>>(g, ctx->F, ctx->H, ctx->fr, ctx->ctl,
                                                                        ctx->sel_part, ctx->sc_part, ctx->kw);
   if (ctx->cap_hub > 0) {
@@ -704,16 +720,14 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
   if (ctx->sweep_on) {
     // per-warp staging in dynamic shared memory (beyond the default 48 KB with the hot window)
     auto attr = [&](const void *fn) { return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepDynSmem); };
-    CK(attr((const void *)k_sweep<false, false>));
-    CK(attr((const void *)k_sweep<false, true>));
-    CK(attr((const void *)k_sweep<true, false>));
-    CK(attr((const void *)k_sweep<true, true>));
-    CK(attr((const void *)k_sweep<false, false, true>));
-    CK(attr((const void *)k_sweep<false, true, true>));
-    CK(attr((const void *)k_sweep<true, false, true>));
-    CK(attr((const void *)k_sweep<true, true, true>));
+    for (int key = 0; key < 3; ++key) {
+      CK(attr((const void *)sweep_fn<false, false>(key)));
+      CK(attr((const void *)sweep_fn<true, false>(key)));
+      CK(attr((const void *)sweep_fn<false, true>(key)));
+      CK(attr((const void *)sweep_fn<true, true>(key)));
+    }
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep<false, true>, kScatterThreads, kSweepDynSmem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep<false, 1>, kScatterThreads, kSweepDynSmem));
     ctx->grid_sweep = (int)std::max(1LL, std::min<long long>((long long)ctx->num_sms * std::max(1, occ),
                                                              (n + kSweepSpan - 1) / kSweepSpan));
   }

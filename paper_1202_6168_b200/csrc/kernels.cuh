@@ -702,7 +702,7 @@ __device__ __forceinline__ void cp_async(void *smem, const void *gmem, int bytes
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" :: "r"(sa), "l"(gmem), "r"(valid ? 4 : 0) : "memory");
 }
 
-template <bool KEY>
+template <int KEY>
 __device__ __forceinline__ void sweep_prefetch(const Graph &g, const double *F, const float *kw, const Frontier &fr,
                                                long long base, const SweepPf &pf) {
   const unsigned lane = lane_id();
@@ -712,7 +712,7 @@ __device__ __forceinline__ void sweep_prefetch(const Graph &g, const double *F, 
     const long long i = base + 32 * k + lane;
     const long long ic = i < n ? i : n - 1;
     cp_async(pf.f + 32 * k + lane, F + ic, 8, i < n);
-    if (KEY) cp_async(pf.w + 32 * k + lane, kw + ic, 4, i < n);
+    if (KEY == 1) cp_async(pf.w + 32 * k + lane, kw + ic, 4, i < n);
     cp_async(pf.cp + 32 * k + lane, g.col_ptr + (i < n ? i : n), 8, true);
   }
   if (lane == 0) {
@@ -724,7 +724,11 @@ __device__ __forceinline__ void sweep_prefetch(const Graph &g, const double *F, 
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-template <bool SIGNED, bool KEY, bool PF, bool DIST>
+// KEY: 0 raw |F_i|; 1 the create-time fp32 weights kw (either key of R3); 2 the
+// per-edge key 1/(#out_i + 1) derived from the span's col_ptr values (fp32 reciprocal
+// rounded to nearest -- no weight stream; sweeps are not compared with the oracle's
+// snapshot log, so the weight's last-bit rounding is free)
+template <bool SIGNED, int KEY, bool PF, bool DIST>
 __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double *__restrict__ F,
                                            double *__restrict__ H, const Frontier &fr, Ctl *ctl,
                                            const float *__restrict__ kw, double T, long long base,
@@ -733,7 +737,7 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
   const unsigned lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
   double f[kSweepItems];
-  float w[KEY ? kSweepItems : 1];
+  float w[KEY == 1 ? kSweepItems : 1];
   long long cp[kSweepItems];
   long long cp_end;
   unsigned dword;
@@ -744,7 +748,7 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
 #pragma unroll
     for (int k = 0; k < kSweepItems; ++k) {
       f[k] = pf.f[32 * k + lane];
-      if (KEY) w[k] = pf.w[32 * k + lane];
+      if (KEY == 1) w[k] = pf.w[32 * k + lane];
       cp[k] = pf.cp[32 * k + lane];
     }
     cp_end = pf.cp[kSweepSpan];
@@ -758,7 +762,7 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
     for (int k = 0; k < kSweepItems; ++k) {
       const long long i = base + 32 * k + lane;
       f[k] = (i < n) ? F[i] : 0.0;
-      if (KEY) w[k] = (i < n) ? __ldcs(kw + i) : 0.0f;
+      if (KEY == 1) w[k] = (i < n) ? __ldcs(kw + i) : 0.0f;
       cp[k] = __ldcs(g.col_ptr + (i < n ? i : n));
     }
     const long long iend = base + kSweepSpan;
@@ -766,13 +770,27 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
     const long long wi = (base >> 5) + lane;
     dword = ((int)lane < kSweepItems && (wi << 5) < n) ? __ldg(fr.dang_bits + wi) : 0u;
   }
+  // #out_i of every node of the span from its col_ptr values: lane 31's successor is
+  // the next item's lane 0 (the last item's: col_ptr at the span's end)
+  int dg[kSweepItems];
+#pragma unroll
+  for (int k = 0; k < kSweepItems; ++k) {
+    long long nxt = __shfl_down_sync(0xffffffffu, cp[k], 1);
+    const long long nxt0 = (k + 1 < kSweepItems) ? __shfl_sync(0xffffffffu, cp[k + 1 < kSweepItems ? k + 1 : k], 0)
+                                                 : cp_end;
+    if (lane == 31) nxt = nxt0;
+    dg[k] = (int)(nxt - cp[k]);
+  }
   // take every selected node of the span (independent atomics, issued together)
   unsigned msel[kSweepItems];
 #pragma unroll
   for (int k = 0; k < kSweepItems; ++k) {
     const long long i = base + 32 * k + lane;
     const double af = fabs(f[k]);
-    const bool sel = (KEY ? af * (double)w[k] : af) > T;     // strict ">" (R7)
+    const double key = KEY == 0 ? af
+                     : KEY == 1 ? af * (double)w[k]
+                                : af * (double)__frcp_rn((float)dg[k] + 1.0f);
+    const bool sel = key > T;                                // strict ">" (R7)
     msel[k] = __ballot_sync(0xffffffffu, sel);
 #if DITER_SWEEP_TAKE_RED
     // take by a fire-and-forget RED of -s_i: F_i = (s_i + pushes since the load) - s_i,
@@ -790,14 +808,9 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
     const long long i = base + 32 * k + lane;
     const bool sel = (m >> lane) & 1u;
     const bool dang = (__shfl_sync(0xffffffffu, dword, k) >> lane) & 1u;
-    // #out_i from the span's col_ptr values: lane 31's successor is the next item's lane 0
-    long long nxt = __shfl_down_sync(0xffffffffu, cp[k], 1);
-    const long long nxt0 = (k + 1 < kSweepItems) ? __shfl_sync(0xffffffffu, cp[k + 1 < kSweepItems ? k + 1 : k], 0)
-                                                 : cp_end;
-    if (lane == 31) nxt = nxt0;
     const double sv = f[k];
     const long long b0 = cp[k];
-    const long long deg = nxt - b0;
+    const long long deg = dg[k];
     long long dpush = 0;
     bool stage = false;
     double wv = 0.0;
@@ -844,7 +857,7 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
   }
 }
 
-template <bool SIGNED, bool KEY, bool DIST = false>
+template <bool SIGNED, int KEY, bool DIST = false>
 __global__ void __launch_bounds__(kScatterThreads, DITER_SWEEP_MIN_BLOCKS)
 k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ctl *ctl,
         SelPartial *__restrict__ sp, ScPartial *__restrict__ part, const float *__restrict__ kw) {
