@@ -376,7 +376,7 @@ def run_reference(args, rank, world):
               f"from F = B when it converges; ~{per:.1f}s per step), full graph")
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "edges/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3 / args.steps,
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic",
            "config": bench_config(args, p, policy_of(args), world, *graph_residency(p, world)),
            "cpu_baseline": {"value": v, "unit": "edges/s", "cores": 1, "kind": "oracle", "host": host_cpu(),
