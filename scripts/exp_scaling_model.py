@@ -45,6 +45,7 @@ ROUND = int(os.environ.get("MODEL_ROUND_PASSES", "4"))      # bench --round-pass
 REMOTE = int(os.environ.get("MODEL_REMOTE_PUSH", "1"))      # bench --remote-push
 RESCALE = int(os.environ.get("MODEL_RESCALE", "1"))          # options.receive_rescale
 SLEEP = int(os.environ.get("MODEL_SLEEP", "0"))              # options.p2p_sleep (0 on, -1 off)
+ADAPT = int(os.environ.get("MODEL_ADAPT", "0"))              # options.adapt_rounds (ASYNC; 0 off)
 P2P = os.environ.get("MODEL_MODE", "async") == "p2p"
 MODE = di.DI_EXCHANGE_P2P if P2P else di.DI_EXCHANGE_ASYNC   # SYNC's di_stats.edges are global totals
 B_P2P, T_CONFIRM = 900e9, 150e-6
@@ -78,7 +79,8 @@ for K in KS:
             lcp, lri, lv, lb = dist.shard_csc(p.col_ptr, p.row_idx, p.values, p.b, bounds, r)
             o = di.default_options(policy=pol, alpha=alpha_k, hybrid_frac=frac_k, select_key=key,
                                    exchange_mode=MODE, check_interval=ROUND, remote_push=REMOTE,
-                                   receive_rescale=RESCALE, p2p_sleep=SLEEP, sweep=SWEEP, scatter_run=RUN)
+                                   receive_rescale=RESCALE, p2p_sleep=SLEEP, sweep=SWEEP, scatter_run=RUN,
+                                   adapt_rounds=ADAPT)
             ctx = di.di_create_dist(r, K, cid, bounds, p.n, lcp, lri, lv, lb, p.d, o)
             di.di_run(ctx, p.stop)
             st[r] = di.di_get_stats(ctx)

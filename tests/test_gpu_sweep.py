@@ -79,3 +79,30 @@ def test_sweep_resume_reset_state():
     for H in (H1, H2):
         assert np.abs(H - X).sum() <= TOL * bn
     _check_state(n, cp, ri, None, None, 0.85, H2, F2, r2, target)
+
+
+def test_sweep_max_passes_and_checkpoint():
+    """max_passes stops a sweep run with a consistent state (NOT_CONVERGED, identity on
+    every row); di_set_state resumes from a checkpoint to the same X; any
+    check_interval (passes per captured graph) gives the same answer."""
+    n = 80_000
+    cp, ri = gen.web_graph(n, 6, gen.XMIN_C4)
+    X, P, bn = _xref(n, cp, ri)
+    target = 1e-9 * bn
+    ctx = di.di_create(n, cp, ri, None, None, 0.85, di.default_options(sweep=1, select_key=1, max_passes=5,
+                                                                       check_interval=3))
+    s = di.di_run(ctx, target, raise_on_not_converged=False)
+    assert s == di.DI_ERR_NOT_CONVERGED
+    H, F = di.di_get_history(ctx), di.di_get_fluid(ctx)
+    r = di.di_get_residual(ctx)
+    assert di.di_get_stats(ctx)["passes"] == 5
+    _check_state(n, cp, ri, None, None, 0.85, H, F, r, float("inf"))
+    di.di_destroy(ctx)
+    for ci in (1, 7, 16):
+        ctx = di.di_create(n, cp, ri, None, None, 0.85, di.default_options(sweep=1, select_key=1, check_interval=ci))
+        di.di_set_state(ctx, F, H)                     # resume from the checkpoint
+        di.di_run(ctx, target)
+        H2, F2, r2 = di.di_get_history(ctx), di.di_get_fluid(ctx), di.di_get_residual(ctx)
+        di.di_destroy(ctx)
+        assert np.abs(H2 - X).sum() <= TOL * bn
+        _check_state(n, cp, ri, None, None, 0.85, H2, F2, r2, target)
