@@ -68,7 +68,7 @@ struct di_ctx {
   cudaStream_t stream = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  int num_sms = 0, grid_select = 0, grid_scatter = 0, grid_l1 = 0, grid_fused = 0;
+  int num_sms = 0, grid_select = 0, grid_scatter = 0, grid_l1 = 0, grid_fused = 0, grid_hubs = 0;
   size_t scatter_smem = 0;  // dynamic shared memory of the scatter: group prefix over segments
   bool fused = false;
   void *h_ctl = nullptr;  // pinned mirror of Ctl

@@ -1122,7 +1122,7 @@ void dist_launch_pass_kernels(di_ctx *ctx, int slot) {
     prof_mark(ctx, slot, 1);
     diter_launch_sweep(ctx);
     prof_mark(ctx, slot, 2);
-    ctx->kernel_launches += ctx->cap_hub > 0 ? 2 : 1;
+    ctx->kernel_launches += (ctx->cap_hub > 0 && !DITER_SWEEP_HUBS) ? 2 : 1;
     return;
   }
   k_select<<<ctx->grid_select, kSelectThreads, 0, ctx->stream>>>(ctx->F, ctx->H, ctx->fr, ctx->n_local, ctx->ctl,
@@ -1136,9 +1136,9 @@ void dist_launch_pass_kernels(di_ctx *ctx, int slot) {
         g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part);
   if (ctx->cap_hub > 0) {
     if (ctx->vals)
-      k_scatter_hubs<true><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
+      k_scatter_hubs<true><<<ctx->grid_hubs, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
     else
-      k_scatter_hubs<false><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
+      k_scatter_hubs<false><<<ctx->grid_hubs, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
   }
   prof_mark(ctx, slot, 2);
   ctx->kernel_launches += ctx->cap_hub > 0 ? 3 : 2;
@@ -1231,7 +1231,7 @@ static di_status dist_run_impl(di_ctx *ctx, double target) {
         // the round's local passes as one captured graph (select, scatter, hubs, finalize)
         CKD(cudaGraphLaunch(ctx->graph_exec, ctx->stream));
         ctx->graph_launches += 1;
-        ctx->kernel_launches += ((ctx->sweep_on ? 2LL : 3LL) + (ctx->cap_hub > 0)) * ctx->check_interval;
+        ctx->kernel_launches += ((ctx->sweep_on ? 2LL : 3LL) + (ctx->cap_hub > 0 && !(ctx->sweep_on && DITER_SWEEP_HUBS))) * ctx->check_interval;
       } else {
         for (int k = 0; k < ctx->check_interval; ++k) {
           dist_launch_pass_kernels(ctx, k);

@@ -140,7 +140,7 @@ static void free_ctx(di_ctx *c) {
   for (cudaEvent_t e : c->prof_ev)
     if (e) cudaEventDestroy(e);
   void *ptrs[] = {c->col_ptr, c->row_idx, c->vals, c->d_b, c->F, c->H, c->fr.ids, c->fr.S, c->fr.seg_cnt, const_cast<unsigned *>(c->fr.dang_bits),
-                  c->fr.hub_w, c->fr.hub_b0, c->fr.hub_deg, c->fr.hub_chunk, c->sel_part, c->sc_part,
+                  c->fr.hub_w, c->fr.hub_b0, c->fr.hub_deg, c->fr.hub_chunk, c->fr.hub_cslot, c->sel_part, c->sc_part,
                   c->l1_part, c->l1_out, c->ctl, c->log, c->far_off, c->far.rows, c->far.vals, c->far.fill, c->kw, c->nloc, c->H_old};
   if (c->stream) cudaStreamSynchronize(c->stream);
   mark("sync");
@@ -203,6 +203,13 @@ static di_status setup_geometry(di_ctx *ctx) {
   // would only zero and flush hot windows (C1: 4 CTAs instead of 444)
   if (!ctx->fused) ctx->grid_scatter = (int)std::max(1LL, std::min<long long>(ctx->grid_scatter, (n + 255) / 256));
   ctx->grid_l1 = (int)std::min<long long>(ctx->num_sms * 8LL, std::max(1LL, (n + 255) / 256));
+  // hub chunks: k_scatter_hubs holds 8-16 edges in flight per thread at 32-48 registers,
+  // so its grid fills every resident CTA slot (DITER_HUB_CTAS_PER_SM caps it; 0 = occupancy)
+  int occ_hub = 0;
+  if (ctx->vals) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_hub, k_scatter_hubs<true>, kScatterThreads, 0));
+  else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_hub, k_scatter_hubs<false>, kScatterThreads, 0));
+  if (DITER_HUB_CTAS_PER_SM > 0) occ_hub = std::min(occ_hub, DITER_HUB_CTAS_PER_SM);
+  ctx->grid_hubs = ctx->num_sms * std::max(1, occ_hub);
   return DI_OK;
 }
 
@@ -481,11 +488,11 @@ void diter_launch_sweep(di_ctx *ctx) {
                     : (ctx->vals ? sweep_fn<true, false>(key) : sweep_fn<false, false>(key));
   sw<<<ctx->grid_sweep, kScatterThreads, kSweepDynSmem, ctx->stream>>>(g, ctx->F, ctx->H, ctx->fr, ctx->ctl,
                                                                        ctx->sel_part, ctx->sc_part, ctx->kw);
-  if (ctx->cap_hub > 0) {
+  if (ctx->cap_hub > 0 && !DITER_SWEEP_HUBS) {
     if (ctx->vals)
-      k_scatter_hubs<true><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
+      k_scatter_hubs<true><<<ctx->grid_hubs, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
     else
-      k_scatter_hubs<false><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
+      k_scatter_hubs<false><<<ctx->grid_hubs, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
   }
 }
 
@@ -536,9 +543,9 @@ di_status diter_capture_graph(di_ctx *ctx) {
           <<<ctx->grid_scatter, kScatterThreads, ctx->scatter_smem, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl, ctx->sc_part);
     if (ctx->cap_hub > 0) {
       if (ctx->vals)
-        k_scatter_hubs<true><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
+        k_scatter_hubs<true><<<ctx->grid_hubs, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
       else
-        k_scatter_hubs<false><<<ctx->grid_scatter, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
+        k_scatter_hubs<false><<<ctx->grid_hubs, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
     }
     if (ctx->far.on)
       k_apply_far<<<ctx->num_sms * 4, kApplyThreads, 0, ctx->stream>>>(ctx->F, ctx->far, ctx->lo, ctx->ctl);
@@ -712,6 +719,12 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
   TRY(dalloc(ctx, &ctx->fr.hub_b0, hc.n_hub));
   TRY(dalloc(ctx, &ctx->fr.hub_deg, hc.n_hub));
   TRY(dalloc(ctx, &ctx->fr.hub_chunk, hc.n_hub));
+  // sweeps: chunk -> slot table (a pass lists each hub at most once: <= nnz/2048 + n_hub chunks)
+  if (hc.n_hub > 0) {
+    const size_t nch = (size_t)(ctx->nnz_local / kHubChunk) + (size_t)hc.n_hub;
+    TRY(dalloc(ctx, &ctx->fr.hub_cslot, nch));
+    CK(cudaMemsetAsync(ctx->fr.hub_cslot, 0, nch * sizeof(unsigned), ctx->stream));
+  }
   // one-kernel async sweeps (options.sweep): one GPU, per-phase launches, no far bins
   // distributed ranks: sweeps for the local passes of ASYNC / P2P rounds (SYNC keeps the
   // snapshot pass, which reproduces the one-GPU pass log)
@@ -868,7 +881,7 @@ extern "C" di_status di_run(di_ctx *ctx, double target) {
       const long long pass_before = h->pass;
       CK(cudaGraphLaunch(ctx->graph_exec, ctx->stream));
       ctx->graph_launches += 1;
-      ctx->kernel_launches += (ctx->sweep_on ? 2LL + (ctx->cap_hub > 0) + (ctx->vals ? 3 : 0)
+      ctx->kernel_launches += (ctx->sweep_on ? 2LL + (ctx->cap_hub > 0 && !DITER_SWEEP_HUBS) + (ctx->vals ? 3 : 0)
                                              : 3LL + (ctx->cap_hub > 0) + (ctx->far.on ? 1 : 0) + (ctx->defer_m ? 2 : 0)) *
                               ctx->check_interval;
       TRY(read_ctl(ctx));

@@ -33,6 +33,8 @@ __device__ __forceinline__ void reset_tickets(Ctl *ctl) {
   for (int k = 0; k < kStripes; ++k) ctl->tickets[32 * k] = 0u;
 #pragma unroll 8
   for (int k = 0; k < kMaxBins; ++k) ctl->far_cnt[32 * k] = 0u;
+  ctl->hub_take = 0u;
+  ctl->spans_done = 0ull;
 }
 
 // ---------------------------------------------------------------- K1 select --
@@ -643,6 +645,80 @@ k_scatter_hubs(Graph g, double *__restrict__ F, Frontier fr, const Ctl *ctl) {
 #define DITER_SWEEP_TAKE_RED 0
 #endif
 constexpr int kSweepItems = DITER_SWEEP_ITEMS;
+
+__device__ __forceinline__ void st_release_gpu_u32(unsigned *p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_gpu_u64(unsigned long long *p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Push hub chunk c (listed this sweep) with the warp's 32 lanes.
+template <bool SIGNED>
+__device__ __forceinline__ void sweep_push_chunk(const Graph &g, const Sink &s, const Frontier &fr, unsigned c) {
+  const unsigned lane = lane_id();
+  long long beg = 0, end = 0;
+  double w = 0.0;
+  if (lane == 0) {
+    unsigned sl;
+    while ((sl = ld_acquire_gpu_u32(fr.hub_cslot + c)) == 0u) __nanosleep(64);
+    --sl;
+    fr.hub_cslot[c] = 0u;           // consumed: the table is all zero again after the sweep
+    w = fr.hub_w[sl];
+    const long long cb = fr.hub_b0[sl], ce = cb + fr.hub_deg[sl];
+    beg = cb + (long long)(c - fr.hub_chunk[sl]) * kHubChunk;
+    end = min(beg + (long long)kHubChunk, ce);
+  }
+  beg = __shfl_sync(0xffffffffu, beg, 0);
+  end = __shfl_sync(0xffffffffu, end, 0);
+  w = __shfl_sync(0xffffffffu, w, 0);
+  push_range<SIGNED>(g, s, beg, end, w, (int)lane, 32);
+}
+
+// Hub columns (> kMidMax edges) selected during a sweep (DITER_SWEEP_HUBS): the taking
+// lane lists the hub's 2048-edge chunks (hub_packed, as for k_scatter_hubs) and publishes
+// each as chunk -> slot + 1; once its stripes are exhausted a warp reports its spans
+// (release) and claims chunks one at a time, pushing each with its 32 lanes
+// (push_range: int4 row loads, the CTA's shared-memory hot window), until every span of
+// the sweep is finished and no listed chunk is left.  Only warps that already hold or
+// finished spans wait, so the wait needs no co-residency of the grid.  The pushes of the
+// hubs thus overlap the sweep's tail instead of following it in a second kernel.
+template <bool SIGNED>
+__device__ __forceinline__ void sweep_drain_hubs(const Graph &g, const Sink &s, const Frontier &fr, Ctl *ctl,
+                                                 unsigned long long my_spans, unsigned long long spans) {
+  const unsigned lane = lane_id();
+  __syncwarp();
+  if (lane == 0) red_release_gpu_u64(&ctl->spans_done, my_spans);
+  for (;;) {
+    unsigned c = 0u;
+    int have = 0;
+    if (lane == 0) c = atomicAdd(&ctl->hub_take, 1u);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    // wait until chunk c is listed, or every span is finished without it
+    if (lane == 0) {
+      for (;;) {
+        if (c < (unsigned)(ld_acquire_gpu_u64(&ctl->hub_packed) & 0xffffffffull)) { have = 1; break; }
+        if (ld_acquire_gpu_u64(&ctl->spans_done) >= spans) {
+          have = c < (unsigned)(ld_acquire_gpu_u64(&ctl->hub_packed) & 0xffffffffull);
+          break;
+        }
+        __nanosleep(200);
+      }
+    }
+    if (!__shfl_sync(0xffffffffu, have, 0)) break;
+    sweep_push_chunk<SIGNED>(g, s, fr, c);
+  }
+}
 constexpr int kSweepSpan = 32 * kSweepItems;
 constexpr int kSweepStage = 32 + kSweepSpan;     // per-warp staging: a partial group + one span
 
@@ -843,8 +919,16 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
           const unsigned long long nch = (unsigned long long)((dpush + kHubChunk - 1) / kHubChunk);
           const unsigned long long old = atomicAdd(&ctl->hub_packed, (1ull << 32) | nch);
           const unsigned sl = (unsigned)(old >> 32);
+          const unsigned c0 = (unsigned)(old & 0xffffffffull);
           fr.hub_w[sl] = wv; fr.hub_b0[sl] = b0; fr.hub_deg[sl] = dpush;
-          fr.hub_chunk[sl] = (unsigned)(old & 0xffffffffull);
+          fr.hub_chunk[sl] = c0;
+#if DITER_SWEEP_HUBS
+          // publish the chunks to the draining warps of this sweep (sweep_drain_hubs): a
+          // release store per chunk orders the slot's fields before it (a fence.acq_rel
+          // instead makes ptxas turn every fire-and-forget REDG of the kernel into ATOMG)
+#pragma unroll 1
+          for (unsigned c = c0; c < c0 + (unsigned)nch; ++c) st_release_gpu_u32(fr.hub_cslot + c, sl + 1u);
+#endif
         }
       }
     }
@@ -891,6 +975,7 @@ k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ct
   const int gw = blockIdx.x * kW + warp;
   const int ns = fr.stripes;
   const int run = fr.run;
+  unsigned long long my_spans = 0;
   for (int k = 0; k < ns; ++k) {
     const int sq = (gw + k) % ns;
     const long long s0 = spans * sq / ns, s1 = spans * (sq + 1) / ns;
@@ -903,6 +988,7 @@ k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ct
         break;
       }
       const long long q1 = min(s1, s0 + (long long)q0 + run);
+      my_spans += (unsigned long long)(q1 - (s0 + (long long)q0));
       // span of the k-th claimed index: ascending, or (odd passes with alternating
       // directions) descending within the stripe
       auto span_of = [&](long long q) { return down ? s1 - 1 - (q - s0) : q; };
@@ -921,6 +1007,9 @@ k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ct
     }
   }
   sweep_flush<SIGNED>(g, s, ctl, st, sg, true);
+#if DITER_SWEEP_HUBS
+  if (fr.hub_cslot) sweep_drain_hubs<SIGNED>(g, s, fr, ctl, my_spans, (unsigned long long)spans);
+#endif
   __syncthreads();
   for (int t = threadIdx.x; t < kHot; t += blockDim.x) {
     const double v = s_hot[t];

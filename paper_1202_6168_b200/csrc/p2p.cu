@@ -668,7 +668,7 @@ di_status p2p_run(di_ctx *ctx, double target) {
     dist_set_target(ctx, 0.0, max_pass_abs);   // local passes never stop on their own
     const bool graph = ctx->graph_exec != nullptr && !ctx->opt.profile;
     bool asleep = false;
-    const int kpp = (ctx->sweep_on ? 2 + 1 : 3) + (ctx->cap_hub > 0 ? 1 : 0) + 3 + (ctx->opt.receive_rescale ? 1 : 0);
+    const int kpp = (ctx->sweep_on ? 2 + 1 : 3) + (ctx->cap_hub > 0 && !(ctx->sweep_on && DITER_SWEEP_HUBS) ? 1 : 0) + 3 + (ctx->opt.receive_rescale ? 1 : 0);
     for (;;) {
       // 1-2. local passes, each after a merge of what has arrived (p2p_pass_merge) --
       //      or, asleep (r_k below this rank's share of the target), only the

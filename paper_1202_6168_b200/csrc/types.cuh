@@ -25,6 +25,12 @@ constexpr int kSelectThreads = 256;
 constexpr int kSelectItems = DITER_SELECT_ITEMS;     // 32-node words per warp iteration
 constexpr int kSelectSpan = 32 * kSelectItems;       // nodes per warp iteration (segment granule)
 constexpr int kScatterThreads = 256;
+#ifndef DITER_HUB_CTAS_PER_SM
+#define DITER_HUB_CTAS_PER_SM 0     // k_scatter_hubs CTAs per SM (0: as many as fit)
+#endif
+#ifndef DITER_SWEEP_HUBS
+#define DITER_SWEEP_HUBS 1          // sweeps push hub chunks inside k_sweep (no k_scatter_hubs launch)
+#endif
 #ifndef DITER_SCATTER_MIN_BLOCKS
 #define DITER_SCATTER_MIN_BLOCKS 3
 #endif
@@ -73,6 +79,10 @@ struct Ctl {
   alignas(128) unsigned tickets[kStripes * 32];
   // far-push chunks opened per destination bin this pass, one counter per 128-byte line
   alignas(128) unsigned far_cnt[kMaxBins * 32];
+  // sweeps with in-kernel hub chunks (DITER_SWEEP_HUBS): chunk claims and spans finished
+  // this pass, each on its own 128-byte line (reset per pass)
+  alignas(128) unsigned hub_take;
+  alignas(128) unsigned long long spans_done;
 };
 
 // k_select partials (one per CTA): r_p and |S_p|.
@@ -148,6 +158,7 @@ struct Frontier {
   long long *hub_b0;
   long long *hub_deg;
   unsigned *hub_chunk;   // first 2048-edge chunk id of the hub (prefix in slot order)
+  unsigned *hub_cslot;   // sweeps: chunk -> hub slot + 1, 0 until published (cleared once pushed)
 };
 
 // Validation + degree census in one pass over the columns.

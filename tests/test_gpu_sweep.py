@@ -44,6 +44,59 @@ def test_sweep_rmat_hubs():
     _check_state(n, cp, ri, None, None, 0.85, H, F, r, target)
 
 
+def _hub_graph(n, seed, hubs):
+    """Uniform graph (out-degree 1..10) whose columns `hubs` (col -> #out) are replaced by
+    hub columns of distinct random rows: every hub is pushed in 2048-edge chunks, the
+    last chunk ragged, some hubs adjacent to each other."""
+    cp, ri = gen.uniform_graph(n, seed)
+    rng = np.random.default_rng(seed)
+    cols = [ri[cp[i]:cp[i + 1]] for i in range(n)]
+    for c, deg in hubs.items():
+        cols[c] = np.sort(rng.choice(n, size=deg, replace=False)).astype(np.int32)
+    lens = np.array([len(x) for x in cols], dtype=np.int64)
+    cp2 = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lens, out=cp2[1:])
+    return cp2, np.concatenate(cols).astype(np.int32)
+
+
+@pytest.mark.parametrize("signed", [False, True])
+def test_sweep_hub_chunks_in_kernel(signed):
+    """Hub columns (> 8192 edges) selected in a sweep: their chunks are listed and pushed
+    inside the sweep kernel by warps whose spans are done.  Many hubs of ragged chunk counts,
+    three solves on one context (di_reset between: the chunk table must come back empty),
+    PageRank and signed P; H vs the oracle's X and the identity on every row each time."""
+    n = 40_000
+    hubs = {0: 30_000, 1: 8_193, 2: 12_288, 5_000: 20_481, 5_001: 9_000, 39_999: 16_384, 20_000: 24_576}
+    cp, ri = _hub_graph(n, 11, hubs)
+    vals = b = None
+    d = 0.85
+    if signed:
+        rng = np.random.default_rng(5)
+        vals = rng.uniform(-1.0, 1.0, size=len(ri))
+        deg = np.diff(cp)
+        colsum = np.add.reduceat(np.abs(vals), cp[:-1][deg > 0])
+        scale = np.zeros(n)
+        scale[deg > 0] = 0.9 / colsum
+        vals *= np.repeat(scale, deg)
+        b = rng.uniform(-1.0, 1.0, size=n)
+        d = 0.9
+    X, P, bn = _xref(n, cp, ri, vals, b, d)
+    target = (5e-10 if signed else 1e-9) * bn
+    ctx = di.di_create(n, cp, ri, vals, b, d, di.default_options(sweep=1, policy=di.DI_POLICY_GEOM))
+    try:
+        for _ in range(3):
+            di.di_reset(ctx)
+            di.di_run(ctx, target)
+            H = di.di_get_history(ctx)
+            F = di.di_get_fluid(ctx)
+            r = di.di_get_residual(ctx)
+            assert di.di_get_pass_log(ctx)["bin_hub"].sum() >= len(hubs)     # every hub diffused
+            assert np.abs(H - X).sum() <= TOL * bn
+            _check_state(n, cp, ri, vals, b, d, H, F, r, target)
+    finally:
+        di.di_destroy(ctx)
+
+
 def test_sweep_signed_and_small():
     n = 30_000
     cp, ri, v, b = gen.signed_system(n, 2)
