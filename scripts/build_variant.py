@@ -17,6 +17,7 @@ if r.returncode:
     sys.exit(r.stderr)
 lines = r.stderr.splitlines()      # register / spill summary of the scatter kernels
 for k, ln in enumerate(lines):
-    if "Compiling entry" in ln and "k_scatter" in ln:
-        print(ln.split("'")[1][:60], *[x.strip() for x in lines[k + 1:k + 4] if "registers" in x or "spill" in x])
+    if "Compiling entry" in ln and ("k_scatter" in ln or "k_sweep" in ln):
+        nm = ln.split("'")[1]
+        print(nm[nm.find("k_s"):][:40], *[x.strip() for x in lines[k + 1:k + 4] if "registers" in x or "spill" in x])
 print(out)

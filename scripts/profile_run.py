@@ -5,6 +5,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import diter_inputs as gen
 import paper_1202_6168_b200 as di
 import bench
+if os.environ.get("DITER_LIB"):
+    di.LIB_PATH = os.environ["DITER_LIB"]   # experiment: another build of the library
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C4")
