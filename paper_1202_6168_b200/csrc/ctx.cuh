@@ -89,7 +89,6 @@ struct di_ctx {
   // far-edge deferral (defer.cu; one GPU, PageRank): nloc = near edges per column
   int defer_m = 0;                // passes between flushes (0 = off)
   int sweep_on = 0;               // one-kernel async sweeps (options.sweep)
-  int sweep_win = 0;              // ... with the local pushes in a shared-memory ring (options.sweep = 2)
   int grid_sweep = 0;
   long long far_edges = 0;        // edges deferred to the flushes
   long long far_flushes = 0;

@@ -303,7 +303,7 @@ static di_status choose_l2_window(di_ctx *ctx) {
   // asynchronous sweeps have no separate streaming select for the set-aside to slow
   // down, so they take larger windows: C4 182.4 -> 178.8 ms at 28 MB, C3 135.6 -> 130.7
   // ms at 36 MB (profiles/r02s_l2_window.txt)
-  const bool sweeps = (ctx->opt.sweep == 1 || ctx->opt.sweep == 2) && !ctx->fused &&
+  const bool sweeps = ctx->opt.sweep == 1 && !ctx->fused &&
                       (!ctx->dist || ctx->opt.exchange_mode != DI_EXCHANGE_SYNC);
   const long long auto_mb = f_bytes <= 2LL * l2 ? (sweeps ? 36 : 28) : (sweeps ? 28 : 20);
   const long long want_rows = ((opt > 0 ? (long long)opt : auto_mb) << 20) / (long long)sizeof(double);
@@ -480,25 +480,14 @@ static int sweep_key_mode(const di_ctx *ctx) {
   return (DITER_SWEEP_KEY_DERIVED && ctx->opt.select_key == DI_KEY_EDGE) ? 2 : 1;
 }
 
-template <bool SIGNED>
-static SweepFn sweep_win_fn(int key) {
-  return key == 0 ? k_sweep_win<SIGNED, 0> : key == 1 ? k_sweep_win<SIGNED, 1> : k_sweep_win<SIGNED, 2>;
-}
-
 void diter_launch_sweep(di_ctx *ctx) {
   const Graph g = diter_graph(ctx);
   const bool dist = ctx->dist != nullptr;
   const int key = sweep_key_mode(ctx);
-  if (ctx->sweep_win) {       // options.sweep = 2: local pushes in a shared-memory ring (one GPU)
-    SweepFn sw = ctx->vals ? sweep_win_fn<true>(key) : sweep_win_fn<false>(key);
-    sw<<<ctx->grid_sweep, kScatterThreads, kSweepWinDynSmem, ctx->stream>>>(g, ctx->F, ctx->H, ctx->fr, ctx->ctl,
-                                                                            ctx->sel_part, ctx->sc_part, ctx->kw);
-    return;
-  }
   SweepFn sw = dist ? (ctx->vals ? sweep_fn<true, true>(key) : sweep_fn<false, true>(key))
                     : (ctx->vals ? sweep_fn<true, false>(key) : sweep_fn<false, false>(key));
-  sw<<<ctx->grid_sweep, kScatterThreads, kSweepDynSmem + (DITER_EXP_FAKE_RING ? 8 * kWinRing : 0), ctx->stream>>>(
-      g, ctx->F, ctx->H, ctx->fr, ctx->ctl, ctx->sel_part, ctx->sc_part, ctx->kw);
+  sw<<<ctx->grid_sweep, kScatterThreads, kSweepDynSmem, ctx->stream>>>(g, ctx->F, ctx->H, ctx->fr, ctx->ctl,
+                                                                       ctx->sel_part, ctx->sc_part, ctx->kw);
   if (ctx->cap_hub > 0 && !DITER_SWEEP_HUBS) {
     if (ctx->vals)
       k_scatter_hubs<true><<<ctx->grid_hubs, kScatterThreads, 0, ctx->stream>>>(g, ctx->F, ctx->fr, ctx->ctl);
@@ -740,14 +729,10 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
   // distributed ranks: sweeps for the local passes of ASYNC / P2P rounds (SYNC keeps the
   // snapshot pass, which reproduces the one-GPU pass log)
   const bool dist_sweepable = ctx->dist && (o.exchange_mode == DI_EXCHANGE_ASYNC || o.exchange_mode == DI_EXCHANGE_P2P);
-  ctx->sweep_on = ((o.sweep == 1 || o.sweep == 2) && (!ctx->dist || dist_sweepable) && !ctx->fused && !ctx->far.on) ? 1 : 0;
-  ctx->sweep_win = (ctx->sweep_on && o.sweep == 2 && !ctx->dist) ? 1 : 0;
+  ctx->sweep_on = (o.sweep == 1 && (!ctx->dist || dist_sweepable) && !ctx->fused && !ctx->far.on) ? 1 : 0;
   if (ctx->sweep_on) {
     // per-warp staging in dynamic shared memory (beyond the default 48 KB with the hot window)
-    auto attr = [&](const void *fn) {
-      return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kSweepDynSmem + (DITER_EXP_FAKE_RING ? 8 * kWinRing : 0));
-    };
+    auto attr = [&](const void *fn) { return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepDynSmem); };
     for (int key = 0; key < 3; ++key) {
       CK(attr((const void *)sweep_fn<false, false>(key)));
       CK(attr((const void *)sweep_fn<true, false>(key)));
@@ -755,23 +740,9 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
       CK(attr((const void *)sweep_fn<true, true>(key)));
     }
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep<false, 1>, kScatterThreads,
-                                                     kSweepDynSmem + (DITER_EXP_FAKE_RING ? 8 * kWinRing : 0)));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep<false, 1>, kScatterThreads, kSweepDynSmem));
     ctx->grid_sweep = (int)std::max(1LL, std::min<long long>((long long)ctx->num_sms * std::max(1, occ),
                                                              (n + kSweepSpan - 1) / kSweepSpan));
-    if (ctx->sweep_win) {
-      auto wattr = [&](const void *fn) {
-        return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepWinDynSmem);
-      };
-      for (int key = 0; key < 3; ++key) {
-        CK(wattr((const void *)sweep_win_fn<false>(key)));
-        CK(wattr((const void *)sweep_win_fn<true>(key)));
-      }
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep_win<false, 1>, kScatterThreads, kSweepWinDynSmem));
-      const long long tile = (long long)(kScatterThreads / 32) * kSweepSpan;
-      ctx->grid_sweep = (int)std::max(1LL, std::min<long long>((long long)ctx->num_sms * std::max(1, occ),
-                                                               (n + tile - 1) / tile));
-    }
   }
   if (!ctx->sweep_on) TRY(diter_setup_defer(ctx));
   tr.mark(ctx->stream, "far-edge deferral");

@@ -171,35 +171,6 @@ __device__ __forceinline__ void push(const Sink &s, int row, double v) {
   }
 }
 
-// Windowed sweeps (k_sweep_win): a CTA scans consecutive tiles of nodes and keeps a ring of
-// kWinRing rows of F around its current tile in shared memory; a push whose row lies in the
-// warp's safe window [lo, lo + kWinSafe) is a shared-memory add (its own pipe: the SM's
-// path of REDs into L2 is what binds the sweep, scripts/micro/l2req_bench.cu), every other
-// push is the RED of `push`.  One GPU only (rows are local ids).
-#ifndef DITER_EXP_FAKE_RING
-#define DITER_EXP_FAKE_RING 0
-#endif
-#ifndef DITER_WIN_RING
-#define DITER_WIN_RING 4096
-#endif
-constexpr int kWinRing = DITER_WIN_RING;       // rows of F held per CTA (power of two)
-struct Win {
-  double *ring;        // [kWinRing] shared memory, slot = row & (kWinRing - 1)
-  int lo;              // first row of the safe window (may be negative at the first tiles)
-  unsigned safe;       // rows in the safe window
-};
-
-__device__ __forceinline__ void push_w(const Sink &s, const Win &wn, int row, double v) {
-  const unsigned h = (unsigned)row - (unsigned)s.hot_lo;
-  if (h < (unsigned)kHot) {
-    atomicAdd(s.s_hot + h, v);
-  } else if ((unsigned)(row - wn.lo) < wn.safe) {
-    atomicAdd(wn.ring + (row & (kWinRing - 1)), v);
-  } else {
-    red_add(s.F + row, v);
-  }
-}
-
 __device__ __forceinline__ int ld_row(const int *p) { return __ldcs(p); }
 __device__ __forceinline__ int4 ld_row4(const int4 *p) { return __ldcs(p); }
 __device__ __forceinline__ double ld_val(const double *p) { return __ldcs(p); }
@@ -323,9 +294,9 @@ __device__ __noinline__ void flush_stage(const Far far, Ctl *ctl, const Sink s, 
   __syncwarp();
 }
 
-template <bool SIGNED, bool FAR = false, bool WIN = false>
+template <bool SIGNED, bool FAR = false>
 __device__ __forceinline__ void push_group(const Graph &g, const Sink &s, Ctl *ctl, int *st, long long b0, int deg,
-                                           double w, int nlo, int nhi, Stage &sg, const Win wn = Win{nullptr, 0, 0u}) {
+                                           double w, int nlo, int nhi, Stage &sg) {
   const unsigned lane = lane_id();
   int incl = deg;
 #pragma unroll
@@ -355,11 +326,7 @@ __device__ __forceinline__ void push_group(const Graph &g, const Sink &s, Ctl *c
       rows[u] = ok ? ld_row(g.row_idx + ei) : -1;
       vals[u] = ok ? (SIGNED ? ow * ld_val(g.vals + ei) : ow) : 0.0;
     }
-    if constexpr (WIN) {
-#pragma unroll
-      for (int u = 0; u < kGroupUnroll; ++u)
-        if (rows[u] >= 0) push_w(s, wn, rows[u], vals[u]);
-    } else if constexpr (!FAR) {
+    if constexpr (!FAR) {
 #pragma unroll
       for (int u = 0; u < kGroupUnroll; ++u)
         if (rows[u] >= 0) push(s, rows[u], vals[u]);
@@ -765,17 +732,17 @@ struct SweepStage {
   int cnt;     // warp-uniform fill
 };
 
-template <bool SIGNED, bool WIN = false>
+template <bool SIGNED>
 __device__ __forceinline__ void sweep_flush(const Graph &g, const Sink &s, Ctl *ctl, SweepStage &st, Stage &sg,
-                                            bool all, const Win wn = Win{nullptr, 0, 0u}) {
+                                            bool all) {
   const unsigned lane = lane_id();
   int done = 0;
   while (st.cnt - done >= 32 || (all && st.cnt - done > 0)) {
     __syncwarp();
     const int e = done + (int)lane;
     const bool ok = e < st.cnt;
-    push_group<SIGNED, false, WIN>(g, s, ctl, nullptr, ok ? st.b0[e] : 0, ok ? st.deg[e] : 0, ok ? st.w[e] : 0.0, 0, 0,
-                                   sg, wn);
+    push_group<SIGNED, false>(g, s, ctl, nullptr, ok ? st.b0[e] : 0, ok ? st.deg[e] : 0, ok ? st.w[e] : 0.0, 0, 0,
+                              sg);
     done += 32;
   }
   if (done > 0) {
@@ -837,13 +804,12 @@ __device__ __forceinline__ void sweep_prefetch(const Graph &g, const double *F, 
 // per-edge key 1/(#out_i + 1) derived from the span's col_ptr values (fp32 reciprocal
 // rounded to nearest -- no weight stream; sweeps are not compared with the oracle's
 // snapshot log, so the weight's last-bit rounding is free)
-template <bool SIGNED, int KEY, bool PF, bool DIST, bool WIN = false>
+template <bool SIGNED, int KEY, bool PF, bool DIST>
 __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double *__restrict__ F,
                                            double *__restrict__ H, const Frontier &fr, Ctl *ctl,
                                            const float *__restrict__ kw, double T, long long base,
                                            ScAcc &acc, int &sel_all, double &dloss, int &dang_cnt,
-                                           SweepStage &st, const SweepPf &pf, long long next_base,
-                                           double *ring = nullptr) {
+                                           SweepStage &st, const SweepPf &pf, long long next_base) {
   const unsigned lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
   double f[kSweepItems];
@@ -896,9 +862,7 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
 #pragma unroll
   for (int k = 0; k < kSweepItems; ++k) {
     const long long i = base + 32 * k + lane;
-    // windowed sweeps: fluid of node i still in the CTA's ring counts for the key and is
-    // taken with F_i (it never reaches global memory when i is diffused in this sweep)
-    const double af = (WIN && i < g.n) ? fabs(f[k] + ring[(int)i & (kWinRing - 1)]) : fabs(f[k]);
+    const double af = fabs(f[k]);
     const double key = KEY == 0 ? af
                      : KEY == 1 ? af * (double)w[k]
                                 : af * (double)__frcp_rn((float)dg[k] + 1.0f);
@@ -909,12 +873,8 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
     // so fluid pushed after the load stays (exact up to the RED's rounding)
     if (sel) red_add(F + i, -f[k]);
 #else
-    if (sel) {                                               // s_i
+    if (sel)                                                 // s_i
       f[k] = __longlong_as_double((long long)atomicExch(reinterpret_cast<unsigned long long *>(F + i), 0ull));
-      if (WIN)
-        f[k] += __longlong_as_double((long long)atomicExch(
-            reinterpret_cast<unsigned long long *>(ring + ((int)i & (kWinRing - 1))), 0ull));
-    }
 #endif
   }
 #pragma unroll
@@ -1005,12 +965,6 @@ k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ct
              reinterpret_cast<unsigned *>(pfb + 2 * kSweepSpan + 1) + kSweepSpan};
   const Sink s{F, s_hot, g.hot_lo, g.lo, g.n, DIST ? g.G : nullptr, DIST ? g.dflags : nullptr};
   Stage sg{nullptr, nullptr, 0};
-#if DITER_EXP_FAKE_RING
-  // EXPERIMENT (wrong results): pushes near the span go to a shared-memory ring that is never flushed
-  double *x_ring = s_dyn + 2 * kW * kSweepStage + (kW * kSweepStage + 1) / 2 + kW * kSweepPfWords;
-  for (int t = threadIdx.x; t < kWinRing; t += blockDim.x) x_ring[t] = 0.0;
-  __syncthreads();
-#endif
   const double T = ctl->T;
   const unsigned lane = lane_id();
   ScAcc acc;
@@ -1043,11 +997,7 @@ k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ct
         for (long long q = s0 + q0; q < q1; ++q) {
           sweep_span<SIGNED, KEY, true, DIST>(g, s, F, H, fr, ctl, kw, T, span_of(q) * kSweepSpan, acc, sel_all,
                                               dloss, dang_cnt, st, pf, q + 1 < q1 ? span_of(q + 1) * kSweepSpan : -1);
-#if DITER_EXP_FAKE_RING
-          sweep_flush<SIGNED, true>(g, s, ctl, st, sg, false, Win{x_ring, (int)(span_of(q) * kSweepSpan) - 1152, 2432u});
-#else
           sweep_flush<SIGNED>(g, s, ctl, st, sg, false);
-#endif
         }
       } else {
         sweep_span<SIGNED, KEY, false, DIST>(g, s, F, H, fr, ctl, kw, T, span_of(s0 + q0) * kSweepSpan, acc, sel_all,
@@ -1097,190 +1047,6 @@ k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ct
     sp[blockIdx.x] = q;
   }
 }
-// ---------------------------------------------------- K1+K2 windowed sweep --
-// options.sweep = 2 (one GPU): the asynchronous sweep of k_sweep with the +-1024-local
-// pushes kept out of L2.  What binds k_sweep is the SM's path of atomics into L2: ~0.78
-// RED lanes per clock per SM whatever the address pattern (~190-230 G lanes/s on the chip),
-// while shared-memory fp64 adds run beside it at full rate (scripts/micro/l2req_bench.cu:
-// 193 G REDs/s alone, 217 G REDs/s + 217 G shared adds/s together).  So a CTA scans
-// consecutive tiles of kW spans (one span per warp) of a chunk of `fr.run` tiles claimed
-// from a ticket, and keeps a ring of kWinRing rows of F around its tile in shared memory:
-//   * a push into the warp's safe window (the blocks its tile can reach with local edges,
-//     [X - RB, X + RB] for tile X) is a shared-memory add, any other push a RED;
-//   * a node is taken as F_i + ring_i (two exchanges): fluid pushed to a node ahead in the
-//     same chunk is diffused in the same sweep without ever reaching global memory;
-//   * block b (the rows of tile b) is final once tiles <= b + RB are finished: the last warp
-//     to finish tile b + RB adds its non-zero rows to F (REDs) and clears it, and publishes
-//     b; a warp starts tile X only when block X + RB - NB has been published (its ring slots
-//     are those of block X + RB), so warps run up to NB - 2 RB - 1 tiles apart with no CTA
-//     barrier inside a chunk.  Arrival / publish / wait are acq_rel / release / acquire
-//     operations on shared memory (a fence would make ptxas turn the REDs into ATOMGs).
-// Same limit X, same partials and bound as k_sweep; the pass log is per sweep.
-template <int TN>
-struct WinGeom {
-  static constexpr int kReach = 1024;                        // rows a local edge can span
-  static constexpr int RB = (kReach + TN - 1) / TN;          // blocks a tile reaches each way
-  static constexpr int NB = kWinRing / TN;                   // blocks in the ring
-  static_assert(kWinRing % TN == 0 && (NB & (NB - 1)) == 0, "ring = power-of-two number of tiles");
-  static_assert(NB >= 2 * RB + 2, "ring too small for one tile of slack");
-};
-__device__ __forceinline__ unsigned atom_add_acq_rel_cta_shared(unsigned *p, unsigned v) {
-  unsigned old;
-  asm volatile("atom.acq_rel.cta.shared.add.u32 %0, [%1], %2;"
-               : "=r"(old) : "r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
-  return old;
-}
-__device__ __forceinline__ void st_release_cta_shared(int *p, int v) {
-  asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
-}
-__device__ __forceinline__ int ld_acquire_cta_shared(const int *p) {
-  int v;
-  asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
-  return v;
-}
-// add the non-zero rows [r0, r1) of the ring to F and clear them (rows outside [0, n) hold nothing)
-__device__ __forceinline__ void win_flush_rows(double *__restrict__ F, double *ring, long long r0, long long r1,
-                                               long long n, int t, int nt) {
-  if (r0 < 0) r0 = 0;
-  if (r1 > n) r1 = n;
-  for (long long r = r0 + t; r < r1; r += nt) {
-    const int slot = (int)r & (kWinRing - 1);
-    const double v = ring[slot];
-    if (v != 0.0) {
-      red_add(F + r, v);
-      ring[slot] = 0.0;
-    }
-  }
-}
-
-template <bool SIGNED, int KEY>
-__global__ void __launch_bounds__(kScatterThreads, DITER_SWEEP_MIN_BLOCKS)
-k_sweep_win(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ctl *ctl,
-            SelPartial *__restrict__ sp, ScPartial *__restrict__ part, const float *__restrict__ kw) {
-  if (ctl->done) return;
-  constexpr int kW = kScatterThreads / 32;
-  constexpr int TN = kW * kSweepSpan;                        // rows per tile = per block
-  using Geo = WinGeom<TN>;
-  constexpr int RB = Geo::RB, NB = Geo::NB;
-  __shared__ double s_hot[kHot];
-  __shared__ unsigned s_cnt[NB];
-  __shared__ int s_flushed;
-  __shared__ unsigned s_chunk;
-  extern __shared__ double s_dyn_all[];   // the ring, then per-warp staging and prefetch buffers (as k_sweep)
-  double *s_ring = s_dyn_all;
-  double *s_dyn = s_dyn_all + kWinRing;
-  for (int t = threadIdx.x; t < kHot; t += blockDim.x) s_hot[t] = 0.0;
-  for (int t = threadIdx.x; t < kWinRing; t += blockDim.x) s_ring[t] = 0.0;
-  const int warp = threadIdx.x >> 5;
-  SweepStage st;
-  st.w = s_dyn + warp * kSweepStage;
-  st.b0 = reinterpret_cast<long long *>(s_dyn + kW * kSweepStage) + warp * kSweepStage;
-  st.deg = reinterpret_cast<int *>(s_dyn + 2 * kW * kSweepStage) + warp * kSweepStage;
-  st.cnt = 0;
-  double *pfb = s_dyn + 2 * kW * kSweepStage + (kW * kSweepStage + 1) / 2 + warp * kSweepPfWords;
-  SweepPf pf{pfb, reinterpret_cast<long long *>(pfb + kSweepSpan), reinterpret_cast<float *>(pfb + 2 * kSweepSpan + 1),
-             reinterpret_cast<unsigned *>(pfb + 2 * kSweepSpan + 1) + kSweepSpan};
-  const Sink s{F, s_hot, g.hot_lo, g.lo, g.n, nullptr, nullptr};
-  Stage sg{nullptr, nullptr, 0};
-  const double T = ctl->T;
-  const unsigned lane = lane_id();
-  ScAcc acc;
-  int sel_all = 0, dang_cnt = 0;
-  double dloss = 0.0;
-  const long long n = g.n;
-  const long long spans = (n + kSweepSpan - 1) / kSweepSpan;
-  const int chunk_tiles = max(1, fr.run);
-  const long long chunk_rows = (long long)chunk_tiles * TN;
-  const long long n_chunks = (n + chunk_rows - 1) / chunk_rows;
-  unsigned long long my_spans = 0;
-  for (;;) {
-    __syncthreads();                   // the previous chunk's ring is flushed and clear
-    if (threadIdx.x == 0) {
-      s_chunk = atomicAdd(&ctl->tickets[0], 1u);
-      s_flushed = -RB - 1;
-      for (int k = 0; k < NB; ++k) s_cnt[k] = 0u;
-    }
-    __syncthreads();
-    const long long c = (long long)s_chunk;
-    if (c >= n_chunks) break;
-    const long long chunk_lo = c * chunk_rows;
-    const int nt = (int)min((long long)chunk_tiles, (n - chunk_lo + TN - 1) / TN);
-    const long long base0 = chunk_lo + (long long)warp * kSweepSpan;
-    if (base0 < n) sweep_prefetch<KEY>(g, F, kw, fr, base0, pf);
-    for (int X = 0; X < nt; ++X) {
-      // the ring slots of block X + RB were block X + RB - NB's: wait until that is flushed
-      const int need = X + RB - NB;
-      if (need > -RB - 1) {
-        if (lane == 0)
-          while (ld_acquire_cta_shared(&s_flushed) < need) __nanosleep(40);
-        __syncwarp();
-      }
-      const long long base = base0 + (long long)X * TN;
-      const Win wn{s_ring, (int)(chunk_lo + (long long)(X - RB) * TN), (unsigned)((2 * RB + 1) * TN)};
-      if (base < n) {
-        my_spans += 1;
-        const long long nb = base + TN;
-        sweep_span<SIGNED, KEY, true, false, true>(g, s, F, H, fr, ctl, kw, T, base, acc, sel_all, dloss, dang_cnt, st,
-                                                   pf, (X + 1 < nt && nb < n) ? nb : -1, s_ring);
-      }
-      // staged nodes are pushed within the safe window of the tile the warp is in; what is
-      // left staged at the chunk's last tile goes before the warp reports it
-      sweep_flush<SIGNED, true>(g, s, ctl, st, sg, X + 1 == nt, wn);
-      __syncwarp();
-      int last = 0;
-      if (lane == 0) last = atom_add_acq_rel_cta_shared(&s_cnt[X & (NB - 1)], 1u) == (unsigned)(kW - 1);
-      last = __shfl_sync(0xffffffffu, last, 0);
-      __syncwarp();
-      if (last) {
-        // tile X is finished by every warp: block X - RB can receive nothing more
-        if (lane == 0) s_cnt[X & (NB - 1)] = 0u;
-        const long long r0 = chunk_lo + (long long)(X - RB) * TN;
-        win_flush_rows(F, s_ring, r0, r0 + TN, n, (int)lane, 32);
-        __syncwarp();
-        if (lane == 0) st_release_cta_shared(&s_flushed, X - RB);
-      }
-    }
-    __syncthreads();                   // every tile finished, block nt - 1 - RB flushed
-    {
-      const long long r0 = chunk_lo + (long long)(nt - RB) * TN;
-      win_flush_rows(F, s_ring, r0, r0 + (long long)(2 * RB) * TN, n, (int)threadIdx.x, (int)blockDim.x);
-    }
-  }
-#if DITER_SWEEP_HUBS
-  if (fr.hub_cslot) sweep_drain_hubs<SIGNED>(g, s, fr, ctl, my_spans, (unsigned long long)spans);
-#endif
-  __syncthreads();
-  for (int t = threadIdx.x; t < kHot; t += blockDim.x) {
-    const double v = s_hot[t];
-    if (v != 0.0) red_add(F + (g.hot_lo - g.lo) + t, v);
-  }
-  acc.loss = warp_sum(acc.loss);
-  acc.edges = warp_sum(acc.edges);
-  acc.lo = warp_sum(acc.lo);
-  acc.mi = warp_sum(acc.mi);
-  acc.hu = warp_sum(acc.hu);
-  dloss = warp_sum(dloss);
-  dang_cnt = warp_sum(dang_cnt);
-  __shared__ ScAcc s_acc[kW];
-  __shared__ double s_dl[kW];
-  __shared__ int s_sel[kW], s_dc[kW];
-  if (lane == 0) {
-    s_acc[warp] = acc; s_dl[warp] = dloss;
-    s_sel[warp] = sel_all; s_dc[warp] = dang_cnt;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    ScPartial p{0.0, 0, 0, 0, 0, 0, 0.0};
-    SelPartial q{0.0, 0, 0.0, 0};
-    for (int k = 0; k < kW; ++k) {
-      p.loss += s_acc[k].loss; p.edges += s_acc[k].edges;
-      p.n_low += s_acc[k].lo; p.n_mid += s_acc[k].mi; p.n_hub += s_acc[k].hu;
-      q.cnt += s_sel[k]; q.loss += s_dl[k]; q.dang += s_dc[k];
-    }
-    part[blockIdx.x] = p;
-    sp[blockIdx.x] = q;
-  }
-}
 // Signed P under sweeps: the carried bound r - sum (1 - d)|s_i| ignores the
 // cancellation of signed pushes and can stay far above |F|_1, so after every sweep
 // the exact |F|_1 (k_l1_partial / k_l1_final into *l1) replaces it when smaller
@@ -1301,8 +1067,6 @@ __global__ void k_rpred_set(Ctl *ctl, const double *l1) { ctl->r_pred = *l1; }
 constexpr size_t kSweepDynSmem = sizeof(double) * ((size_t)2 * (kScatterThreads / 32) * kSweepStage +
                                                    ((kScatterThreads / 32) * kSweepStage + 1) / 2 +
                                                    (size_t)(kScatterThreads / 32) * kSweepPfWords);
-
-constexpr size_t kSweepWinDynSmem = kSweepDynSmem + sizeof(double) * (size_t)kWinRing;
 
 // ------------------------------------------------------- K4b far-push apply --
 // Opened chunks of every bin, bins in ascending order (prefix of the chunk

@@ -18,33 +18,28 @@ from test_gpu_parity import TOL, _check_state, _gpu, _xref
 pytestmark = pytest.mark.gpu
 
 
-SWEEPS = [1, 2]      # 1: k_sweep; 2: k_sweep_win (local pushes in a shared-memory ring)
-
-
-@pytest.mark.parametrize("sweep", SWEEPS)
 @pytest.mark.parametrize("key", [0, 1, 2])
 @pytest.mark.parametrize("policy", [di.DI_POLICY_GEOM, di.DI_POLICY_HYBRID])
-def test_sweep_web(key, policy, sweep):
+def test_sweep_web(key, policy):
     n = 150_001
     cp, ri = gen.web_graph(n, 2, gen.XMIN_C4)
     X, P, bn = _xref(n, cp, ri)
     target = 1e-9 * bn
-    H, F, log, r, st = _gpu(n, cp, ri, target, sweep=sweep, select_key=key, policy=policy, alpha=2.0,
+    H, F, log, r, st = _gpu(n, cp, ri, target, sweep=1, select_key=key, policy=policy, alpha=2.0,
                             hybrid_frac=0.5)
     assert np.abs(H - X).sum() <= TOL * bn
     _check_state(n, cp, ri, None, None, 0.85, H, F, r, target)
     assert st["edges"] == log["edges"].sum() and st["passes"] == len(log)
 
 
-@pytest.mark.parametrize("sweep", SWEEPS)
-def test_sweep_rmat_hubs(sweep):
+def test_sweep_rmat_hubs():
     """R-MAT scale 16 (columns > 8192 edges go through the hub kernel after the sweep)."""
     src, dst = gen.rmat_coo(16, 1)
     n = 1 << 16
     cp, ri = di.di_csc_from_coo(n, src, dst)
     X, P, bn = _xref(n, cp, ri)
     target = 1e-9 * bn
-    H, F, log, r, st = _gpu(n, cp, ri, target, sweep=sweep, select_key=1)
+    H, F, log, r, st = _gpu(n, cp, ri, target, sweep=1, select_key=1)
     assert np.abs(H - X).sum() <= TOL * bn
     _check_state(n, cp, ri, None, None, 0.85, H, F, r, target)
 
@@ -64,9 +59,8 @@ def _hub_graph(n, seed, hubs):
     return cp2, np.concatenate(cols).astype(np.int32)
 
 
-@pytest.mark.parametrize("sweep", SWEEPS)
 @pytest.mark.parametrize("signed", [False, True])
-def test_sweep_hub_chunks_in_kernel(signed, sweep):
+def test_sweep_hub_chunks_in_kernel(signed):
     """Hub columns (> 8192 edges) selected in a sweep: their chunks are listed and pushed
     inside the sweep kernel by warps whose spans are done.  Many hubs of ragged chunk counts,
     three solves on one context (di_reset between: the chunk table must come back empty),
@@ -88,7 +82,7 @@ def test_sweep_hub_chunks_in_kernel(signed, sweep):
         d = 0.9
     X, P, bn = _xref(n, cp, ri, vals, b, d)
     target = (5e-10 if signed else 1e-9) * bn
-    ctx = di.di_create(n, cp, ri, vals, b, d, di.default_options(sweep=sweep, policy=di.DI_POLICY_GEOM))
+    ctx = di.di_create(n, cp, ri, vals, b, d, di.default_options(sweep=1, policy=di.DI_POLICY_GEOM))
     try:
         for _ in range(3):
             di.di_reset(ctx)
@@ -103,20 +97,19 @@ def test_sweep_hub_chunks_in_kernel(signed, sweep):
         di.di_destroy(ctx)
 
 
-@pytest.mark.parametrize("sweep", SWEEPS)
-def test_sweep_signed_and_small(sweep):
+def test_sweep_signed_and_small():
     n = 30_000
     cp, ri, v, b = gen.signed_system(n, 2)
     X, P, bn = _xref(n, cp, ri, v, b, 0.9)
     target = 5e-10 * bn
-    H, F, log, r, st = _gpu(n, cp, ri, target, vals=v, b=b, d=0.9, sweep=sweep)
+    H, F, log, r, st = _gpu(n, cp, ri, target, vals=v, b=b, d=0.9, sweep=1)
     assert np.abs(H - X).sum() <= TOL * bn
     _check_state(n, cp, ri, v, b, 0.9, H, F, r, target)
     for n in (1, 33, 257, 1000):
         cp, ri = gen.uniform_graph(max(n, 2), 3)
         n = max(n, 2)
         X, P, bn = _xref(n, cp, ri)
-        H, F, log, r, st = _gpu(n, cp, ri, 1e-12, sweep=sweep)
+        H, F, log, r, st = _gpu(n, cp, ri, 1e-12, sweep=1)
         assert np.abs(H - X).sum() <= TOL * bn
         _check_state(n, cp, ri, None, None, 0.85, H, F, r, 1e-12)
 
@@ -166,17 +159,3 @@ def test_sweep_max_passes_and_checkpoint():
         di.di_destroy(ctx)
         assert np.abs(H2 - X).sum() <= TOL * bn
         _check_state(n, cp, ri, None, None, 0.85, H2, F2, r2, target)
-
-
-@pytest.mark.parametrize("run", [1, 3, 16])
-@pytest.mark.parametrize("n", [700, 5_000, 150_001])
-def test_sweep_win_chunks(n, run):
-    """Windowed sweeps (options.sweep = 2): chunks of `scatter_run` tiles -- a graph smaller
-    than a tile, ragged last tiles and chunks, chunk boundaries crossed by local edges; the
-    ring must be flushed completely at every chunk end (identity on every row)."""
-    cp, ri = gen.web_graph(n, 7, gen.XMIN_C4)
-    X, P, bn = _xref(n, cp, ri)
-    target = 1e-9 * bn
-    H, F, log, r, st = _gpu(n, cp, ri, target, sweep=2, select_key=2, scatter_run=run)
-    assert np.abs(H - X).sum() <= TOL * bn
-    _check_state(n, cp, ri, None, None, 0.85, H, F, r, target)
