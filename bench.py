@@ -131,6 +131,11 @@ def parse():
                     help="edge-balanced contiguous ranges by out-edges (default: with remote edges "
                          "pushed by the senders as H increments, receiving is a cheap merge; "
                          "scripts/exp_scaling_model.py) or by in+out edges")
+    ap.add_argument("--pilot-solves", type=int, default=0,
+                    help="N > 1: untimed pilot solves before the warm-up; after each, the ranges are "
+                         "re-balanced by the ranks' measured diffusion work (dist.partition_bounds_measured, "
+                         "the paper's adaptation of the sets Omega_k applied between solves) and the "
+                         "contexts are rebuilt on the new ranges")
     a = ap.parse_args()
     if a.round_passes is None:
         a.round_passes = 2 if a.exchange == "p2p" else 4
@@ -173,7 +178,8 @@ def graph_residency(p, world=1):
 def bench_config(args, p, pol, world, resident, flushed):
     """The workload description both arms print (the reference arm times the oracle on
     this same configuration)."""
-    par = "dp1" if world == 1 else (f"node-partition x{world} ({args.partition}-balanced ranges, {args.exchange} exchange, "
+    par = "dp1" if world == 1 else (f"node-partition x{world} ({args.partition}-balanced ranges"
+                                    f"{', re-balanced by %d pilot solves' % args.pilot_solves if args.pilot_solves else ''}, {args.exchange} exchange, "
                                     f"rounds every {args.round_passes} passes, remote edges "
                                     f"{'as H increments' if args.remote_push else 'per diffusion'})")
     return {"workload": WORKLOADS[args.config], "n": p.n, "nnz": p.nnz,
@@ -431,6 +437,22 @@ def run_ours(args, rank, world, local_rank):
     t = time.perf_counter()
     ctx = make_ctx(args, p, opts, di, rank, world, comm_id, bounds, shard)
     log(f"[bench] rank {rank} create {time.perf_counter() - t:.2f}s")
+    for it in range(args.pilot_solves if dist else 0):
+        # pilot solve on the current ranges; every rank derives the same new bounds from
+        # the gathered work (pushes performed: dist.pushes_performed)
+        torch.distributed.barrier()
+        di.di_run(ctx, p.stop)
+        s = di.di_get_stats(ctx)
+        rho = dd.remote_fraction(shard[1], int(bounds[rank]), int(bounds[rank + 1]))
+        mine = torch.tensor([dd.pushes_performed(s, rho, args.remote_push)], dtype=torch.float64, device="cuda")
+        works = [torch.zeros_like(mine) for _ in range(world)]
+        torch.distributed.all_gather(works, mine)
+        di.di_destroy(ctx)
+        bounds = dd.partition_bounds_measured(p.col_ptr, world, bounds, [float(w.item()) for w in works])
+        comm_id = dd.nccl_comm_id()
+        shard = dd.shard_csc(p.col_ptr, p.row_idx, p.values, p.b, bounds, rank)
+        ctx = make_ctx(args, p, opts, di, rank, world, comm_id, bounds, shard)
+        log(f"[bench] rank {rank} pilot {it + 1}: bounds {[int(b) for b in bounds]}")
     resident, flushed = graph_residency(p, world)
     flush = None
     if flushed:

@@ -147,6 +147,9 @@ k_select(double *__restrict__ F, double *__restrict__ H, Frontier fr, long long 
 // to the remote outbox G (global ids, RED) and mark their 32-row block dirty
 // (an idempotent byte store), to be compacted and shipped at the exchange
 // (algorithm (*) P:237-246 made exact by outboxing).
+#ifndef DITER_PUSH_LOCAL_FOLD
+#define DITER_PUSH_LOCAL_FOLD 0
+#endif
 struct Sink {
   double *F;            // local fluid, index row - lo
   double *s_hot;
@@ -162,7 +165,13 @@ __device__ __forceinline__ void push(const Sink &s, int row, double v) {
     atomicAdd(s.s_hot + h, v);
   } else {
     const long long lr = (long long)row - s.lo;
+#if DITER_PUSH_LOCAL_FOLD
+    // a context without an outbox (one GPU: G is a compile-time nullptr after inlining)
+    // owns every row (validated at create), so the range test and the outbox path fold away
+    if (s.G == nullptr || (unsigned long long)lr < (unsigned long long)s.n_local) {
+#else
     if ((unsigned long long)lr < (unsigned long long)s.n_local) {
+#endif
       red_add(s.F + lr, v);
     } else {
       red_add(s.G + row, v);
@@ -216,6 +225,9 @@ __device__ __forceinline__ void push_range(const Graph &g, const Sink &s, long l
 #define DITER_GROUP_UNROLL 7
 #endif
 constexpr int kGroupUnroll = DITER_GROUP_UNROLL;
+#ifndef DITER_GROUP_TRIM
+#define DITER_GROUP_TRIM 0
+#endif
 
 // Far push (see Far in types.cuh).  Lanes with the same bin are aggregated by
 // __match_any_sync; the lowest lane of each bin group appends the group to this
@@ -312,6 +324,10 @@ __device__ __forceinline__ void push_group(const Graph &g, const Sink &s, Ctl *c
 #pragma unroll
     for (int u = 0; u < kGroupUnroll; ++u) {
       const int e = base + (int)lane + 32 * u;
+#if DITER_GROUP_TRIM
+      // edge slots past the group's last edge (warp-uniform): no owner search, no load
+      if (base + 32 * u >= total) { rows[u] = -1; vals[u] = 0.0; continue; }
+#endif
       int lo = 0;
 #pragma unroll
       for (int step = 16; step > 0; step >>= 1) {
@@ -641,6 +657,9 @@ k_scatter_hubs(Graph g, double *__restrict__ F, Frontier fr, const Ctl *ctl) {
 #ifndef DITER_SWEEP_MIN_BLOCKS
 #define DITER_SWEEP_MIN_BLOCKS kScatterMinBlocks
 #endif
+#ifndef DITER_SWEEP_ROW_PF
+#define DITER_SWEEP_ROW_PF 0       // L2 prefetch of the row indices that follow the span's (the next span's)
+#endif
 #ifndef DITER_SWEEP_TAKE_RED
 #define DITER_SWEEP_TAKE_RED 0
 #endif
@@ -770,6 +789,27 @@ struct SweepPf {
   unsigned *dw;       // [kSweepItems]
 };
 
+// DITER_SWEEP_EF bits: 1 the scan's col_ptr / dangling-word copies, 2 the H_i += s_i REDs,
+// 4 the scan's F copies carry an L2 evict-first policy (read or written once per sweep, so
+// they should not displace the rows of F that the Zipf-tail pushes find in L2)
+#ifndef DITER_SWEEP_EF
+#define DITER_SWEEP_EF 0
+#endif
+__device__ __forceinline__ unsigned long long l2_evict_first_policy() {
+  unsigned long long pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void cp_async_ef(void *smem, const void *gmem, int bytes, bool valid, unsigned long long pol) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2, %3;" :: "r"(sa), "l"(gmem), "r"(valid ? 8 : 0), "l"(pol) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2, %3;" :: "r"(sa), "l"(gmem), "r"(valid ? 4 : 0), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void red_add_ef(double *addr, double v, unsigned long long pol) {
+  asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" :: "l"(addr), "d"(v), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void cp_async(void *smem, const void *gmem, int bytes, bool valid) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   if (bytes == 8)
@@ -783,20 +823,35 @@ __device__ __forceinline__ void sweep_prefetch(const Graph &g, const double *F, 
                                                long long base, const SweepPf &pf) {
   const unsigned lane = lane_id();
   const long long n = g.n;
+#if DITER_SWEEP_EF
+  const unsigned long long pol = l2_evict_first_policy();
+#endif
 #pragma unroll
   for (int k = 0; k < kSweepItems; ++k) {
     const long long i = base + 32 * k + lane;
     const long long ic = i < n ? i : n - 1;
+#if DITER_SWEEP_EF & 4
+    cp_async_ef(pf.f + 32 * k + lane, F + ic, 8, i < n, pol);
+#else
     cp_async(pf.f + 32 * k + lane, F + ic, 8, i < n);
+#endif
     if (KEY == 1) cp_async(pf.w + 32 * k + lane, kw + ic, 4, i < n);
+#if DITER_SWEEP_EF & 1
+    cp_async_ef(pf.cp + 32 * k + lane, g.col_ptr + (i < n ? i : n), 8, true, pol);
+#else
     cp_async(pf.cp + 32 * k + lane, g.col_ptr + (i < n ? i : n), 8, true);
+#endif
   }
   if (lane == 0) {
     const long long iend = base + kSweepSpan;
     cp_async(pf.cp + kSweepSpan, g.col_ptr + (iend < n ? iend : n), 8, true);
   }
   const long long wi = (base >> 5) + lane;
+#if DITER_SWEEP_EF & 1
+  if ((int)lane < kSweepItems) cp_async_ef(pf.dw + lane, fr.dang_bits + ((wi << 5) < n ? wi : 0), 4, (wi << 5) < n, pol);
+#else
   if ((int)lane < kSweepItems) cp_async(pf.dw + lane, fr.dang_bits + ((wi << 5) < n ? wi : 0), 4, (wi << 5) < n);
+#endif
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
@@ -857,6 +912,17 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
     if (lane == 31) nxt = nxt0;
     dg[k] = (int)(nxt - cp[k]);
   }
+#if DITER_SWEEP_ROW_PF
+  // the next span's row indices start at cp_end: 128-byte lines of the following
+  // DITER_SWEEP_ROW_PF x 4 KB of row_idx into L2 while this span is taken and pushed
+  {
+    const int *rp = g.row_idx + cp_end + 32 * (long long)lane;
+#pragma unroll
+    for (int k = 0; k < DITER_SWEEP_ROW_PF; ++k)
+      if (cp_end + 32 * (long long)lane + 1024 * k < g.nnz)
+        asm volatile("prefetch.global.L2 [%0];" :: "l"(rp + 1024 * k));
+  }
+#endif
   // take every selected node of the span (independent atomics, issued together)
   unsigned msel[kSweepItems];
 #pragma unroll
@@ -892,7 +958,11 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
     double wv = 0.0;
     sel_all += __popc(m);
     if (sel) {
+#if DITER_SWEEP_EF & 2
+      red_add_ef(H + i, sv, l2_evict_first_policy());        // H_i += s_i
+#else
       red_add(H + i, sv);                                    // H_i += s_i
+#endif
       const double asv = fabs(sv);
       if (dang || deg <= 0) {
         dloss += asv;                                        // fluid leaves (App. A.2)

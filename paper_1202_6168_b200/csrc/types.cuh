@@ -7,7 +7,10 @@ namespace diter {
 
 // Degree classes (edges of the column = #out_i).
 constexpr int kLowMax = 32;      // 1..32     : "low"  (statistics only; same warp path as mid)
-constexpr int kMidMax = 8192;    // 33..8192  : "mid"  -- both: 32 selected nodes per warp,
+#ifndef DITER_MID_MAX
+#define DITER_MID_MAX 8192
+#endif
+constexpr int kMidMax = DITER_MID_MAX;    // 33..8192  : "mid"  -- both: 32 selected nodes per warp,
                                  //             lanes over the group's concatenated edges
 constexpr int kHubChunk = 2048;  // > 8192    : "hub"  -- one CTA per 2048-edge chunk
 #ifndef DITER_HOT_ROWS
@@ -139,6 +142,7 @@ struct Graph {
                              // far-edge deferral: near edges of each column (stored first); else nullptr
   int local_only;            // DI_REMOTE_INCREMENT: the scatter pushes [b0, b0 + nloc) only
   int defer;                 // one GPU: far-edge deferral on (the scatter pushes [b0, b0 + nloc))
+  long long nnz;             // stored edges of the owned columns (bound of row_idx prefetches)
 };
 
 // Frontier of one pass, compacted per select warp: warp w scans the owned nodes

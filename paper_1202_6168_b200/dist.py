@@ -6,6 +6,7 @@ the passes, the outbox compaction, the exchange and the merge run in
 libditer.so (csrc/dist.cu).
 
     bounds = partition_bounds(col_ptr, K, cost="out")      # Cost-Balanced ranges
+    bounds = partition_bounds_measured(col_ptr, K, bounds, work)   # re-balanced by a pilot solve's work
     cp, ri, v, b = shard_csc(col_ptr, row_idx, values, b, bounds, rank)
     cid = loopback_comm_id("test")    # K contexts of one process on one GPU (tests)
     cid = shm_comm_id("job42")        # K processes of one host, host-side collectives (tests)
@@ -47,6 +48,61 @@ def partition_bounds(col_ptr, K: int, cost: str = "out", row_idx=None) -> np.nda
     else:
         raise ValueError(cost)
     return di_partition_cb(prefix, K)
+
+
+def partition_bounds_measured(col_ptr, K: int, prev_bounds, prev_work) -> np.ndarray:
+    """Ranges re-balanced by MEASURED work (the paper's dynamic adaptation of the sets
+    Omega_k, PAPER.md:178-184 and :523-543 / reading R22, applied between two solves instead of between
+    rounds -- DI_EXCHANGE_P2P fixes its outbox slots at create, so it cannot move
+    boundaries mid-run).
+
+    prev_work[k] = diffusion work rank k did on prev_bounds in a pilot solve (pushes:
+    di_stats edges + remote_pushes).  Each node's cost becomes #out_n x (work per
+    stored edge of the rank that held it), i.e. the pilot's work spread over the rank's
+    columns in proportion to their out-degree, and the Cost-Balanced split (R10) is
+    taken over that cost.  Integer arithmetic on a fixed-point density so that every
+    rank derives the same bounds from the same gathered numbers."""
+    col_ptr = np.asarray(col_ptr, dtype=np.int64)
+    prev_bounds = np.asarray(prev_bounds, dtype=np.int64)
+    work = np.asarray(prev_work, dtype=np.float64)
+    Kp = len(prev_bounds) - 1
+    if len(work) != Kp or Kp < 1 or np.any(work < 0) or work.sum() <= 0:
+        raise ValueError("prev_work needs one non-negative entry per previous range")
+    stored = (col_ptr[prev_bounds[1:]] - col_ptr[prev_bounds[:-1]]).astype(np.float64)
+    dens = work / np.maximum(stored, 1.0)
+    dens = dens / dens.max()
+    q = np.maximum(1, np.rint(dens * 4096.0)).astype(np.int64)     # fixed-point work per stored edge
+    prefix = np.empty_like(col_ptr)
+    base = 0
+    for k in range(Kp):
+        lo, hi = int(prev_bounds[k]), int(prev_bounds[k + 1])
+        prefix[lo:hi + 1] = base + (col_ptr[lo:hi + 1] - col_ptr[lo]) * q[k]
+        base = int(prefix[hi])
+    return di_partition_cb(prefix, K)
+
+
+def remote_fraction(row_idx_local, lo: int, hi: int) -> float:
+    """Share of a rank's stored edges whose row lies outside its range [lo, hi)."""
+    ri = np.asarray(row_idx_local)
+    if ri.size == 0:
+        return 0.0
+    out = 0
+    for a in range(0, ri.size, 1 << 26):                      # chunked: no N-sized temporaries
+        c = ri[a:a + (1 << 26)]
+        out += int(np.count_nonzero((c < lo) | (c >= hi)))
+    return out / ri.size
+
+
+def pushes_performed(stats: dict, rho: float, remote_push: int) -> float:
+    """Pushes a rank executed in a solve, from its di_stats.  di_stats.edges counts every
+    edge of a diffused node (the metric's E_p); with remote edges delivered as H
+    increments (DI_REMOTE_INCREMENT) the passes push only the local ones and the
+    increments are counted in remote_pushes, so the work is edges x (1 - rho) +
+    remote_pushes with rho the rank's static remote-edge share (selection does not
+    depend on where an edge leads).  Per-diffusion mode pushes every edge in the pass."""
+    if remote_push:
+        return stats["edges"] * (1.0 - rho) + stats["remote_pushes"]
+    return float(stats["edges"])
 
 
 def shard_csc(col_ptr, row_idx, values, b, bounds, rank: int):

@@ -68,15 +68,22 @@ di.di_run(c1, p.stop)
 P1 = di.di_get_stats(c1)["passes"]
 di.di_destroy(c1)
 out = {"mode": "p2p" if P2P else "async", "sweep": SWEEP, "config": cfg, "partition": COST, "round_passes": ROUND, "remote_push": REMOTE, "T1_ms": T1, "select_share": s_sel, "E1": E1, "passes_1": P1, "K": {}}
-for K in KS:
-    bounds = dist.partition_bounds(p.col_ptr, K, cost=COST, row_idx=p.row_idx)
+PILOT = int(os.environ.get("MODEL_PILOT", "0"))               # pilot solves whose measured work re-balances the ranges
+for K, pilot in [(K, it) for K in KS for it in range(PILOT + 1)]:
+    if pilot == 0:
+        bounds = dist.partition_bounds(p.col_ptr, K, cost=COST, row_idx=p.row_idx)
+    else:
+        bounds = dist.partition_bounds_measured(p.col_ptr, K, bounds, [dist.pushes_performed(s, rh, REMOTE) for s, rh in zip(st, rho)])
+        print(f"K={K} pilot {pilot}: bounds {[int(b) for b in bounds]}", flush=True)
     st = [None] * K
     err = [None] * K
-    cid = dist.loopback_comm_id(f"model{cfg}{K}")
+    rho = [0.0] * K
+    cid = dist.loopback_comm_id(f"model{cfg}{K}p{pilot}")
 
     def w(r):
         try:
             lcp, lri, lv, lb = dist.shard_csc(p.col_ptr, p.row_idx, p.values, p.b, bounds, r)
+            rho[r] = dist.remote_fraction(lri, int(bounds[r]), int(bounds[r + 1]))
             o = di.default_options(policy=pol, alpha=alpha_k, hybrid_frac=frac_k, select_key=key,
                                    exchange_mode=MODE, check_interval=ROUND, remote_push=REMOTE,
                                    receive_rescale=RESCALE, p2p_sleep=SLEEP, sweep=SWEEP, scatter_run=RUN,
@@ -96,8 +103,17 @@ for K in KS:
             raise e
     wall = time.perf_counter() - t
     rounds = max(s["exchanges"] for s in st)
-    comps = [s_sel * (s["passes"] * s["n_local"]) / (P1 * p.n) + (1 - s_sel) * (s["edges"] + s["remote_pushes"]) / E1
-             for s in st]
+    # conservative work term (rounds 1-2 of this model): every edge of a diffused node plus
+    # every increment push, i.e. remote edges counted twice in DI_REMOTE_INCREMENT mode
+    comps_cons = [s_sel * (s["passes"] * s["n_local"]) / (P1 * p.n) + (1 - s_sel) * (s["edges"] + s["remote_pushes"]) / E1
+                  for s in st]
+    # pushes actually performed (dist.pushes_performed): MODEL_WORK=performed (default) / conservative
+    # + the increment kernel's scan of the rank's nodes at every round (col_ptr, nloc, H, H_old:
+    # 28 B per node at the measured HBM copy rate), which the edge term does not hold
+    inc_scan = [(s["passes"] / ROUND) * s["n_local"] * 28.0 / 6.5e12 / (T1 * 1e-3) if REMOTE else 0.0 for s in st]
+    comps_perf = [s_sel * (s["passes"] * s["n_local"]) / (P1 * p.n) + (1 - s_sel) * dist.pushes_performed(s, rh, REMOTE) / E1 + x
+                  for s, rh, x in zip(st, rho, inc_scan)]
+    comps = comps_cons if os.environ.get("MODEL_WORK", "performed") == "conservative" else comps_perf
     comp = max(comps)
     per_round = max(s["exchanged_bytes"] for s in st) / max(1, rounds)
     if P2P:
@@ -107,11 +123,13 @@ for K in KS:
     else:
         TK = T1 * 1e-3 * comp + rounds * (per_round / B_LINK + T_ROUND)
     eff = T1 * 1e-3 / (K * TK)
-    out["K"][K] = {"passes": [s["passes"] for s in st], "n_local": [s["n_local"] for s in st],
+    out["K"][K if pilot == 0 else f"{K} pilot {pilot}"] = {"bounds": [int(b) for b in bounds], "passes": [s["passes"] for s in st], "n_local": [s["n_local"] for s in st],
                    "edges": [s["edges"] for s in st], "remote_pushes": [s["remote_pushes"] for s in st],
                    "rounds": rounds, "bytes_per_round_max": per_round,
                    "exchanged_bytes_total": sum(s["exchanged_bytes"] for s in st),
-                   "compute_fraction_of_T1": comp, "compute_per_rank": comps, "T_K_model_ms": TK * 1e3,
+                   "compute_fraction_of_T1": comp, "compute_per_rank": comps,
+                   "compute_per_rank_conservative": comps_cons, "remote_edge_share": rho,
+                   "efficiency_model_conservative": T1 * 1e-3 / (K * (max(T1 * 1e-3 * c + (s["passes"] / ROUND) * T_ROUND + s["exchanged_bytes"] / B_P2P for c, s in zip(comps_cons, st)) + max(s["confirms"] for s in st) * T_CONFIRM)) if P2P else None, "T_K_model_ms": TK * 1e3,
                    "efficiency_model": eff, "confirms": [s["confirms"] for s in st],
                    "collectives": [s["collectives"] for s in st],
                    "exchange_bytes_resident": [s["exchange_bytes_resident"] for s in st],

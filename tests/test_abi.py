@@ -74,3 +74,32 @@ def test_library_then_torch_import_order():
             "di.load_library(); import torch; print('ok')") % ROOT
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+
+
+def test_partition_bounds_measured():
+    """Pilot re-balancing of the ranges (dist.partition_bounds_measured): equal work per
+    stored edge reproduces the Cost-Balanced split; a rank with k times the work per edge
+    keeps 1/K of the measured work; K may differ from the pilot's; bad input is rejected."""
+    from paper_1202_6168_b200 import dist as dd
+    rng = np.random.default_rng(5)
+    deg = rng.integers(0, 30, 20_000)
+    cp = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
+    b = dd.partition_bounds(cp, 4)
+    stored = np.diff(cp[b]).astype(float)
+    np.testing.assert_array_equal(dd.partition_bounds_measured(cp, 4, b, stored), b)
+    np.testing.assert_array_equal(dd.partition_bounds_measured(cp, 4, b, 3.5 * stored), b)
+    work = stored * np.array([3.0, 1.0, 1.0, 2.0])
+    nb = dd.partition_bounds_measured(cp, 4, b, work)
+    dens = np.repeat(np.array([3.0, 1.0, 1.0, 2.0]), np.diff(b))
+    wcum = np.concatenate([[0.0], np.cumsum(deg * dens)])
+    for k in range(1, 4):
+        assert abs(wcum[nb[k]] / wcum[-1] - k / 4) < 2e-3
+    nb2 = dd.partition_bounds_measured(cp, 2, b, work)         # pilot on 4 ranks, 2 new ranges
+    assert abs(wcum[nb2[1]] / wcum[-1] - 0.5) < 2e-3
+    for bad in ([1.0, 1.0], [0.0, 0.0, 0.0, 0.0], [1.0, -1.0, 1.0, 1.0]):
+        with pytest.raises(ValueError):
+            dd.partition_bounds_measured(cp, 4, b, bad)
+    st = {"edges": 1000, "remote_pushes": 50}
+    assert dd.pushes_performed(st, 0.25, 1) == 800.0 and dd.pushes_performed(st, 0.25, 0) == 1000.0
+    ri = np.array([0, 5, 9, 10, 19, 3], dtype=np.int32)
+    assert dd.remote_fraction(ri, 5, 10) == 4 / 6 and dd.remote_fraction(ri[:0], 0, 1) == 0.0

@@ -51,6 +51,26 @@ def _host_logic(rank, world, port):
             re_cp = np.concatenate([cps[0]] + [c[1:] + sum(x[-1] for x in cps[:k]) for k, c in enumerate(cps) if k > 0])
             np.testing.assert_array_equal(re_cp, cp)
             np.testing.assert_array_equal(np.concatenate([np.asarray(s[1]) for s in shards]), ri)
+        # pilot re-balancing (bench --pilot-solves): every rank gathers the same work numbers and
+        # derives the same new ranges; the rank with twice the work density gives columns away
+        bounds = dd.partition_bounds(cp, world)
+        shard = dd.shard_csc(cp, ri, None, None, bounds, rank)
+        rho = dd.remote_fraction(shard[1], int(bounds[rank]), int(bounds[rank + 1]))
+        ri_np = np.asarray(shard[1])
+        assert rho == np.mean((ri_np < bounds[rank]) | (ri_np >= bounds[rank + 1]))
+        stats = {"edges": int(shard[0][-1]) * (2 if rank == 0 else 1), "remote_pushes": 0}
+        work = [None] * world
+        dist.all_gather_object(work, dd.pushes_performed(stats, 0.0, 1))
+        nb = dd.partition_bounds_measured(cp, world, bounds, work)
+        allb = [None] * world
+        dist.all_gather_object(allb, nb.tolist())
+        assert all(x == allb[0] for x in allb)
+        assert nb[0] == 0 and nb[-1] == len(cp) - 1 and np.all(np.diff(nb) > 0)
+        assert nb[1] < bounds[1]
+        # rank 0's new share of the measured work is 1 / world (within one column's cost)
+        dens = np.where(np.arange(len(cp) - 1) < bounds[1], 2.0, 1.0)
+        wcum = np.concatenate([[0.0], np.cumsum(np.diff(cp) * dens)])
+        assert abs(wcum[nb[1]] / wcum[-1] - 1.0 / world) < 1e-3
         cid = dd.nccl_comm_id()                               # rank 0 creates, broadcast over gloo
         ids = [None] * world
         dist.all_gather_object(ids, cid)

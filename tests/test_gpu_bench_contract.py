@@ -48,12 +48,15 @@ def test_bench_distributed_path_one_rank(exchange):
     collectives run, the exchange mode's stats reach the line."""
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "C2", "--steps", "2",
                           "--warmup", "3", "--cpu-seconds", "1", "--dist-path", "--exchange", exchange,
-                          "--no-cpu-baseline"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+                          "--no-cpu-baseline"] + (["--pilot-solves", "1"] if exchange == "p2p" else []),
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-3000:]
     d = json.loads(out.stdout.strip().splitlines()[-1])
     assert d["n_gpus"] == 1 and d["value"] > 0
     assert d["collectives_per_solve"] > 0 and d["exchange_bytes_resident"] > 0
     if exchange == "p2p":
+        # the pilot solve's re-balancing ran (one rank: the range stays [0, n)) and is reported
+        assert "pilot 1: bounds [0, 1000000]" in out.stderr and "pilot" in d["config"]["parallelism"]
         assert d["confirms_per_solve"] >= 1
         assert d["collectives_per_solve"] == 1 + 4 * d["confirms_per_solve"]
     assert d["e2e"]["value"] > 0

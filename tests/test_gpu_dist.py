@@ -545,3 +545,37 @@ def test_sweeps_on_ranks(mode, K, remote):
     ledger = np.abs(F).sum() + 0.15 * H.sum() + 0.85 * H[deg == 0].sum()
     assert abs(ledger - bn) <= 1e-12 * bn
     assert all(o[4] < p.parity_stop for o in outs)
+
+
+def test_pilot_rebalanced_ranges_keep_parity_and_level_the_work():
+    """Ranges re-balanced by a pilot solve's measured work (dist.partition_bounds_measured,
+    bench --pilot-solves): the second solve, on the new ranges, still matches the oracle
+    with a closed ledger, and the ranks' performed pushes are closer to level than on the
+    out-edge partition (the Zipf head makes rank 0 the busiest there)."""
+    K = 4
+    p = gen.config("C2", 2, n=400_000)
+    bn = 0.15
+    opts = dict(check_interval=2, remote_push=di.DI_REMOTE_INCREMENT, sweep=1, select_key=di.DI_KEY_EDGE)
+
+    def solve(bounds, tag):
+        H, F, outs = run_ranks(K, p.n, p.col_ptr, p.row_idx, None, None, 0.85, p.parity_stop, bounds,
+                               di.DI_EXCHANGE_P2P, tag, **opts)
+        work = []
+        for r, o in enumerate(outs):
+            lri = dist.shard_csc(p.col_ptr, p.row_idx, None, None, bounds, r)[1]
+            rho = dist.remote_fraction(lri, int(bounds[r]), int(bounds[r + 1]))
+            work.append(dist.pushes_performed(o[3], rho, 1))
+        return H, F, np.asarray(work)
+
+    b0 = dist.partition_bounds(p.col_ptr, K, cost="out")
+    _, _, w0 = solve(b0, "pilot0")
+    b1 = dist.partition_bounds_measured(p.col_ptr, K, b0, w0)
+    assert b1[0] == 0 and b1[-1] == p.n and np.all(np.diff(b1) > 0)
+    H, F, w1 = solve(b1, "pilot1")
+    X = oracle.Problem(p.n, p.col_ptr, p.row_idx).solve(1e-12 * bn * 0.15).H
+    assert np.abs(H - X).sum() <= 1e-8 * bn
+    deg = np.diff(p.col_ptr)
+    ledger = np.abs(F).sum() + 0.15 * H.sum() + 0.85 * H[deg == 0].sum()
+    assert abs(ledger - bn) <= 1e-12 * bn
+    assert b1[1] < b0[1]                                   # the head rank gave columns away
+    assert w1.max() / w1.mean() < w0.max() / w0.mean(), (w0, w1)
