@@ -612,6 +612,8 @@ def run_ours(args, rank, world, local_rank):
            # fabric collectives (all-reduce, all-to-all) and P2P confirmations per timed solve, rank 0
            "collectives_per_solve": (coll1["collectives"] - coll0["collectives"]) / args.steps if dist else 0,
            "confirms_per_solve": (coll1["confirms"] - coll0["confirms"]) / args.steps if dist else 0,
+           # untimed pilot solves whose measured work re-balanced the ranges before the warm-up
+           "pilot_solves": args.pilot_solves if dist else 0,
            "exchange_bytes_resident": coll1["exchange_bytes_resident"] if dist else 0,
            "wall_s_timed": wall}
     if rank == 0:

@@ -459,7 +459,6 @@ Graph diter_graph(const di_ctx *ctx) {
           ctx->lo, ctx->G, ctx->dflags, ctx->far, ctx->nloc,
           ctx->opt.remote_push != DI_REMOTE_PER_DIFFUSION ? 1 : 0};
   g.defer = ctx->defer_m > 0 ? 1 : 0;
-  g.nnz = ctx->nnz_local;
   return g;
 }
 

@@ -657,9 +657,6 @@ k_scatter_hubs(Graph g, double *__restrict__ F, Frontier fr, const Ctl *ctl) {
 #ifndef DITER_SWEEP_MIN_BLOCKS
 #define DITER_SWEEP_MIN_BLOCKS kScatterMinBlocks
 #endif
-#ifndef DITER_SWEEP_ROW_PF
-#define DITER_SWEEP_ROW_PF 0       // L2 prefetch of the row indices that follow the span's (the next span's)
-#endif
 #ifndef DITER_SWEEP_TAKE_RED
 #define DITER_SWEEP_TAKE_RED 0
 #endif
@@ -912,17 +909,6 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
     if (lane == 31) nxt = nxt0;
     dg[k] = (int)(nxt - cp[k]);
   }
-#if DITER_SWEEP_ROW_PF
-  // the next span's row indices start at cp_end: 128-byte lines of the following
-  // DITER_SWEEP_ROW_PF x 4 KB of row_idx into L2 while this span is taken and pushed
-  {
-    const int *rp = g.row_idx + cp_end + 32 * (long long)lane;
-#pragma unroll
-    for (int k = 0; k < DITER_SWEEP_ROW_PF; ++k)
-      if (cp_end + 32 * (long long)lane + 1024 * k < g.nnz)
-        asm volatile("prefetch.global.L2 [%0];" :: "l"(rp + 1024 * k));
-  }
-#endif
   // take every selected node of the span (independent atomics, issued together)
   unsigned msel[kSweepItems];
 #pragma unroll

@@ -312,7 +312,10 @@ __global__ void k_p2p_floor(Ctl *ctl, const P2PHeader *my, int W, int rank) {
   double m = 0.0;
   for (int q = 0; q < W; ++q)
     if (q != rank) m = fmax(m, *(volatile const double *)&my->tval[q]);
-  ctl->T_floor = m / (ctl->alpha * ctl->alpha);
+#ifndef DITER_P2P_FLOOR_POW
+#define DITER_P2P_FLOOR_POW 2
+#endif
+  ctl->T_floor = DITER_P2P_FLOOR_POW == 2 ? m / (ctl->alpha * ctl->alpha) : DITER_P2P_FLOOR_POW == 1 ? m / ctl->alpha : m;
 }
 
 // Quiesce request: epoch into every rank's header

@@ -142,7 +142,6 @@ struct Graph {
                              // far-edge deferral: near edges of each column (stored first); else nullptr
   int local_only;            // DI_REMOTE_INCREMENT: the scatter pushes [b0, b0 + nloc) only
   int defer;                 // one GPU: far-edge deferral on (the scatter pushes [b0, b0 + nloc))
-  long long nnz;             // stored edges of the owned columns (bound of row_idx prefetches)
 };
 
 // Frontier of one pass, compacted per select warp: warp w scans the owned nodes

@@ -33,6 +33,8 @@ import diter_inputs as gen
 import paper_1202_6168_b200 as di
 from paper_1202_6168_b200 import dist
 import bench
+if os.environ.get("DITER_LIB"):
+    di.LIB_PATH = os.environ["DITER_LIB"]   # experiment: another build of the library
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C4"
 T1 = float(sys.argv[2]) if len(sys.argv) > 2 else 248.7
