@@ -657,6 +657,9 @@ k_scatter_hubs(Graph g, double *__restrict__ F, Frontier fr, const Ctl *ctl) {
 #ifndef DITER_SWEEP_MIN_BLOCKS
 #define DITER_SWEEP_MIN_BLOCKS kScatterMinBlocks
 #endif
+#ifndef DITER_SWEEP_DANG_EVERY
+#define DITER_SWEEP_DANG_EVERY 1   // sweeps take dangling nodes only every m-th sweep (and near the target)
+#endif
 #ifndef DITER_SWEEP_TAKE_RED
 #define DITER_SWEEP_TAKE_RED 0
 #endif
@@ -861,7 +864,8 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
                                            double *__restrict__ H, const Frontier &fr, Ctl *ctl,
                                            const float *__restrict__ kw, double T, long long base,
                                            ScAcc &acc, int &sel_all, double &dloss, int &dang_cnt,
-                                           SweepStage &st, const SweepPf &pf, long long next_base) {
+                                           SweepStage &st, const SweepPf &pf, long long next_base,
+                                           bool take_dang) {
   const unsigned lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
   double f[kSweepItems];
@@ -918,7 +922,12 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
     const double key = KEY == 0 ? af
                      : KEY == 1 ? af * (double)w[k]
                                 : af * (double)__frcp_rn((float)dg[k] + 1.0f);
-    const bool sel = key > T;                                // strict ">" (R7)
+    bool sel = key > T;                                      // strict ">" (R7)
+#if DITER_SWEEP_DANG_EVERY > 1
+    // a dangling node pushes nothing, so its take can wait for a later sweep (any order is a
+    // valid D-iteration): between take sweeps its fluid just accumulates
+    if (!take_dang && (((__shfl_sync(0xffffffffu, dword, k) >> lane) & 1u) || dg[k] <= 0)) sel = false;
+#endif
     msel[k] = __ballot_sync(0xffffffffu, sel);
 #if DITER_SWEEP_TAKE_RED
     // take by a fire-and-forget RED of -s_i: F_i = (s_i + pushes since the load) - s_i,
@@ -1022,6 +1031,10 @@ k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ct
   const Sink s{F, s_hot, g.hot_lo, g.lo, g.n, DIST ? g.G : nullptr, DIST ? g.dflags : nullptr};
   Stage sg{nullptr, nullptr, 0};
   const double T = ctl->T;
+  // dangling nodes are taken every DITER_SWEEP_DANG_EVERY-th sweep, and in every sweep once the
+  // carried bound is within 4 x the target (the stop needs their fluid gone from |F|_1)
+  const bool take_dang = DITER_SWEEP_DANG_EVERY <= 1 || ctl->pass % DITER_SWEEP_DANG_EVERY == 0 ||
+                         !(ctl->r_pred > 4.0 * ctl->target);
   const unsigned lane = lane_id();
   ScAcc acc;
   int sel_all = 0, dang_cnt = 0;
@@ -1052,12 +1065,13 @@ k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ct
         sweep_prefetch<KEY>(g, F, kw, fr, span_of(s0 + q0) * kSweepSpan, pf);
         for (long long q = s0 + q0; q < q1; ++q) {
           sweep_span<SIGNED, KEY, true, DIST>(g, s, F, H, fr, ctl, kw, T, span_of(q) * kSweepSpan, acc, sel_all,
-                                              dloss, dang_cnt, st, pf, q + 1 < q1 ? span_of(q + 1) * kSweepSpan : -1);
+                                              dloss, dang_cnt, st, pf, q + 1 < q1 ? span_of(q + 1) * kSweepSpan : -1,
+                                              take_dang);
           sweep_flush<SIGNED>(g, s, ctl, st, sg, false);
         }
       } else {
         sweep_span<SIGNED, KEY, false, DIST>(g, s, F, H, fr, ctl, kw, T, span_of(s0 + q0) * kSweepSpan, acc, sel_all,
-                                             dloss, dang_cnt, st, pf, -1);
+                                             dloss, dang_cnt, st, pf, -1, take_dang);
         sweep_flush<SIGNED>(g, s, ctl, st, sg, false);
       }
     }
