@@ -131,14 +131,18 @@ def parse():
                     help="edge-balanced contiguous ranges by out-edges (default: with remote edges "
                          "pushed by the senders as H increments, receiving is a cheap merge; "
                          "scripts/exp_scaling_model.py) or by in+out edges")
-    ap.add_argument("--pilot-solves", type=int, default=0,
-                    help="N > 1: untimed pilot solves before the warm-up; after each, the ranges are "
+    ap.add_argument("--pilot-solves", type=int, default=None,
+                    help="N > 1 (default 1; 0 with --dist-path on one GPU): untimed pilot solves before the warm-up; after each, the ranges are "
                          "re-balanced by the ranks' measured diffusion work (dist.partition_bounds_measured, "
                          "the paper's adaptation of the sets Omega_k applied between solves) and the "
                          "contexts are rebuilt on the new ranges")
     a = ap.parse_args()
     if a.round_passes is None:
         a.round_passes = 2 if a.exchange == "p2p" else 4
+    if a.pilot_solves is None:
+        # one pilot: C4 K = 8 modeled 0.56 -> 0.71 (profiles/r04_sweep_variants.md); a second does not
+        # improve on it.  Both arms resolve it here, so their `config` strings agree.
+        a.pilot_solves = 1 if max(a.gpus, int(os.environ.get("WORLD_SIZE", "1"))) > 1 else 0
     return a
 
 
