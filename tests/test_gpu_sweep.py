@@ -159,3 +159,39 @@ def test_sweep_max_passes_and_checkpoint():
         di.di_destroy(ctx)
         assert np.abs(H2 - X).sum() <= TOL * bn
         _check_state(n, cp, ri, None, None, 0.85, H2, F2, r2, target)
+
+
+def test_sweep_degenerate_graphs():
+    """The degenerate cases of the method under sweeps: one node with a self-loop (its own
+    push lands in the F_i it just took: X = b / (1 - d)), one dangling node,
+    P = 0 (every column dangling: X = B exactly after one sweep), a graph of isolated
+    self-loops, and a target already met (no sweep runs)."""
+    cp = np.array([0, 1], np.int64)
+    ri = np.array([0], np.int32)
+    H, F, log, r, _ = _gpu(1, cp, ri, 1e-14, sweep=1)
+    assert abs(H[0] - 1.0) <= 1e-14 / 0.15 + 1e-15 and r < 1e-14
+    H0, F0, log0, r0, _ = _gpu(1, np.array([0, 0], np.int64), np.zeros(0, np.int32), 1e-30, sweep=1)
+    assert H0[0] == pytest.approx(0.15, rel=1e-15) and F0[0] == 0.0 and len(log0) == 1
+    n = 1000
+    b = np.linspace(0, 1, n)
+    H, F, log, r, _ = _gpu(n, np.zeros(n + 1, np.int64), np.zeros(0, np.int32), 1e-300, b=b, sweep=1)
+    np.testing.assert_array_equal(H, b)
+    assert r == 0.0 and not F.any()
+    n = 777
+    cp = np.arange(n + 1, dtype=np.int64)
+    ri = np.arange(n, dtype=np.int32)
+    H, F, log, r, _ = _gpu(n, cp, ri, 1e-13, sweep=1, select_key=1)
+    np.testing.assert_allclose(H, np.full(n, 0.15 / n / 0.15), rtol=1e-10)      # b_i / (1 - d)
+    H, F, log, r, st = _gpu(n, cp, ri, 1.0, sweep=1)                          # |B|_1 = 0.15 < 1
+    assert st["passes"] == 0 and not H.any() and r == pytest.approx(0.15, rel=1e-12)
+
+
+@pytest.mark.parametrize("n", [31, 127, 129, 4099, 1_000_003])
+def test_sweep_ragged_sizes(n):
+    """Sizes around the sweep's 128-node span and 32-node item, and one that spans many
+    ticket stripes with a ragged last span, with the bench's stripe / run settings."""
+    cp, ri = gen.web_graph(n, 11, window=min(1000, n // 2 or 1), max_deg=min(5000, n - 1))
+    X, P, bn = _xref(n, cp, ri)
+    H, F, log, r, _ = _gpu(n, cp, ri, 1e-9 * bn, sweep=1, select_key=1, scatter_run=6, scatter_stripes=4)
+    assert np.abs(H - X).sum() <= TOL * bn
+    _check_state(n, cp, ri, None, None, 0.85, H, F, r, 1e-9 * bn)
