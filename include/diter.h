@@ -152,7 +152,9 @@ typedef struct {
   int32_t p2p_sleep;       /* DI_EXCHANGE_P2P: a rank whose local residual r_k is below target / K
                               sleeps: its rounds only merge, send and measure,
                               no local passes, until received fluid lifts r_k again; 0 = on
-                              (default), -1 = off */
+                              (default), -1 = off; k > 0 = also asleep while r_k is below k % of
+                              the rank's even share (1 / K) of the fluid on the board (every
+                              rank's r + s + in flight as last published) */
   int32_t far_defer;       /* one GPU, PageRank: far-edge deferral -- a column's
                               edges to rows more than 2048 ids away and outside the L2 persisting
                               window (else the shared-memory hot window) are pushed not at every

@@ -711,10 +711,14 @@ di_status p2p_run(di_ctx *ctx, double target) {
       ctx->passes_done = h->pass;
       const double s_k = hb->round[kRoundS] + hb->round[kRoundPend];
       const double r_k = hb->round[kRoundR];
-      asleep = ctx->opt.p2p_sleep >= 0 && r_k < target / W;
       ds->s_k = s_k;
       double board = 0.0;
       for (int q = 0; q < W; ++q) board += hb->hdr.board[q];
+      // sleep: r_k below this rank's share of the target, or (p2p_sleep = k > 0) below
+      // k % of its even share of the fluid the board still holds -- a rank left with crumbs waits
+      // for its peers' shipments instead of diffusing them at ever lower thresholds
+      asleep = ctx->opt.p2p_sleep >= 0 &&
+               (r_k < target / W || (ctx->opt.p2p_sleep > 0 && r_k < 0.01 * ctx->opt.p2p_sleep * board / W));
       const bool oop = h->pass >= max_pass_abs;
       // 4. termination: a trigger raises the epoch in every header; every rank confirms
       if (hb->hdr.quiesce > P.epoch || board < target || oop) {

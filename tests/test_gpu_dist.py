@@ -579,3 +579,29 @@ def test_pilot_rebalanced_ranges_keep_parity_and_level_the_work():
     assert abs(ledger - bn) <= 1e-12 * bn
     assert b1[1] < b0[1]                                   # the head rank gave columns away
     assert w1.max() / w1.mean() < w0.max() / w0.mean(), (w0, w1)
+
+
+@pytest.mark.parametrize("sleep", [-1, 0, 60])
+def test_p2p_sleep_modes_keep_parity(sleep):
+    """P2P sleep: off, the absolute rule r_k < target / K, and the relative
+    rule (asleep below 60 % of the rank's even share of the fluid on the board).  Sleeping ranks
+    keep merging and sending, so every mode ends at the oracle's X with a closed ledger; the
+    relative rule does put ranks to sleep on a Zipf-head graph."""
+    K = 3
+    p = gen.config("C2", 2, n=300_000)
+    bn = 0.15
+    bounds = dist.partition_bounds(p.col_ptr, K, cost="out")
+    H, F, outs = run_ranks(K, p.n, p.col_ptr, p.row_idx, None, None, 0.85, p.parity_stop, bounds,
+                           di.DI_EXCHANGE_P2P, f"sleep{sleep}", check_interval=2,
+                           remote_push=di.DI_REMOTE_INCREMENT, sweep=1, select_key=di.DI_KEY_EDGE, p2p_sleep=sleep)
+    X = oracle.Problem(p.n, p.col_ptr, p.row_idx).solve(1e-12 * bn * 0.15).H
+    assert np.abs(H - X).sum() <= 1e-8 * bn
+    deg = np.diff(p.col_ptr)
+    ledger = np.abs(F).sum() + 0.15 * H.sum() + 0.85 * H[deg == 0].sum()
+    assert abs(ledger - bn) <= 1e-12 * bn
+    assert all(o[4] < p.parity_stop for o in outs)
+    slept = sum(o[3]["sleep_rounds"] for o in outs)
+    if sleep < 0:
+        assert slept == 0
+    if sleep == 60:
+        assert slept > 0
