@@ -79,6 +79,12 @@ SCATTER_RUN = {"C3": 1, "C4": 6}
 SNAPSHOT_SCATTER_RUN = {"C3": 1, "C4": 3}
 # Ticket stripes (options.scatter_stripes; default 8): C4 sweeps 4 (193.1 vs 193.8 ms).
 SCATTER_STRIPES = {"C4": 4}
+# options.key_offset: under sweeps the derived per-edge key is |F_i| / (#out_i + c) (reading R27).
+# Measured on C4: c = 8 with f = 0.55 reaches the target in 172.7 ms instead of 176.1 (59 sweeps,
+# 2.22e10 edges) but diffuses fewer edges per second (1.285e11 vs 1.309e11) at a lower k_sweep
+# fraction (0.528 vs 0.551): the headline metric is edges/s and the roofline fraction, so the
+# bench keeps the paper-style key c = 1 (profiles/r04_sweep_variants.md, r04_bench_c4_key_offset8.json).
+KEY_OFFSET = {}
 
 # The raw key |F_i| > T_p (north_star's literal selection) on C4, reported beside the
 # headline as `raw_key`: HYBRID alpha = 2, f = 0.15 (its best schedule).
@@ -192,6 +198,7 @@ def bench_config(args, p, pol, world, resident, flushed):
             "select_key": ["raw", "per-edge", "paper"][args.key],
             "scatter_run": SCATTER_RUN.get(args.config, 2),
             "scatter_stripes": SCATTER_STRIPES.get(args.config, 8),
+            "key_offset": KEY_OFFSET.get(args.config, 1) if args.sweep and args.key == 1 else 1,
             "passes": ("one-kernel asynchronous sweeps (options.sweep = 1, reading R26)"
                        if args.sweep and (world == 1 or args.exchange != "sync")
                        else "snapshot passes (select, then scatter)"),
@@ -432,7 +439,8 @@ def run_ours(args, rank, world, local_rank):
                               alpha=args.alpha, hybrid_frac=args.hybrid_frac, select_key=args.key,
                               scatter_run=SCATTER_RUN.get(args.config, 0), l2_persist=args.l2_persist,
                               far_defer=args.far_defer, sweep=args.sweep,
-                              scatter_stripes=SCATTER_STRIPES.get(args.config, 0), **dist_kw)
+                              scatter_stripes=SCATTER_STRIPES.get(args.config, 0),
+                              key_offset=KEY_OFFSET.get(args.config, 0), **dist_kw)
     comm_id, bounds, shard = None, None, None
     if dist:
         bounds = dd.partition_bounds(p.col_ptr, world, cost=args.partition, row_idx=p.row_idx)

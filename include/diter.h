@@ -170,6 +170,11 @@ typedef struct {
                               nodes scanned later in the same sweep; no frontier list.  Same fixed
                               point X; the pass log is per sweep and not the snapshot
                               oracle's.  0 = snapshot passes (select, then scatter; default) */
+  int32_t key_offset;      /* sweeps with select_key = DI_KEY_EDGE: the key the sweep derives from
+                              col_ptr is |F_i| / (#out_i + c) with c = key_offset; 0 = default
+                              (c = 1, the per-edge key).  A larger c charges a node's take like c
+                              pushes (cost-aware variant of the weighting heuristic, PAPER.md:208-212;
+                              DESIGN.md reading R27); any c reaches the same X */
 } di_options;
 
 /* One record per executed pass (device-logged, read with di_get_pass_log). */

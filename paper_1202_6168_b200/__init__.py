@@ -60,7 +60,8 @@ class di_options(ctypes.Structure):
                 ("select_key", ctypes.c_int32), ("remote_push", ctypes.c_int32),
                 ("receive_rescale", ctypes.c_int32), ("adapt_rounds", ctypes.c_int32),
                 ("l2_persist", ctypes.c_int32), ("p2p_sleep", ctypes.c_int32),
-                ("far_defer", ctypes.c_int32), ("sweep", ctypes.c_int32)]
+                ("far_defer", ctypes.c_int32), ("sweep", ctypes.c_int32),
+                ("key_offset", ctypes.c_int32)]
 
 
 class di_pass_log(ctypes.Structure):

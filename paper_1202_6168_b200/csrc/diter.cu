@@ -608,7 +608,8 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
   di_options o;
   if (opt) o = *opt; else di_default_options(&o);
   if (!(o.alpha > 1.0) || o.check_interval < 1 || o.check_interval > 4096 || o.max_passes < 1 ||
-      (o.policy != DI_POLICY_GEOM && o.policy != DI_POLICY_HYBRID) || !(o.hybrid_frac >= 0.0)) {
+      (o.policy != DI_POLICY_GEOM && o.policy != DI_POLICY_HYBRID) || !(o.hybrid_frac >= 0.0) ||
+      o.key_offset < 0 || o.key_offset > (1 << 20)) {
     diter_set_err(ctx, "invalid options");
     return DI_ERR_INVALID_ARG;
   }
@@ -770,6 +771,7 @@ di_status diter_setup_finish(di_ctx *ctx) {
   hc0.policy = o.policy;
   hc0.defer_m = ctx->defer_m;
   hc0.sweep = ctx->sweep_on;
+  hc0.key_off = o.key_offset > 0 ? (float)o.key_offset : 1.0f;
   hc0.done = 1;
   hc0.max_pass = o.max_passes;
   hc0.log_cap = ctx->log_cap;

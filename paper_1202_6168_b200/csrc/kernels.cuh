@@ -865,7 +865,7 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
                                            const float *__restrict__ kw, double T, long long base,
                                            ScAcc &acc, int &sel_all, double &dloss, int &dang_cnt,
                                            SweepStage &st, const SweepPf &pf, long long next_base,
-                                           bool take_dang) {
+                                           bool take_dang, float koff) {
   const unsigned lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
   double f[kSweepItems];
@@ -921,7 +921,7 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
     const double af = fabs(f[k]);
     const double key = KEY == 0 ? af
                      : KEY == 1 ? af * (double)w[k]
-                                : af * (double)__frcp_rn((float)dg[k] + 1.0f);
+                                : af * (double)__frcp_rn((float)dg[k] + koff);
     bool sel = key > T;                                      // strict ">" (R7)
 #if DITER_SWEEP_DANG_EVERY > 1
     // a dangling node pushes nothing, so its take can wait for a later sweep (any order is a
@@ -1031,6 +1031,7 @@ k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ct
   const Sink s{F, s_hot, g.hot_lo, g.lo, g.n, DIST ? g.G : nullptr, DIST ? g.dflags : nullptr};
   Stage sg{nullptr, nullptr, 0};
   const double T = ctl->T;
+  const float koff = ctl->key_off;
   // dangling nodes are taken every DITER_SWEEP_DANG_EVERY-th sweep, and in every sweep once the
   // carried bound is within 4 x the target (the stop needs their fluid gone from |F|_1)
   const bool take_dang = DITER_SWEEP_DANG_EVERY <= 1 || ctl->pass % DITER_SWEEP_DANG_EVERY == 0 ||
@@ -1066,12 +1067,12 @@ k_sweep(Graph g, double *__restrict__ F, double *__restrict__ H, Frontier fr, Ct
         for (long long q = s0 + q0; q < q1; ++q) {
           sweep_span<SIGNED, KEY, true, DIST>(g, s, F, H, fr, ctl, kw, T, span_of(q) * kSweepSpan, acc, sel_all,
                                               dloss, dang_cnt, st, pf, q + 1 < q1 ? span_of(q + 1) * kSweepSpan : -1,
-                                              take_dang);
+                                              take_dang, koff);
           sweep_flush<SIGNED>(g, s, ctl, st, sg, false);
         }
       } else {
         sweep_span<SIGNED, KEY, false, DIST>(g, s, F, H, fr, ctl, kw, T, span_of(s0 + q0) * kSweepSpan, acc, sel_all,
-                                             dloss, dang_cnt, st, pf, -1, take_dang);
+                                             dloss, dang_cnt, st, pf, -1, take_dang, koff);
         sweep_flush<SIGNED>(g, s, ctl, st, sg, false);
       }
     }

@@ -77,6 +77,7 @@ struct Ctl {
   int stop_after_flush;   // the bound met the target with mass pending: stop once it is delivered
   long long flushes;   // flushes executed since create
   int sweep;           // one-kernel async sweeps (options.sweep): r_p is the carried bound r_pred
+  float key_off;       // sweeps, derived per-edge key: |F_i| / (#out_i + key_off) (options.key_offset)
   // scatter tickets: one counter per stripe of the frontier groups, each on its
   // own 128-byte line (reset per pass)
   alignas(128) unsigned tickets[kStripes * 32];

@@ -64,7 +64,7 @@ SWEEP = int(os.environ.get("MODEL_SWEEP", bench.SWEEP.get(cfg, 0)))     # option
 RUN = bench.SCATTER_RUN.get(cfg, 0)
 # passes of the 1-GPU solve (scan term of the model)
 o1 = di.default_options(policy=pol, alpha=alpha, hybrid_frac=frac, select_key=key, sweep=SWEEP, scatter_run=RUN,
-                        scatter_stripes=bench.SCATTER_STRIPES.get(cfg, 0))
+                        scatter_stripes=bench.SCATTER_STRIPES.get(cfg, 0), key_offset=bench.KEY_OFFSET.get(cfg, 0))
 c1 = di.di_create(p.n, p.col_ptr, p.row_idx, p.values, p.b, p.d, o1)
 di.di_run(c1, p.stop)
 P1 = di.di_get_stats(c1)["passes"]
@@ -89,7 +89,7 @@ for K, pilot in [(K, it) for K in KS for it in range(PILOT + 1)]:
             o = di.default_options(policy=pol, alpha=alpha_k, hybrid_frac=frac_k, select_key=key,
                                    exchange_mode=MODE, check_interval=ROUND, remote_push=REMOTE,
                                    receive_rescale=RESCALE, p2p_sleep=SLEEP, sweep=SWEEP, scatter_run=RUN,
-                                   adapt_rounds=ADAPT)
+                                   adapt_rounds=ADAPT, key_offset=bench.KEY_OFFSET.get(cfg, 0))
             ctx = di.di_create_dist(r, K, cid, bounds, p.n, lcp, lri, lv, lb, p.d, o)
             di.di_run(ctx, p.stop)
             st[r] = di.di_get_stats(ctx)

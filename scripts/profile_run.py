@@ -23,7 +23,8 @@ if a.config == "C3":
 pol, alpha, frac, key = bench.SCHEDULES[a.config]
 kw = dict(policy=pol, alpha=alpha, hybrid_frac=frac, select_key=key, check_interval=8, pass_kernel=1,
           max_passes=a.max_passes, scatter_run=bench.SCATTER_RUN.get(a.config, 0),
-          sweep=bench.SWEEP.get(a.config, 0), scatter_stripes=bench.SCATTER_STRIPES.get(a.config, 0))
+          sweep=bench.SWEEP.get(a.config, 0), scatter_stripes=bench.SCATTER_STRIPES.get(a.config, 0),
+          key_offset=bench.KEY_OFFSET.get(a.config, 0))
 kw.update({k: int(v) for k, v in (o.split("=") for o in a.opt)})
 ctx = di.di_create(p.n, p.col_ptr, p.row_idx, p.values, p.b, p.d, di.default_options(**kw))
 t = time.perf_counter()

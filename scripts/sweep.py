@@ -35,7 +35,8 @@ for v in [x for x in a.variants.split(";")] or [""]:
         import bench
         pol, alpha, frac, key = bench.SCHEDULES[a.config]
         for k_, v_ in (("policy", pol), ("alpha", alpha), ("hybrid_frac", frac), ("select_key", key),
-                       ("scatter_run", bench.SCATTER_RUN.get(a.config, 0))):
+                       ("scatter_run", bench.SCATTER_RUN.get(a.config, 0)),
+                       ("key_offset", bench.KEY_OFFSET.get(a.config, 0))):
             kw.setdefault(k_, v_)
     kw.setdefault("policy", di.DI_POLICY_GEOM if a.policy == "geom" else di.DI_POLICY_HYBRID)
     kw["policy"] = int(kw["policy"])

@@ -39,7 +39,7 @@ def _bench_opts(cfg, **over):
     pol, alpha, frac, key = bench.SCHEDULES[cfg]
     kw = dict(policy=pol, profile=1, alpha=alpha, hybrid_frac=frac, select_key=key,
               scatter_run=bench.SCATTER_RUN.get(cfg, 0), sweep=bench.SWEEP.get(cfg, 0),
-              scatter_stripes=bench.SCATTER_STRIPES.get(cfg, 0))
+              scatter_stripes=bench.SCATTER_STRIPES.get(cfg, 0), key_offset=bench.KEY_OFFSET.get(cfg, 0))
     kw.update(over)
     return di.default_options(**kw)
 

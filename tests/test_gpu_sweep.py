@@ -195,3 +195,22 @@ def test_sweep_ragged_sizes(n):
     H, F, log, r, _ = _gpu(n, cp, ri, 1e-9 * bn, sweep=1, select_key=1, scatter_run=6, scatter_stripes=4)
     assert np.abs(H - X).sum() <= TOL * bn
     _check_state(n, cp, ri, None, None, 0.85, H, F, r, 1e-9 * bn)
+
+
+@pytest.mark.parametrize("c", [0, 8, 64])
+def test_sweep_key_offset(c):
+    """options.key_offset (reading R27): the sweep's derived per-edge key |F_i| / (#out_i + c).
+    Any c is another selection order of the same method (P:93-94): same X, exact identity;
+    c = 0 is the default c = 1; a negative value is rejected."""
+    n = 150_001
+    cp, ri = gen.web_graph(n, 3, gen.XMIN_C4)
+    X, P, bn = _xref(n, cp, ri)
+    target = 1e-9 * bn
+    H, F, log, r, st = _gpu(n, cp, ri, target, sweep=1, select_key=1, alpha=2.0, hybrid_frac=0.55, key_offset=c)
+    assert np.abs(H - X).sum() <= TOL * bn
+    _check_state(n, cp, ri, None, None, 0.85, H, F, r, target)
+    if c == 0:
+        H1, F1, log1, r1, st1 = _gpu(n, cp, ri, target, sweep=1, select_key=1, alpha=2.0, hybrid_frac=0.55, key_offset=1)
+        assert st1["passes"] == st["passes"]
+        with pytest.raises(di.DiError):
+            di.di_create(n, cp, ri, None, None, 0.85, di.default_options(sweep=1, key_offset=-1))
