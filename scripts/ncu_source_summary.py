@@ -1,3 +1,9 @@
+"""Summarise the source page of an ncu report (ncu -i x.ncu-rep --page source --csv > x.csv):
+stall totals, the top instructions by stall samples with their two main stall reasons, and
+an opcode census (samples, executed warp instructions, thread instructions).
+
+    python scripts/ncu_source_summary.py x.csv [top-N]
+"""
 import csv, sys, re
 rows = list(csv.reader(open(sys.argv[1])))
 hdr = rows[1]

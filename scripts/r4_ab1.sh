@@ -1,4 +1,5 @@
 # Round-2 session 5: A/B of k_sweep build variants (bench launch configuration) + source-level ncu of the base
+# (variants/ built with scripts/build_variant.py; the rowpf flag, DITER_SWEEP_ROW_PF, was removed again after this run)
 cd ${GRAFT_REPO_ROOT:-.}
 mkdir -p gpurun_out
 run() { c=$1; v=$2
