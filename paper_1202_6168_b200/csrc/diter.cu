@@ -139,7 +139,7 @@ static void free_ctx(di_ctx *c) {
   mark("graph exec");
   for (cudaEvent_t e : c->prof_ev)
     if (e) cudaEventDestroy(e);
-  void *ptrs[] = {c->col_ptr, c->row_idx, c->vals, c->d_b, c->F, c->H, c->fr.ids, c->fr.S, c->fr.seg_cnt, const_cast<unsigned *>(c->fr.dang_bits),
+  void *ptrs[] = {c->col_ptr, c->row_idx, c->vals, c->d_b, c->F, c->H, c->fr.ids, c->fr.S, c->fr.seg_cnt, const_cast<unsigned *>(c->fr.dang_bits), const_cast<unsigned *>(c->fr.cp32),
                   c->fr.hub_w, c->fr.hub_b0, c->fr.hub_deg, c->fr.hub_chunk, c->fr.hub_cslot, c->sel_part, c->sc_part,
                   c->l1_part, c->l1_out, c->ctl, c->log, c->far_off, c->far.rows, c->far.vals, c->far.fill, c->kw, c->nloc, c->H_old};
   if (c->stream) cudaStreamSynchronize(c->stream);
@@ -744,6 +744,13 @@ di_status diter_setup(di_ctx *ctx, const int64_t *col_ptr, const int32_t *row_id
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sweep<false, 1>, kScatterThreads, kSweepDynSmem));
     ctx->grid_sweep = (int)std::max(1LL, std::min<long long>((long long)ctx->num_sms * std::max(1, occ),
                                                              (n + kSweepSpan - 1) / kSweepSpan));
+  }
+  if (ctx->sweep_on && ctx->nnz_local < (1LL << 32)) {
+    // the scan's 4-byte col_ptr copy (built last: nothing moves col_ptr after this point)
+    unsigned *c32 = nullptr;
+    TRY(dalloc(ctx, &c32, (size_t)n + 1));
+    k_col_ptr32<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ctx->col_ptr, n, c32);
+    ctx->fr.cp32 = c32;
   }
   if (!ctx->sweep_on) TRY(diter_setup_defer(ctx));
   tr.mark(ctx->stream, "far-edge deferral");

@@ -839,12 +839,16 @@ __device__ __forceinline__ void sweep_prefetch(const Graph &g, const double *F, 
 #if DITER_SWEEP_EF & 1
     cp_async_ef(pf.cp + 32 * k + lane, g.col_ptr + (i < n ? i : n), 8, true, pol);
 #else
-    cp_async(pf.cp + 32 * k + lane, g.col_ptr + (i < n ? i : n), 8, true);
+    if (fr.cp32) cp_async(reinterpret_cast<unsigned *>(pf.cp) + 32 * k + lane, fr.cp32 + (i < n ? i : n), 4, true);
+    else cp_async(pf.cp + 32 * k + lane, g.col_ptr + (i < n ? i : n), 8, true);
 #endif
   }
   if (lane == 0) {
     const long long iend = base + kSweepSpan;
-    cp_async(pf.cp + kSweepSpan, g.col_ptr + (iend < n ? iend : n), 8, true);
+    if (fr.cp32 && !(DITER_SWEEP_EF & 1))
+      cp_async(reinterpret_cast<unsigned *>(pf.cp) + kSweepSpan, fr.cp32 + (iend < n ? iend : n), 4, true);
+    else
+      cp_async(pf.cp + kSweepSpan, g.col_ptr + (iend < n ? iend : n), 8, true);
   }
   const long long wi = (base >> 5) + lane;
 #if DITER_SWEEP_EF & 1
@@ -873,6 +877,7 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
   long long cp[kSweepItems];
   long long cp_end;
   unsigned dword;
+  const bool cp32 = fr.cp32 != nullptr && !(DITER_SWEEP_EF & 1);   // 32-bit col_ptr copy in use (warp-uniform)
   if (PF) {
     // this span's inputs, prefetched into the warp's buffer
     asm volatile("cp.async.wait_all;" ::: "memory");
@@ -881,9 +886,9 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
     for (int k = 0; k < kSweepItems; ++k) {
       f[k] = pf.f[32 * k + lane];
       if (KEY == 1) w[k] = pf.w[32 * k + lane];
-      cp[k] = pf.cp[32 * k + lane];
+      cp[k] = cp32 ? (long long)reinterpret_cast<const unsigned *>(pf.cp)[32 * k + lane] : pf.cp[32 * k + lane];
     }
-    cp_end = pf.cp[kSweepSpan];
+    cp_end = cp32 ? (long long)reinterpret_cast<const unsigned *>(pf.cp)[kSweepSpan] : pf.cp[kSweepSpan];
     dword = (int)lane < kSweepItems ? pf.dw[lane] : 0u;
     __syncwarp();
     if (next_base >= 0) sweep_prefetch<KEY>(g, F, kw, fr, next_base, pf);
@@ -895,10 +900,10 @@ __device__ __forceinline__ void sweep_span(const Graph &g, const Sink &s, double
       const long long i = base + 32 * k + lane;
       f[k] = (i < n) ? F[i] : 0.0;
       if (KEY == 1) w[k] = (i < n) ? __ldcs(kw + i) : 0.0f;
-      cp[k] = __ldcs(g.col_ptr + (i < n ? i : n));
+      cp[k] = cp32 ? (long long)__ldcs(fr.cp32 + (i < n ? i : n)) : __ldcs(g.col_ptr + (i < n ? i : n));
     }
     const long long iend = base + kSweepSpan;
-    cp_end = __ldcs(g.col_ptr + (iend < n ? iend : n));
+    cp_end = cp32 ? (long long)__ldcs(fr.cp32 + (iend < n ? iend : n)) : __ldcs(g.col_ptr + (iend < n ? iend : n));
     const long long wi = (base >> 5) + lane;
     dword = ((int)lane < kSweepItems && (wi << 5) < n) ? __ldg(fr.dang_bits + wi) : 0u;
   }
@@ -1496,6 +1501,12 @@ __global__ void k_key_weights(const long long *col_ptr, long long n, const unsig
     else if (key == DI_KEY_PAPER) x = 1.0 / (((double)indeg[i] + 1.0) * (out + 1.0));
     w[i] = __double2float_rn(x);
   }
+}
+
+// 32-bit copy of col_ptr for the sweep's scan (setup; only when col_ptr[n] < 2^32).
+__global__ void k_col_ptr32(const long long *col_ptr, long long n, unsigned *cp32) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += stride) cp32[i] = (unsigned)col_ptr[i];
 }
 
 // Dangling bitmap (setup): bit i%32 of word i/32 set when column i has no out-edge.

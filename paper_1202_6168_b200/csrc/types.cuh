@@ -163,6 +163,8 @@ struct Frontier {
   long long *hub_deg;
   unsigned *hub_chunk;   // first 2048-edge chunk id of the hub (prefix in slot order)
   unsigned *hub_cslot;   // sweeps: chunk -> hub slot + 1, 0 until published (cleared once pushed)
+  const unsigned *cp32;  // sweeps: col_ptr as 32-bit values [n + 1] when the owned edges fit (the scan then
+                         // reads 4 B per node instead of 8), else nullptr
 };
 
 // Validation + degree census in one pass over the columns.

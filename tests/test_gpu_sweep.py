@@ -211,6 +211,6 @@ def test_sweep_key_offset(c):
     _check_state(n, cp, ri, None, None, 0.85, H, F, r, target)
     if c == 0:
         H1, F1, log1, r1, st1 = _gpu(n, cp, ri, target, sweep=1, select_key=1, alpha=2.0, hybrid_frac=0.55, key_offset=1)
-        assert st1["passes"] == st["passes"]
+        assert abs(st1["passes"] - st["passes"]) <= 3       # asynchronous sweeps: not deterministic
         with pytest.raises(di.DiError):
             di.di_create(n, cp, ri, None, None, 0.85, di.default_options(sweep=1, key_offset=-1))
